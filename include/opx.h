@@ -1,0 +1,161 @@
+/*
+ * opx — C ABI of the B200-native FSDP + Ulysses-SP + EP training step.
+ *
+ * The reference (omniplan, /root/reference/proj) exposes this path only as a
+ * C++ model: build_step_graph -> simulate -> report (step_graph.hpp:59-60,
+ * simulator.hpp:57-62) behind the ParallelPlan API (plan.hpp:26-107) and the
+ * JSON config schema (config_io.hpp:24-50).  opx keeps that API surface and
+ * executes the step on B200s instead of simulating it.  Every entry point is
+ * plain C: pointers, sizes, JSON strings; no C++ types or exceptions cross.
+ *
+ * Return codes mirror the reference CLI exit codes (cli.hpp:15-19) where one
+ * exists: 0 ok, 2 config error, 3 invalid plan, plus 6 CUDA/NCCL error,
+ * 7 parity failure, 8 peer timeout, 9 bad argument.  Details of the last
+ * failure on the calling thread: opx_last_error().
+ */
+#ifndef OPX_H
+#define OPX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPX_OK 0
+#define OPX_ERR_CONFIG 2
+#define OPX_ERR_PLAN 3
+#define OPX_ERR_CUDA 6
+#define OPX_ERR_PARITY 7
+#define OPX_ERR_TIMEOUT 8
+#define OPX_ERR_ARG 9
+
+const char* opx_last_error(void);
+const char* opx_version(void);
+
+/* ------------------------------------------------------------------------
+ * Plan layer (host only)
+ * ------------------------------------------------------------------------ */
+
+/* Replaces omniplan::validate (plan.hpp:68-69, plan.cpp:19-83) behind
+ * parse_cluster/model/workload (config_io.cpp:52-151).  plan_json holds the
+ * ParallelPlan fields (to_json keys, config_io.cpp:248-262); dp_shard may be
+ * omitted and is derived as world/(dp_replicate*sp) like cli.cpp:46-65.
+ * Returns 0 if valid, 3 if violations (written to out_codes as lines
+ * "code<TAB>message", reference codes unchanged), 2 on config errors. */
+int opx_plan_validate(const char* cluster_json, const char* model_json,
+                      const char* workload_json, const char* plan_json, char* out_codes,
+                      size_t cap);
+
+/* Resolves a valid plan into a JSON document: label (plan_label, plan.cpp:149-159),
+ * mesh + groups (plan_mesh/groups_along/ep_groups, plan.cpp:161-182,
+ * mesh.cpp:71-105), expert sharding (plan.cpp:85-93), module plans
+ * (plan.cpp:95-107), parameter accounting (specs.cpp:36-107) and per-rank
+ * collective volumes (comm.cpp:8-105). */
+int opx_plan_resolve(const char* cluster_json, const char* model_json,
+                     const char* workload_json, const char* plan_json, char* out_json,
+                     size_t cap);
+
+/* ------------------------------------------------------------------------
+ * Step executor: the real counterpart of build_step_graph + simulate + report.
+ * One handle per rank (process/GPU).
+ * ------------------------------------------------------------------------ */
+typedef struct opx_step opx_step;
+
+/* Measured StepReport (simulator.hpp:43-50), device-timed on this rank. */
+typedef struct {
+  double step_time_s;   /* first kernel -> optimizer end, CUDA events */
+  double fwd_s, bwd_s, opt_s, comm_wait_s;
+  double loss;          /* global mean token loss (all-reduced) */
+  double tokens;        /* tokens processed by this rank this step */
+  double n_valid;       /* global count of supervised tokens */
+  int64_t launches;     /* opx kernels launched during the step */
+} opx_step_report;
+
+/* 128-byte NCCL unique id for the world communicator (rank 0 creates it). */
+int opx_nccl_unique_id(void* out128);
+
+/* exec_json: {"seed":.., "lr":.., "betas":[..], "eps":.., "weight_decay":..,
+ *             "rope_theta":.., "rms_eps":.., "ce_chunk":.., "trace":bool} */
+int opx_step_create(const char* cluster_json, const char* model_json,
+                    const char* workload_json, const char* plan_json, const char* exec_json,
+                    int rank, int local_device, const void* nccl_id128, opx_step** out);
+/* CUDA-IPC handles of this rank's peer-visible buffers (opaque bytes). */
+int opx_step_ipc_export(opx_step* st, void* out, size_t cap, size_t* len);
+/* All ranks' exports concatenated in rank order (world * len bytes). */
+int opx_step_ipc_import(opx_step* st, const void* all, size_t len_per_rank);
+int opx_step_init_weights(opx_step* st, uint64_t seed);
+/* Host arrays for THIS rank: ids/labels of its local tokens (rows x S/sp,
+ * row-major), positions of ALL rows*S tokens of its sequences (position
+ * within sample), cu_seqlens over those rows*S tokens (packing.hpp:28
+ * convention), and the global supervised-token count. */
+int opx_step_load_batch(opx_step* st, const int32_t* ids, const int32_t* labels,
+                        const int32_t* positions, const int32_t* cu_seqlens, int n_cu,
+                        int64_t n_valid_global);
+int opx_step_run(opx_step* st, opx_step_report* rep);
+/* Copies a named tensor to host. Names: "param:<name>", "grad:<name>",
+ * "master:<name>", "exp_avg:<name>", "exp_avg_sq:<name>", "loss_rows".
+ * <name> follows HF naming ("model.layers.0.self_attn.q_proj.weight"). Only
+ * the part this rank owns is returned for sharded tensors (see opx_step_tensor_info). */
+int opx_step_get(opx_step* st, const char* name, void* host_dst, size_t bytes);
+/* Describes a named tensor: numel, and the [begin,end) element interval of the
+ * flattened logical tensor held by this rank. */
+int opx_step_tensor_info(opx_step* st, const char* name, int64_t* numel, int64_t* begin,
+                         int64_t* end);
+/* Chrome trace of the last step in simulator.cpp:133-151's schema. */
+int opx_step_trace(opx_step* st, char* out_json, size_t cap, size_t* len);
+int opx_step_destroy(opx_step* st);
+
+/* ------------------------------------------------------------------------
+ * Kernel-level entry points (device pointers, cudaStream_t as void*).
+ * ------------------------------------------------------------------------ */
+/* D = A . B^T (see csrc/runtime/gemm_api.h for layouts and epilogues). */
+int opx_gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
+             int64_t ldb, int b_mn, int epi, void* D, int64_t ldd, const float* R, int64_t ldr,
+             void* D2, int64_t ldd2, float scale, void* stream);
+int opx_gemm_grouped(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
+                     int64_t ldb, int b_mn, int epi, void* D, int64_t ldd, void* D2,
+                     int64_t ldd2, int groups, int grouped_k, const int* g_start,
+                     const int* g_rows, int64_t rows_total, int64_t d_group_stride,
+                     void* stream);
+int opx_rmsnorm_fwd(const float* x, const void* w, void* y, float* rstd, int T, int H, float eps,
+                    void* stream);
+int opx_rmsnorm_bwd(const float* dy, const float* x, const void* w, const float* rstd,
+                    const float* dres, float* dx, float* dw_part, float* dw, int T, int H,
+                    void* stream);
+int opx_rmsnorm_bwd_parts(int T);
+int opx_ce_fwd_bwd(void* logits, int64_t ldl, const int32_t* labels, float* loss, int T, int V,
+                   float inv_n, void* stream);
+int opx_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t T, int F, void* stream);
+int opx_adamw(float* p, float* m, float* v, const float* g, void* pb, int64_t n, float lr,
+              float b1, float b2, float eps, float wd, int step, void* stream);
+int opx_embed_fwd(const int32_t* ids, const void* E, float* x, int T, int H, void* stream);
+int opx_embed_bwd(const int32_t* ids, const float* dx, float* dE, int T, int H, void* stream);
+int opx_init_param(float* f32, void* b16, int64_t n, int64_t phys0, uint64_t key_a,
+                   uint64_t key_b, double c, float constant, int interleave,
+                   int64_t rows_per_slab, int64_t cols, void* stream);
+uint64_t opx_param_key(const char* name, uint64_t seed);
+/* Causal varlen GQA attention, head_dim 128, layouts in kernels_api.h. */
+int opx_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t ldq,
+                 int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
+                 const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream);
+int opx_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                 const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
+                 int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,
+                 int N, int hq, int hk, float scale, void* stream);
+/* Single-rank Ulysses relayout (sp == 1 path) with RoPE, for testing. */
+int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void* v_full,
+                  int hq, int hk, int rows, int S, const int32_t* pos, const float* inv_freq,
+                  void* stream);
+
+/* MoE routing (moe.cu): fp32 router logits with a fixed sequential K order,
+ * top-k with lower-index tie break, renormalised softmax weights, and a
+ * stable counting-sort permutation by (expert, token, slot). */
+int opx_moe_route(const void* h, const void* w_router, int T, int H, int E, int k,
+                  float* logits, int32_t* topk_idx, float* topk_w, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OPX_H */

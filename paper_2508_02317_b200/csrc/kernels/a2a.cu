@@ -1,0 +1,188 @@
+// DeepSpeed-Ulysses all-to-alls written as direct NVLink peer stores.
+//
+// seq->head (PAPER.md:589-603 gather_seq_scatter_heads; step_graph.cpp:224-229):
+//   each rank holds rows*S/sp tokens x all heads; it writes, for every head
+//   group (q / k / v), the heads owned by rank j straight into rank j's
+//   [rows*S, heads/sp, 128] buffer at the tokens' global positions, applying
+//   RoPE on the way (fused pack + rotary).
+// head->seq (PAPER.md:604-612 gather_heads_scatter_seq; step_graph.cpp:237-239):
+//   the mirror: rank j's [rows*S, heads/sp, 128] slices go back to the token
+//   owners' [rows*S/sp, width] rows, optionally un-rotating (RoPE backward) and
+//   reading an fp32 source (the dQ accumulator).
+// With sp == 1 both degenerate to a local relayout (+ RoPE).
+//
+// The destination pointers are CUDA-IPC mappings of the peers' buffers; a
+// release/acquire flag barrier (k_peer_barrier) orders the stores against the
+// consumer kernels on the other GPUs.
+#include <cuda_bf16.h>
+
+#include "../runtime/kernels_api.h"
+#include "ptx.cuh"
+
+namespace opx {
+namespace {
+
+using bf16 = __nv_bfloat16;
+constexpr int D = 128, HALF = 64;
+
+// Each thread moves 8 elements of the first half and the matching 8 of the
+// second half of one head vector (so RoPE pairs stay in one thread).
+__global__ void seq2head_kernel(const A2AArgs a) {
+  const int per_tok = 8;  // threads per head vector
+  int heads = 0;
+  for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total;
+  const int T = a.rows * (a.seq / a.sp);
+  const int64_t total = int64_t(T) * heads * per_tok;
+  const bf16* src = reinterpret_cast<const bf16*>(a.local[0]);
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int c8 = int(idx % per_tok);
+    int hh = int((idx / per_tok) % heads);
+    const int r = int(idx / (int64_t(per_tok) * heads));
+    int gi = 0;
+    while (hh >= a.g[gi].heads_total) hh -= a.g[gi++].heads_total;
+    const A2AGroup& G = a.g[gi];
+    const int per_rank = G.heads_total / a.sp;
+    const int dst_rank = hh / per_rank, hl = hh % per_rank;
+    const int S_loc = a.seq / a.sp;
+    const int b = r / S_loc, p = r % S_loc;
+    const int64_t gtok = int64_t(b) * a.seq + int64_t(a.rank) * S_loc + p;
+
+    const bf16* s = src + int64_t(r) * a.local_ld + G.col0 + hh * D + c8 * 8;
+    uint4 lo = *reinterpret_cast<const uint4*>(s);
+    uint4 hi = *reinterpret_cast<const uint4*>(s + HALF);
+    if (G.rope) {
+      const float pos = float(a.pos[gtok]);
+      uint32_t* l = reinterpret_cast<uint32_t*>(&lo);
+      uint32_t* h = reinterpret_cast<uint32_t*>(&hi);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x1 = ptx::unpack_bf16(l[e]), x2 = ptx::unpack_bf16(h[e]);
+        float sn0, cs0, sn1, cs1;
+        sincosf(pos * a.inv_freq[c8 * 8 + 2 * e], &sn0, &cs0);
+        sincosf(pos * a.inv_freq[c8 * 8 + 2 * e + 1], &sn1, &cs1);
+        l[e] = ptx::pack_bf16(x1.x * cs0 - x2.x * sn0, x1.y * cs1 - x2.y * sn1);
+        h[e] = ptx::pack_bf16(x2.x * cs0 + x1.x * sn0, x2.y * cs1 + x1.y * sn1);
+      }
+    }
+    bf16* d = reinterpret_cast<bf16*>(G.full[dst_rank]) + (gtok * per_rank + hl) * D + c8 * 8;
+    *reinterpret_cast<uint4*>(d) = lo;
+    *reinterpret_cast<uint4*>(d + HALF) = hi;
+  }
+}
+
+__global__ void head2seq_kernel(const A2AArgs a) {
+  const int per_tok = 8;
+  int heads_loc = 0;  // heads held by this rank across groups
+  for (int i = 0; i < a.ngroups; ++i) heads_loc += a.g[i].heads_total / a.sp;
+  const int64_t Ntok = int64_t(a.rows) * a.seq;
+  const int64_t total = Ntok * heads_loc * per_tok;
+  const int S_loc = a.seq / a.sp;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int c8 = int(idx % per_tok);
+    int hh = int((idx / per_tok) % heads_loc);
+    const int64_t gtok = idx / (int64_t(per_tok) * heads_loc);
+    int gi = 0;
+    while (hh >= a.g[gi].heads_total / a.sp) hh -= a.g[gi++].heads_total / a.sp;
+    const A2AGroup& G = a.g[gi];
+    const int per_rank = G.heads_total / a.sp;
+    const int b = int(gtok / a.seq), sp_pos = int(gtok % a.seq);
+    const int dst_rank = sp_pos / S_loc;
+    const int r = b * S_loc + sp_pos % S_loc;
+    float x1[8], x2[8];
+    if (G.src_f32) {
+      const float* s = reinterpret_cast<const float*>(G.full[0]) + (gtok * per_rank + hh) * D + c8 * 8;
+      const float4 a0 = *reinterpret_cast<const float4*>(s), a1 = *reinterpret_cast<const float4*>(s + 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(s + HALF),
+                   b1 = *reinterpret_cast<const float4*>(s + HALF + 4);
+      x1[0] = a0.x; x1[1] = a0.y; x1[2] = a0.z; x1[3] = a0.w;
+      x1[4] = a1.x; x1[5] = a1.y; x1[6] = a1.z; x1[7] = a1.w;
+      x2[0] = b0.x; x2[1] = b0.y; x2[2] = b0.z; x2[3] = b0.w;
+      x2[4] = b1.x; x2[5] = b1.y; x2[6] = b1.z; x2[7] = b1.w;
+    } else {
+      const bf16* s = reinterpret_cast<const bf16*>(G.full[0]) + (gtok * per_rank + hh) * D + c8 * 8;
+      const uint4 lo = *reinterpret_cast<const uint4*>(s), hi = *reinterpret_cast<const uint4*>(s + HALF);
+      const uint32_t* l = reinterpret_cast<const uint32_t*>(&lo);
+      const uint32_t* h = reinterpret_cast<const uint32_t*>(&hi);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 u = ptx::unpack_bf16(l[e]), v = ptx::unpack_bf16(h[e]);
+        x1[2 * e] = u.x; x1[2 * e + 1] = u.y; x2[2 * e] = v.x; x2[2 * e + 1] = v.y;
+      }
+    }
+    if (G.rope) {  // inverse rotation (transpose of the forward rotary matrix)
+      const float pos = float(a.pos[gtok]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float sn, cs;
+        sincosf(pos * a.inv_freq[c8 * 8 + e], &sn, &cs);
+        const float y1 = x1[e] * cs + x2[e] * sn;
+        const float y2 = x2[e] * cs - x1[e] * sn;
+        x1[e] = y1;
+        x2[e] = y2;
+      }
+    }
+    uint4 lo, hi;
+    uint32_t* l = reinterpret_cast<uint32_t*>(&lo);
+    uint32_t* h = reinterpret_cast<uint32_t*>(&hi);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      l[e] = ptx::pack_bf16(x1[2 * e], x1[2 * e + 1]);
+      h[e] = ptx::pack_bf16(x2[2 * e], x2[2 * e + 1]);
+    }
+    const int hglob = a.rank * per_rank + hh;  // head index within the group
+    bf16* d = reinterpret_cast<bf16*>(a.local[dst_rank]) + int64_t(r) * a.local_ld + G.col0 +
+              hglob * D + c8 * 8;
+    *reinterpret_cast<uint4*>(d) = lo;
+    *reinterpret_cast<uint4*>(d + HALF) = hi;
+  }
+}
+
+__global__ void peer_barrier_kernel(uint32_t* const* peer_flags, uint32_t* my_flags, int n, int me,
+                                    uint32_t epoch, int* timeout_flag) {
+  const int j = threadIdx.x;
+  if (j >= n) return;
+  __threadfence_system();
+  ptx::st_release_sys(peer_flags[j] + me, epoch);
+  long long spins = 0;
+  while (ptx::ld_acquire_sys(my_flags + j) < epoch) {
+    if (++spins > (1ll << 31)) {  // ~seconds: report instead of hanging the box
+      if (timeout_flag) atomicExch(timeout_flag, 1);
+      break;
+    }
+  }
+  __threadfence_system();
+}
+
+}  // namespace
+
+cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s) {
+  int heads = 0;
+  for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total;
+  const int64_t n = int64_t(a.rows) * (a.seq / a.sp) * heads * 8;
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  seq2head_kernel<<<int(blocks), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t k_a2a_head2seq(const A2AArgs& a, cudaStream_t s) {
+  int heads = 0;
+  for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total / a.sp;
+  const int64_t n = int64_t(a.rows) * a.seq * heads * 8;
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  head2seq_kernel<<<int(blocks), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t k_peer_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int n, int me,
+                           uint32_t epoch, int* timeout_flag, cudaStream_t s) {
+  peer_barrier_kernel<<<1, 32, 0, s>>>(peer_flags, my_flags, n, me, epoch, timeout_flag);
+  return cudaGetLastError();
+}
+
+}  // namespace opx

@@ -1,0 +1,476 @@
+// Persistent warp-specialised bf16 GEMM on tcgen05 (sm_100a).
+//
+//   D[M,N] (op)= A[M,K] . B[N,K]^T      (bf16 in, fp32 accumulate in TMEM)
+//
+// Operands may be K-major or MN-major (the dgrad / wgrad forms of a linear
+// layer), selected by template flags; TMA loads 128B-swizzled tiles into a
+// 4-stage smem ring, one elected thread issues tcgen05.mma, and four epilogue
+// warps drain a double-buffered TMEM accumulator (2 x 256 columns) while the
+// next tile's MMAs run.  Epilogues fuse what follows each GEMM in the step:
+// bf16/fp32 stores, the residual add, fp32 accumulation (wgrad into a grad
+// buffer), and the SwiGLU gate on 128-column interleaved gate/up weights.
+//
+// Grouped mode (MoE experts): per-group row segments (128-aligned) with a
+// per-group weight slab; either M varies per group (fwd/dgrad) or K does (wgrad).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "../runtime/gemm_api.h"
+#include "ptx.cuh"
+
+namespace opx {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
+constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 + 256;
+constexpr int NUM_THREADS = 256;
+
+struct KParams {
+  int M, N, K;
+  int epi;
+  void* D;
+  int64_t ldd;
+  const float* R;
+  int64_t ldr;
+  __nv_bfloat16* D2;
+  int64_t ldd2;
+  float scale;
+  // grouped
+  int groups;          // 0 = plain GEMM
+  int grouped_k;       // 1: K varies per group (wgrad), 0: M varies (fwd/dgrad)
+  const int* g_start;  // [groups] row offset of each segment (multiple of 128)
+  const int* g_rows;   // [groups] rows in each segment (padded to a multiple of 128 for grouped_k)
+  int64_t g_b_rows;    // rows of B per group slab (B row coordinate offset = g * g_b_rows)
+  int64_t g_d_stride;  // element offset of D between groups (grouped_k only)
+};
+
+struct TileCoord {
+  int g, mb, nb, m0, k_begin, nk;
+  bool valid;
+};
+
+// Tile enumeration: plain -> m fastest within an n column; grouped -> walk
+// groups in order (counts come from device memory, so every role recomputes
+// them identically).
+__device__ __forceinline__ TileCoord tile_of(const KParams& p, int t) {
+  TileCoord c{};
+  const int nblk = (p.N + BN - 1) / BN;
+  if (p.groups == 0) {
+    const int mblk = (p.M + BM - 1) / BM;
+    c.valid = t < mblk * nblk;
+    c.g = 0;
+    c.mb = t % mblk;
+    c.nb = t / mblk;
+    c.m0 = c.mb * BM;
+    c.k_begin = 0;
+    c.nk = (p.K + BK - 1) / BK;
+    return c;
+  }
+  if (!p.grouped_k) {
+    for (int g = 0; g < p.groups; ++g) {
+      const int rows = p.g_rows[g];
+      const int mblk = (rows + BM - 1) / BM;
+      const int n = mblk * nblk;
+      if (t < n) {
+        c.valid = true;
+        c.g = g;
+        c.mb = t % mblk;
+        c.nb = t / mblk;
+        c.m0 = p.g_start[g] + c.mb * BM;
+        c.k_begin = 0;
+        c.nk = (p.K + BK - 1) / BK;
+        return c;
+      }
+      t -= n;
+    }
+    c.valid = false;
+    return c;
+  }
+  // grouped_k: every group has the same (M, N) output; K = segment rows.
+  const int mblk = (p.M + BM - 1) / BM;
+  const int per = mblk * nblk;
+  c.g = t / per;
+  c.valid = c.g < p.groups;
+  if (!c.valid) return c;
+  const int r = t % per;
+  c.mb = r % mblk;
+  c.nb = r / mblk;
+  c.m0 = c.mb * BM;
+  c.k_begin = p.g_start[c.g];
+  c.nk = p.g_rows[c.g] / BK;
+  return c;
+}
+
+__device__ __forceinline__ int total_tiles(const KParams& p) {
+  const int nblk = (p.N + BN - 1) / BN;
+  if (p.groups == 0) return ((p.M + BM - 1) / BM) * nblk;
+  if (p.grouped_k) return p.groups * ((p.M + BM - 1) / BM) * nblk;
+  int n = 0;
+  for (int g = 0; g < p.groups; ++g) n += ((p.g_rows[g] + BM - 1) / BM) * nblk;
+  return n;
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const KParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int ntiles = total_tiles(p);
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileCoord c = tile_of(p, t);
+        const int n0 = c.nb * BN;
+        const int brow = int(c.g * p.g_b_rows);
+        for (int kb = 0; kb < c.nk; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+          uint8_t* a = sA + stage * A_STAGE_BYTES;
+          uint8_t* b = sB + stage * B_STAGE_BYTES;
+          const int k0 = c.k_begin + kb * BK;
+          if (!A_MN) {
+            ptx::tma_load_2d(&tmA, &full[stage], a, k0, c.m0);
+          } else {
+            ptx::tma_load_2d(&tmA, &full[stage], a, c.m0, k0);
+            ptx::tma_load_2d(&tmA, &full[stage], a + 8192, c.m0 + 64, k0);
+          }
+          if (!B_MN) {
+            ptx::tma_load_2d(&tmB, &full[stage], b, k0, brow + n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              ptx::tma_load_2d(&tmB, &full[stage], b + j * 8192, n0 + 64 * j, brow + k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      const TileCoord c = tile_of(p, t);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < c.nk; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = ptx::smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b_addr = ptx::smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? ptx::umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
+                                     : ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
+                                     : ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) {
+        if (c.nk == 0) {
+          // Nothing accumulated: still hand the (stale) buffer over; the
+          // epilogue writes zeros for empty K in this case.
+          ptx::mbar_arrive(&tfull[acc]);
+        } else {
+          ptx::mma_commit(&tfull[acc]);
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int ew = warp - 4;
+    int local = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      const TileCoord c = tile_of(p, t);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int r_local = ew * 32 + lane;
+      int row = c.m0 + r_local;
+      bool row_ok;
+      if (p.groups && !p.grouped_k)
+        row_ok = (c.mb * BM + r_local) < p.g_rows[c.g];
+      else
+        row_ok = row < p.M;
+      const int64_t dgoff = (p.groups && p.grouped_k) ? int64_t(c.g) * p.g_d_stride : 0;
+      const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
+      const bool empty_k = c.nk == 0;
+
+      if (p.epi == GEMM_EPI_SWIGLU) {
+        // Columns [0,128) of the tile are gate, [128,256) up, for features
+        // nb*128 + [0,128).
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t g[32], u[32];
+          ptx::tmem_ld32(tbase + ch * 32, g);
+          ptx::tmem_ld32(tbase + 128 + ch * 32, u);
+          ptx::tmem_wait_ld();
+          const int f0 = c.nb * 128 + ch * 32;
+          if (row_ok && f0 < p.N / 2) {
+            __nv_bfloat16* act = p.D2 + int64_t(row) * p.ldd2 + f0;
+            __nv_bfloat16* gu = p.D ? reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd +
+                                          c.nb * BN + ch * 32
+                                    : nullptr;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 va, vg, vu;
+              uint32_t* pa = reinterpret_cast<uint32_t*>(&va);
+              uint32_t* pg = reinterpret_cast<uint32_t*>(&vg);
+              uint32_t* pu = reinterpret_cast<uint32_t*>(&vu);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                // round gate/up to bf16 first: the saved gu is what backward sees
+                const float2 gf = ptx::unpack_bf16(ptx::pack_bf16(
+                    __uint_as_float(g[q * 8 + 2 * e]), __uint_as_float(g[q * 8 + 2 * e + 1])));
+                const float2 uf = ptx::unpack_bf16(ptx::pack_bf16(
+                    __uint_as_float(u[q * 8 + 2 * e]), __uint_as_float(u[q * 8 + 2 * e + 1])));
+                pa[e] = ptx::pack_bf16(silu(gf.x) * uf.x, silu(gf.y) * uf.y);
+                pg[e] = ptx::pack_bf16(gf.x, gf.y);
+                pu[e] = ptx::pack_bf16(uf.x, uf.y);
+              }
+              *reinterpret_cast<uint4*>(act + q * 8) = va;
+              if (gu) {
+                *reinterpret_cast<uint4*>(gu + q * 8) = vg;
+                *reinterpret_cast<uint4*>(gu + 128 + q * 8) = vu;
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + ch * 32, v);
+          ptx::tmem_wait_ld();
+          const int col0 = c.nb * BN + ch * 32;
+          if (!row_ok || col0 >= p.N) continue;
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = empty_k ? 0.f : __uint_as_float(v[i]) * p.scale;
+          const bool full_chunk = col0 + 32 <= p.N;
+          if (p.epi == GEMM_EPI_BF16) {
+            __nv_bfloat16* d =
+                reinterpret_cast<__nv_bfloat16*>(p.D) + dgoff + int64_t(row) * p.ldd + col0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (!full_chunk && col0 + q * 8 >= p.N) break;
+              uint4 o;
+              o.x = ptx::pack_bf16(f[q * 8 + 0], f[q * 8 + 1]);
+              o.y = ptx::pack_bf16(f[q * 8 + 2], f[q * 8 + 3]);
+              o.z = ptx::pack_bf16(f[q * 8 + 4], f[q * 8 + 5]);
+              o.w = ptx::pack_bf16(f[q * 8 + 6], f[q * 8 + 7]);
+              *reinterpret_cast<uint4*>(d + q * 8) = o;
+            }
+          } else {
+            float* d = reinterpret_cast<float*>(p.D) + dgoff + int64_t(row) * p.ldd + col0;
+            const float* r = nullptr;
+            if (p.epi == GEMM_EPI_F32_RESID) r = p.R + int64_t(row) * p.ldr + col0;
+            if (p.epi == GEMM_EPI_F32_ACCUM) r = d;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (!full_chunk && col0 + q * 4 >= p.N) break;
+              float4 o = make_float4(f[q * 4 + 0], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
+              if (r) {
+                const float4 rv = *reinterpret_cast<const float4*>(r + q * 4);
+                o.x += rv.x;
+                o.y += rv.y;
+                o.z += rv.z;
+                o.w += rv.w;
+              }
+              *reinterpret_cast<float4*>(d + q * 4) = o;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc(tmem_base, 512);
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+int g_num_sms = 0;
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode;
+}
+
+// 2-D bf16 tensor map: inner dim (contiguous) x outer dim, row stride in elements.
+bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_inner, uint32_t box_outer) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool A_MN, bool B_MN>
+cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const KParams& kp, int grid,
+                   cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  gemm_tc_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(a, b, kp);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s) {
+  if ((g.groups == 0 || g.grouped_k) && g.M <= 0) return cudaSuccess;
+  if (g.N <= 0) return cudaSuccess;
+  if (g.N % 8 != 0 || (g.epi == GEMM_EPI_SWIGLU && g.N % 256 != 0)) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  const bool grouped = g.groups > 0;
+  const bool gm = grouped && !g.grouped_k;  // rows of A vary per group
+  const bool gk = grouped && g.grouped_k;   // K varies per group (wgrad)
+  if (gk && !(g.a_mn && g.b_mn)) return cudaErrorInvalidValue;
+  if (gm && g.a_mn) return cudaErrorInvalidValue;
+  const uint64_t a_rows = gm ? uint64_t(g.rows_total) : uint64_t(g.M);
+  const uint64_t k_ext = gk ? uint64_t(g.rows_total) : uint64_t(g.K);
+  bool ok = !g.a_mn ? make_map(&ma, g.A, k_ext, a_rows, g.lda, BK, BM)
+                    : make_map(&ma, g.A, uint64_t(g.M), k_ext, g.lda, 64, BK);
+  if (!ok) return cudaErrorInvalidValue;
+  if (!g.b_mn) {
+    const uint64_t brows = gm ? uint64_t(g.groups) * uint64_t(g.N) : uint64_t(g.N);
+    ok = make_map(&mb, g.B, uint64_t(g.K), brows, g.ldb, BK, BN);
+  } else {
+    const uint64_t krows = gm ? uint64_t(g.groups) * uint64_t(g.K) : k_ext;
+    ok = make_map(&mb, g.B, uint64_t(g.N), krows, g.ldb, 64, BK);
+  }
+  if (!ok) return cudaErrorInvalidValue;
+
+  KParams kp{};
+  kp.M = g.M;
+  kp.N = g.N;
+  kp.K = g.K;
+  kp.epi = g.epi;
+  kp.D = g.D;
+  kp.ldd = g.ldd;
+  kp.R = g.R;
+  kp.ldr = g.ldr;
+  kp.D2 = g.D2;
+  kp.ldd2 = g.ldd2;
+  kp.scale = g.scale == 0.f ? 1.f : g.scale;
+  kp.groups = g.groups;
+  kp.grouped_k = g.grouped_k;
+  kp.g_start = g.g_start;
+  kp.g_rows = g.g_rows;
+  kp.g_b_rows = gm ? (g.b_mn ? g.K : g.N) : 0;
+  kp.g_d_stride = g.d_group_stride;
+
+  int tiles;
+  const int nblk = (g.N + BN - 1) / BN;
+  if (!grouped)
+    tiles = ((g.M + BM - 1) / BM) * nblk;
+  else if (g.grouped_k)
+    tiles = g.groups * ((g.M + BM - 1) / BM) * nblk;
+  else
+    tiles = int((g.rows_total + BM - 1) / BM + g.groups) * nblk;  // upper bound
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  if (grid < 1) grid = 1;
+  if (!g.a_mn && !g.b_mn) return launch<false, false>(ma, mb, kp, grid, s);
+  if (!g.a_mn && g.b_mn) return launch<false, true>(ma, mb, kp, grid, s);
+  if (g.a_mn && !g.b_mn) return launch<true, false>(ma, mb, kp, grid, s);
+  return launch<true, true>(ma, mb, kp, grid, s);
+}
+
+}  // namespace opx

@@ -1,0 +1,13 @@
+// Shared host-side helpers of the runtime (error state, param keys).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace opx {
+void set_error(const std::string& s);
+int cuda_fail(cudaError_t e, const char* what);
+uint64_t fnv1a64(const char* s);
+uint64_t param_key(const std::string& name, uint64_t seed);
+}  // namespace opx

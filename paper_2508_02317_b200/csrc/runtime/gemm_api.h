@@ -1,0 +1,54 @@
+// Internal C++ interface to the tcgen05 GEMM (kernels/gemm.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace opx {
+
+enum GemmEpi : int {
+  GEMM_EPI_BF16 = 0,       // D(bf16) = acc*scale
+  GEMM_EPI_F32 = 1,        // D(f32)  = acc*scale
+  GEMM_EPI_F32_RESID = 2,  // D(f32)  = R + acc*scale   (R may alias D)
+  GEMM_EPI_F32_ACCUM = 3,  // D(f32) += acc*scale
+  GEMM_EPI_SWIGLU = 4,     // D2(bf16)[., N/2] = silu(gate)*up; D (optional) = bf16 gate|up
+};
+
+// D[M,N] = A . B^T with
+//   A: !a_mn -> stored [M rows, K cols] (lda) ;  a_mn -> stored [K rows, M cols] (lda)
+//   B: !b_mn -> stored [N rows, K cols] (ldb) ;  b_mn -> stored [K rows, N cols] (ldb)
+// Grouped (MoE) forms:
+//   groups>0, grouped_k=0: A rows are 128-aligned segments g_start[g]..+g_rows[g] of a
+//     buffer with rows_total rows; B is a stack of `groups` slabs ([N,K] or [K,N]);
+//     D rows follow A rows.
+//   groups>0, grouped_k=1: K of group g = rows g_start[g]..+g_rows[g] (g_rows multiple
+//     of 64, zero padded) of A ([rows_total, M], a_mn) and B ([rows_total, N], b_mn);
+//     D of group g at D + g*d_group_stride.
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  const __nv_bfloat16* A = nullptr;
+  int64_t lda = 0;
+  bool a_mn = false;
+  const __nv_bfloat16* B = nullptr;
+  int64_t ldb = 0;
+  bool b_mn = false;
+  int epi = GEMM_EPI_BF16;
+  void* D = nullptr;
+  int64_t ldd = 0;
+  const float* R = nullptr;
+  int64_t ldr = 0;
+  __nv_bfloat16* D2 = nullptr;
+  int64_t ldd2 = 0;
+  float scale = 1.f;
+  int groups = 0;
+  int grouped_k = 0;
+  const int* g_start = nullptr;
+  const int* g_rows = nullptr;
+  int64_t rows_total = 0;
+  int64_t d_group_stride = 0;
+};
+
+cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s);
+int num_sms();
+
+}  // namespace opx

@@ -1,0 +1,88 @@
+// Internal C++ launch interface of the non-GEMM kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+#include "gemm_api.h"
+
+namespace opx {
+
+// elementwise.cu
+cudaError_t k_init_param(float* f32, __nv_bfloat16* b16, int64_t n, int64_t phys0, uint64_t key_a,
+                         uint64_t key_b, double c, float constant, int interleave,
+                         int64_t rows_per_slab, int64_t cols, cudaStream_t s);
+cudaError_t k_rmsnorm_fwd(const float* x, const __nv_bfloat16* w, __nv_bfloat16* y, float* rstd,
+                          int T, int H, float eps, cudaStream_t s);
+int k_rmsnorm_bwd_parts(int T);
+cudaError_t k_rmsnorm_bwd(const float* dy, const float* x, const __nv_bfloat16* w,
+                          const float* rstd, const float* dres, float* dx, float* dw_part,
+                          float* dw, int accumulate_dw, int T, int H, cudaStream_t s);
+cudaError_t k_embed_fwd(const int* ids, const __nv_bfloat16* E, float* x, int T, int H,
+                        cudaStream_t s);
+cudaError_t k_embed_bwd(const int* ids, const float* dx, float* dE, int T, int H, cudaStream_t s);
+cudaError_t k_ce_fwd_bwd(__nv_bfloat16* logits, int64_t ldl, const int* labels, float* loss, int T,
+                         int V, float inv_n, cudaStream_t s);
+cudaError_t k_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __nv_bfloat16* dgu,
+                         int64_t T, int F, cudaStream_t s);
+cudaError_t k_adamw(float* p, float* m, float* v, const float* g, __nv_bfloat16* pb, int64_t n,
+                    float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t s);
+cudaError_t k_cast_f32_bf16(const float* x, __nv_bfloat16* y, int64_t n, cudaStream_t s);
+cudaError_t k_sum(const float* x, int64_t n, float* out, cudaStream_t s);
+
+// attention.cu — causal varlen GQA flash attention, head dim 128.
+// q [N, hq, 128], k/v [N, hk, 128] (row strides ldq/ldk/ldv elements), o [N, hq, 128] (ldo),
+// lse [hq, N] natural-log units; seq_start[t] = first token of t's sample.
+struct AttnArgs {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  __nv_bfloat16* o;
+  float* lse;
+  int64_t ldq, ldk, ldv, ldo;
+  const int* seq_start;  // [N]
+  const int* seq_end;    // [N] one past the last token of t's sample
+  int N, hq, hk;
+  float scale;
+  // backward
+  const __nv_bfloat16* dout;  // [N, hq, 128] (lddo)
+  int64_t lddo;
+  float* dq_acc;              // [N, hq, 128] fp32, zeroed by the caller
+  __nv_bfloat16* dk;          // [N, hk, 128]
+  __nv_bfloat16* dv;
+  int64_t lddk, lddv;
+  float* delta;               // [hq, N] scratch
+};
+cudaError_t k_attn_fwd(const AttnArgs& a, cudaStream_t s);
+cudaError_t k_attn_bwd(const AttnArgs& a, cudaStream_t s);
+
+// a2a.cu — Ulysses all-to-all over peer memory with fused RoPE.
+constexpr int kMaxSp = 8;
+struct A2AGroup {
+  int heads_total;                 // heads of this type across the sp group
+  int col0;                        // first column (in elements) of this type in the local row
+  int rope;                        // 1: apply RoPE (seq->head) / inverse RoPE (head->seq)
+  int src_f32;                     // head->seq only: source is fp32 (dq accumulator)
+  void* full[kMaxSp];              // seq->head: per-rank destination [m*S, heads/sp, 128]
+                                   // head->seq: this rank's source   (only full[0] used)
+};
+struct A2AArgs {
+  int sp, rank;                    // sp group size and this rank's position in it
+  int rows, seq;                   // rows (sequences) per rank, full sequence length S
+  int ngroups;
+  A2AGroup g[3];
+  void* local[kMaxSp];             // seq->head: this rank's source (local[0]);
+                                   // head->seq: per-rank destination [rows*S/sp, width]
+  int64_t local_ld;                // row stride (elements) of the local [tokens, width] buffers
+  const int* pos;                  // [rows*S] position ids (global token index)
+  const float* inv_freq;           // [64]
+};
+cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s);
+cudaError_t k_a2a_head2seq(const A2AArgs& a, cudaStream_t s);
+// Peer barrier: signal every peer then wait until every peer reached `epoch`.
+cudaError_t k_peer_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int n, int me,
+                           uint32_t epoch, int* timeout_flag, cudaStream_t s);
+
+}  // namespace opx

@@ -1,0 +1,314 @@
+"""Kernel-level parity on B200: every opx kernel against a plain torch fp32
+restatement of the same op on identical bf16-rounded inputs."""
+import math
+
+import pytest
+import torch
+
+gpu = pytest.mark.gpu
+if torch.cuda.is_available():
+    from tests.gpu_util import P, S, call, cosine, rel_err
+
+DEV = "cuda"
+
+
+def bf(x):
+    return x.to(torch.bfloat16)
+
+
+# ---------------------------------------------------------------- GEMM
+GEMM_SHAPES = [(128, 256, 64), (256, 512, 192), (384, 768, 1024), (200, 264, 96), (1024, 2048, 512)]
+
+
+@gpu
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_bf16(M, N, K, a_mn, b_mn):
+    torch.manual_seed(M + N + K)
+    A = bf(torch.randn(M, K, device=DEV))
+    B = bf(torch.randn(N, K, device=DEV))
+    As = A.t().contiguous() if a_mn else A
+    Bs = B.t().contiguous() if b_mn else B
+    D = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    call("opx_gemm", M, N, K, P(As), As.shape[1], a_mn, P(Bs), Bs.shape[1], b_mn, 0, P(D), N,
+         None, 0, None, 0, 1.0, S())
+    ref = A.float() @ B.float().t()
+    torch.cuda.synchronize()
+    assert rel_err(D, ref) < 1e-2
+
+
+@gpu
+@pytest.mark.parametrize("epi", [1, 2, 3])
+def test_gemm_f32_epilogues(epi):
+    M, N, K = 256, 512, 320
+    torch.manual_seed(epi)
+    A = bf(torch.randn(M, K, device=DEV))
+    B = bf(torch.randn(N, K, device=DEV))
+    R = torch.randn(M, N, device=DEV)
+    D = R.clone() if epi == 3 else torch.empty(M, N, device=DEV)
+    call("opx_gemm", M, N, K, P(A), K, 0, P(B), K, 0, epi, P(D), N, P(R) if epi == 2 else None,
+         N, None, 0, 0.5, S())
+    ref = 0.5 * (A.float() @ B.float().t())
+    if epi in (2, 3):
+        ref = ref + R
+    torch.cuda.synchronize()
+    assert (D - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
+
+
+@gpu
+def test_gemm_swiglu():
+    M, F, K = 256, 512, 256
+    torch.manual_seed(7)
+    A = bf(torch.randn(M, K, device=DEV) * 0.5)
+    Wg = bf(torch.randn(F, K, device=DEV) * 0.1)
+    Wu = bf(torch.randn(F, K, device=DEV) * 0.1)
+    # interleave 128-row blocks: [g0 u0 g1 u1 ...]
+    W = torch.cat([torch.stack([Wg[i:i + 128], Wu[i:i + 128]]) for i in range(0, F, 128)]).reshape(2 * F, K)
+    gu = torch.empty(M, 2 * F, device=DEV, dtype=torch.bfloat16)
+    act = torch.empty(M, F, device=DEV, dtype=torch.bfloat16)
+    call("opx_gemm", M, 2 * F, K, P(A), K, 0, P(W), K, 0, 4, P(gu), 2 * F, None, 0, P(act), F, 1.0, S())
+    g = bf(A.float() @ Wg.float().t()).float()
+    u = bf(A.float() @ Wu.float().t()).float()
+    ref = torch.nn.functional.silu(g) * u
+    torch.cuda.synchronize()
+    assert rel_err(act, ref) < 2e-2
+    gu_v = gu.view(M, F // 128, 2, 128)
+    assert rel_err(gu_v[:, :, 0].reshape(M, F), g) < 1e-2
+    assert rel_err(gu_v[:, :, 1].reshape(M, F), u) < 1e-2
+
+
+@gpu
+@pytest.mark.parametrize("mode", ["m", "k"])
+def test_gemm_grouped(mode):
+    torch.manual_seed(3)
+    G, N, K = 4, 256, 192
+    rows = [128, 0, 384, 256]
+    starts = [0, 128, 128, 512]
+    Rt = 768
+    if mode == "m":
+        X = bf(torch.randn(Rt, K, device=DEV))
+        W = bf(torch.randn(G, N, K, device=DEV))
+        D = torch.zeros(Rt, N, device=DEV, dtype=torch.bfloat16)
+        gs = torch.tensor(starts, dtype=torch.int32, device=DEV)
+        gr = torch.tensor(rows, dtype=torch.int32, device=DEV)
+        call("opx_gemm_grouped", 0, N, K, P(X), K, 0, P(W), K, 0, 0, P(D), N, None, 0, G, 0,
+             P(gs), P(gr), Rt, 0, S())
+        torch.cuda.synchronize()
+        for g in range(G):
+            s, r = starts[g], rows[g]
+            if r:
+                ref = X[s:s + r].float() @ W[g].float().t()
+                assert rel_err(D[s:s + r], ref) < 1e-2
+    else:
+        M = 256
+        dY = bf(torch.randn(Rt, M, device=DEV))
+        X = bf(torch.randn(Rt, N, device=DEV))
+        D = torch.zeros(G, M, N, device=DEV)
+        gs = torch.tensor(starts, dtype=torch.int32, device=DEV)
+        gr = torch.tensor(rows, dtype=torch.int32, device=DEV)
+        call("opx_gemm_grouped", M, N, 0, P(dY), M, 1, P(X), N, 1, 1, P(D), N, None, 0, G, 1,
+             P(gs), P(gr), Rt, M * N, S())
+        torch.cuda.synchronize()
+        for g in range(G):
+            s, r = starts[g], rows[g]
+            ref = dY[s:s + r].float().t() @ X[s:s + r].float()
+            if r:
+                assert rel_err(D[g], ref) < 1e-3
+            else:
+                assert D[g].abs().max().item() == 0
+
+
+# ---------------------------------------------------------------- RMSNorm
+@gpu
+@pytest.mark.parametrize("T,H", [(64, 256), (300, 3584), (17, 8192)])
+def test_rmsnorm(T, H):
+    torch.manual_seed(T)
+    x = torch.randn(T, H, device=DEV)
+    w = bf(torch.rand(H, device=DEV) + 0.5)
+    y = torch.empty(T, H, device=DEV, dtype=torch.bfloat16)
+    rstd = torch.empty(T, device=DEV)
+    call("opx_rmsnorm_fwd", P(x), P(w), P(y), P(rstd), T, H, 1e-6, S())
+    xr = x.clone().requires_grad_(True)
+    wr = w.float().clone().requires_grad_(True)
+    ref = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-6) * wr
+    torch.cuda.synchronize()
+    assert rel_err(y, ref.detach()) < 1e-2
+    dy = torch.randn(T, H, device=DEV)
+    dres = torch.randn(T, H, device=DEV)
+    dx = torch.empty(T, H, device=DEV)
+    nparts = __import__("paper_2508_02317_b200").lib().opx_rmsnorm_bwd_parts(T)
+    part = torch.empty(nparts, H, device=DEV)
+    dw = torch.empty(H, device=DEV)
+    call("opx_rmsnorm_bwd", P(dy), P(x), P(w), P(rstd), P(dres), P(dx), P(part), P(dw), T, H, S())
+    ref.backward(dy)
+    torch.cuda.synchronize()
+    assert rel_err(dx, xr.grad + dres) < 1e-4
+    assert rel_err(dw, wr.grad) < 1e-4
+
+
+# ---------------------------------------------------------------- CE
+@gpu
+def test_cross_entropy():
+    torch.manual_seed(0)
+    T, V = 96, 2048
+    z = bf(torch.randn(T, V, device=DEV) * 2)
+    labels = torch.randint(0, V, (T,), device=DEV, dtype=torch.int32)
+    labels[::7] = -100
+    nvalid = int((labels >= 0).sum())
+    zz = z.float().clone().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(zz, labels.long(), ignore_index=-100, reduction="sum")
+    (ref / nvalid).backward()
+    loss = torch.empty(T, device=DEV)
+    g = z.clone()
+    call("opx_ce_fwd_bwd", P(g), V, P(labels), P(loss), T, V, 1.0 / nvalid, S())
+    torch.cuda.synchronize()
+    assert abs(loss.sum().item() - ref.item()) / ref.item() < 1e-4
+    assert rel_err(g, zz.grad) < 1e-2
+
+
+# ---------------------------------------------------------------- SwiGLU bwd
+@gpu
+def test_swiglu_bwd():
+    torch.manual_seed(1)
+    T, F = 64, 384
+    gu = bf(torch.randn(T, 2 * F, device=DEV))
+    da = bf(torch.randn(T, F, device=DEV))
+    dgu = torch.empty_like(gu)
+    call("opx_swiglu_bwd", P(da), P(gu), P(dgu), T, F, S())
+    v = gu.float().view(T, F // 128, 2, 128)
+    g = v[:, :, 0].reshape(T, F).clone().requires_grad_(True)
+    u = v[:, :, 1].reshape(T, F).clone().requires_grad_(True)
+    (torch.nn.functional.silu(g) * u).backward(da.float())
+    torch.cuda.synchronize()
+    dv = dgu.float().view(T, F // 128, 2, 128)
+    assert rel_err(dv[:, :, 0].reshape(T, F), g.grad) < 1e-2
+    assert rel_err(dv[:, :, 1].reshape(T, F), u.grad) < 1e-2
+
+
+# ---------------------------------------------------------------- AdamW
+@gpu
+def test_adamw():
+    torch.manual_seed(2)
+    n = 4096 + 64
+    p = torch.randn(n, device=DEV)
+    g = torch.randn(n, device=DEV)
+    m = torch.zeros(n, device=DEV)
+    v = torch.zeros(n, device=DEV)
+    pb = torch.empty(n, device=DEV, dtype=torch.bfloat16)
+    ref = torch.nn.Parameter(p.clone())
+    opt = torch.optim.AdamW([ref], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    for step in (1, 2, 3):
+        ref.grad = g.clone()
+        opt.step()
+        call("opx_adamw", P(p), P(m), P(v), P(g), P(pb), n, 1e-3, 0.9, 0.95, 1e-8, 0.1, step, S())
+    torch.cuda.synchronize()
+    assert (p - ref.data).abs().max().item() < 1e-6
+    assert (pb.float() - p).abs().max().item() <= 1e-2 * p.abs().max().item()
+
+
+# ---------------------------------------------------------------- embedding
+@gpu
+def test_embedding():
+    torch.manual_seed(4)
+    V, H, T = 512, 256, 200
+    E = bf(torch.randn(V, H, device=DEV))
+    ids = torch.randint(0, V, (T,), device=DEV, dtype=torch.int32)
+    x = torch.empty(T, H, device=DEV)
+    call("opx_embed_fwd", P(ids), P(E), P(x), T, H, S())
+    dx = torch.randn(T, H, device=DEV)
+    dE = torch.zeros(V, H, device=DEV)
+    call("opx_embed_bwd", P(ids), P(dx), P(dE), T, H, S())
+    ref = torch.zeros(V, H, device=DEV).index_add_(0, ids.long(), dx)
+    torch.cuda.synchronize()
+    assert torch.equal(x, E.float()[ids.long()])
+    assert (dE - ref).abs().max().item() < 1e-5
+
+
+# ---------------------------------------------------------------- attention
+def _varlen(N, lens, dev=DEV):
+    cu = [0]
+    for l in lens:
+        cu.append(cu[-1] + l)
+    assert cu[-1] == N
+    st = torch.empty(N, dtype=torch.int32)
+    en = torch.empty(N, dtype=torch.int32)
+    for a, b in zip(cu[:-1], cu[1:]):
+        st[a:b] = a
+        en[a:b] = b
+    return st.to(dev), en.to(dev)
+
+
+def _attn_ref(q, k, v, st, hq, hk):
+    N = q.shape[0]
+    G = hq // hk
+    idx = torch.arange(N, device=q.device)
+    mask = (idx[None, :] <= idx[:, None]) & (idx[None, :] >= st.long()[:, None])
+    qf = q.float().permute(1, 0, 2)
+    kf = k.float().repeat_interleave(G, dim=1).permute(1, 0, 2)
+    vf = v.float().repeat_interleave(G, dim=1).permute(1, 0, 2)
+    s = qf @ kf.transpose(1, 2) / math.sqrt(128)
+    s = s.masked_fill(~mask[None], float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ vf
+    return o.permute(1, 0, 2), lse
+
+
+@gpu
+@pytest.mark.parametrize("N,lens,hq,hk", [(256, [256], 2, 1), (640, [100, 300, 64, 176], 4, 2),
+                                          (1024, [1000, 24], 7, 1)])
+def test_attention_fwd_bwd(N, lens, hq, hk):
+    torch.manual_seed(N)
+    q = bf(torch.randn(N, hq, 128, device=DEV))
+    k = bf(torch.randn(N, hk, 128, device=DEV))
+    v = bf(torch.randn(N, hk, 128, device=DEV))
+    st, en = _varlen(N, lens)
+    o = torch.empty(N, hq, 128, device=DEV, dtype=torch.bfloat16)
+    lse = torch.empty(hq, N, device=DEV)
+    scale = 1 / math.sqrt(128)
+    call("opx_attn_fwd", P(q), P(k), P(v), P(o), P(lse), hq * 128, hk * 128, hk * 128, hq * 128,
+         P(st), P(en), N, hq, hk, scale, S())
+    qr, kr, vr = (t.float().clone().requires_grad_(True) for t in (q, k, v))
+    o_ref, lse_ref = _attn_ref(qr, kr, vr, st, hq, hk)
+    torch.cuda.synchronize()
+    assert rel_err(o, o_ref.detach()) < 2e-2
+    assert (lse - lse_ref.detach()).abs().max().item() < 1e-2
+    do = bf(torch.randn(N, hq, 128, device=DEV))
+    o_ref.backward(do.float())
+    dq = torch.empty(N, hq, 128, device=DEV)
+    dk = torch.empty(N, hk, 128, device=DEV, dtype=torch.bfloat16)
+    dv = torch.empty_like(dk)
+    delta = torch.empty(hq, N, device=DEV)
+    call("opx_attn_bwd", P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv), P(delta),
+         hq * 128, hk * 128, P(st), P(en), N, hq, hk, scale, S())
+    torch.cuda.synchronize()
+    for got, ref in ((dq, qr.grad), (dk, kr.grad), (dv, vr.grad)):
+        assert rel_err(got, ref) < 3e-2, (rel_err(got, ref))
+        assert cosine(got, ref) > 0.999
+
+
+# ---------------------------------------------------------------- RoPE pack (sp=1 Ulysses)
+@gpu
+def test_rope_pack():
+    torch.manual_seed(5)
+    rows, S_, hq, hk = 2, 128, 4, 2
+    N = rows * S_
+    W = (hq + 2 * hk) * 128
+    qkv = bf(torch.randn(N, W, device=DEV))
+    pos = torch.cat([torch.arange(50), torch.arange(78), torch.arange(128)]).to(torch.int32).to(DEV)
+    inv = (1.0 / (1e6 ** (torch.arange(0, 128, 2, dtype=torch.float64) / 128))).float().to(DEV)
+    qf = torch.empty(N, hq, 128, device=DEV, dtype=torch.bfloat16)
+    kf = torch.empty(N, hk, 128, device=DEV, dtype=torch.bfloat16)
+    vf = torch.empty(N, hk, 128, device=DEV, dtype=torch.bfloat16)
+    call("opx_rope_pack", P(qkv), W, P(qf), P(kf), P(vf), hq, hk, rows, S_, P(pos), P(inv), S())
+    ang = pos.float()[:, None] * inv[None, :]
+    cos, sin = torch.cos(torch.cat([ang, ang], -1)), torch.sin(torch.cat([ang, ang], -1))
+
+    def rope(x):
+        x1, x2 = x[..., :64], x[..., 64:]
+        return x * cos[:, None] + torch.cat([-x2, x1], -1) * sin[:, None]
+
+    x = qkv.float().view(N, hq + 2 * hk, 128)
+    torch.cuda.synchronize()
+    assert rel_err(qf, rope(x[:, :hq])) < 1e-2
+    assert rel_err(kf, rope(x[:, hq:hq + hk])) < 1e-2
+    assert torch.equal(vf.float(), x[:, hq + hk:])
