@@ -164,6 +164,7 @@ cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
   if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  ++g_kernel_launches;
   seq2head_kernel<<<int(blocks), 256, 0, s>>>(a);
   return cudaGetLastError();
 }
@@ -175,12 +176,14 @@ cudaError_t k_a2a_head2seq(const A2AArgs& a, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
   if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  ++g_kernel_launches;
   head2seq_kernel<<<int(blocks), 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t k_peer_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int n, int me,
                            uint32_t epoch, int* timeout_flag, cudaStream_t s) {
+  ++g_kernel_launches;
   peer_barrier_kernel<<<1, 32, 0, s>>>(peer_flags, my_flags, n, me, epoch, timeout_flag);
   return cudaGetLastError();
 }

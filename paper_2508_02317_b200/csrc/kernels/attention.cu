@@ -478,6 +478,7 @@ cudaError_t k_attn_fwd(const AttnArgs& a, cudaStream_t s) {
     cfg = true;
   }
   dim3 grid((a.N + BQ - 1) / BQ, a.hq);
+  ++g_kernel_launches;
   attn_fwd_kernel<<<grid, 128, FWD_SMEM, s>>>(a);
   return cudaGetLastError();
 }
@@ -491,10 +492,12 @@ cudaError_t k_attn_bwd(const AttnArgs& a, cudaStream_t s) {
     cfg = true;
   }
   const int64_t warps = int64_t(a.N) * a.hq;
+  ++g_kernel_launches;
   attn_delta_kernel<<<int((warps * 32 + 255) / 256), 256, 0, s>>>(a);
   cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(a.N) * a.hq * D * sizeof(float), s);
   if (e != cudaSuccess) return e;
   dim3 grid((a.N + BKV - 1) / BKV, a.hk);
+  ++g_kernel_launches;
   attn_bwd_kernel<<<grid, 128, BWD_SMEM, s>>>(a);
   return cudaGetLastError();
 }

@@ -422,6 +422,7 @@ cudaError_t k_init_param(float* f32, __nv_bfloat16* b16, int64_t n, int64_t phys
                          uint64_t key_b, double c, float constant, int interleave,
                          int64_t rows_per_slab, int64_t cols, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
+  ++g_kernel_launches;
   init_kernel<<<grid_for(n), NT, 0, s>>>(f32, b16, n, phys0, key_a, key_b, c, constant,
                                          interleave, rows_per_slab, cols);
   return cudaGetLastError();
@@ -431,6 +432,7 @@ cudaError_t k_rmsnorm_fwd(const float* x, const __nv_bfloat16* w, __nv_bfloat16*
                           int T, int H, float eps, cudaStream_t s) {
   if (H % 4 || H > NT * 4 * MAXV) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
+  ++g_kernel_launches;
   rmsnorm_fwd_kernel<<<T, NT, 0, s>>>(x, w, y, rstd, H, eps);
   return cudaGetLastError();
 }
@@ -443,7 +445,9 @@ cudaError_t k_rmsnorm_bwd(const float* dy, const float* x, const __nv_bfloat16* 
   if (H % 4 || H > NT * 4 * MAXV) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
   const int nb = k_rmsnorm_bwd_parts(T);
+  ++g_kernel_launches;
   rmsnorm_bwd_kernel<<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
+  ++g_kernel_launches;
   colsum_kernel<<<(H + 127) / 128, 128, 0, s>>>(dw_part, nb, H, dw, accumulate_dw);
   return cudaGetLastError();
 }
@@ -452,6 +456,7 @@ cudaError_t k_embed_fwd(const int* ids, const __nv_bfloat16* E, float* x, int T,
                         cudaStream_t s) {
   if (H % 8) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
+  ++g_kernel_launches;
   embed_fwd_kernel<<<T, 128, 0, s>>>(ids, E, x, T, H);
   return cudaGetLastError();
 }
@@ -459,6 +464,7 @@ cudaError_t k_embed_fwd(const int* ids, const __nv_bfloat16* E, float* x, int T,
 cudaError_t k_embed_bwd(const int* ids, const float* dx, float* dE, int T, int H, cudaStream_t s) {
   if (H % 4) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
+  ++g_kernel_launches;
   embed_bwd_kernel<<<T, 128, 0, s>>>(ids, dx, dE, T, H);
   return cudaGetLastError();
 }
@@ -467,6 +473,7 @@ cudaError_t k_ce_fwd_bwd(__nv_bfloat16* logits, int64_t ldl, const int* labels, 
                          int V, float inv_n, cudaStream_t s) {
   if (V % 8 || ldl % 8) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
+  ++g_kernel_launches;
   ce_kernel<<<T, NT, 0, s>>>(logits, ldl, labels, loss, V, inv_n);
   return cudaGetLastError();
 }
@@ -475,6 +482,7 @@ cudaError_t k_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __n
                          int64_t T, int F, cudaStream_t s) {
   if (F % 128) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
+  ++g_kernel_launches;
   swiglu_bwd_kernel<<<grid_for(T * F / 8), NT, 0, s>>>(dact, gu, dgu, T, F);
   return cudaGetLastError();
 }
@@ -485,6 +493,7 @@ cudaError_t k_adamw(float* p, float* m, float* v, const float* g, __nv_bfloat16*
   if (n <= 0) return cudaSuccess;
   const double bc1 = 1.0 - std::pow(double(b1), step);
   const double bc2 = 1.0 - std::pow(double(b2), step);
+  ++g_kernel_launches;
   adamw_kernel<<<grid_for(n / 4), NT, 0, s>>>(p, m, v, g, pb, n, lr, b1, b2, eps, wd, float(bc1),
                                                float(std::sqrt(bc2)));
   return cudaGetLastError();
@@ -493,11 +502,13 @@ cudaError_t k_adamw(float* p, float* m, float* v, const float* g, __nv_bfloat16*
 cudaError_t k_cast_f32_bf16(const float* x, __nv_bfloat16* y, int64_t n, cudaStream_t s) {
   if (n % 4) return cudaErrorInvalidValue;
   if (n <= 0) return cudaSuccess;
+  ++g_kernel_launches;
   cast_f32_bf16_kernel<<<grid_for(n / 4), NT, 0, s>>>(x, y, n);
   return cudaGetLastError();
 }
 
 cudaError_t k_sum(const float* x, int64_t n, float* out, cudaStream_t s) {
+  ++g_kernel_launches;
   sum_kernel<<<1, NT, 0, s>>>(x, n, out);
   return cudaGetLastError();
 }

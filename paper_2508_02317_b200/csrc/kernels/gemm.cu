@@ -19,6 +19,7 @@
 #include <mutex>
 
 #include "../runtime/gemm_api.h"
+#include "../runtime/kernels_api.h"
 #include "ptx.cuh"
 
 namespace opx {
@@ -399,6 +400,7 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const KParams& kp
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  ++g_kernel_launches;
   gemm_tc_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(a, b, kp);
   return cudaGetLastError();
 }

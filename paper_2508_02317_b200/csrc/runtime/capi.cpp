@@ -12,6 +12,7 @@
 
 namespace opx {
 thread_local std::string g_last_error;
+int64_t g_kernel_launches = 0;
 void set_error(const std::string& s) { g_last_error = s; }
 
 int cuda_fail(cudaError_t e, const char* what) {

@@ -10,6 +10,10 @@
 
 namespace opx {
 
+// Number of opx kernels launched so far in this process (the executor reports
+// the delta over a step as opx_step_report.launches).
+extern int64_t g_kernel_launches;
+
 // elementwise.cu
 cudaError_t k_init_param(float* f32, __nv_bfloat16* b16, int64_t n, int64_t phys0, uint64_t key_a,
                          uint64_t key_b, double c, float constant, int interleave,

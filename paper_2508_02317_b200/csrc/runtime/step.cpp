@@ -1,0 +1,1164 @@
+// Training-step executor: one instance per rank (process / GPU).
+//
+// Executes, with real kernels and collectives, the per-layer schedule that
+// omniplan's GraphBuilder only models (step_graph.cpp:75-409):
+//   fwd:  AG(layer) on the comm stream, prefetched one layer ahead
+//         (issue_gather, :179-189) -> norm -> QKV GEMM -> seq->head a2a (+RoPE)
+//         -> attention -> head->seq a2a -> out GEMM(+residual) -> norm ->
+//         gate|up GEMM(+SwiGLU) -> down GEMM(+residual)
+//   head: final norm -> LM-head GEMM -> fused CE fwd/bwd (chunked) -> dgrad/wgrad
+//   bwd:  per layer (high to low) full recompute of the layer (recompute=full,
+//         plan.hpp:32), the mirrored GEMMs, the four backward Ulysses
+//         exchanges the reference model omits (test_simulator.cpp:205), grad
+//         reduce-scatter on the comm stream (:351-354) + HSDP all-reduce (:356-364)
+//   opt:  fused AdamW on the local fp32 shard (:392-409).
+// Node names and phases follow step_graph.cpp so measured traces line up with
+// the simulated ones.
+#include "step.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "common.h"
+#include "json.hpp"
+
+namespace opx {
+
+namespace {
+constexpr int64_t kAlign = 64;
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+int Step::check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return OPX_OK;
+  return cuda_fail(e, what);
+}
+int Step::nccl(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return OPX_OK;
+  set_error(std::string(what) + ": " + ncclGetErrorString(r));
+  return OPX_ERR_CUDA;
+}
+
+#define TRY(x)                  \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_ != OPX_OK) return rc_; \
+  } while (0)
+#define CU(x) TRY(check((x), #x))
+#define NC(x) TRY(nccl((x), #x))
+
+template <class T>
+T* Step::alloc(size_t n, bool zero) {
+  void* p = nullptr;
+  const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  if (zero) cudaMemset(p, 0, bytes);
+  allocs_.push_back(p);
+  bytes_alloc_ += int64_t(bytes);
+  return static_cast<T*>(p);
+}
+
+cudaEvent_t Step::ev() {
+  if (ev_next_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_next_++];
+}
+
+void Step::mark(const std::string& name, const std::string& phase, int tid, cudaEvent_t a,
+                cudaEvent_t b) {
+  trace_.push_back({name, phase, tid, a, b});
+}
+
+Step::~Step() {
+  if (cs_) cudaStreamSynchronize(cs_);
+  if (ms_) cudaStreamSynchronize(ms_);
+  for (size_t r = 0; r < peer_arena_.size(); ++r)
+    if (peer_arena_[r] && peer_arena_[r] != arena_) cudaIpcCloseMemHandle(peer_arena_[r]);
+  for (void* p : allocs_) cudaFree(p);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (auto* v : {&ev_ag_, &ev_use_done_, &ev_grad_done_, &ev_rs_done_})
+    for (auto e : *v) cudaEventDestroy(e);
+  for (auto e : {ev_start_, ev_fwd_, ev_bwd_, ev_end_, ev_head_ag_, ev_head_rs_})
+    if (e) cudaEventDestroy(e);
+  if (rep_comm_) ncclCommDestroy(rep_comm_);
+  if (shard_comm_) ncclCommDestroy(shard_comm_);
+  if (world_comm_) ncclCommDestroy(world_comm_);
+  if (cs_) cudaStreamDestroy(cs_);
+  if (ms_) cudaStreamDestroy(ms_);
+}
+
+// ---------------------------------------------------------------------------
+// setup
+// ---------------------------------------------------------------------------
+int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan& p,
+                 const ExecCfg& ex, int rank, int device, const void* nccl_id) {
+  c_ = c;
+  m_ = m;
+  w_ = w;
+  p_ = p;
+  ex_ = ex;
+  rank_ = rank;
+  world_ = int(p.world());
+  dev_ = device;
+  const Module* f = m.foundation();
+  if (!f || !f->arch) {
+    set_error("model has no foundation arch");
+    return OPX_ERR_CONFIG;
+  }
+  a_ = *f->arch;
+  if (a_.moe) {
+    set_error("MoE layers are not supported by this executor build yet");
+    return OPX_ERR_CONFIG;
+  }
+  if (a_.head_dim != 128 || a_.hidden % 128 || a_.ffn % 128) {
+    set_error("executor requires head_dim == 128 and hidden, ffn multiples of 128");
+    return OPX_ERR_CONFIG;
+  }
+  if (p.sp > kMaxSp) {
+    set_error("sp > 8 is not supported (one NVSwitch domain)");
+    return OPX_ERR_CONFIG;
+  }
+  CU(cudaSetDevice(device));
+  CU(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&ev_start_, &ev_fwd_, &ev_bwd_, &ev_end_, &ev_head_ag_, &ev_head_rs_})
+    CU(cudaEventCreate(e));
+
+  // mesh coordinates (plan_mesh: dp_replicate x dp_shard x sp, row-major)
+  const int sp = int(p.sp), sh = int(p.dp_shard);
+  sp_i_ = rank % sp;
+  shard_i_ = (rank / sp) % sh;
+  rep_i_ = rank / (sp * sh);
+  for (int j = 0; j < sp; ++j) sp_members_.push_back((rep_i_ * sh + shard_i_) * sp + j);
+  for (int j = 0; j < sh * sp; ++j) shard_members_.push_back(int64_t(rep_i_) * sh * sp + j);
+  for (int j = 0; j < int(p.dp_replicate); ++j)
+    rep_members_.push_back(int64_t(j) * sh * sp + shard_i_ * sp + sp_i_);
+
+  if (world_ > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    NC(ncclCommInitRank(&world_comm_, world_, id, rank_));
+    if (sh * sp > 1) NC(ncclCommSplit(world_comm_, rep_i_, rank_, &shard_comm_, nullptr));
+    if (p.dp_replicate > 1)
+      NC(ncclCommSplit(world_comm_, shard_i_ * sp + sp_i_, rank_, &rep_comm_, nullptr));
+    else
+      NC(ncclCommSplit(world_comm_, NCCL_SPLIT_NOCOLOR, rank_, &rep_comm_, nullptr));
+  }
+
+  rows_ = int(p.micro_batch);
+  S_ = int(w.seq_len);
+  S_loc_ = S_ / sp;
+  T_ = rows_ * S_loc_;
+  Ntok_ = rows_ * S_;
+  H_ = int(a_.hidden);
+  hq_ = int(a_.heads);
+  hk_ = int(a_.kv_heads);
+  hql_ = hq_ / sp;
+  hkl_ = hk_ / sp;
+  Wqkv_ = (hq_ + 2 * hk_) * 128;
+  F_ = int(a_.ffn);
+  V_ = int(a_.vocab);
+  nslots_ = int(std::max<int64_t>(p.prefetch_depth, 0)) + 1;
+  if (nslots_ < 2) nslots_ = 2;
+  TRY(build_units());
+  TRY(alloc_acts());
+  return OPX_OK;
+}
+
+int Step::build_units() {
+  const int P = int(p_.shard_degree());
+  const int my = shard_i_ * int(p_.sp) + sp_i_;
+  auto finish = [&](Unit& u) -> int {
+    u.P = P;
+    u.idx = my;
+    u.comm = shard_comm_;
+    u.rep_comm = p_.dp_replicate > 1 ? rep_comm_ : nullptr;
+    u.padded = round_up(u.numel, kAlign * P);
+    u.shard = u.padded / P;
+    u.master = alloc<float>(size_t(u.shard));
+    u.m = alloc<float>(size_t(u.shard));
+    u.v = alloc<float>(size_t(u.shard));
+    u.gshard = alloc<float>(size_t(u.shard));
+    u.pshard = alloc<bf16>(size_t(u.shard));
+    if (!u.master || !u.m || !u.v || !u.gshard || !u.pshard) {
+      set_error("out of device memory for parameter shards");
+      return OPX_ERR_CUDA;
+    }
+    if (P == 1) {
+      u.full = u.pshard;
+      u.gfull = u.gshard;
+    }
+    return OPX_OK;
+  };
+  auto add = [](Unit& u, const std::string& name, std::vector<int64_t> shape, bool ones,
+                int interleave = 0, const std::string& ka = "", const std::string& kb = "") {
+    Param q;
+    q.name = name;
+    q.shape = shape;
+    q.numel = 1;
+    for (auto s : shape) q.numel *= s;
+    q.off = u.numel;
+    q.ones = ones;
+    q.interleave = interleave;
+    q.key_a = ka.empty() ? name : ka;
+    q.key_b = kb;
+    if (interleave) {
+      q.rows_per_slab = shape[shape.size() - 2];
+      q.cols = shape.back();
+    }
+    u.numel += round_up(q.numel, 128);
+    u.params.push_back(q);
+  };
+  const int64_t H = H_, V = V_, F = F_;
+  units_.clear();
+  {
+    Unit u;
+    u.name = "head";
+    add(u, "model.embed_tokens.weight", {V, H}, false);
+    add(u, "model.norm.weight", {H}, true);
+    add(u, "lm_head.weight", {V, H}, false);
+    TRY(finish(u));
+    units_.push_back(std::move(u));
+  }
+  for (int l = 0; l < a_.layers; ++l) {
+    Unit u;
+    const std::string p = "model.layers." + std::to_string(l) + ".";
+    u.name = "layer" + std::to_string(l);
+    add(u, p + "input_layernorm.weight", {H}, true);
+    add(u, p + "self_attn.q_proj.weight", {int64_t(hq_) * 128, H}, false);
+    add(u, p + "self_attn.k_proj.weight", {int64_t(hk_) * 128, H}, false);
+    add(u, p + "self_attn.v_proj.weight", {int64_t(hk_) * 128, H}, false);
+    add(u, p + "self_attn.o_proj.weight", {H, int64_t(hq_) * 128}, false);
+    add(u, p + "post_attention_layernorm.weight", {H}, true);
+    add(u, p + "mlp.gate_up_proj.weight", {2 * F, H}, false, 1, p + "mlp.gate_proj.weight",
+        p + "mlp.up_proj.weight");
+    add(u, p + "mlp.down_proj.weight", {H, F}, false);
+    TRY(finish(u));
+    units_.push_back(std::move(u));
+  }
+  if (P > 1) {
+    int64_t mx = 0;
+    for (size_t i = 1; i < units_.size(); ++i) mx = std::max(mx, units_[i].padded);
+    for (int s = 0; s < nslots_; ++s) {
+      gslot_.push_back(alloc<bf16>(size_t(mx), false));
+      if (!gslot_.back()) return cuda_fail(cudaErrorMemoryAllocation, "gather slots");
+    }
+    for (int s = 0; s < 2; ++s) {
+      gradslot_.push_back(alloc<float>(size_t(mx)));
+      if (!gradslot_.back()) return cuda_fail(cudaErrorMemoryAllocation, "grad slots");
+    }
+    Unit& hu = units_[0];
+    hu.full = alloc<bf16>(size_t(hu.padded), false);
+    hu.gfull = alloc<float>(size_t(hu.padded));
+    if (!hu.full || !hu.gfull) return cuda_fail(cudaErrorMemoryAllocation, "head gather");
+  }
+  const int L = int(a_.layers);
+  ev_ag_.resize(size_t(L));
+  ev_use_done_.resize(size_t(L));
+  ev_grad_done_.resize(size_t(L));
+  ev_rs_done_.resize(size_t(L));
+  for (auto* v : {&ev_ag_, &ev_use_done_, &ev_grad_done_, &ev_rs_done_})
+    for (auto& e : *v) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return OPX_OK;
+}
+
+int Step::alloc_acts() {
+  const size_t T = size_t(T_), H = size_t(H_), N = size_t(Ntok_);
+  // peer-visible arena: flags + the Ulysses exchange buffers (double-buffered)
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += round_up(int64_t(bytes), 256);
+    return o;
+  };
+  off_flags_ = take(64 * sizeof(uint32_t));
+  for (int b = 0; b < 2; ++b) {
+    off_q_[b] = take(N * size_t(hql_) * 128 * 2);
+    off_k_[b] = take(N * size_t(hkl_) * 128 * 2);
+    off_v_[b] = take(N * size_t(hkl_) * 128 * 2);
+    off_o_[b] = take(T * size_t(hq_) * 128 * 2);
+    off_do_[b] = take(N * size_t(hql_) * 128 * 2);
+    off_dqkv_[b] = take(T * size_t(Wqkv_) * 2);
+  }
+  arena_bytes_ = off;
+  CU(cudaMalloc(&arena_, arena_bytes_));
+  CU(cudaMemset(arena_, 0, arena_bytes_));
+  allocs_.push_back(arena_);
+  bytes_alloc_ += int64_t(arena_bytes_);
+  peer_arena_.assign(size_t(world_), nullptr);
+  peer_arena_[size_t(rank_)] = arena_;
+  d_peer_flags_ = alloc<uint32_t*>(kMaxSp);
+  d_timeout_ = alloc<int>(1);
+
+  const int L = int(a_.layers);
+  for (int l = 0; l <= L; ++l) x_saved_.push_back(alloc<float>(T * H, false));
+  h_ = alloc<bf16>(T * H, false);
+  qkv_ = alloc<bf16>(T * size_t(Wqkv_), false);
+  ofull_ = alloc<bf16>(N * size_t(hql_) * 128, false);
+  lse_ = alloc<float>(N * size_t(hql_), false);
+  x2_ = alloc<float>(T * H, false);
+  r1_ = alloc<float>(T, false);
+  r2_ = alloc<float>(T, false);
+  h2_ = alloc<bf16>(T * H, false);
+  gu_ = alloc<bf16>(T * size_t(2 * F_), false);
+  act_ = alloc<bf16>(T * size_t(F_), false);
+  dx_ = alloc<float>(T * H, false);
+  dtmp_ = alloc<float>(T * H, false);
+  dxb_ = alloc<bf16>(T * H, false);
+  dact_ = alloc<bf16>(T * size_t(F_), false);
+  dgu_ = alloc<bf16>(T * size_t(2 * F_), false);
+  dq_acc_ = alloc<float>(N * size_t(hql_) * 128, false);
+  dk_ = alloc<bf16>(N * size_t(hkl_) * 128, false);
+  dv_ = alloc<bf16>(N * size_t(hkl_) * 128, false);
+  delta_ = alloc<float>(N * size_t(hql_), false);
+  dw_part_ = alloc<float>(size_t(k_rmsnorm_bwd_parts(T_)) * H, false);
+  hf_ = alloc<bf16>(T * H, false);
+  rf_ = alloc<float>(T, false);
+  dhf_ = alloc<float>(T * H, false);
+  const int64_t chunk = std::min<int64_t>(ex_.ce_chunk, T_);
+  logits_ = alloc<bf16>(size_t(chunk) * size_t(V_), false);
+  loss_rows_ = alloc<float>(T);
+  loss_sum_ = alloc<float>(4);
+  d_ids_ = alloc<int32_t>(T);
+  d_labels_ = alloc<int32_t>(T);
+  d_pos_ = alloc<int32_t>(N);
+  d_sstart_ = alloc<int32_t>(N);
+  d_send_ = alloc<int32_t>(N);
+  d_inv_freq_ = alloc<float>(64);
+  for (void* q : {(void*)h_, (void*)logits_, (void*)dq_acc_, (void*)d_inv_freq_, (void*)x2_})
+    if (!q) return cuda_fail(cudaErrorMemoryAllocation, "activations");
+  std::vector<float> inv(64);
+  for (int i = 0; i < 64; ++i)
+    inv[size_t(i)] = float(1.0 / std::pow(ex_.rope_theta, double(2 * i) / 128.0));
+  CU(cudaMemcpy(d_inv_freq_, inv.data(), 64 * sizeof(float), cudaMemcpyHostToDevice));
+  if (p_.sp == 1) {  // no peers: flags point at ourselves
+    uint32_t* f = reinterpret_cast<uint32_t*>(arena_ + off_flags_);
+    CU(cudaMemcpy(d_peer_flags_, &f, sizeof(f), cudaMemcpyHostToDevice));
+  }
+  return OPX_OK;
+}
+
+int Step::ipc_export(void* out, size_t cap, size_t* len) {
+  if (cap < sizeof(cudaIpcMemHandle_t)) {
+    set_error("ipc export buffer too small");
+    return OPX_ERR_ARG;
+  }
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, arena_));
+  std::memcpy(out, &h, sizeof(h));
+  *len = sizeof(h);
+  return OPX_OK;
+}
+
+int Step::ipc_import(const void* all, size_t len) {
+  if (len != sizeof(cudaIpcMemHandle_t)) {
+    set_error("ipc import: unexpected handle size");
+    return OPX_ERR_ARG;
+  }
+  const char* base = static_cast<const char*>(all);
+  // Only the SP group exchanges through peer memory.
+  for (int64_t r : sp_members_) {
+    if (r == rank_) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, base + size_t(r) * len, len);
+    void* p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    peer_arena_[size_t(r)] = static_cast<char*>(p);
+  }
+  std::vector<uint32_t*> flags(size_t(kMaxSp), nullptr);
+  for (int j = 0; j < int(p_.sp); ++j)
+    flags[size_t(j)] = reinterpret_cast<uint32_t*>(peer(j, off_flags_));
+  CU(cudaMemcpy(d_peer_flags_, flags.data(), kMaxSp * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  return OPX_OK;
+}
+
+int Step::init_weights(uint64_t seed) {
+  const double c = 0.02 * std::sqrt(3.0) / 16777216.0;
+  for (Unit& u : units_) {
+    const int64_t sb = int64_t(u.idx) * u.shard, se = sb + u.shard;
+    CU(cudaMemsetAsync(u.master, 0, size_t(u.shard) * 4, cs_));
+    CU(cudaMemsetAsync(u.pshard, 0, size_t(u.shard) * 2, cs_));
+    CU(cudaMemsetAsync(u.m, 0, size_t(u.shard) * 4, cs_));
+    CU(cudaMemsetAsync(u.v, 0, size_t(u.shard) * 4, cs_));
+    CU(cudaMemsetAsync(u.gshard, 0, size_t(u.shard) * 4, cs_));
+    for (const Param& q : u.params) {
+      const int64_t lo = std::max(sb, q.off), hi = std::min(se, q.off + q.numel);
+      if (hi <= lo) continue;
+      const uint64_t ka = param_key(q.key_a, seed);
+      const uint64_t kb = q.key_b.empty() ? 0 : param_key(q.key_b, seed);
+      CU(k_init_param(u.master + (lo - sb), u.pshard + (lo - sb), hi - lo, lo - q.off, ka, kb,
+                      q.ones ? 0.0 : c, 1.0f, q.interleave, q.rows_per_slab, q.cols, cs_));
+    }
+  }
+  step_count_ = 0;
+  CU(cudaStreamSynchronize(cs_));
+  return OPX_OK;
+}
+
+int Step::load_batch(const int32_t* ids, const int32_t* labels, const int32_t* pos,
+                     const int32_t* cu, int n_cu, int64_t n_valid) {
+  if (n_cu < 2 || cu[0] != 0 || cu[n_cu - 1] != Ntok_) {
+    set_error("cu_seqlens must start at 0 and end at rows*seq_len (packing.hpp:28)");
+    return OPX_ERR_ARG;
+  }
+  std::vector<int32_t> st(static_cast<size_t>(Ntok_)), en(static_cast<size_t>(Ntok_));
+  for (int i = 0; i + 1 < n_cu; ++i) {
+    if (cu[i + 1] <= cu[i]) {
+      set_error("cu_seqlens must be strictly increasing");
+      return OPX_ERR_ARG;
+    }
+    if (cu[i] / S_ != (cu[i + 1] - 1) / S_) {
+      set_error("a packed sample crosses a row boundary");
+      return OPX_ERR_ARG;
+    }
+    for (int t = cu[i]; t < cu[i + 1]; ++t) {
+      st[size_t(t)] = cu[i];
+      en[size_t(t)] = cu[i + 1];
+    }
+  }
+  n_valid_ = std::max<int64_t>(n_valid, 1);
+  CU(cudaMemcpyAsync(d_ids_, ids, size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_labels_, labels, size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_pos_, pos, size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_sstart_, st.data(), size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_send_, en.data(), size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaStreamSynchronize(cs_));
+  return OPX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// collectives
+// ---------------------------------------------------------------------------
+int Step::gather(Unit& u, int slot, cudaEvent_t wait_ev) {
+  if (u.P == 1) return OPX_OK;
+  if (wait_ev) CU(cudaStreamWaitEvent(ms_, wait_ev, 0));
+  bf16* dst = slot < 0 ? u.full : gslot_[size_t(slot)];
+  u.full = dst;
+  NC(ncclAllGather(u.pshard, dst, size_t(u.shard), ncclBfloat16, u.comm, ms_));
+  return OPX_OK;
+}
+
+int Step::barrier_sp(cudaStream_t s) {
+  if (p_.sp == 1) return OPX_OK;
+  ++epoch_;
+  CU(k_peer_barrier(d_peer_flags_, reinterpret_cast<uint32_t*>(arena_ + off_flags_), int(p_.sp),
+                    sp_i_, epoch_, d_timeout_, s));
+  return OPX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one layer
+// ---------------------------------------------------------------------------
+namespace {
+struct LayerW {
+  const bf16 *ln1, *qkv, *o, *ln2, *gu, *down;
+};
+LayerW layer_w(const Unit& u, const bf16* base) {
+  LayerW w;
+  w.ln1 = base + u.params[0].off;
+  w.qkv = base + u.params[1].off;
+  w.o = base + u.params[4].off;
+  w.ln2 = base + u.params[5].off;
+  w.gu = base + u.params[6].off;
+  w.down = base + u.params[7].off;
+  return w;
+}
+GemmDesc gd(int M, int N, int K, const bf16* A, int64_t lda, bool amn, const bf16* B, int64_t ldb,
+            bool bmn, int epi, void* D, int64_t ldd) {
+  GemmDesc g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.A = A;
+  g.lda = lda;
+  g.a_mn = amn;
+  g.B = B;
+  g.ldb = ldb;
+  g.b_mn = bmn;
+  g.epi = epi;
+  g.D = D;
+  g.ldd = ldd;
+  return g;
+}
+}  // namespace
+
+int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& qb, int& ob) {
+  const LayerW W = layer_w(u, u.full);
+  const int T = T_, H = H_, F = F_;
+  const std::string pre = "fwd.layer" + std::to_string(l) + ".m0";
+  const std::string ph = "fwd.layer" + std::to_string(l);
+  const bool tr = ex_.trace;
+  cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
+  if (tr) cudaEventRecord(e0, cs_);
+  CU(k_rmsnorm_fwd(x_in, W.ln1, h_, r1_, T, H, ex_.rms_eps, cs_));
+  CU(gemm_run(gd(T, Wqkv_, H, h_, H, false, W.qkv, H, false, GEMM_EPI_BF16, qkv_, Wqkv_), cs_));
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".qkv_proj", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  qb = xq_;
+  xq_ ^= 1;
+  {
+    A2AArgs a{};
+    a.sp = int(p_.sp);
+    a.rank = sp_i_;
+    a.rows = rows_;
+    a.seq = S_;
+    a.ngroups = 3;
+    a.g[0].heads_total = hq_;
+    a.g[0].col0 = 0;
+    a.g[0].rope = 1;
+    a.g[1].heads_total = hk_;
+    a.g[1].col0 = hq_ * 128;
+    a.g[1].rope = 1;
+    a.g[2].heads_total = hk_;
+    a.g[2].col0 = (hq_ + hk_) * 128;
+    a.g[2].rope = 0;
+    for (int j = 0; j < int(p_.sp); ++j) {
+      a.g[0].full[j] = peer(j, off_q_[qb]);
+      a.g[1].full[j] = peer(j, off_k_[qb]);
+      a.g[2].full[j] = peer(j, off_v_[qb]);
+    }
+    a.local[0] = qkv_;
+    a.local_ld = Wqkv_;
+    a.pos = d_pos_;
+    a.inv_freq = d_inv_freq_;
+    CU(k_a2a_seq2head(a, cs_));
+    TRY(barrier_sp(cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".a2a_qkv", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  ob = xo_;
+  xo_ ^= 1;
+  bf16* attn_out = p_.sp == 1 ? o_loc(ob) : ofull_;
+  {
+    AttnArgs a{};
+    a.q = q_full(qb);
+    a.k = k_full(qb);
+    a.v = v_full(qb);
+    a.o = attn_out;
+    a.lse = lse_;
+    a.ldq = hql_ * 128;
+    a.ldk = a.ldv = hkl_ * 128;
+    a.ldo = hql_ * 128;
+    a.seq_start = d_sstart_;
+    a.seq_end = d_send_;
+    a.N = Ntok_;
+    a.hq = hql_;
+    a.hk = hkl_;
+    a.scale = 1.0f / std::sqrt(128.0f);
+    CU(k_attn_fwd(a, cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".attn_core", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  if (p_.sp > 1) {
+    A2AArgs a{};
+    a.sp = int(p_.sp);
+    a.rank = sp_i_;
+    a.rows = rows_;
+    a.seq = S_;
+    a.ngroups = 1;
+    a.g[0].heads_total = hq_;
+    a.g[0].full[0] = ofull_;
+    for (int j = 0; j < int(p_.sp); ++j) a.local[j] = peer(j, off_o_[ob]);
+    a.local_ld = hq_ * 128;
+    a.pos = d_pos_;
+    a.inv_freq = d_inv_freq_;
+    CU(k_a2a_head2seq(a, cs_));
+    TRY(barrier_sp(cs_));
+    if (tr) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_out", ph, 0, e0, e1);
+      e0 = e1;
+    }
+  }
+  {
+    GemmDesc g = gd(T, H, hq_ * 128, o_loc(ob), hq_ * 128, false, W.o, hq_ * 128, false,
+                    GEMM_EPI_F32_RESID, x2_, H);
+    g.R = x_in;
+    g.ldr = H;
+    CU(gemm_run(g, cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".out_proj", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  CU(k_rmsnorm_fwd(x2_, W.ln2, h2_, r2_, T, H, ex_.rms_eps, cs_));
+  {
+    GemmDesc g = gd(T, 2 * F, H, h2_, H, false, W.gu, H, false, GEMM_EPI_SWIGLU, gu_, 2 * F);
+    g.D2 = act_;
+    g.ldd2 = F;
+    CU(gemm_run(g, cs_));
+  }
+  {
+    GemmDesc g = gd(T, H, F, act_, F, false, W.down, F, false, GEMM_EPI_F32_RESID, x_out, H);
+    g.R = x2_;
+    g.ldr = H;
+    CU(gemm_run(g, cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".mlp", ph, 0, e0, e1);
+  }
+  return OPX_OK;
+}
+
+int Step::layer_bwd(int l, Unit& u, float* G) {
+  const int T = T_, H = H_, F = F_, Q = hq_ * 128;
+  const LayerW W = layer_w(u, u.full);
+  const bool tr = ex_.trace;
+  const std::string pre = "bwd.layer" + std::to_string(l) + ".m0";
+  const std::string ph = "bwd.layer" + std::to_string(l);
+  cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
+  if (tr) cudaEventRecord(e0, cs_);
+  // full recompute of the layer (recompute=full); x_out goes to scratch
+  int qb = 0, ob = 0;
+  TRY(layer_fwd(l, u, x_saved_[size_t(l)], dtmp_, qb, ob));
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".recompute", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  float* g_ln1 = G + u.params[0].off;
+  float* g_qkv = G + u.params[1].off;
+  float* g_o = G + u.params[4].off;
+  float* g_ln2 = G + u.params[5].off;
+  float* g_gu = G + u.params[6].off;
+  float* g_down = G + u.params[7].off;
+
+  // ---- MLP
+  CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
+  CU(gemm_run(gd(T, F, H, dxb_, H, false, W.down, F, true, GEMM_EPI_BF16, dact_, F), cs_));
+  CU(gemm_run(gd(H, F, T, dxb_, H, true, act_, F, true, GEMM_EPI_F32, g_down, F), cs_));
+  CU(k_swiglu_bwd(dact_, gu_, dgu_, T, F, cs_));
+  CU(gemm_run(gd(T, H, 2 * F, dgu_, 2 * F, false, W.gu, H, true, GEMM_EPI_F32, dtmp_, H), cs_));
+  CU(gemm_run(gd(2 * F, H, T, dgu_, 2 * F, true, h2_, H, true, GEMM_EPI_F32, g_gu, H), cs_));
+  CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".mlp", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  // ---- attention output projection
+  CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
+  const int db = xdo_;
+  xdo_ ^= 1;
+  bf16* do_loc = p_.sp == 1 ? do_full(db) : ofull_ + 0;  // see below for sp > 1
+  bf16* do_scratch = nullptr;
+  if (p_.sp > 1) {
+    // ofull_ still holds the attention output needed by attn_bwd: use dact_
+    // (dead after the MLP backward, >= T*hq*128 elements) as the local dO.
+    do_scratch = dact_;
+    do_loc = do_scratch;
+  }
+  CU(gemm_run(gd(T, Q, H, dxb_, H, false, W.o, Q, true, GEMM_EPI_BF16, do_loc, Q), cs_));
+  CU(gemm_run(gd(H, Q, T, dxb_, H, true, o_loc(ob), Q, true, GEMM_EPI_F32, g_o, Q), cs_));
+  if (p_.sp > 1) {
+    A2AArgs a{};
+    a.sp = int(p_.sp);
+    a.rank = sp_i_;
+    a.rows = rows_;
+    a.seq = S_;
+    a.ngroups = 1;
+    a.g[0].heads_total = hq_;
+    for (int j = 0; j < int(p_.sp); ++j) a.g[0].full[j] = peer(j, off_do_[db]);
+    a.local[0] = do_loc;
+    a.local_ld = Q;
+    a.pos = d_pos_;
+    a.inv_freq = d_inv_freq_;
+    CU(k_a2a_seq2head(a, cs_));
+    TRY(barrier_sp(cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".out_proj", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  // ---- attention core
+  {
+    AttnArgs a{};
+    a.q = q_full(qb);
+    a.k = k_full(qb);
+    a.v = v_full(qb);
+    a.o = p_.sp == 1 ? o_loc(ob) : ofull_;
+    a.lse = lse_;
+    a.ldq = hql_ * 128;
+    a.ldk = a.ldv = hkl_ * 128;
+    a.ldo = hql_ * 128;
+    a.seq_start = d_sstart_;
+    a.seq_end = d_send_;
+    a.N = Ntok_;
+    a.hq = hql_;
+    a.hk = hkl_;
+    a.scale = 1.0f / std::sqrt(128.0f);
+    a.dout = do_full(db);
+    a.lddo = hql_ * 128;
+    a.dq_acc = dq_acc_;
+    a.dk = dk_;
+    a.dv = dv_;
+    a.lddk = a.lddv = hkl_ * 128;
+    a.delta = delta_;
+    CU(k_attn_bwd(a, cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".attn_core", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  // ---- head->seq for dq (fp32, un-rotate), dk (un-rotate), dv
+  const int xb = xd_;
+  xd_ ^= 1;
+  {
+    A2AArgs a{};
+    a.sp = int(p_.sp);
+    a.rank = sp_i_;
+    a.rows = rows_;
+    a.seq = S_;
+    a.ngroups = 3;
+    a.g[0] = A2AGroup{hq_, 0, 1, 1, {dq_acc_}};
+    a.g[1] = A2AGroup{hk_, hq_ * 128, 1, 0, {dk_}};
+    a.g[2] = A2AGroup{hk_, (hq_ + hk_) * 128, 0, 0, {dv_}};
+    for (int j = 0; j < int(p_.sp); ++j) a.local[j] = peer(j, off_dqkv_[xb]);
+    a.local_ld = Wqkv_;
+    a.pos = d_pos_;
+    a.inv_freq = d_inv_freq_;
+    CU(k_a2a_head2seq(a, cs_));
+    TRY(barrier_sp(cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".a2a_dqkv", ph, 0, e0, e1);
+    e0 = e1;
+  }
+  bf16* dqkv = dqkv_loc(xb);
+  CU(gemm_run(gd(T, H, Wqkv_, dqkv, Wqkv_, false, W.qkv, H, true, GEMM_EPI_F32, dtmp_, H), cs_));
+  CU(gemm_run(gd(Wqkv_, H, T, dqkv, Wqkv_, true, h_, H, true, GEMM_EPI_F32, g_qkv, H), cs_));
+  CU(k_rmsnorm_bwd(dtmp_, x_saved_[size_t(l)], W.ln1, r1_, dx_, dx_, dw_part_, g_ln1, 0, T, H,
+                   cs_));
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".qkv_proj", ph, 0, e0, e1);
+  }
+  return OPX_OK;
+}
+
+int Step::head_fwd_bwd(Unit& u, float* G) {
+  const int T = T_, H = H_, V = V_;
+  const bf16* W_norm = u.full + u.params[1].off;
+  const bf16* W_head = u.full + u.params[2].off;
+  float* g_norm = G + u.params[1].off;
+  float* g_head = G + u.params[2].off;
+  const float* xf = x_saved_.back();
+  const bool tr = ex_.trace;
+  cudaEvent_t e0 = tr ? ev() : nullptr;
+  if (tr) cudaEventRecord(e0, cs_);
+  CU(k_rmsnorm_fwd(xf, W_norm, hf_, rf_, T, H, ex_.rms_eps, cs_));
+  const int C = int(std::min<int64_t>(ex_.ce_chunk, T));
+  for (int c0 = 0; c0 < T; c0 += C) {
+    const int n = std::min(C, T - c0);
+    CU(gemm_run(gd(n, V, H, hf_ + int64_t(c0) * H, H, false, W_head, H, false, GEMM_EPI_BF16,
+                   logits_, V),
+                cs_));
+    CU(k_ce_fwd_bwd(logits_, V, d_labels_ + c0, loss_rows_ + c0, n, V, 1.0f / float(n_valid_),
+                    cs_));
+    CU(gemm_run(gd(n, H, V, logits_, V, false, W_head, H, true, GEMM_EPI_F32,
+                   dhf_ + int64_t(c0) * H, H),
+                cs_));
+    CU(gemm_run(gd(V, H, n, logits_, V, true, hf_ + int64_t(c0) * H, H, true,
+                   c0 == 0 ? GEMM_EPI_F32 : GEMM_EPI_F32_ACCUM, g_head, H),
+                cs_));
+  }
+  CU(k_rmsnorm_bwd(dhf_, xf, W_norm, rf_, nullptr, dx_, dw_part_, g_norm, 0, T, H, cs_));
+  if (tr) {
+    cudaEvent_t e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark("fwd_bwd.head.m0", "head", 0, e0, e1);
+  }
+  return OPX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the step
+// ---------------------------------------------------------------------------
+int Step::run(opx_step_report* rep) {
+  const int L = int(a_.layers);
+  const bool tr = ex_.trace;
+  trace_.clear();
+  ev_next_ = 0;
+  ++step_count_;
+  const int64_t launches0 = g_kernel_launches;
+  CU(cudaMemsetAsync(d_timeout_, 0, sizeof(int), cs_));
+  CU(cudaEventRecord(ev_start_, cs_));
+  CU(cudaStreamWaitEvent(ms_, ev_start_, 0));
+  Unit& hu = units_[0];
+  const int P = hu.P;
+
+  // ---------------- forward ----------------
+  if (P > 1) {
+    cudaEvent_t a = tr ? ev() : nullptr;
+    if (tr) cudaEventRecord(a, ms_);
+    TRY(gather(hu, -1, nullptr));
+    CU(cudaEventRecord(ev_head_ag_, ms_));
+    if (tr) mark("fwd.ag.head.m0", "fwd.head", 1, a, ev_head_ag_);
+    CU(cudaStreamWaitEvent(cs_, ev_head_ag_, 0));
+  }
+  // embedding grad region is scatter-added: zero it
+  CU(cudaMemsetAsync(hu.gfull + hu.params[0].off, 0, size_t(hu.params[0].numel) * 4, cs_));
+  CU(k_embed_fwd(d_ids_, hu.full + hu.params[0].off, x_saved_[0], T_, H_, cs_));
+
+  auto issue_gather = [&](int l, bool bwd) -> int {
+    Unit& u = units_[size_t(1 + l)];
+    if (u.P == 1) return OPX_OK;
+    const int slot = l % nslots_;
+    // the slot was last used by layer l + nslots (bwd) or l - nslots (fwd)
+    const int prev = bwd ? l + nslots_ : l - nslots_;
+    cudaEvent_t wait = (prev >= 0 && prev < L) ? ev_use_done_[size_t(prev)] : nullptr;
+    cudaEvent_t a = tr ? ev() : nullptr;
+    if (wait) CU(cudaStreamWaitEvent(ms_, wait, 0));
+    if (tr) cudaEventRecord(a, ms_);
+    TRY(gather(u, slot, nullptr));
+    CU(cudaEventRecord(ev_ag_[size_t(l)], ms_));
+    if (tr)
+      mark(std::string(bwd ? "bwd" : "fwd") + ".ag.layer" + std::to_string(l) + ".m0",
+           std::string(bwd ? "bwd" : "fwd") + ".layer" + std::to_string(l), 1, a,
+           ev_ag_[size_t(l)]);
+    return OPX_OK;
+  };
+
+  for (int l = 0; l < std::min(L, nslots_ - 1); ++l) TRY(issue_gather(l, false));
+  for (int l = 0; l < L; ++l) {
+    Unit& u = units_[size_t(1 + l)];
+    if (u.P > 1) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
+    if (l + nslots_ - 1 < L) TRY(issue_gather(l + nslots_ - 1, false));
+    int qb, ob;
+    TRY(layer_fwd(l, u, x_saved_[size_t(l)], x_saved_[size_t(l + 1)], qb, ob));
+    CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
+  }
+  CU(cudaEventRecord(ev_fwd_, cs_));
+
+  // ---------------- head (fwd + CE + bwd) ----------------
+  TRY(head_fwd_bwd(hu, hu.gfull));
+
+  // ---------------- backward ----------------
+  // layers L-nslots .. L-1 are still resident in their slots from the forward
+  const int resident_from = std::max(0, L - nslots_);
+  for (int l = L - 1; l >= 0; --l) {
+    Unit& u = units_[size_t(1 + l)];
+    if (u.P > 1) {
+      if (l < resident_from) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
+      // prefetch the next (lower) layer that is not resident
+      const int nxt = l - 1;
+      if (nxt >= 0 && nxt < resident_from) {
+        // only issue once per layer: when l is the first layer above nxt
+        TRY(issue_gather(nxt, true));
+      }
+      u.full = gslot_[size_t(l % nslots_)];
+      u.gfull = gradslot_[size_t(l % 2)];
+      if (l + 2 < L) CU(cudaStreamWaitEvent(cs_, ev_rs_done_[size_t(l + 2)], 0));
+    }
+    TRY(layer_bwd(l, u, u.gfull));
+    CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
+    if (u.P > 1 || u.rep_comm) {
+      CU(cudaEventRecord(ev_grad_done_[size_t(l)], cs_));
+      CU(cudaStreamWaitEvent(ms_, ev_grad_done_[size_t(l)], 0));
+      cudaEvent_t a = tr ? ev() : nullptr;
+      if (tr) cudaEventRecord(a, ms_);
+      if (u.P > 1) {
+        if (u.padded > u.numel)
+          CU(cudaMemsetAsync(u.gfull + u.numel, 0, size_t(u.padded - u.numel) * 4, ms_));
+        NC(ncclReduceScatter(u.gfull, u.gshard, size_t(u.shard), ncclFloat, ncclSum, u.comm,
+                             ms_));
+      }
+      if (u.rep_comm)
+        NC(ncclAllReduce(u.gshard, u.gshard, size_t(u.shard), ncclFloat, ncclSum, u.rep_comm,
+                         ms_));
+      CU(cudaEventRecord(ev_rs_done_[size_t(l)], ms_));
+      if (tr)
+        mark("bwd.rs.layer" + std::to_string(l) + ".m0", "bwd.layer" + std::to_string(l), 1, a,
+             ev_rs_done_[size_t(l)]);
+    }
+  }
+  CU(k_embed_bwd(d_ids_, dx_, hu.gfull + hu.params[0].off, T_, H_, cs_));
+  if (P > 1 || hu.rep_comm) {
+    CU(cudaEventRecord(ev_head_rs_, cs_));
+    CU(cudaStreamWaitEvent(ms_, ev_head_rs_, 0));
+    if (P > 1) {
+      if (hu.padded > hu.numel)
+        CU(cudaMemsetAsync(hu.gfull + hu.numel, 0, size_t(hu.padded - hu.numel) * 4, ms_));
+      NC(ncclReduceScatter(hu.gfull, hu.gshard, size_t(hu.shard), ncclFloat, ncclSum, hu.comm,
+                           ms_));
+    }
+    if (hu.rep_comm)
+      NC(ncclAllReduce(hu.gshard, hu.gshard, size_t(hu.shard), ncclFloat, ncclSum, hu.rep_comm,
+                       ms_));
+  }
+  // join the comm stream
+  cudaEvent_t join = ev();
+  CU(cudaEventRecord(join, ms_));
+  CU(cudaStreamWaitEvent(cs_, join, 0));
+  CU(cudaEventRecord(ev_bwd_, cs_));
+
+  // ---------------- optimizer ----------------
+  for (Unit& u : units_)
+    CU(k_adamw(u.master, u.m, u.v, u.gshard, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps,
+               ex_.wd, step_count_, cs_));
+  CU(cudaEventRecord(ev_end_, cs_));
+  if (tr) mark("optimizer", "optimizer", 0, ev_bwd_, ev_end_);
+
+  // loss: local sum -> world all-reduce (reporting only, off the timed path)
+  CU(k_sum(loss_rows_, T_, loss_sum_, cs_));
+  if (world_comm_) NC(ncclAllReduce(loss_sum_, loss_sum_, 1, ncclFloat, ncclSum, world_comm_, cs_));
+  float loss = 0.f;
+  int timeout = 0;
+  CU(cudaMemcpyAsync(&loss, loss_sum_, 4, cudaMemcpyDeviceToHost, cs_));
+  CU(cudaMemcpyAsync(&timeout, d_timeout_, 4, cudaMemcpyDeviceToHost, cs_));
+  CU(cudaStreamSynchronize(cs_));
+  if (timeout) {
+    set_error("peer barrier timed out (a peer rank stalled)");
+    return OPX_ERR_TIMEOUT;
+  }
+  float t_all = 0, t_fwd = 0, t_bwd = 0, t_opt = 0;
+  CU(cudaEventElapsedTime(&t_all, ev_start_, ev_end_));
+  CU(cudaEventElapsedTime(&t_fwd, ev_start_, ev_fwd_));
+  CU(cudaEventElapsedTime(&t_bwd, ev_fwd_, ev_bwd_));
+  CU(cudaEventElapsedTime(&t_opt, ev_bwd_, ev_end_));
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->step_time_s = t_all * 1e-3;
+    rep->fwd_s = t_fwd * 1e-3;
+    rep->bwd_s = t_bwd * 1e-3;
+    rep->opt_s = t_opt * 1e-3;
+    rep->loss = double(loss) / double(n_valid_);
+    rep->tokens = double(T_);
+    rep->n_valid = double(n_valid_);
+    rep->launches = g_kernel_launches - launches0 - 1;  // minus the loss reduction
+  }
+  return OPX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// inspection
+// ---------------------------------------------------------------------------
+int Step::info(const std::string& full, int64_t* numel, int64_t* b, int64_t* e) {
+  const size_t colon = full.find(':');
+  const std::string name = colon == std::string::npos ? full : full.substr(colon + 1);
+  for (const Unit& u : units_) {
+    const Param* q = u.find(name);
+    if (!q) continue;
+    const int64_t sb = int64_t(u.idx) * u.shard, se = sb + u.shard;
+    const int64_t lo = std::max(sb, q->off), hi = std::min(se, q->off + q->numel);
+    *numel = q->numel;
+    *b = std::min(std::max<int64_t>(lo - q->off, 0), q->numel);
+    *e = std::max(*b, std::min<int64_t>(hi - q->off, q->numel));
+    return OPX_OK;
+  }
+  set_error("unknown tensor '" + name + "'");
+  return OPX_ERR_ARG;
+}
+
+int Step::get(const std::string& full, void* dst, size_t bytes) {
+  if (full == "loss_rows") {
+    if (bytes != size_t(T_) * 4) {
+      set_error("loss_rows: size mismatch");
+      return OPX_ERR_ARG;
+    }
+    CU(cudaMemcpy(dst, loss_rows_, bytes, cudaMemcpyDeviceToHost));
+    return OPX_OK;
+  }
+  const size_t colon = full.find(':');
+  if (colon == std::string::npos) {
+    set_error("tensor names are kind:name");
+    return OPX_ERR_ARG;
+  }
+  const std::string kind = full.substr(0, colon), name = full.substr(colon + 1);
+  for (const Unit& u : units_) {
+    const Param* q = u.find(name);
+    if (!q) continue;
+    const int64_t sb = int64_t(u.idx) * u.shard;
+    int64_t n, b, e;
+    TRY(info(full, &n, &b, &e));
+    const int64_t cnt = e - b, src0 = q->off + b - sb;
+    if (kind == "param") {
+      if (bytes != size_t(cnt) * 2) {
+        set_error("size mismatch for " + full);
+        return OPX_ERR_ARG;
+      }
+      if (cnt) CU(cudaMemcpy(dst, u.pshard + src0, bytes, cudaMemcpyDeviceToHost));
+      return OPX_OK;
+    }
+    const float* src = kind == "master" ? u.master
+                       : kind == "grad" ? u.gshard
+                       : kind == "exp_avg" ? u.m
+                       : kind == "exp_avg_sq" ? u.v
+                                              : nullptr;
+    if (!src) {
+      set_error("unknown tensor kind '" + kind + "'");
+      return OPX_ERR_ARG;
+    }
+    if (bytes != size_t(cnt) * 4) {
+      set_error("size mismatch for " + full);
+      return OPX_ERR_ARG;
+    }
+    if (cnt) CU(cudaMemcpy(dst, src + src0, bytes, cudaMemcpyDeviceToHost));
+    return OPX_OK;
+  }
+  set_error("unknown tensor '" + name + "'");
+  return OPX_ERR_ARG;
+}
+
+std::string Step::trace_json() {
+  nlohmann::json evs = nlohmann::json::array();
+  for (auto& t : trace_) {
+    float s = 0, e = 0;
+    if (cudaEventElapsedTime(&s, ev_start_, t.a) != cudaSuccess) continue;
+    if (cudaEventElapsedTime(&e, ev_start_, t.b) != cudaSuccess) continue;
+    evs.push_back({{"name", t.name},
+                   {"cat", t.tid == 0 ? "compute" : "comm"},
+                   {"ph", "X"},
+                   {"ts", double(s) * 1e3},
+                   {"dur", double(e - s) * 1e3},
+                   {"pid", rank_},
+                   {"tid", t.tid},
+                   {"args", {{"phase", t.phase}}}});
+  }
+  nlohmann::json j{{"traceEvents", evs}, {"displayTimeUnit", "ms"}};
+  return j.dump();
+}
+
+}  // namespace opx
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+using namespace opx;
+
+struct opx_step {
+  Step impl;
+};
+
+extern "C" {
+
+int opx_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    return OPX_ERR_CUDA;
+  }
+  std::memcpy(out128, &id, sizeof(id));
+  return OPX_OK;
+}
+
+int opx_step_create(const char* cj, const char* mj, const char* wj, const char* pj,
+                    const char* ej, int rank, int device, const void* nccl_id, opx_step** out) {
+  *out = nullptr;
+  Cluster c;
+  Model m;
+  Workload w;
+  Plan p;
+  ExecCfg ex;
+  try {
+    c = parse_cluster_json(cj ? cj : "");
+    m = parse_model_json(mj ? mj : "");
+    w = parse_workload_json(wj ? wj : "");
+    p = parse_plan_json(pj ? pj : "{}");
+    if (p.dp_shard < 0) p.dp_shard = c.world() / std::max<int64_t>(1, p.dp_replicate * p.sp);
+    nlohmann::json e = nlohmann::json::parse(ej && *ej ? ej : "{}");
+    ex.seed = e.value("seed", ex.seed);
+    ex.lr = e.value("lr", ex.lr);
+    if (e.contains("betas")) {
+      ex.b1 = e["betas"][0].get<float>();
+      ex.b2 = e["betas"][1].get<float>();
+    }
+    ex.eps = e.value("eps", ex.eps);
+    ex.wd = e.value("weight_decay", ex.wd);
+    ex.rope_theta = e.value("rope_theta", ex.rope_theta);
+    ex.rms_eps = e.value("rms_eps", ex.rms_eps);
+    ex.ce_chunk = e.value("ce_chunk", ex.ce_chunk);
+    ex.trace = e.value("trace", false);
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return OPX_ERR_CONFIG;
+  }
+  auto v = validate_plan(p, c, m, w);
+  if (!v.empty()) {
+    std::string s;
+    for (auto& x : v) s += x.code + " ";
+    set_error("plan invalid: " + s);
+    return OPX_ERR_PLAN;
+  }
+  if (w.global_batch != p.dp_width() * p.micro_batch) {
+    set_error("executor runs one micro-batch per dp rank: global_batch must equal "
+              "dp_replicate*dp_shard*micro_batch");
+    return OPX_ERR_CONFIG;
+  }
+  auto* st = new opx_step;
+  int rc = st->impl.create(c, m, w, p, ex, rank, device, nccl_id);
+  if (rc != OPX_OK) {
+    delete st;
+    return rc;
+  }
+  *out = st;
+  return OPX_OK;
+}
+
+int opx_step_ipc_export(opx_step* st, void* out, size_t cap, size_t* len) {
+  return st->impl.ipc_export(out, cap, len);
+}
+int opx_step_ipc_import(opx_step* st, const void* all, size_t len) {
+  return st->impl.ipc_import(all, len);
+}
+int opx_step_init_weights(opx_step* st, uint64_t seed) { return st->impl.init_weights(seed); }
+int opx_step_load_batch(opx_step* st, const int32_t* ids, const int32_t* labels,
+                        const int32_t* positions, const int32_t* cu, int n_cu, int64_t n_valid) {
+  return st->impl.load_batch(ids, labels, positions, cu, n_cu, n_valid);
+}
+int opx_step_run(opx_step* st, opx_step_report* rep) { return st->impl.run(rep); }
+int opx_step_get(opx_step* st, const char* name, void* dst, size_t bytes) {
+  return st->impl.get(name, dst, bytes);
+}
+int opx_step_tensor_info(opx_step* st, const char* name, int64_t* numel, int64_t* b, int64_t* e) {
+  return st->impl.info(name, numel, b, e);
+}
+int opx_step_trace(opx_step* st, char* out, size_t cap, size_t* len) {
+  const std::string s = st->impl.trace_json();
+  *len = s.size();
+  if (!out || cap <= s.size()) {
+    set_error("trace buffer too small");
+    return OPX_ERR_ARG;
+  }
+  std::memcpy(out, s.data(), s.size());
+  out[s.size()] = 0;
+  return OPX_OK;
+}
+int opx_step_destroy(opx_step* st) {
+  delete st;
+  return OPX_OK;
+}
+
+}  // extern "C"

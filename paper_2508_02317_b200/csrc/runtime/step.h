@@ -1,0 +1,177 @@
+// The training-step executor behind opx_step_* (the measured counterpart of
+// omniplan's build_step_graph + simulate, step_graph.cpp:441-448 /
+// simulator.cpp:14-65).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../host/plan.hpp"
+#include "kernels_api.h"
+#include "opx.h"
+
+namespace opx {
+
+using bf16 = __nv_bfloat16;
+
+struct ExecCfg {
+  uint64_t seed = 2508;
+  float lr = 1e-4f, b1 = 0.9f, b2 = 0.95f, eps = 1e-8f, wd = 0.1f;
+  double rope_theta = 1e6;
+  float rms_eps = 1e-6f;
+  int64_t ce_chunk = 8192;
+  bool trace = false;
+};
+
+// One parameter inside an FSDP flat unit.  `phys_name` is the name exposed by
+// opx_step_get; `interleave` marks a [2F, H] gate|up matrix stored as 128-row
+// interleaved blocks (logical names key_a = gate, key_b = up).
+struct Param {
+  std::string name;
+  int64_t off = 0, numel = 0;
+  std::vector<int64_t> shape;
+  bool ones = false;
+  int interleave = 0;
+  std::string key_a, key_b;
+  int64_t rows_per_slab = 0, cols = 0;
+  int64_t logical_offset = 0;  // element offset of this slab in the logical tensor (experts)
+};
+
+// FSDP unit: a flat parameter buffer sharded over `P` ranks with the
+// reference's ceil-chunk convention (reshard.cpp:11-18) applied to the
+// numel padded to a multiple of 64*P.
+struct Unit {
+  std::string name;
+  std::vector<Param> params;
+  int64_t numel = 0, padded = 0, shard = 0;
+  int P = 1, idx = 0;          // shard-group size and this rank's index in it
+  ncclComm_t comm = nullptr;   // shard group
+  ncclComm_t rep_comm = nullptr;  // HSDP replicate group (nullptr if none)
+  float *master = nullptr, *m = nullptr, *v = nullptr, *gshard = nullptr;
+  bf16* pshard = nullptr;
+  bf16* full = nullptr;        // gathered params (alias of pshard when P == 1)
+  float* gfull = nullptr;      // full-layout grads (alias of gshard when P == 1)
+  const Param* find(const std::string& n) const {
+    for (auto& p : params)
+      if (p.name == n) return &p;
+    return nullptr;
+  }
+};
+
+struct TraceEv {
+  std::string name, phase;
+  int tid;
+  cudaEvent_t a, b;
+};
+
+class Step {
+ public:
+  ~Step();
+  int create(const Cluster& c, const Model& m, const Workload& w, const Plan& p, const ExecCfg& ex,
+             int rank, int device, const void* nccl_id);
+  int ipc_export(void* out, size_t cap, size_t* len);
+  int ipc_import(const void* all, size_t len_per_rank);
+  int init_weights(uint64_t seed);
+  int load_batch(const int32_t* ids, const int32_t* labels, const int32_t* pos, const int32_t* cu,
+                 int n_cu, int64_t n_valid);
+  int run(opx_step_report* rep);
+  int get(const std::string& name, void* dst, size_t bytes);
+  int info(const std::string& name, int64_t* numel, int64_t* b, int64_t* e);
+  std::string trace_json();
+
+ private:
+  // ---- configuration
+  Cluster c_;
+  Model m_;
+  Workload w_;
+  Plan p_;
+  Arch a_;
+  ExecCfg ex_;
+  int rank_ = 0, world_ = 1, dev_ = 0;
+  int rep_i_ = 0, shard_i_ = 0, sp_i_ = 0;
+  std::vector<int64_t> sp_members_, shard_members_, rep_members_;
+  int rows_ = 1, S_ = 1, S_loc_ = 1, T_ = 1, Ntok_ = 1;
+  int H_ = 0, d_ = 128, hq_ = 0, hk_ = 0, hql_ = 0, hkl_ = 0, Wqkv_ = 0, F_ = 0, V_ = 0;
+  int step_count_ = 0;
+  int64_t n_valid_ = 1;
+  int64_t bytes_alloc_ = 0;
+
+  // ---- streams, comms, events
+  cudaStream_t cs_ = nullptr, ms_ = nullptr;
+  ncclComm_t world_comm_ = nullptr, shard_comm_ = nullptr, rep_comm_ = nullptr;
+  cudaEvent_t ev_start_ = nullptr, ev_fwd_ = nullptr, ev_bwd_ = nullptr, ev_end_ = nullptr;
+  std::vector<cudaEvent_t> ev_ag_, ev_use_done_, ev_grad_done_, ev_rs_done_;
+  cudaEvent_t ev_head_ag_ = nullptr, ev_head_rs_ = nullptr;
+  std::vector<TraceEv> trace_;
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_next_ = 0;
+
+  // ---- parameters
+  std::vector<Unit> units_;  // [0] head, [1+l] layer l
+  std::vector<bf16*> gslot_;     // gathered-param slots (P > 1)
+  std::vector<float*> gradslot_; // full-grad slots (P > 1)
+  int nslots_ = 2;
+
+  // ---- peer-visible arena (Ulysses exchanges)
+  char* arena_ = nullptr;
+  size_t arena_bytes_ = 0;
+  std::vector<char*> peer_arena_;  // by world rank
+  std::vector<cudaIpcMemHandle_t> opened_;
+  size_t off_flags_ = 0, off_q_[2] = {0, 0}, off_k_[2] = {0, 0}, off_v_[2] = {0, 0},
+         off_o_[2] = {0, 0}, off_do_[2] = {0, 0}, off_dqkv_[2] = {0, 0};
+  uint32_t** d_peer_flags_ = nullptr;  // device array [sp] of peer flag pointers
+  int* d_timeout_ = nullptr;
+  uint32_t epoch_ = 0;
+  int xq_ = 0, xo_ = 0, xdo_ = 0, xd_ = 0;  // double-buffer selectors
+
+  // ---- batch
+  int32_t *d_ids_ = nullptr, *d_labels_ = nullptr, *d_pos_ = nullptr, *d_sstart_ = nullptr,
+          *d_send_ = nullptr;
+  float* d_inv_freq_ = nullptr;
+
+  // ---- activations
+  std::vector<float*> x_saved_;  // layer inputs [L+1][T,H] fp32 (x_saved_[L] = final)
+  bf16 *h_ = nullptr, *qkv_ = nullptr, *ofull_ = nullptr, *h2_ = nullptr, *gu_ = nullptr,
+       *act_ = nullptr;
+  float *x2_ = nullptr, *r1_ = nullptr, *r2_ = nullptr, *lse_ = nullptr;
+  // backward scratch
+  float *dx_ = nullptr, *dtmp_ = nullptr, *dq_acc_ = nullptr, *delta_ = nullptr,
+        *dw_part_ = nullptr;
+  bf16 *dxb_ = nullptr, *dact_ = nullptr, *dgu_ = nullptr, *dk_ = nullptr, *dv_ = nullptr;
+  // head
+  bf16 *hf_ = nullptr, *logits_ = nullptr;
+  float *rf_ = nullptr, *dhf_ = nullptr, *loss_rows_ = nullptr, *loss_sum_ = nullptr;
+
+  // ---- helpers
+  template <class T>
+  T* alloc(size_t n, bool zero = true);
+  std::vector<void*> allocs_;
+  cudaEvent_t ev();
+  void mark(const std::string& name, const std::string& phase, int tid, cudaEvent_t a,
+            cudaEvent_t b);
+  int build_units();
+  int alloc_acts();
+  int gather(Unit& u, int slot, cudaEvent_t wait_ev);
+  bf16* q_full(int b) { return reinterpret_cast<bf16*>(arena_ + off_q_[b]); }
+  bf16* k_full(int b) { return reinterpret_cast<bf16*>(arena_ + off_k_[b]); }
+  bf16* v_full(int b) { return reinterpret_cast<bf16*>(arena_ + off_v_[b]); }
+  bf16* o_loc(int b) { return reinterpret_cast<bf16*>(arena_ + off_o_[b]); }
+  bf16* do_full(int b) { return reinterpret_cast<bf16*>(arena_ + off_do_[b]); }
+  bf16* dqkv_loc(int b) { return reinterpret_cast<bf16*>(arena_ + off_dqkv_[b]); }
+  char* peer(int sp_j, size_t off) {
+    return (sp_j == sp_i_ ? arena_ : peer_arena_[size_t(sp_members_[size_t(sp_j)])]) + off;
+  }
+  int barrier_sp(cudaStream_t s);
+  // layer pieces
+  int layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& qb, int& ob);
+  int layer_bwd(int l, Unit& u, float* grads);
+  int head_fwd_bwd(Unit& u, float* grads);
+  int check(cudaError_t e, const char* what);
+  int nccl(ncclResult_t r, const char* what);
+};
+
+}  // namespace opx

@@ -1,0 +1,200 @@
+"""Host-side session around the opx step executor (C ABI ``opx_step_*``).
+
+Mirrors the reference's driver flow (cli.cpp:239-289 cmd_simulate:
+load configs -> validate plan -> build the step -> run -> StepReport), with
+the simulation replaced by execution on the local GPU.  torch.distributed is
+used only as the out-of-band rendezvous for the NCCL unique id and the CUDA
+IPC handles of the peer-memory arenas.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import os
+
+import numpy as np
+
+from . import OpxError, check, lib
+
+
+class StepReport(ctypes.Structure):
+    _fields_ = [("step_time_s", ctypes.c_double), ("fwd_s", ctypes.c_double),
+                ("bwd_s", ctypes.c_double), ("opt_s", ctypes.c_double),
+                ("comm_wait_s", ctypes.c_double), ("loss", ctypes.c_double),
+                ("tokens", ctypes.c_double), ("n_valid", ctypes.c_double),
+                ("launches", ctypes.c_int64)]
+
+
+def _s(x) -> bytes:
+    return (json.dumps(x) if not isinstance(x, str) else x).encode()
+
+
+# ---------------------------------------------------------------------------
+# synthetic packed batches
+# ---------------------------------------------------------------------------
+def pack_row_lengths(S: int, rng: np.random.Generator, min_len: int = 64) -> list[int]:
+    """One row of exactly S tokens cut into samples with
+    l ~ clamp(round(LogNormal(ln(S/8), 1)), min_len, S); the last sample takes
+    the remainder (padding ratio 0, packing.cpp:53-64)."""
+    out, used = [], 0
+    while used < S:
+        l = int(np.clip(round(rng.lognormal(math.log(S / 8), 1.0)), min(min_len, S), S))
+        l = min(l, S - used)
+        out.append(l)
+        used += l
+    return out
+
+
+def synthetic_batch(vocab: int, seq_len: int, rows: int, seed: int = 2508, single_sample: bool = False):
+    """Global batch: ids/labels/pos [rows, S] int32, cu_rows: per-row cumulative
+    boundaries (PackedBatch.boundaries convention, packing.hpp:28)."""
+    rng = np.random.default_rng(seed)
+    ids = rng.integers(0, vocab, size=(rows, seq_len), dtype=np.int64).astype(np.int32)
+    labels = np.full((rows, seq_len), -100, np.int32)
+    pos = np.zeros((rows, seq_len), np.int32)
+    cu_rows = []
+    for r in range(rows):
+        lens = [seq_len] if single_sample else pack_row_lengths(seq_len, rng)
+        cu = [0]
+        for l in lens:
+            a = cu[-1]
+            pos[r, a:a + l] = np.arange(l)
+            labels[r, a:a + l - 1] = ids[r, a + 1:a + l]
+            cu.append(a + l)
+        cu_rows.append(cu)
+    return {"ids": ids, "labels": labels, "pos": pos, "cu_rows": cu_rows}
+
+
+def rank_coords(rank: int, plan: dict):
+    sp, sh = plan["sp"], plan["dp_shard"]
+    return rank // (sp * sh), (rank // sp) % sh, rank % sp  # rep, shard, sp
+
+
+def local_slice(batch, rank: int, plan: dict):
+    """What rank `rank` feeds its executor: its dp rows, its SP token slice."""
+    rep, sh, spi = rank_coords(rank, plan)
+    m, sp = plan["micro_batch"], plan["sp"]
+    dp = rep * plan["dp_shard"] + sh
+    rows = slice(dp * m, (dp + 1) * m)
+    S = batch["ids"].shape[1]
+    Sl = S // sp
+    tok = slice(spi * Sl, (spi + 1) * Sl)
+    ids = np.ascontiguousarray(batch["ids"][rows, tok]).reshape(-1)
+    labels = np.ascontiguousarray(batch["labels"][rows, tok]).reshape(-1)
+    pos = np.ascontiguousarray(batch["pos"][rows]).reshape(-1)
+    cu = [0]
+    for i, c in enumerate(batch["cu_rows"][rows]):
+        cu += [i * S + x for x in c[1:]]
+    n_valid = int((batch["labels"] >= 0).sum())
+    return ids, labels, pos, np.array(cu, np.int32), n_valid
+
+
+# ---------------------------------------------------------------------------
+# session
+# ---------------------------------------------------------------------------
+class Session:
+    """One rank's executor.  ``dist`` (optional) is an initialised
+    torch.distributed default group used for rendezvous only."""
+
+    def __init__(self, cluster, model, workload, plan, exec_cfg=None, rank=0, device=0, dist=None):
+        L = lib()
+        self.cluster, self.model, self.workload = cluster, model, workload
+        self.plan = dict(plan)
+        world = cluster["num_nodes"] * cluster["gpus_per_node"]
+        if self.plan.get("dp_shard", -1) in (-1, None):
+            self.plan["dp_shard"] = world // (self.plan.get("dp_replicate", 1) * self.plan.get("sp", 1))
+        for k, v in (("dp_replicate", 1), ("sp", 1), ("ep", 1), ("micro_batch", 1)):
+            self.plan.setdefault(k, v)
+        self.rank, self.world, self.dist = rank, world, dist
+        nid = ctypes.create_string_buffer(128)
+        if world > 1:
+            if rank == 0:
+                check(L.opx_nccl_unique_id(nid))
+            nid = ctypes.create_string_buffer(self._bcast(bytes(nid.raw)), 128)
+        self.h = ctypes.c_void_p()
+        rc = L.opx_step_create(_s(cluster), _s(model), _s(workload), _s(self.plan),
+                               _s(exec_cfg or {}), rank, device, nid, ctypes.byref(self.h))
+        if rc:
+            raise OpxError(rc, L.opx_last_error().decode())
+        buf = ctypes.create_string_buffer(256)
+        n = ctypes.c_size_t()
+        check(L.opx_step_ipc_export(self.h, buf, 256, ctypes.byref(n)))
+        mine = bytes(buf.raw[:n.value])
+        allh = self._allgather(mine) if world > 1 else [mine]
+        blob = b"".join(allh)
+        check(L.opx_step_ipc_import(self.h, blob, n.value))
+
+    # -- rendezvous helpers (bytes only; never tensors of the step)
+    def _bcast(self, b: bytes) -> bytes:
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def _allgather(self, b: bytes):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, b)
+        return out
+
+    def init_weights(self, seed: int = 2508):
+        check(lib().opx_step_init_weights(self.h, seed))
+
+    def load(self, batch):
+        ids, labels, pos, cu, n_valid = local_slice(batch, self.rank, self.plan)
+        i32 = ctypes.POINTER(ctypes.c_int32)
+        check(lib().opx_step_load_batch(self.h, ids.ctypes.data_as(ctypes.c_void_p),
+                                        labels.ctypes.data_as(ctypes.c_void_p),
+                                        pos.ctypes.data_as(ctypes.c_void_p),
+                                        cu.ctypes.data_as(ctypes.c_void_p), len(cu), n_valid))
+        return n_valid
+
+    def run(self) -> StepReport:
+        r = StepReport()
+        check(lib().opx_step_run(self.h, ctypes.byref(r)))
+        return r
+
+    def info(self, name):
+        n, b, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib().opx_step_tensor_info(self.h, name.encode(), ctypes.byref(n), ctypes.byref(b), ctypes.byref(e)))
+        return n.value, b.value, e.value
+
+    def get(self, name):
+        """This rank's [begin, end) slice of a flattened tensor (fp32, or bf16 bits as uint16 for param:)."""
+        n, b, e = self.info(name)
+        dt = np.uint16 if name.startswith("param:") else np.float32
+        out = np.empty(e - b, dt)
+        check(lib().opx_step_get(self.h, name.encode(), out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
+        return out, n, b, e
+
+    def loss_rows(self, T):
+        out = np.empty(T, np.float32)
+        check(lib().opx_step_get(self.h, b"loss_rows", out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
+        return out
+
+    def trace(self) -> dict:
+        cap = 1 << 24
+        buf = ctypes.create_string_buffer(cap)
+        n = ctypes.c_size_t()
+        check(lib().opx_step_trace(self.h, buf, cap, ctypes.byref(n)))
+        return json.loads(buf.value.decode())
+
+    def close(self):
+        if self.h:
+            lib().opx_step_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def deinterleave_gate_up(flat: np.ndarray, F: int, H: int):
+    """[2F, H] 128-row interleaved gate|up -> (gate [F,H], up [F,H])."""
+    v = flat.reshape(F // 128, 2, 128, H)
+    return v[:, 0].reshape(F, H), v[:, 1].reshape(F, H)
+
+
+def bf16_bits_to_f32(u16: np.ndarray) -> np.ndarray:
+    return (u16.astype(np.uint32) << 16).view(np.float32)

@@ -1,0 +1,88 @@
+"""Shared configs and the GPU-vs-oracle comparison for full training steps."""
+import numpy as np
+
+from oracle import model as om
+
+CLUSTER1 = {"num_nodes": 1, "gpus_per_node": 1, "gpu": {"peak_flops": 2.25e15, "hbm_bytes": 180e9},
+            "link": {"intra_node_bw": 9e11, "inter_node_bw": 5e10, "intra_latency": 5e-6,
+                     "inter_latency": 2e-5}}
+
+
+def cluster(n):
+    c = dict(CLUSTER1)
+    c["gpus_per_node"] = n
+    return c
+
+
+def tiny_dense(layers=2, hidden=256, heads=2, kv=2, ffn=768, vocab=2048):
+    return {"param_dtype_bytes": 2, "modules": [{"name": "core", "kind": "foundation", "trainable": True,
+            "arch": {"layers": layers, "hidden": hidden, "heads": heads, "kv_heads": kv,
+                     "head_dim": hidden // heads, "ffn_dim": ffn, "vocab": vocab}}]}
+
+
+EXEC = {"seed": 2508, "lr": 1e-4, "betas": [0.9, 0.95], "eps": 1e-8, "weight_decay": 0.1}
+
+TOL_LOSS = 1e-3   # relative, north_star
+TOL_GRAD = 2e-2   # max-abs-err / max-abs-ref, north_star
+TOL_COS = 0.999
+
+
+def gather_full(sessions, kind, name):
+    """Reassemble a flattened tensor from every rank's slice (FSDP shards)."""
+    parts = {}
+    n = None
+    for s in sessions:
+        v, n, b, e = s.get(f"{kind}:{name}")
+        if e > b:
+            parts[b] = v
+    out = np.zeros(n, np.float32)
+    for b, v in parts.items():
+        out[b:b + len(v)] = v
+    return out
+
+
+def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
+    """Runs the oracle on the same batch/weights and compares loss, every
+    gradient and the AdamW-updated master weights.  Returns a report dict."""
+    arch = om.Arch.from_model_json(model)
+    P0 = om.init_params(arch, EXEC["seed"])
+    loss_ref, G = om.simulate_ranks(arch, P0, batch, plan)
+    rep = {"loss": step_loss, "loss_ref": loss_ref, "grads": {}}
+    assert abs(step_loss - loss_ref) / abs(loss_ref) < TOL_LOSS, (step_loss, loss_ref)
+    F, H = arch.ffn, arch.hidden
+    names = {}
+    for name, shape, _ in om.param_specs(arch):
+        names[name] = shape
+    got = {}
+    for l in range(arch.layers):
+        p = f"model.layers.{l}.mlp."
+        gu = gather_full(sessions, "grad", p + "gate_up_proj.weight")
+        g, u = om_deint(gu, F, H)
+        got[p + "gate_proj.weight"] = g
+        got[p + "up_proj.weight"] = u
+    for name in names:
+        if name not in got:
+            got[name] = gather_full(sessions, "grad", name).reshape(names[name])
+    for name, ref in G.items():
+        x = got[name].reshape(ref.shape)
+        err = np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-30)
+        cos = float(np.dot(x.ravel().astype(np.float64), ref.ravel()) /
+                    max(np.linalg.norm(x) * np.linalg.norm(ref), 1e-30))
+        rep["grads"][name] = (float(err), cos)
+        assert err < TOL_GRAD and cos > TOL_COS, (name, err, cos)
+    if check_params:
+        P1 = om.adamw(P0, G, {}, 1, lr=EXEC["lr"], betas=tuple(EXEC["betas"]), eps=EXEC["eps"],
+                      wd=EXEC["weight_decay"])
+        for name, ref in P1.items():
+            if name.endswith("gate_proj.weight") or name.endswith("up_proj.weight"):
+                continue
+            x = gather_full(sessions, "master", name).reshape(ref.shape)
+            d = np.abs(x - ref)
+            assert d.max() <= 2.05 * EXEC["lr"], (name, d.max())
+            assert d.mean() <= 0.02 * EXEC["lr"], (name, d.mean())
+    return rep
+
+
+def om_deint(flat, F, H):
+    v = flat.reshape(F // 128, 2, 128, H)
+    return v[:, 0].reshape(F, H), v[:, 1].reshape(F, H)

@@ -312,3 +312,32 @@ def test_rope_pack():
     assert rel_err(qf, rope(x[:, :hq])) < 1e-2
     assert rel_err(kf, rope(x[:, hq:hq + hk])) < 1e-2
     assert torch.equal(vf.float(), x[:, hq + hk:])
+
+
+# ---------------------------------------------------------------- deterministic init
+@gpu
+def test_init_bit_identical_to_oracle():
+    import numpy as np
+
+    from oracle import model as om
+    from paper_2508_02317_b200 import lib
+
+    n = 3 * 256 * 128
+    key_a = lib().opx_param_key(b"model.layers.0.mlp.gate_proj.weight", 2508)
+    key_b = lib().opx_param_key(b"model.layers.0.mlp.up_proj.weight", 2508)
+    assert key_a == om.param_key("model.layers.0.mlp.gate_proj.weight", 2508)
+    f = torch.empty(n, device=DEV)
+    b = torch.empty(n, device=DEV, dtype=torch.bfloat16)
+    c = 0.02 * math.sqrt(3.0) / 16777216.0
+    call("opx_init_param", P(f), P(b), n, 0, key_a, 0, c, 1.0, 0, 0, 0, S())
+    torch.cuda.synchronize()
+    assert np.array_equal(f.cpu().numpy(), om.init_values(key_a, n))
+    # interleaved gate|up [2F, H] with F=384, H=128 (second slab offset 0)
+    F, H = 384, 128
+    n2 = 2 * F * H
+    f2 = torch.empty(n2, device=DEV)
+    call("opx_init_param", P(f2), None, n2, 0, key_a, key_b, c, 1.0, 1, 2 * F, H, S())
+    torch.cuda.synchronize()
+    v = f2.cpu().numpy().reshape(F // 128, 2, 128, H)
+    assert np.array_equal(v[:, 0].reshape(-1), om.init_values(key_a, F * H))
+    assert np.array_equal(v[:, 1].reshape(-1), om.init_values(key_b, F * H))
