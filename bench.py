@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark of the fwd+bwd+AdamW training step (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c0] [--impl opx|reference]
+
+N > 1 is launched by the driver under torchrun (one rank per GPU).  Rank 0
+prints ONE JSON line.  `value` is whole-job tokens/s from device time (CUDA
+events inside the executor, max over ranks); `e2e` is the same metric through
+the public C ABI with host input buffers (H2D of ids/labels/positions and the
+D2H loss read inside the timed region); `--impl reference` times the CPU
+reference path (the numpy oracle; the reference itself computes no tensors).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train tokens/sec/GPU and MFU (fwd+bwd+opt step) at 1/2/4/8 B200 vs CPU ref"
+
+QWEN2_7B = {"layers": 28, "hidden": 3584, "heads": 28, "kv_heads": 4, "head_dim": 128,
+            "ffn_dim": 18944, "vocab": 152064}
+TINY = {"layers": 2, "hidden": 256, "heads": 2, "kv_heads": 2, "head_dim": 128, "ffn_dim": 768,
+        "vocab": 2048}
+
+
+def plan_for(cfg: str, n: int) -> dict:
+    """Parallel plan per GPU count: C1 FSDP1 -> SP2 -> SP4 -> FSDP2xSP4."""
+    if cfg == "c1":
+        sp = min(n, 4)
+        return {"dp_replicate": 1, "dp_shard": n // sp, "sp": sp, "ep": 1, "micro_batch": 1,
+                "recompute": "full", "fsdp_prefetch_depth": 1}
+    return {"dp_replicate": 1, "dp_shard": n, "sp": 1, "ep": 1, "micro_batch": 1,
+            "recompute": "full", "fsdp_prefetch_depth": 1}
+
+
+def model_for(cfg: str) -> dict:
+    arch = {"c1": QWEN2_7B, "c0": TINY}[cfg]
+    return {"param_dtype_bytes": 2,
+            "modules": [{"name": "core", "kind": "foundation", "trainable": True, "arch": arch}]}
+
+
+def seq_for(cfg: str) -> int:
+    return {"c1": 32768, "c0": 1024}[cfg]
+
+
+def cluster_for(n: int) -> dict:
+    return {"num_nodes": 1, "gpus_per_node": n, "gpu": {"peak_flops": 2.25e15, "hbm_bytes": 180e9},
+            "link": {"intra_node_bw": 9e11, "inter_node_bw": 5e10, "intra_latency": 5e-6,
+                     "inter_latency": 2e-5}}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"] * 1e12, p.get("bf16_tflops_sustained", p["bf16_tflops"]) * 1e12, \
+            p["hbm_gbs"], "measured"
+    except Exception:
+        return 1.59e15, 1.4e15, 6650.0, "fallback"
+
+
+def exact_flops_per_step(arch: dict, batch, T_total: int) -> float:
+    """6*N_active,strict per token + exact causal attention 6*L*H*sum(l_i^2)
+    (SURVEY.md §8d); N_active,strict excludes the embedding gather."""
+    H, L, V, F = arch["hidden"], arch["layers"], arch["vocab"], arch["ffn_dim"]
+    kvw = arch["kv_heads"] * arch["head_dim"]
+    per_layer = H * (H + 2 * kvw) + H + H * H + 3 * H * F + H
+    n_strict = L * per_layer + V * H + H
+    sq = 0
+    for cu in batch["cu_rows"]:
+        for a, b in zip(cu[:-1], cu[1:]):
+            sq += (b - a) ** 2
+    return 6.0 * n_strict * T_total + 6.0 * L * H * sq
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, dev: int):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / baseline: the numpy oracle on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference(cfg: str, budget_s: float = 20.0) -> dict:
+    import numpy as np
+
+    from oracle import model as om
+
+    arch = dict(model_for(cfg)["modules"][0]["arch"])
+    full_arch = dict(arch)
+    arch["layers"] = 1
+    a = om.Arch.from_model_json({"modules": [{"kind": "foundation", "arch": arch}]})
+    a.vocab = 512  # the sample times one transformer block; the head is accounted analytically
+    S = 256
+    from paper_2508_02317_b200.runtime import synthetic_batch
+
+    P = om.init_params(a, 2508)
+    b = synthetic_batch(a.vocab, S, 1, seed=2508)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        st = om.Step(a, P)
+        st.run(b["ids"][0], b["labels"][0], b["pos"][0], np.array(b["cu_rows"][0]), S)
+        n += 1
+        if time.perf_counter() - t0 > budget_s or n >= 50:
+            break
+    dt = (time.perf_counter() - t0) / n
+    # FLOPs of the timed sample: one block fwd+bwd over S tokens + the small head
+    H, F, kvw = arch["hidden"], arch["ffn_dim"], arch["kv_heads"] * arch["head_dim"]
+    block = H * (H + 2 * kvw) + H * H + 3 * H * F
+    sq = sum((y - x) ** 2 for x, y in zip(b["cu_rows"][0][:-1], b["cu_rows"][0][1:]))
+    sample_flops = 6.0 * (block + a.vocab * H) * S + 6.0 * H * sq
+    rate = sample_flops / dt
+    # tokens/s of the full model on this host at that FLOP rate (extrapolated)
+    L, V = full_arch["layers"], full_arch["vocab"]
+    fpt = 6.0 * (L * (block + 2 * H) + V * H + H) + 6.0 * L * H * seq_for(cfg) / 2.0
+    return {"value": rate / fpt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"numpy oracle fwd+bwd of 1 {cfg} block (H={H}, ffn={F}) on {S} packed tokens, "
+                      f"{n} reps in {dt * n:.1f}s; {rate / 1e9:.1f} GFLOP/s extrapolated to the full "
+                      f"{L}-layer model at S={seq_for(cfg)}",
+            "gflops": rate / 1e9}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--impl", default="opx", choices=["opx", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.gpus
+    if world != n and world != 1:
+        n = world
+    cfg = args.config
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(cfg)
+        steps = []
+        for _ in range(max(args.steps, 1)):
+            steps.append(ref["value"])
+        v = statistics.median(steps)
+        line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": n, "steps": args.steps,
+                "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": cfg, "model": "qwen2-7b-shaped" if cfg == "c1" else cfg,
+                           "seq_len": seq_for(cfg)},
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+
+        td.init_process_group("gloo")
+        dist = td
+    from paper_2508_02317_b200.runtime import Session, local_slice, synthetic_batch
+
+    plan = plan_for(cfg, n)
+    model = model_for(cfg)
+    arch = model["modules"][0]["arch"]
+    S = seq_for(cfg)
+    rows = plan["dp_replicate"] * plan["dp_shard"] * plan["micro_batch"]
+    wl = {"seq_len": S, "micro_batch": plan["micro_batch"], "global_batch": rows}
+    ex = {"seed": 2508, "lr": 1e-4, "betas": [0.9, 0.95], "eps": 1e-8, "weight_decay": 0.1,
+          "trace": True}
+    sess = Session(cluster_for(n), model, wl, plan, ex, rank=rank, device=local, dist=dist)
+    sess.init_weights(2508)
+    batch = synthetic_batch(arch["vocab"], S, rows, seed=2508)
+    ids, labels, pos, cu, n_valid = local_slice(batch, rank, plan)
+    h2d = ids.nbytes + labels.nbytes + pos.nbytes + cu.nbytes
+    sess.load(batch)
+    for _ in range(args.warmup):
+        sess.run()
+    if dist:
+        dist.barrier()
+    times, walls, launches, losses = [], [], 0, []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            sess.load(batch)          # H2D of this step's inputs (host buffers)
+            r = sess.run()            # device-timed step + D2H of the loss
+            walls.append(time.perf_counter() - t0)
+            times.append(r.step_time_s)
+            launches += r.launches
+            losses.append(r.loss)
+    trace = sess.trace()
+    if dist:
+        import torch.distributed as td
+
+        t = torch.tensor([max(times), statistics.mean(times), statistics.mean(walls)], dtype=torch.float64)
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+        t_max, t_mean, w_mean = t.tolist()
+    else:
+        t_max, t_mean, w_mean = max(times), statistics.mean(times), statistics.mean(walls)
+    if rank != 0:
+        sess.close()
+        return
+
+    tokens_step = rows * S
+    value = tokens_step / t_mean
+    peak, peak_sus, hbm, peak_kind = peaks()
+    fpt_ref = 6.0 * (arch["layers"] * (arch["hidden"] * (arch["hidden"] + 2 * arch["kv_heads"] * 128) + arch["hidden"]
+                     + arch["hidden"] ** 2 + 3 * arch["hidden"] * arch["ffn_dim"] + arch["hidden"])
+                     + 2 * arch["vocab"] * arch["hidden"] + arch["hidden"]) + 6.0 * arch["layers"] * arch["hidden"] * S
+    exact = exact_flops_per_step(arch, batch, tokens_step)
+    per_gpu = value / n
+    # roofline: dominant kernel = the forward MLP block (gate|up GEMM + SwiGLU
+    # epilogue + down GEMM), 6*T*H*F algorithmic FLOPs per layer-call
+    T_loc = S // plan["sp"] * plan["micro_batch"]
+    mlp = [e["dur"] for e in trace["traceEvents"] if e["name"].startswith("fwd.layer") and e["name"].endswith(".mlp")]
+    node_s = statistics.mean(mlp) * 1e-6 if mlp else float("nan")
+    mlp_flops = 6.0 * T_loc * arch["hidden"] * arch["ffn_dim"]
+    achieved = mlp_flops / node_s
+    share = {}
+    for e in trace["traceEvents"]:
+        if e["tid"] != 0:
+            continue
+        key = e["name"].split(".m0.")[-1] if ".m0." in e["name"] else e["name"]
+        key = ("bwd." if e["name"].startswith("bwd") else "fwd." if e["name"].startswith("fwd.layer") else "") + key
+        share[key] = share.get(key, 0.0) + e["dur"] * 1e-6
+    tot = sum(share.values()) or 1.0
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_mean * 1e3, "ms_per_step_max": t_max * 1e3,
+        "higher_is_better": True, "scaling": "strong" if n <= 4 else "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "tokens_per_s_per_gpu": per_gpu,
+        "mfu_ref": per_gpu * fpt_ref / peak, "mfu_ref_datasheet": per_gpu * fpt_ref / 2.25e15,
+        "mfu_exact": exact / t_mean / n / peak, "model_flops_per_token_ref": fpt_ref,
+        "config": {"workload": cfg, "model": "qwen2-7b-shaped (random init)" if cfg == "c1" else cfg,
+                   "global_batch": rows, "seq_len": S, "tokens_per_step": tokens_step,
+                   "parallelism": f"fsdp{plan['dp_shard']}xsp{plan['sp']}",
+                   "recompute": plan["recompute"], "packing": "lognormal varlen, 0 padding",
+                   "l2": "inputs+weights >> 126 MB L2 (no flush needed)",
+                   "peak_kind": peak_kind},
+        "loss": losses[-1],
+        "e2e": {"value": tokens_step / w_mean, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "kernel": "fwd MLP block (tcgen05 gate|up GEMM+SwiGLU, down GEMM)",
+                     "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "flops_per_launch": mlp_flops, "launch_ms": node_s * 1e3},
+        "phase_share": {k: round(v / tot, 4) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:12]},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and n == 1:
+        ref = cpu_reference(cfg, budget_s=15.0)
+        line["cpu_baseline"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+    sess.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,34 @@
+"""Worker for multi-rank step tests: one process per GPU (or per CPU rank for
+the gloo host-logic tests).  Returns this rank's loss and tensor slices."""
+import os
+
+
+def step_worker(rank, world, port, model, plan, S, rows, q, names):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import torch.distributed as td
+
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_02317_b200.runtime import Session, synthetic_batch
+        from tests.step_common import EXEC, cluster
+
+        wl = {"seq_len": S, "micro_batch": plan["micro_batch"], "global_batch": rows}
+        s = Session(cluster(world), model, wl, plan, EXEC, rank=rank, device=rank, dist=td)
+        s.init_weights(EXEC["seed"])
+        batch = synthetic_batch(model["modules"][0]["arch"]["vocab"], S, rows, seed=2508)
+        s.load(batch)
+        r = s.run()
+        out = {}
+        for kind in ("grad", "master"):
+            for n in names:
+                v, numel, b, e = s.get(f"{kind}:{n}")
+                out[(kind, n)] = (v, numel, b, e)
+        q.put((rank, r.loss, out, None))
+        s.close()
+    except Exception as ex:  # report instead of hanging the parent
+        import traceback
+
+        q.put((rank, None, None, traceback.format_exc()))
+    finally:
+        td.destroy_process_group()
