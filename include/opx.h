@@ -140,20 +140,21 @@ uint64_t opx_param_key(const char* name, uint64_t seed);
 int opx_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t ldq,
                  int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
                  const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream);
+int opx_attn_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse,
+                    int64_t ldq, int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
+                    const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream);
 int opx_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
                  const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
                  int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,
                  int N, int hq, int hk, float scale, void* stream);
+int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                    const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
+                    int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,
+                    int N, int hq, int hk, float scale, void* stream);
 /* Single-rank Ulysses relayout (sp == 1 path) with RoPE, for testing. */
 int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void* v_full,
                   int hq, int hk, int rows, int S, const int32_t* pos, const float* inv_freq,
                   void* stream);
-
-/* MoE routing (moe.cu): fp32 router logits with a fixed sequential K order,
- * top-k with lower-index tie break, renormalised softmax weights, and a
- * stable counting-sort permutation by (expert, token, slot). */
-int opx_moe_route(const void* h, const void* w_router, int T, int H, int E, int k,
-                  float* logits, int32_t* topk_idx, float* topk_w, void* stream);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,9 @@ struct AttnArgs {
 };
 cudaError_t k_attn_fwd(const AttnArgs& a, cudaStream_t s);
 cudaError_t k_attn_bwd(const AttnArgs& a, cudaStream_t s);
+// attention_tc.cu — the same forward on tcgen05/TMEM/TMA.
+cudaError_t k_attn_fwd_tc(const AttnArgs& a, cudaStream_t s);
+cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s);
 
 // a2a.cu — Ulysses all-to-all over peer memory with fused RoPE.
 constexpr int kMaxSp = 8;
