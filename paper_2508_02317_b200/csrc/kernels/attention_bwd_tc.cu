@@ -1,0 +1,405 @@
+// Causal packed-varlen GQA flash attention BACKWARD on tcgen05 (sm_100a).
+//
+// One CTA per (128-key tile, kv head).  K and V stay in smem; the CTA walks
+// the q heads of its GQA group and the 64-query tiles that can see its keys
+// (q in [k0, seq_end(last key))), with Q/dO double-buffered by TMA.
+//
+//   TMEM: S^T [0,64) | dP^T [64,128) | dQ^T [128,192) | dV [256,384) | dK [384,512)
+//   per q tile i (MMA warp, one elected lane):
+//     S^T  = K  Q_i^T    (M=128 keys, N=64 q, K=128 d)            -> s_full
+//     dP^T = V  dO_i^T
+//     -- softmax warps: P^T = exp2(S^T c - lse), dS^T = P^T (dP^T - delta),
+//        bf16 -> SW128 smem [keys][q] (one key row per thread) -> p_ready
+//     dV  += P^T  dO_i   (M=128 keys, N=128 d, K=64 q)
+//     dK  += dS^T Q_i
+//     dQ^T = K^T  dS^T   (M=128 d, N=64 q, K=128 keys)            -> dq_full
+//     -- softmax warps: dQ^T rows (one d per thread) -> fp32 smem [q][d]
+//        -> one TMA bulk reduce-add into the fp32 dQ accumulator
+// The S^T/dP^T MMAs of tile i+1 overlap the dQ readout/reduction of tile i.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "../runtime/kernels_api.h"
+#include "attn_common.cuh"
+#include "ptx.cuh"
+
+namespace opx {
+namespace {
+
+using bf16 = __nv_bfloat16;
+using namespace attn;
+constexpr int BQ = 64, BK = 128, D = 128;
+constexpr int THREADS = 320;  // TMA, MMA, 8 softmax/dQ warps (2 per TMEM lane quadrant)
+constexpr int NSM = 256;       // softmax threads
+constexpr float LOG2E = 1.4426950408889634f;
+// smem map (bytes, 1024-aligned base)
+constexpr int OFF_K = 0, OFF_V = 32768, OFF_Q = 65536 /*[2] x 16K*/, OFF_O = 98304 /*[2] x 16K*/,
+              OFF_P = 131072, OFF_S = 147456, OFF_STAGE = 163840 /*32K fp32*/,
+              OFF_MISC = 196608;
+constexpr int SMEM = 1024 + OFF_MISC + 3 * 2 * BQ * 4 + 256;
+
+struct Params {
+  const float* lse;
+  const float* delta;
+  bf16* dk;
+  bf16* dv;
+  int64_t lddk, lddv;
+  const int* seq_start;
+  const int* seq_end;
+  int N, hq, hk;
+  float scale, scale_log2;
+  int skip_dq;  // debug: measure without the dQ reduction
+};
+
+__device__ __forceinline__ uint64_t kd(uint32_t base, int k, int blk) {
+  return ptx::umma_desc_sw128(base + (k >> 2) * blk + (k & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t md(uint32_t base, int k, int lbo) {
+  return ptx::umma_desc_sw128(base + k * 2048, lbo, 1024);
+}
+__device__ __forceinline__ void bar_sync_softmax() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                       const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+                       const __grid_constant__ CUtensorMap tdq, const Params p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1024-B alignment by pointer arithmetic on the __shared__ array keeps the
+  // shared address space (no generic LD/ST on the hot path).
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* s_lse = reinterpret_cast<float*>(smem + OFF_MISC);  // [2][64]
+  float* s_dlt = s_lse + 2 * BQ;
+  int* s_sst = reinterpret_cast<int*>(s_dlt + 2 * BQ);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_sst + 2 * BQ);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* qdo_full = bars + 1;   // [2]
+  uint64_t* qdo_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_ready = bars + 6;
+  uint64_t* dq_full = bars + 7;
+  uint64_t* dqt_free = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  float* stage = reinterpret_cast<float*>(smem + OFF_STAGE);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k0 = blockIdx.x * BK;
+  const int kh = blockIdx.y;
+  const int G = p.hq / p.hk;
+  const int klast = min(k0 + BK, p.N) - 1;
+  const int qend = p.seq_end[klast];
+  const int nq = (qend - k0 + BQ - 1) / BQ;
+  const int niter = G * nq;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tq);
+    ptx::tma_prefetch(&tk);
+    ptx::tma_prefetch(&tv);
+    ptx::tma_prefetch(&tdo);
+    ptx::tma_prefetch(&tdq);
+    ptx::mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&qdo_full[i], 1);
+      ptx::mbar_init(&qdo_empty[i], 1);
+    }
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(p_ready, NSM);
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dqt_free, NSM);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t TST = tmem, TDP = tmem + 64, TDQ = tmem + 128, TDV = tmem + 256, TDK = tmem + 384;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      ptx::mbar_expect_tx(kv_full, 4 * 16384);
+      ptx::tma_load_3d(&tk, kv_full, smem + OFF_K, 0, kh, k0);
+      ptx::tma_load_3d(&tk, kv_full, smem + OFF_K + 16384, 64, kh, k0);
+      ptx::tma_load_3d(&tv, kv_full, smem + OFF_V, 0, kh, k0);
+      ptx::tma_load_3d(&tv, kv_full, smem + OFF_V + 16384, 64, kh, k0);
+      for (int it = 0; it < niter; ++it) {
+        const int st = it & 1;
+        const int h = kh * G + it / nq;
+        const int q0 = k0 + (it % nq) * BQ;
+        if (it >= 2) ptx::mbar_wait(&qdo_empty[st], ((it >> 1) - 1) & 1);
+        ptx::mbar_expect_tx(&qdo_full[st], 4 * 8192);
+        uint8_t* q = smem + OFF_Q + st * 16384;
+        uint8_t* o = smem + OFF_O + st * 16384;
+        ptx::tma_load_3d(&tq, &qdo_full[st], q, 0, h, q0);
+        ptx::tma_load_3d(&tq, &qdo_full[st], q + 8192, 64, h, q0);
+        ptx::tma_load_3d(&tdo, &qdo_full[st], o, 0, h, q0);
+        ptx::tma_load_3d(&tdo, &qdo_full[st], o + 8192, 64, h, q0);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, BQ, false, false);   // S^T, dP^T
+    constexpr uint32_t id_kv = ptx::idesc_bf16_f32(128, D, false, true);    // dV, dK
+    constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, BQ, true, true);     // dQ^T
+    const uint32_t ak = ptx::smem_u32(smem + OFF_K), av = ptx::smem_u32(smem + OFF_V),
+                   ap = ptx::smem_u32(smem + OFF_P), as = ptx::smem_u32(smem + OFF_S);
+    ptx::mbar_wait(kv_full, 0);
+    // issue order: S/dP(i+1) right after P(i) is ready, then dV/dK/dQ(i), so
+    // the softmax of tile i+1 overlaps the gradient MMAs of tile i.
+    auto issue_sdp = [&](int it) {
+      const int st = it & 1;
+      const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
+      const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
+      ptx::mbar_wait(&qdo_full[st], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          ptx::mma_bf16_ss(TST, kd(ak, k, 16384), kd(aq, k, 8192), id_s, k != 0);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          ptx::mma_bf16_ss(TDP, kd(av, k, 16384), kd(ao, k, 8192), id_s, k != 0);
+        ptx::mma_commit(s_full);
+      }
+      __syncwarp();
+    };
+    if (niter > 0) issue_sdp(0);
+    for (int it = 0; it < niter; ++it) {
+      const int st = it & 1;
+      const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
+      const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
+      ptx::mbar_wait(p_ready, it & 1);   // P/dS(it) in smem; S^T/dP^T(it) consumed
+      if (it + 1 < niter) issue_sdp(it + 1);
+      if (it > 0) ptx::mbar_wait(dqt_free, (it - 1) & 1);  // dQ^T(it-1) read out
+      ptx::tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k)
+          ptx::mma_bf16_ss(TDV, kd(ap, k, 0), md(ao, k, 8192), id_kv, (it | k) != 0);
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k)
+          ptx::mma_bf16_ss(TDK, kd(as, k, 0), md(aq, k, 8192), id_kv, (it | k) != 0);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          ptx::mma_bf16_ss(TDQ, md(ak, k, 16384), md(as, k, 8192), id_q, k != 0);
+        ptx::mma_commit(dq_full);
+        ptx::mma_commit(&qdo_empty[st]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- softmax / dQ warps ----------------
+    // warps 2..9: lane quadrant = warp & 3 (TMEM access rule), column half =
+    // (warp - 2) / 4, so every quadrant is served by two warps.
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = quad * 32 + lane;  // key row for S^T/dP^T, d row for dQ^T
+    const int c0 = half * 32;        // first of this thread's 32 q columns
+    const int key = k0 + r;
+    const uint32_t lane_off = uint32_t(quad * 32) << 16;
+    uint8_t* sP = smem + OFF_P;
+    uint8_t* sS = smem + OFF_S;
+    const bool issuer = threadIdx.x == 64;
+    auto load_cols = [&](int it) {  // lse/delta/seq_start of tile it -> smem buffer it&1
+      if (half == 0 && r < BQ) {
+        const int h = kh * G + it / nq;
+        const int q = k0 + (it % nq) * BQ + r;
+        const bool ok = q < p.N;
+        const int buf = it & 1;
+        s_lse[buf * BQ + r] = ok ? p.lse[int64_t(h) * p.N + q] * LOG2E : INFINITY;
+        s_dlt[buf * BQ + r] = ok ? p.delta[int64_t(h) * p.N + q] : 0.f;
+        s_sst[buf * BQ + r] = ok ? p.seq_start[q] : 0x7fffffff;
+      }
+    };
+    // dQ^T(j) (thread: d row r, q columns c0..c0+31) -> fp32 staging [q][d] -> bulk reduce-add
+    auto drain_dq = [&](int j) {
+      const int h = kh * G + j / nq;
+      const int q0 = k0 + (j % nq) * BQ;
+      ptx::mbar_wait(dq_full, j & 1);
+      ptx::tc_fence_after();
+      uint32_t qv[32];
+      ptx::tmem_ld32(TDQ + lane_off + c0, qv);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dqt_free);
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      bar_sync_softmax();  // staging buffer free
+#pragma unroll
+      for (int q = 0; q < 32; ++q) stage[(c0 + q) * D + r] = __uint_as_float(qv[q]) * p.scale;
+      ptx::fence_proxy_async();
+      bar_sync_softmax();
+      if (issuer && !p.skip_dq) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&tdq)),
+            "r"(ptx::smem_u32(stage)), "r"(0), "r"(h), "r"(q0)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    };
+    if (niter > 0) load_cols(0);
+    bar_sync_softmax();
+    for (int it = 0; it < niter; ++it) {
+      const int q0 = k0 + (it % nq) * BQ;
+      const int buf = it & 1;
+      // broadcast vector loads of this thread's 32 columns
+      float lv[32], dl[32];
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(s_lse + buf * BQ + c0 + i);
+        const float4 b = *reinterpret_cast<const float4*>(s_dlt + buf * BQ + c0 + i);
+        lv[i] = a.x; lv[i + 1] = a.y; lv[i + 2] = a.z; lv[i + 3] = a.w;
+        dl[i] = b.x; dl[i + 1] = b.y; dl[i + 2] = b.z; dl[i + 3] = b.w;
+      }
+      const int* sst = s_sst + buf * BQ;
+      const bool full_vis = key <= q0 + c0 && q0 + c0 + 31 < p.N && sst[c0 + 31] <= key;
+      ptx::mbar_wait(s_full, it & 1);
+      ptx::tc_fence_after();
+      uint32_t sv[32], dv[32];
+      ptx::tmem_ld32(TST + lane_off + c0, sv);
+      ptx::tmem_ld32(TDP + lane_off + c0, dv);
+      ptx::tmem_wait_ld();
+      uint32_t pw[16], dw[16];
+      if (full_vis) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = exp2f(fmaf(__uint_as_float(sv[i]), p.scale_log2, -lv[i]));
+          const float p1 = exp2f(fmaf(__uint_as_float(sv[i + 1]), p.scale_log2, -lv[i + 1]));
+          pw[i / 2] = ptx::pack_bf16(p0, p1);
+          dw[i / 2] = ptx::pack_bf16(p0 * (__uint_as_float(dv[i]) - dl[i]),
+                                     p1 * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float pp[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int q = q0 + c0 + i + e;
+            const bool ok = (key <= q) & (key >= sst[c0 + i + e]) & (key < p.N);
+            const float x = exp2f(fmaf(__uint_as_float(sv[i + e]), p.scale_log2, -lv[i + e]));
+            pp[e] = ok ? x : 0.f;
+          }
+          pw[i / 2] = ptx::pack_bf16(pp[0], pp[1]);
+          dw[i / 2] = ptx::pack_bf16(pp[0] * (__uint_as_float(dv[i]) - dl[i]),
+                                     pp[1] * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
+        }
+      }
+      // the gradient MMAs of tile it-1 read sP/sS: wait for them, drain their
+      // dQ^T, then publish P/dS(it)
+      if (it > 0) drain_dq(it - 1);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int chunk = half * 4 + cc;
+        *reinterpret_cast<uint4*>(sP + sw_off64(r, chunk)) =
+            make_uint4(pw[cc * 4], pw[cc * 4 + 1], pw[cc * 4 + 2], pw[cc * 4 + 3]);
+        *reinterpret_cast<uint4*>(sS + sw_off64(r, chunk)) =
+            make_uint4(dw[cc * 4], dw[cc * 4 + 1], dw[cc * 4 + 2], dw[cc * 4 + 3]);
+      }
+      ptx::fence_proxy_async();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_ready);
+      if (it + 1 < niter) load_cols(it + 1);
+      bar_sync_softmax();  // next tile's column data visible
+    }
+    if (niter > 0) drain_dq(niter - 1);
+    if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // ---- dK (scaled), dV rows -> bf16 (each thread: 64 of the 128 d columns)
+    const bool ok = key < p.N;
+    bf16* dkr = p.dk + int64_t(ok ? key : 0) * p.lddk + int64_t(kh) * D;
+    bf16* dvr = p.dv + int64_t(ok ? key : 0) * p.lddv + int64_t(kh) * D;
+#pragma unroll 1
+    for (int c = half * 2; c < half * 2 + 2; ++c) {
+      uint32_t a[32], b[32];
+      ptx::tmem_ld32(TDK + lane_off + c * 32, a);
+      ptx::tmem_ld32(TDV + lane_off + c * 32, b);
+      ptx::tmem_wait_ld();
+      if (ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 ka, va;
+          uint32_t* kp = reinterpret_cast<uint32_t*>(&ka);
+          uint32_t* vp = reinterpret_cast<uint32_t*>(&va);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float k0f = niter ? __uint_as_float(a[q * 8 + 2 * e]) * p.scale : 0.f;
+            const float k1f = niter ? __uint_as_float(a[q * 8 + 2 * e + 1]) * p.scale : 0.f;
+            const float v0f = niter ? __uint_as_float(b[q * 8 + 2 * e]) : 0.f;
+            const float v1f = niter ? __uint_as_float(b[q * 8 + 2 * e + 1]) : 0.f;
+            kp[e] = ptx::pack_bf16(k0f, k1f);
+            vp[e] = ptx::pack_bf16(v0f, v1f);
+          }
+          *reinterpret_cast<uint4*>(dkr + c * 32 + q * 8) = ka;
+          *reinterpret_cast<uint4*>(dvr + c * 32 + q * 8) = va;
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
+// delta[h, t] = sum_d dO[t,h,d] * O[t,h,d]   (one warp per (t, h))
+__global__ void delta_kernel(const bf16* __restrict__ dout, int64_t lddo, const bf16* __restrict__ o,
+                             int64_t ldo, float* __restrict__ delta, int N, int hq) {
+  const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= int64_t(N) * hq) return;
+  const int tok = int(w / hq), h = int(w % hq);
+  const uint2 x = *reinterpret_cast<const uint2*>(dout + int64_t(tok) * lddo + h * D + lane * 4);
+  const uint2 y = *reinterpret_cast<const uint2*>(o + int64_t(tok) * ldo + h * D + lane * 4);
+  const float2 x0 = ptx::unpack_bf16(x.x), x1 = ptx::unpack_bf16(x.y);
+  const float2 y0 = ptx::unpack_bf16(y.x), y1 = ptx::unpack_bf16(y.y);
+  float s = x0.x * y0.x + x0.y * y0.y + x1.x * y1.x + x1.y * y1.y;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) delta[int64_t(h) * N + tok] = s;
+}
+
+}  // namespace
+
+// dq_acc must be a dense [N, hq, 128] fp32 buffer (it is zeroed here).
+cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
+  if (a.N <= 0) return cudaSuccess;
+  if (a.hq % a.hk) return cudaErrorInvalidValue;
+  CUtensorMap mq, mk, mv, mdo, mdq;
+  if (!head_map(&mq, a.q, a.N, a.hq, a.ldq, BQ) || !head_map(&mk, a.k, a.N, a.hk, a.ldk, BK) ||
+      !head_map(&mv, a.v, a.N, a.hk, a.ldv, BK) || !head_map(&mdo, a.dout, a.N, a.hq, a.lddo, BQ) ||
+      !head_map_f32(&mdq, a.dq_acc, a.N, a.hq, BQ))
+    return cudaErrorInvalidValue;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    cfg = true;
+  }
+  const int64_t warps = int64_t(a.N) * a.hq;
+  ++g_kernel_launches;
+  delta_kernel<<<int((warps * 32 + 255) / 256), 256, 0, s>>>(a.dout, a.lddo, a.o, a.ldo, a.delta, a.N, a.hq);
+  cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(a.N) * a.hq * D * sizeof(float), s);
+  if (e != cudaSuccess) return e;
+  Params p;
+  p.lse = a.lse;
+  p.delta = a.delta;
+  p.dk = a.dk;
+  p.dv = a.dv;
+  p.lddk = a.lddk;
+  p.lddv = a.lddv;
+  p.seq_start = a.seq_start;
+  p.seq_end = a.seq_end;
+  p.N = a.N;
+  p.hq = a.hq;
+  p.hk = a.hk;
+  p.scale = a.scale;
+  p.scale_log2 = a.scale * LOG2E;
+  p.skip_dq = getenv("OPX_DEBUG_SKIP_DQ") != nullptr;
+  dim3 grid((a.N + BK - 1) / BK, a.hk);
+  ++g_kernel_launches;
+  attn_bwd_tc_kernel<<<grid, THREADS, SMEM, s>>>(mq, mk, mv, mdo, mdq, p);
+  return cudaGetLastError();
+}
+
+}  // namespace opx

@@ -1,0 +1,75 @@
+// Shared pieces of the tcgen05 attention kernels: UMMA descriptors for the
+// [rows][128] bf16 tiles (two 64-column SW128 blocks), the matching smem
+// swizzle, and 3-D TMA maps over the [tokens, heads, 128] Ulysses layout.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "ptx.cuh"
+
+namespace opx {
+namespace attn {
+
+static __device__ __forceinline__ uint64_t kdesc(uint32_t base, int k) {
+  // K-major SW128 operand of a [128][128] tile stored as two 64-col blocks
+  return ptx::umma_desc_sw128(base + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+}
+static __device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) {
+  // MN-major SW128 operand: K rows of 128 B, the two 64-element MN chunks 16 KB apart
+  return ptx::umma_desc_sw128(base + k * 2048, 16384, 1024);
+}
+// byte offset of 16-B chunk c (0..15) of row r in a [128][128] bf16 SW128 tile
+static __device__ __forceinline__ uint32_t sw_off(int r, int c) {
+  return (c >> 3) * 16384 + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
+
+
+// byte offset of 16-B chunk c (0..7) of row r in a [rows][64] bf16 SW128 tile
+static __device__ __forceinline__ uint32_t sw_off64(int r, int c) {
+  return r * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
+
+static inline PFN_cuTensorMapEncodeTiled_v12000 enc_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// [tokens, heads, 128] bf16 with token stride ld (elements) -> box {64, 1, 128}
+static inline bool head_map(CUtensorMap* m, const void* base, int N, int heads, int64_t ld, int rows = 128) {
+  auto enc = enc_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {128, cuuint64_t(heads), cuuint64_t(N)};
+  cuuint64_t strides[2] = {256, cuuint64_t(ld) * 2};
+  cuuint32_t box[3] = {64, 1, uint32_t(rows)};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+
+// fp32 [tokens, heads, 128] map for bulk reduce-add of dQ: box {128, 1, rows}, no swizzle
+static inline bool head_map_f32(CUtensorMap* m, const void* base, int N, int heads, int rows) {
+  auto enc = enc_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {128, cuuint64_t(heads), cuuint64_t(N)};
+  cuuint64_t strides[2] = {512, cuuint64_t(heads) * 512};
+  cuuint32_t box[3] = {128, 1, uint32_t(rows)};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace attn
+}  // namespace opx

@@ -48,6 +48,7 @@ struct KParams {
   const int* g_rows;   // [groups] rows in each segment (padded to a multiple of 128 for grouped_k)
   int64_t g_b_rows;    // rows of B per group slab (B row coordinate offset = g * g_b_rows)
   int64_t g_d_stride;  // element offset of D between groups (grouped_k only)
+  int band;            // plain GEMMs: n-blocks per raster band (L2 reuse, chosen on host)
 };
 
 struct TileCoord {
@@ -62,11 +63,15 @@ __device__ __forceinline__ TileCoord tile_of(const KParams& p, int t) {
   TileCoord c{};
   const int nblk = (p.N + BN - 1) / BN;
   if (p.groups == 0) {
+    // raster: bands of `band` n-blocks; m-blocks walk inside a band, n fastest
     const int mblk = (p.M + BM - 1) / BM;
     c.valid = t < mblk * nblk;
+    const int per_band = p.band * mblk;
+    const int b = t / per_band, r = t % per_band;
+    const int bw = min(p.band, nblk - b * p.band);
     c.g = 0;
-    c.mb = t % mblk;
-    c.nb = t / mblk;
+    c.mb = r / bw;
+    c.nb = b * p.band + r % bw;
     c.m0 = c.mb * BM;
     c.k_begin = 0;
     c.nk = (p.K + BK - 1) / BK;
@@ -122,9 +127,10 @@ template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const KParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1024-B alignment by pointer arithmetic on the __shared__ array keeps the
+  // shared address space (no generic LD/ST on the hot path).
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
@@ -461,6 +467,30 @@ cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s) {
 
   int tiles;
   const int nblk = (g.N + BN - 1) / BN;
+  kp.band = 1;
+  if (!grouped) {
+    // Pick the raster band minimising a DRAM-traffic estimate: inside a band
+    // the (band x 256)-row B panel should stay L2-resident while every m-block
+    // streams its A panel once per band.
+    const double a_bytes = double(g.M) * g.K * 2, b_blk = 256.0 * g.K * 2;
+    const int mblk = (g.M + BM - 1) / BM;
+    const double budget = 80e6, wave = num_sms();
+    double best = 1e300;
+    for (int nb = 1;; nb = nb * 2 > nblk ? nblk : nb * 2) {
+      const double bands = double((nblk + nb - 1) / nb);
+      double b_traffic = double(nblk) * b_blk;
+      if (nb * b_blk > budget) {
+        const double m_per_wave = wave / nb < 1 ? 1 : wave / nb;
+        b_traffic *= double(mblk) / m_per_wave;
+      }
+      const double tot = a_bytes * bands + b_traffic;
+      if (tot < best * 0.999) {
+        best = tot;
+        kp.band = nb;
+      }
+      if (nb == nblk) break;
+    }
+  }
   if (!grouped)
     tiles = ((g.M + BM - 1) / BM) * nblk;
   else if (g.grouped_k)

@@ -1,0 +1,477 @@
+// MoE expert parallelism (VeOmni EP plan; omniplan
+// build_moe_block step_graph.cpp:253-293, ep_groups plan.cpp:168-182).
+//
+// Routing contract (bit-exact with the CPU oracle given identical inputs):
+//   * router logits in fp32 with a fixed sequential K order and separately
+//     rounded multiply/add (no FMA contraction);
+//   * top-k on the logits (softmax is monotone), ties -> lower expert index;
+//   * weights = softmax renormalised over the selected experts (Qwen3 norm_topk_prob);
+//   * permutation = stable counting sort of (token, slot) pairs by expert.
+// EP data movement is written as peer stores into the expert ranks' receive
+// buffers (CUDA-IPC mappings), laid out as per-local-expert segments padded to
+// 128 rows (so grouped-GEMM M tiles never straddle experts and wgrad K blocks
+// read zeros), ordered by source rank then by the source's pair order.
+#include <cuda_bf16.h>
+
+#include "../runtime/kernels_api.h"
+#include "ptx.cuh"
+
+namespace opx {
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+// ---------------------------------------------------------------------------
+// router logits: logits[t, e] = sum_k h[t,k] * w[e,k], k ascending, fmul/fadd rn
+// block: 128 experts x 16 tokens; K staged through smem in chunks of 64
+// ---------------------------------------------------------------------------
+constexpr int RT = 16, RK = 64;
+__global__ void __launch_bounds__(128) router_kernel(const bf16* __restrict__ h,
+                                                     const bf16* __restrict__ w,
+                                                     float* __restrict__ logits, int T, int H,
+                                                     int E) {
+  __shared__ float sh[RT][RK];
+  __shared__ float sw[128][RK + 1];
+  const int t0 = blockIdx.x * RT;
+  const int e0 = blockIdx.y * 128;
+  const int e = e0 + threadIdx.x;
+  float acc[RT];
+#pragma unroll
+  for (int i = 0; i < RT; ++i) acc[i] = 0.f;
+  for (int k0 = 0; k0 < H; k0 += RK) {
+    for (int i = threadIdx.x; i < RT * RK; i += 128) {
+      const int tt = i / RK, kk = i % RK;
+      const int t = t0 + tt;
+      sh[tt][kk] = t < T ? __bfloat162float(h[int64_t(t) * H + k0 + kk]) : 0.f;
+    }
+    for (int i = threadIdx.x; i < 128 * RK; i += 128) {
+      const int ee = i / RK, kk = i % RK;
+      sw[ee][kk] = (e0 + ee) < E ? __bfloat162float(w[int64_t(e0 + ee) * H + k0 + kk]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < RK; ++kk) {
+      const float wv = sw[threadIdx.x][kk];
+#pragma unroll
+      for (int tt = 0; tt < RT; ++tt) acc[tt] = __fadd_rn(acc[tt], __fmul_rn(sh[tt][kk], wv));
+    }
+    __syncthreads();
+  }
+  if (e < E)
+#pragma unroll
+    for (int tt = 0; tt < RT; ++tt)
+      if (t0 + tt < T) logits[int64_t(t0 + tt) * E + e] = acc[tt];
+}
+
+// top-k per token (one warp per token), E <= 256, k <= 16
+__global__ void topk_kernel(const float* __restrict__ logits, int T, int E, int k,
+                            int* __restrict__ idx, float* __restrict__ wts) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  float v[8];
+  const int per = (E + 31) / 32;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = (i < per && e < E) ? logits[int64_t(t) * E + e] : -INFINITY;
+  }
+  float sel[16];
+  int seli[16];
+  for (int j = 0; j < k; ++j) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      if (v[i] > bv || (v[i] == bv && e < bi)) {
+        bv = v[i];
+        bi = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    sel[j] = bv;
+    seli[j] = bi;
+    if ((bi & 31) == lane) v[bi >> 5] = -INFINITY;  // remove the winner
+  }
+  if (lane == 0) {
+    float s = 0.f;
+    for (int j = 0; j < k; ++j) s += expf(sel[j] - sel[0]);
+    for (int j = 0; j < k; ++j) {
+      idx[int64_t(t) * k + j] = seli[j];
+      wts[int64_t(t) * k + j] = expf(sel[j] - sel[0]) / s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// stable counting sort of pairs p = t*k + j by expert idx[p]
+// pass 1: per-chunk histograms; pass 2: per-expert exclusive scan over chunks
+// (+ expert offsets); pass 3: each chunk assigns positions in pair order.
+// ---------------------------------------------------------------------------
+constexpr int CHUNK = 1024;
+__global__ void hist_kernel(const int* __restrict__ idx, int P, int E, int* __restrict__ hist) {
+  extern __shared__ int sh_hist[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) sh_hist[e] = 0;
+  __syncthreads();
+  const int p0 = blockIdx.x * CHUNK;
+  for (int p = p0 + threadIdx.x; p < min(p0 + CHUNK, P); p += blockDim.x)
+    atomicAdd(&sh_hist[idx[p]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[int64_t(blockIdx.x) * E + e] = sh_hist[e];
+}
+
+// one thread per expert: chunk offsets (in place) and totals; then one block scan
+__global__ void scan_kernel(int* __restrict__ hist, int nchunks, int E, int* __restrict__ counts,
+                            int* __restrict__ excl) {
+  const int e = threadIdx.x;
+  __shared__ int tot[1024];
+  if (e < E) {
+    int run = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int v = hist[int64_t(c) * E + e];
+      hist[int64_t(c) * E + e] = run;
+      run += v;
+    }
+    counts[e] = run;
+    tot[e] = run;
+  }
+  __syncthreads();
+  if (e == 0) {
+    int run = 0;
+    for (int i = 0; i < E; ++i) {
+      excl[i] = run;
+      run += tot[i];
+    }
+  }
+}
+
+__global__ void place_kernel(const int* __restrict__ idx, int P, int E, const int* __restrict__ hist,
+                             const int* __restrict__ excl, int* __restrict__ pos_of_pair,
+                             int* __restrict__ pair_at) {
+  extern __shared__ int run[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    run[e] = excl[e] + hist[int64_t(blockIdx.x) * E + e];
+  __syncthreads();
+  // one warp walks the chunk in order, 32 pairs at a time
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int p0 = blockIdx.x * CHUNK;
+    for (int base = p0; base < min(p0 + CHUNK, P); base += 32) {
+      const int p = base + lane;
+      const bool ok = p < P;
+      const int e = ok ? idx[p] : -1 - lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      const int rank_in = __popc(peers & ((1u << lane) - 1));
+      const int leader = __ffs(peers) - 1;
+      int basepos = 0;
+      if (ok && lane == leader) basepos = run[e];
+      basepos = __shfl_sync(0xffffffffu, basepos, leader);
+      if (ok) {
+        const int pos = basepos + rank_in;
+        pos_of_pair[p] = pos;
+        pair_at[pos] = p;
+      }
+      __syncwarp();
+      if (ok && lane == leader) run[e] = basepos + __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// EP layout helpers.  counts_all[s*E + e] = pairs source rank s routes to
+// expert e (every EP rank holds the full matrix after the count exchange).
+// Destination rank d owns experts [d*El, (d+1)*El).
+// ---------------------------------------------------------------------------
+struct Layout {
+  int ep, E, El;
+};
+
+__device__ __forceinline__ int seg_len(const int* counts_all, const Layout& L, int e) {
+  int n = 0;
+  for (int s = 0; s < L.ep; ++s) n += counts_all[s * L.E + e];
+  return n;
+}
+
+// segment starts of rank d's local experts (128-row padded), computed into smem by one warp
+__device__ void seg_starts(const int* counts_all, const Layout& L, int d, int* out /*[El+1]*/) {
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int le = 0; le < L.El; ++le) {
+      out[le] = run;
+      run += (seg_len(counts_all, L, d * L.El + le) + 127) / 128 * 128;
+    }
+    out[L.El] = run;
+  }
+}
+
+// g_start/g_rows (valid rows and 128-padded rows) of this rank's local experts
+__global__ void groups_kernel(const int* __restrict__ counts_all, Layout L, int me,
+                              int* __restrict__ g_start, int* __restrict__ g_rows,
+                              int* __restrict__ g_rows_pad, int* __restrict__ total_rows) {
+  __shared__ int st[1025];
+  seg_starts(counts_all, L, me, st);
+  __syncthreads();
+  for (int le = threadIdx.x; le < L.El; le += blockDim.x) {
+    g_start[le] = st[le];
+    g_rows[le] = seg_len(counts_all, L, me * L.El + le);
+    g_rows_pad[le] = st[le + 1] - st[le];
+  }
+  if (threadIdx.x == 0) *total_rows = st[L.El];
+}
+
+// Zero the padding rows of every local segment of a [rows, W] bf16 buffer.
+__global__ void zero_pad_kernel(bf16* __restrict__ buf, int64_t ld, int W,
+                                const int* __restrict__ g_start, const int* __restrict__ g_rows,
+                                const int* __restrict__ g_rows_pad, int El) {
+  const int le = blockIdx.y;
+  if (le >= El) return;
+  const int r0 = g_start[le] + g_rows[le], r1 = g_start[le] + g_rows_pad[le];
+  const int n8 = W / 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (r1 - r0) * n8; i += gridDim.x * blockDim.x) {
+    const int r = r0 + i / n8, c = (i % n8) * 8;
+    *reinterpret_cast<uint4*>(buf + int64_t(r) * ld + c) = make_uint4(0, 0, 0, 0);
+  }
+}
+
+// Dispatch: for every pair in this rank's sorted order, copy its token row
+// (src row = pair / k, or the pair row itself when per_pair) to the expert
+// rank's receive buffer.  One warp per pair, 16 B per lane.
+__global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, int per_pair,
+                                const int* __restrict__ pair_at, int P, int k,
+                                const int* __restrict__ counts_all, const int* __restrict__ excl,
+                                Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst,
+                                int W) {
+  extern __shared__ int st[];  // [ep][El+1] segment starts of every destination rank
+  if (threadIdx.x < L.ep) {
+    const int d = threadIdx.x;
+    int run = 0;
+    for (int le = 0; le < L.El; ++le) {
+      st[d * (L.El + 1) + le] = run;
+      run += (seg_len(counts_all, L, d * L.El + le) + 127) / 128 * 128;
+    }
+    st[d * (L.El + 1) + L.El] = run;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int pos = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pos < P;
+       pos += (gridDim.x * blockDim.x) >> 5) {
+    const int p = pair_at[pos];
+    // expert of this sorted position: largest e with excl[e] <= pos (E <= 1024)
+    int lo = 0, hi = L.E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (excl[mid] <= pos) lo = mid; else hi = mid - 1;
+    }
+    const int e = lo;
+    const int d = e / L.El, le = e % L.El;
+    int before = 0;
+    for (int s = 0; s < me; ++s) before += counts_all[s * L.E + e];
+    const int row = st[d * (L.El + 1) + le] + before + (pos - excl[e]);
+    const bf16* s = src + int64_t(per_pair ? pos : p / k) * ld_src;
+    bf16* o = dst[d] + int64_t(row) * ld_dst;
+    for (int c = lane * 8; c < W; c += 256)
+      *reinterpret_cast<uint4*>(o + c) = *reinterpret_cast<const uint4*>(s + c);
+  }
+}
+
+// Combine: every valid row of this rank's receive buffer goes back to its
+// source rank, at the source's sorted position of that pair.
+__global__ void combine_kernel(const bf16* __restrict__ src, int64_t ld_src,
+                               const int* __restrict__ counts_all, Layout L, int me,
+                               const int* __restrict__ g_start, bf16* const* __restrict__ dst,
+                               int64_t ld_dst, int W) {
+  const int lane = threadIdx.x & 31;
+  const int le = blockIdx.y;
+  const int e = me * L.El + le;
+  const int n = seg_len(counts_all, L, e);
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+    int s = 0, off = r;
+    while (off >= counts_all[s * L.E + e]) off -= counts_all[s * L.E + e], ++s;
+    int excl_src = 0;  // source s's sorted offset of expert e
+    for (int e2 = 0; e2 < e; ++e2) excl_src += counts_all[s * L.E + e2];
+    const bf16* a = src + int64_t(g_start[le] + r) * ld_src;
+    bf16* o = dst[s] + int64_t(excl_src + off) * ld_dst;
+    for (int c = lane * 8; c < W; c += 256)
+      *reinterpret_cast<uint4*>(o + c) = *reinterpret_cast<const uint4*>(a + c);
+  }
+}
+
+// out[t] = resid[t] + sum_j w[t,j] * Y[pos(t,j)]  (fp32; one warp per token)
+__global__ void unpermute_kernel(const bf16* __restrict__ Y, int64_t ldy, const int* __restrict__ pos_of_pair,
+                                 const float* __restrict__ wts, int T, int k, int H,
+                                 const float* resid, float* out) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  for (int c = lane * 4; c < H; c += 128) {
+    float4 acc = resid ? *reinterpret_cast<const float4*>(resid + int64_t(t) * H + c)
+                       : make_float4(0, 0, 0, 0);
+    for (int j = 0; j < k; ++j) {
+      const int pos = pos_of_pair[t * k + j];
+      const float wj = wts ? wts[t * k + j] : 1.f;
+      const uint2 q = *reinterpret_cast<const uint2*>(Y + int64_t(pos) * ldy + c);
+      const float2 a = ptx::unpack_bf16(q.x), b = ptx::unpack_bf16(q.y);
+      acc.x += wj * a.x;
+      acc.y += wj * a.y;
+      acc.z += wj * b.x;
+      acc.w += wj * b.y;
+    }
+    *reinterpret_cast<float4*>(out + int64_t(t) * H + c) = acc;
+  }
+}
+
+// backward of the weighted combine:
+//   dYp[pos(t,j)] = bf16(w[t,j] * dx[t]);  dw[t,j] = <dx[t], Y[pos(t,j)]>
+__global__ void combine_bwd_kernel(const float* __restrict__ dx, const bf16* __restrict__ Y, int64_t ldy,
+                                   const int* __restrict__ pos_of_pair, const float* __restrict__ wts,
+                                   int T, int k, int H, bf16* __restrict__ dYp, float* __restrict__ dw) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  for (int j = 0; j < k; ++j) {
+    const int pos = pos_of_pair[t * k + j];
+    const float wj = wts[t * k + j];
+    float dot = 0.f;
+    for (int c = lane * 4; c < H; c += 128) {
+      const float4 g = *reinterpret_cast<const float4*>(dx + int64_t(t) * H + c);
+      const uint2 q = *reinterpret_cast<const uint2*>(Y + int64_t(pos) * ldy + c);
+      const float2 a = ptx::unpack_bf16(q.x), b = ptx::unpack_bf16(q.y);
+      dot += g.x * a.x + g.y * a.y + g.z * b.x + g.w * b.y;
+      uint2 o;
+      o.x = ptx::pack_bf16(wj * g.x, wj * g.y);
+      o.y = ptx::pack_bf16(wj * g.z, wj * g.w);
+      *reinterpret_cast<uint2*>(dYp + int64_t(pos) * ldy + c) = o;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) dw[t * k + j] = dot;
+  }
+}
+
+// router backward (renormalised softmax over the selected experts):
+//   dsel_j = w_j (dw_j - sum_i w_i dw_i);  dlogits[t, idx_j] = dsel_j, else 0 (bf16)
+__global__ void router_bwd_kernel(const float* __restrict__ dw, const float* __restrict__ wts,
+                                  const int* __restrict__ idx, int T, int k, int E,
+                                  bf16* __restrict__ dlogits) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  bf16* row = dlogits + int64_t(t) * E;
+  for (int e = 0; e < E; ++e) row[e] = __float2bfloat16_rn(0.f);
+  float s = 0.f;
+  for (int j = 0; j < k; ++j) s += wts[t * k + j] * dw[t * k + j];
+  for (int j = 0; j < k; ++j)
+    row[idx[t * k + j]] = __float2bfloat16_rn(wts[t * k + j] * (dw[t * k + j] - s));
+}
+
+}  // namespace
+
+cudaError_t k_moe_router(const __nv_bfloat16* h, const __nv_bfloat16* w, float* logits, int T,
+                         int H, int E, cudaStream_t s) {
+  if (H % RK) return cudaErrorInvalidValue;
+  dim3 grid((T + RT - 1) / RT, (E + 127) / 128);
+  ++g_kernel_launches;
+  router_kernel<<<grid, 128, 0, s>>>(h, w, logits, T, H, E);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_topk(const float* logits, int T, int E, int k, int* idx, float* wts,
+                       cudaStream_t s) {
+  if (E > 256 || k > 16 || k > E) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  topk_kernel<<<(T * 32 + 255) / 256, 256, 0, s>>>(logits, T, E, k, idx, wts);
+  return cudaGetLastError();
+}
+
+int k_moe_sort_chunks(int P) { return (P + CHUNK - 1) / CHUNK; }
+
+cudaError_t k_moe_sort(const int* idx, int P, int E, int* hist, int* counts, int* excl,
+                       int* pos_of_pair, int* pair_at, cudaStream_t s) {
+  if (E > 1024) return cudaErrorInvalidValue;
+  const int nc = k_moe_sort_chunks(P);
+  g_kernel_launches += 3;
+  hist_kernel<<<nc, 256, E * sizeof(int), s>>>(idx, P, E, hist);
+  scan_kernel<<<1, 1024, 0, s>>>(hist, nc, E, counts, excl);
+  place_kernel<<<nc, 64, E * sizeof(int), s>>>(idx, P, E, hist, excl, pos_of_pair, pair_at);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_groups(const int* counts_all, int ep, int E, int me, int* g_start, int* g_rows,
+                         int* g_rows_pad, int* total_rows, cudaStream_t s) {
+  Layout L{ep, E, E / ep};
+  if (L.El > 1024) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  groups_kernel<<<1, 128, 0, s>>>(counts_all, L, me, g_start, g_rows, g_rows_pad, total_rows);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_zero_pad(__nv_bfloat16* buf, int64_t ld, int W, const int* g_start,
+                           const int* g_rows, const int* g_rows_pad, int El, cudaStream_t s) {
+  dim3 grid(8, El);
+  ++g_kernel_launches;
+  zero_pad_kernel<<<grid, 256, 0, s>>>(buf, ld, W, g_start, g_rows, g_rows_pad, El);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pair,
+                           const int* pair_at, int P, int k, const int* counts_all,
+                           const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
+                           int64_t ld_dst, int W, cudaStream_t s) {
+  Layout L{ep, E, E / ep};
+  const int smem = ep * (L.El + 1) * int(sizeof(int));
+  int blocks = (P * 32 + 255) / 256;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  if (blocks < 1) blocks = 1;
+  ++g_kernel_launches;
+  dispatch_kernel<<<blocks, 256, smem, s>>>(src, ld_src, per_pair, pair_at, P, k, counts_all,
+                                            excl, L, me, dst, ld_dst, W);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* counts_all, int ep,
+                          int E, int me, const int* g_start, __nv_bfloat16* const* dst,
+                          int64_t ld_dst, int W, int max_rows, cudaStream_t s) {
+  Layout L{ep, E, E / ep};
+  int bx = (max_rows * 32 + 255) / 256 / L.El + 1;
+  if (bx > 64) bx = 64;
+  dim3 grid(bx, L.El);
+  ++g_kernel_launches;
+  combine_kernel<<<grid, 256, 0, s>>>(src, ld_src, counts_all, L, me, g_start, dst, ld_dst, W);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_of_pair,
+                            const float* wts, int T, int k, int H, const float* resid, float* out,
+                            cudaStream_t s) {
+  if (H % 128) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  unpermute_kernel<<<(T * 32 + 255) / 256, 256, 0, s>>>(Y, ldy, pos_of_pair, wts, T, k, H, resid, out);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t ldy,
+                              const int* pos_of_pair, const float* wts, int T, int k, int H,
+                              __nv_bfloat16* dYp, float* dw, cudaStream_t s) {
+  if (H % 128) return cudaErrorInvalidValue;
+  ++g_kernel_launches;
+  combine_bwd_kernel<<<(T * 32 + 255) / 256, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, int T, int k, int E,
+                             __nv_bfloat16* dlogits, cudaStream_t s) {
+  ++g_kernel_launches;
+  router_bwd_kernel<<<(T + 127) / 128, 128, 0, s>>>(dw, wts, idx, T, k, E, dlogits);
+  return cudaGetLastError();
+}
+
+}  // namespace opx

@@ -93,3 +93,33 @@ cudaError_t k_peer_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int 
                            uint32_t epoch, int* timeout_flag, cudaStream_t s);
 
 }  // namespace opx
+
+namespace opx {
+// moe.cu — routing, permutation and EP exchange (see the file header).
+cudaError_t k_moe_router(const __nv_bfloat16* h, const __nv_bfloat16* w, float* logits, int T,
+                         int H, int E, cudaStream_t s);
+cudaError_t k_moe_topk(const float* logits, int T, int E, int k, int* idx, float* wts,
+                       cudaStream_t s);
+int k_moe_sort_chunks(int P);
+cudaError_t k_moe_sort(const int* idx, int P, int E, int* hist, int* counts, int* excl,
+                       int* pos_of_pair, int* pair_at, cudaStream_t s);
+cudaError_t k_moe_groups(const int* counts_all, int ep, int E, int me, int* g_start, int* g_rows,
+                         int* g_rows_pad, int* total_rows, cudaStream_t s);
+cudaError_t k_moe_zero_pad(__nv_bfloat16* buf, int64_t ld, int W, const int* g_start,
+                           const int* g_rows, const int* g_rows_pad, int El, cudaStream_t s);
+cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pair,
+                           const int* pair_at, int P, int k, const int* counts_all,
+                           const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
+                           int64_t ld_dst, int W, cudaStream_t s);
+cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* counts_all, int ep,
+                          int E, int me, const int* g_start, __nv_bfloat16* const* dst,
+                          int64_t ld_dst, int W, int max_rows, cudaStream_t s);
+cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_of_pair,
+                            const float* wts, int T, int k, int H, const float* resid, float* out,
+                            cudaStream_t s);
+cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t ldy,
+                              const int* pos_of_pair, const float* wts, int T, int k, int H,
+                              __nv_bfloat16* dYp, float* dw, cudaStream_t s);
+cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, int T, int k, int E,
+                             __nv_bfloat16* dlogits, cudaStream_t s);
+}  // namespace opx

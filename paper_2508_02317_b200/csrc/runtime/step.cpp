@@ -558,7 +558,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& 
     a.hq = hql_;
     a.hk = hkl_;
     a.scale = 1.0f / std::sqrt(128.0f);
-    CU(k_attn_fwd(a, cs_));
+    CU(k_attn_fwd_tc(a, cs_));
   }
   if (tr) {
     e1 = ev();
@@ -720,7 +720,7 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     a.dv = dv_;
     a.lddk = a.lddv = hkl_ * 128;
     a.delta = delta_;
-    CU(k_attn_bwd(a, cs_));
+    CU(k_attn_bwd_tc(a, cs_));
   }
   if (tr) {
     e1 = ev();

@@ -375,7 +375,7 @@ def test_attention_bwd_tc(N, lens, hq, hk):
     scale = 1 / math.sqrt(128)
     qr, kr, vr = (t.float().clone().requires_grad_(True) for t in (q, k, v))
     o_ref, lse_ref = _attn_ref(qr, kr, vr, st, hq, hk)
-    o = bf(o_ref.detach())
+    o = bf(o_ref.detach()).contiguous()
     lse = lse_ref.detach().contiguous()
     do = bf(torch.randn(N, hq, 128, device=DEV))
     o_ref.backward(do.float())
