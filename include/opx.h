@@ -156,6 +156,19 @@ int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void*
                   int hq, int hk, int rows, int S, const int32_t* pos, const float* inv_freq,
                   void* stream);
 
+/* MoE routing (moe.cu): fp32 router logits with a fixed sequential K order and
+ * separately rounded multiply/add, top-k with lower-index tie break, weights =
+ * softmax renormalised over the selected experts (Qwen3 norm_topk_prob). */
+int opx_moe_route(const void* h, const void* w_router, int T, int H, int E, int k,
+                  float* logits, int32_t* topk_idx, float* topk_w, void* stream);
+/* Stable counting sort of the T*k (token, slot) pairs by expert: pos_of_pair[p]
+ * is the sorted position of pair p = t*k + j, pair_at[pos] its inverse,
+ * counts/excl the per-expert counts and exclusive offsets.  hist needs
+ * opx_moe_sort_chunks(P) * E ints of scratch. */
+int opx_moe_sort_chunks(int P);
+int opx_moe_sort(const int32_t* topk_idx, int P, int E, int32_t* hist, int32_t* counts,
+                 int32_t* excl, int32_t* pos_of_pair, int32_t* pair_at, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -373,6 +373,58 @@ __global__ void router_bwd_kernel(const float* __restrict__ dw, const float* __r
     row[idx[t * k + j]] = __float2bfloat16_rn(wts[t * k + j] * (dw[t * k + j] - s));
 }
 
+// every EP rank receives this rank's per-expert counts as row `me` of its table
+__global__ void publish_counts_kernel(const int* __restrict__ counts, int* const* __restrict__ tables,
+                                      int ep, int me, int E) {
+  for (int i = threadIdx.x; i < ep * E; i += blockDim.x) {
+    const int j = i / E, e = i % E;
+    tables[j][me * E + e] = counts[e];
+  }
+}
+
+// SwiGLU backward over the valid rows of every local expert segment; the
+// 128-row padding of each segment is written as zeros (it feeds grouped wgrad).
+__global__ void swiglu_bwd_grouped_kernel(const bf16* __restrict__ dact, const bf16* __restrict__ gu,
+                                          bf16* __restrict__ dgu, const int* __restrict__ g_start,
+                                          const int* __restrict__ g_rows,
+                                          const int* __restrict__ g_rows_pad, int F) {
+  const int le = blockIdx.y;
+  const int r0 = g_start[le], nv = g_rows[le], np = g_rows_pad[le];
+  const int n8 = F / 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np * n8; i += gridDim.x * blockDim.x) {
+    const int64_t row = r0 + i / n8;
+    const int f = (i % n8) * 8;
+    const int64_t gcol = int64_t(f / 128) * 256 + f % 128;
+    if (i / n8 >= nv) {
+      *reinterpret_cast<uint4*>(dgu + row * 2 * F + gcol) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(dgu + row * 2 * F + gcol + 128) = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4 da = *reinterpret_cast<const uint4*>(dact + row * F + f);
+    const uint4 gq = *reinterpret_cast<const uint4*>(gu + row * 2 * F + gcol);
+    const uint4 uq = *reinterpret_cast<const uint4*>(gu + row * 2 * F + gcol + 128);
+    const uint32_t a[4] = {da.x, da.y, da.z, da.w}, g[4] = {gq.x, gq.y, gq.z, gq.w},
+                   u[4] = {uq.x, uq.y, uq.z, uq.w};
+    uint32_t og[4], ou[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 av = ptx::unpack_bf16(a[e]), gv = ptx::unpack_bf16(g[e]), uv = ptx::unpack_bf16(u[e]);
+      const float gg[2] = {gv.x, gv.y}, uu[2] = {uv.x, uv.y}, aa[2] = {av.x, av.y};
+      float dg[2], du[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float sg = 1.f / (1.f + __expf(-gg[k]));
+        du[k] = aa[k] * gg[k] * sg;
+        dg[k] = aa[k] * uu[k] * sg * (1.f + gg[k] * (1.f - sg));
+      }
+      og[e] = ptx::pack_bf16(dg[0], dg[1]);
+      ou[e] = ptx::pack_bf16(du[0], du[1]);
+    }
+    *reinterpret_cast<uint4*>(dgu + row * 2 * F + gcol) = make_uint4(og[0], og[1], og[2], og[3]);
+    *reinterpret_cast<uint4*>(dgu + row * 2 * F + gcol + 128) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+  }
+}
+
 }  // namespace
 
 cudaError_t k_moe_router(const __nv_bfloat16* h, const __nv_bfloat16* w, float* logits, int T,
@@ -471,6 +523,25 @@ cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, 
                              __nv_bfloat16* dlogits, cudaStream_t s) {
   ++g_kernel_launches;
   router_bwd_kernel<<<(T + 127) / 128, 128, 0, s>>>(dw, wts, idx, T, k, E, dlogits);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_publish_counts(const int* counts, int* const* tables, int ep, int me, int E,
+                                 cudaStream_t s) {
+  ++g_kernel_launches;
+  publish_counts_kernel<<<1, 256, 0, s>>>(counts, tables, ep, me, E);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __nv_bfloat16* dgu,
+                             const int* g_start, const int* g_rows, const int* g_rows_pad, int El,
+                             int F, int max_rows, cudaStream_t s) {
+  if (F % 128) return cudaErrorInvalidValue;
+  int bx = (max_rows / El * (F / 8) + 255) / 256 + 1;
+  if (bx > 64) bx = 64;
+  dim3 grid(bx, El);
+  ++g_kernel_launches;
+  swiglu_bwd_grouped_kernel<<<grid, 256, 0, s>>>(dact, gu, dgu, g_start, g_rows, g_rows_pad, F);
   return cudaGetLastError();
 }
 

@@ -423,4 +423,19 @@ int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void*
   OPX_CALL(k_a2a_seq2head(a, static_cast<cudaStream_t>(stream)), "opx_rope_pack");
 }
 
+int opx_moe_route(const void* h, const void* w, int T, int H, int E, int k, float* logits,
+                  int32_t* idx, float* wts, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = k_moe_router(static_cast<const __nv_bfloat16*>(h),
+                               static_cast<const __nv_bfloat16*>(w), logits, T, H, E, s);
+  if (e != cudaSuccess) return cuda_fail(e, "opx_moe_route");
+  OPX_CALL(k_moe_topk(logits, T, E, k, idx, wts, s), "opx_moe_route");
+}
+int opx_moe_sort_chunks(int P) { return k_moe_sort_chunks(P); }
+int opx_moe_sort(const int32_t* idx, int P, int E, int32_t* hist, int32_t* counts, int32_t* excl,
+                 int32_t* pos, int32_t* pair_at, void* stream) {
+  OPX_CALL(k_moe_sort(idx, P, E, hist, counts, excl, pos, pair_at, static_cast<cudaStream_t>(stream)),
+           "opx_moe_sort");
+}
+
 }  // extern "C"

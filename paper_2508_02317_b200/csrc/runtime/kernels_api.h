@@ -120,6 +120,11 @@ cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_
 cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t ldy,
                               const int* pos_of_pair, const float* wts, int T, int k, int H,
                               __nv_bfloat16* dYp, float* dw, cudaStream_t s);
+cudaError_t k_moe_publish_counts(const int* counts, int* const* tables, int ep, int me, int E,
+                                 cudaStream_t s);
+cudaError_t k_moe_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __nv_bfloat16* dgu,
+                             const int* g_start, const int* g_rows, const int* g_rows_pad, int El,
+                             int F, int max_rows, cudaStream_t s);
 cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, int T, int k, int E,
                              __nv_bfloat16* dlogits, cudaStream_t s);
 }  // namespace opx

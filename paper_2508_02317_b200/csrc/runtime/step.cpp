@@ -49,17 +49,6 @@ int Step::nccl(ncclResult_t r, const char* what) {
 #define CU(x) TRY(check((x), #x))
 #define NC(x) TRY(nccl((x), #x))
 
-template <class T>
-T* Step::alloc(size_t n, bool zero) {
-  void* p = nullptr;
-  const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
-  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-  if (zero) cudaMemset(p, 0, bytes);
-  allocs_.push_back(p);
-  bytes_alloc_ += int64_t(bytes);
-  return static_cast<T*>(p);
-}
-
 cudaEvent_t Step::ev() {
   if (ev_next_ == ev_pool_.size()) {
     cudaEvent_t e;
@@ -85,6 +74,7 @@ Step::~Step() {
     for (auto e : *v) cudaEventDestroy(e);
   for (auto e : {ev_start_, ev_fwd_, ev_bwd_, ev_end_, ev_head_ag_, ev_head_rs_})
     if (e) cudaEventDestroy(e);
+  if (expert_comm_) ncclCommDestroy(expert_comm_);
   if (rep_comm_) ncclCommDestroy(rep_comm_);
   if (shard_comm_) ncclCommDestroy(shard_comm_);
   if (world_comm_) ncclCommDestroy(world_comm_);
@@ -111,10 +101,6 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
     return OPX_ERR_CONFIG;
   }
   a_ = *f->arch;
-  if (a_.moe) {
-    set_error("MoE layers are not supported by this executor build yet");
-    return OPX_ERR_CONFIG;
-  }
   if (a_.head_dim != 128 || a_.hidden % 128 || a_.ffn % 128) {
     set_error("executor requires head_dim == 128 and hidden, ffn multiples of 128");
     return OPX_ERR_CONFIG;
@@ -165,6 +151,13 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
   V_ = int(a_.vocab);
   nslots_ = int(std::max<int64_t>(p.prefetch_depth, 0)) + 1;
   if (nslots_ < 2) nslots_ = 2;
+  if (a_.moe) {
+    if (a_.moe->experts % 64) {
+      set_error("MoE executor requires num_experts % 64 == 0");
+      return OPX_ERR_CONFIG;
+    }
+    TRY(moe_setup_groups());
+  }
   TRY(build_units());
   TRY(alloc_acts());
   return OPX_OK;
@@ -235,9 +228,13 @@ int Step::build_units() {
     add(u, p + "self_attn.v_proj.weight", {int64_t(hk_) * 128, H}, false);
     add(u, p + "self_attn.o_proj.weight", {H, int64_t(hq_) * 128}, false);
     add(u, p + "post_attention_layernorm.weight", {H}, true);
-    add(u, p + "mlp.gate_up_proj.weight", {2 * F, H}, false, 1, p + "mlp.gate_proj.weight",
-        p + "mlp.up_proj.weight");
-    add(u, p + "mlp.down_proj.weight", {H, F}, false);
+    if (a_.is_moe_layer(l)) {
+      add(u, p + "mlp.gate.weight", {int64_t(a_.moe->experts), H}, false);
+    } else {
+      add(u, p + "mlp.gate_up_proj.weight", {2 * F, H}, false, 1, p + "mlp.gate_proj.weight",
+          p + "mlp.up_proj.weight");
+      add(u, p + "mlp.down_proj.weight", {H, F}, false);
+    }
     TRY(finish(u));
     units_.push_back(std::move(u));
   }
@@ -257,6 +254,7 @@ int Step::build_units() {
     hu.gfull = alloc<float>(size_t(hu.padded));
     if (!hu.full || !hu.gfull) return cuda_fail(cudaErrorMemoryAllocation, "head gather");
   }
+  if (moe_) TRY(moe_build_units());
   const int L = int(a_.layers);
   ev_ag_.resize(size_t(L));
   ev_use_done_.resize(size_t(L));
@@ -285,6 +283,7 @@ int Step::alloc_acts() {
     off_do_[b] = take(N * size_t(hql_) * 128 * 2);
     off_dqkv_[b] = take(T * size_t(Wqkv_) * 2);
   }
+  if (moe_) off = moe_arena(off);
   arena_bytes_ = off;
   CU(cudaMalloc(&arena_, arena_bytes_));
   CU(cudaMemset(arena_, 0, arena_bytes_));
@@ -336,6 +335,7 @@ int Step::alloc_acts() {
   for (int i = 0; i < 64; ++i)
     inv[size_t(i)] = float(1.0 / std::pow(ex_.rope_theta, double(2 * i) / 128.0));
   CU(cudaMemcpy(d_inv_freq_, inv.data(), 64 * sizeof(float), cudaMemcpyHostToDevice));
+  if (moe_) TRY(moe_alloc());
   if (p_.sp == 1) {  // no peers: flags point at ourselves
     uint32_t* f = reinterpret_cast<uint32_t*>(arena_ + off_flags_);
     CU(cudaMemcpy(d_peer_flags_, &f, sizeof(f), cudaMemcpyHostToDevice));
@@ -361,9 +361,13 @@ int Step::ipc_import(const void* all, size_t len) {
     return OPX_ERR_ARG;
   }
   const char* base = static_cast<const char*>(all);
-  // Only the SP group exchanges through peer memory.
-  for (int64_t r : sp_members_) {
-    if (r == rank_) continue;
+  // The SP group (Ulysses) and the EP group (dispatch/combine) exchange
+  // through peer memory.
+  std::vector<int64_t> peers = sp_members_;
+  for (int64_t r : ep_members_)
+    if (std::find(peers.begin(), peers.end(), r) == peers.end()) peers.push_back(r);
+  for (int64_t r : peers) {
+    if (r == rank_ || peer_arena_[size_t(r)]) continue;
     cudaIpcMemHandle_t h;
     std::memcpy(&h, base + size_t(r) * len, len);
     void* p = nullptr;
@@ -374,12 +378,18 @@ int Step::ipc_import(const void* all, size_t len) {
   for (int j = 0; j < int(p_.sp); ++j)
     flags[size_t(j)] = reinterpret_cast<uint32_t*>(peer(j, off_flags_));
   CU(cudaMemcpy(d_peer_flags_, flags.data(), kMaxSp * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  if (moe_) TRY(moe_import());
   return OPX_OK;
 }
 
 int Step::init_weights(uint64_t seed) {
   const double c = 0.02 * std::sqrt(3.0) / 16777216.0;
-  for (Unit& u : units_) {
+  std::vector<Unit*> all;
+  for (Unit& u : units_) all.push_back(&u);
+  for (Unit& u : expert_units_)
+    if (!u.params.empty()) all.push_back(&u);
+  for (Unit* up : all) {
+    Unit& u = *up;
     const int64_t sb = int64_t(u.idx) * u.shard, se = sb + u.shard;
     CU(cudaMemsetAsync(u.master, 0, size_t(u.shard) * 4, cs_));
     CU(cudaMemsetAsync(u.pshard, 0, size_t(u.shard) * 2, cs_));
@@ -391,7 +401,8 @@ int Step::init_weights(uint64_t seed) {
       if (hi <= lo) continue;
       const uint64_t ka = param_key(q.key_a, seed);
       const uint64_t kb = q.key_b.empty() ? 0 : param_key(q.key_b, seed);
-      CU(k_init_param(u.master + (lo - sb), u.pshard + (lo - sb), hi - lo, lo - q.off, ka, kb,
+      CU(k_init_param(u.master + (lo - sb), u.pshard + (lo - sb), hi - lo,
+                      lo - q.off + q.logical_offset, ka, kb,
                       q.ones ? 0.0 : c, 1.0f, q.interleave, q.rows_per_slab, q.cols, cs_));
     }
   }
@@ -464,8 +475,8 @@ LayerW layer_w(const Unit& u, const bf16* base) {
   w.qkv = base + u.params[1].off;
   w.o = base + u.params[4].off;
   w.ln2 = base + u.params[5].off;
-  w.gu = base + u.params[6].off;
-  w.down = base + u.params[7].off;
+  w.gu = u.params.size() > 7 ? base + u.params[6].off : nullptr;
+  w.down = u.params.size() > 7 ? base + u.params[7].off : nullptr;
   return w;
 }
 GemmDesc gd(int M, int N, int K, const bf16* A, int64_t lda, bool amn, const bf16* B, int64_t ldb,
@@ -602,6 +613,15 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& 
     e0 = e1;
   }
   CU(k_rmsnorm_fwd(x2_, W.ln2, h2_, r2_, T, H, ex_.rms_eps, cs_));
+  if (a_.is_moe_layer(l)) {
+    TRY(moe_fwd(l, u, expert_units_[size_t(l)], x2_, x_out));
+    if (tr) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".moe", ph, 0, e0, e1);
+    }
+    return OPX_OK;
+  }
   {
     GemmDesc g = gd(T, 2 * F, H, h2_, H, false, W.gu, H, false, GEMM_EPI_SWIGLU, gu_, 2 * F);
     g.D2 = act_;
@@ -643,10 +663,15 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
   float* g_qkv = G + u.params[1].off;
   float* g_o = G + u.params[4].off;
   float* g_ln2 = G + u.params[5].off;
-  float* g_gu = G + u.params[6].off;
-  float* g_down = G + u.params[7].off;
+  float* g_gu = u.params.size() > 7 ? G + u.params[6].off : nullptr;
+  float* g_down = u.params.size() > 7 ? G + u.params[7].off : nullptr;
 
-  // ---- MLP
+  // ---- MLP (dense) or MoE block
+  if (a_.is_moe_layer(l)) {
+    Unit& eu = expert_units_[size_t(l)];
+    TRY(moe_bwd(l, u, eu, G, eu.gfull, dtmp_));
+    CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
+  } else {
   CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
   CU(gemm_run(gd(T, F, H, dxb_, H, false, W.down, F, true, GEMM_EPI_BF16, dact_, F), cs_));
   CU(gemm_run(gd(H, F, T, dxb_, H, true, act_, F, true, GEMM_EPI_F32, g_down, F), cs_));
@@ -654,10 +679,11 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
   CU(gemm_run(gd(T, H, 2 * F, dgu_, 2 * F, false, W.gu, H, true, GEMM_EPI_F32, dtmp_, H), cs_));
   CU(gemm_run(gd(2 * F, H, T, dgu_, 2 * F, true, h2_, H, true, GEMM_EPI_F32, g_gu, H), cs_));
   CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
+  }
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
-    mark(pre + ".mlp", ph, 0, e0, e1);
+    mark(pre + (a_.is_moe_layer(l) ? ".moe" : ".mlp"), ph, 0, e0, e1);
     e0 = e1;
   }
   // ---- attention output projection
@@ -856,6 +882,11 @@ int Step::run(opx_step_report* rep) {
     if (u.P > 1) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
     if (l + nslots_ - 1 < L) TRY(issue_gather(l + nslots_ - 1, false));
     int qb, ob;
+    if (moe_ && a_.is_moe_layer(l) && De_ > 1) {
+      Unit& eu = expert_units_[size_t(l)];
+      eu.full = eslot_;
+      NC(ncclAllGather(eu.pshard, eslot_, size_t(eu.shard), ncclBfloat16, eu.comm, cs_));
+    }
     TRY(layer_fwd(l, u, x_saved_[size_t(l)], x_saved_[size_t(l + 1)], qb, ob));
     CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
   }
@@ -881,7 +912,26 @@ int Step::run(opx_step_report* rep) {
       u.gfull = gradslot_[size_t(l % 2)];
       if (l + 2 < L) CU(cudaStreamWaitEvent(cs_, ev_rs_done_[size_t(l + 2)], 0));
     }
+    if (moe_ && a_.is_moe_layer(l) && De_ > 1) {
+      Unit& eu = expert_units_[size_t(l)];
+      eu.full = eslot_;
+      eu.gfull = egrad_slot_;
+      NC(ncclAllGather(eu.pshard, eslot_, size_t(eu.shard), ncclBfloat16, eu.comm, cs_));
+    }
     TRY(layer_bwd(l, u, u.gfull));
+    if (moe_ && a_.is_moe_layer(l)) {
+      // expert grads: sum over the ranks holding the same experts, then replicas
+      Unit& eu = expert_units_[size_t(l)];
+      if (eu.P > 1) {
+        if (eu.padded > eu.numel)
+          CU(cudaMemsetAsync(eu.gfull + eu.numel, 0, size_t(eu.padded - eu.numel) * 4, cs_));
+        NC(ncclReduceScatter(eu.gfull, eu.gshard, size_t(eu.shard), ncclFloat, ncclSum, eu.comm,
+                             cs_));
+      }
+      if (eu.rep_comm)
+        NC(ncclAllReduce(eu.gshard, eu.gshard, size_t(eu.shard), ncclFloat, ncclSum,
+                         eu.rep_comm, cs_));
+    }
     CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
     if (u.P > 1 || u.rep_comm) {
       CU(cudaEventRecord(ev_grad_done_[size_t(l)], cs_));
@@ -927,6 +977,10 @@ int Step::run(opx_step_report* rep) {
   for (Unit& u : units_)
     CU(k_adamw(u.master, u.m, u.v, u.gshard, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps,
                ex_.wd, step_count_, cs_));
+  for (Unit& u : expert_units_)
+    if (!u.params.empty())
+      CU(k_adamw(u.master, u.m, u.v, u.gshard, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2,
+                 ex_.eps, ex_.wd, step_count_, cs_));
   CU(cudaEventRecord(ev_end_, cs_));
   if (tr) mark("optimizer", "optimizer", 0, ev_bwd_, ev_end_);
 
@@ -967,14 +1021,20 @@ int Step::run(opx_step_report* rep) {
 int Step::info(const std::string& full, int64_t* numel, int64_t* b, int64_t* e) {
   const size_t colon = full.find(':');
   const std::string name = colon == std::string::npos ? full : full.substr(colon + 1);
-  for (const Unit& u : units_) {
+  std::vector<const Unit*> all;
+  for (const Unit& u : units_) all.push_back(&u);
+  for (const Unit& u : expert_units_) all.push_back(&u);
+  for (const Unit* up : all) {
+    const Unit& u = *up;
     const Param* q = u.find(name);
     if (!q) continue;
     const int64_t sb = int64_t(u.idx) * u.shard, se = sb + u.shard;
     const int64_t lo = std::max(sb, q->off), hi = std::min(se, q->off + q->numel);
-    *numel = q->numel;
+    *numel = q->logical_numel ? q->logical_numel : q->numel;
     *b = std::min(std::max<int64_t>(lo - q->off, 0), q->numel);
     *e = std::max(*b, std::min<int64_t>(hi - q->off, q->numel));
+    *b += q->logical_offset;
+    *e += q->logical_offset;
     return OPX_OK;
   }
   set_error("unknown tensor '" + name + "'");
@@ -996,13 +1056,17 @@ int Step::get(const std::string& full, void* dst, size_t bytes) {
     return OPX_ERR_ARG;
   }
   const std::string kind = full.substr(0, colon), name = full.substr(colon + 1);
-  for (const Unit& u : units_) {
+  std::vector<const Unit*> all;
+  for (const Unit& u : units_) all.push_back(&u);
+  for (const Unit& u : expert_units_) all.push_back(&u);
+  for (const Unit* up : all) {
+    const Unit& u = *up;
     const Param* q = u.find(name);
     if (!q) continue;
     const int64_t sb = int64_t(u.idx) * u.shard;
     int64_t n, b, e;
     TRY(info(full, &n, &b, &e));
-    const int64_t cnt = e - b, src0 = q->off + b - sb;
+    const int64_t cnt = e - b, src0 = q->off + (b - q->logical_offset) - sb;
     if (kind == "param") {
       if (bytes != size_t(cnt) * 2) {
         set_error("size mismatch for " + full);

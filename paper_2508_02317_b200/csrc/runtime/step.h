@@ -39,6 +39,7 @@ struct Param {
   std::string key_a, key_b;
   int64_t rows_per_slab = 0, cols = 0;
   int64_t logical_offset = 0;  // element offset of this slab in the logical tensor (experts)
+  int64_t logical_numel = 0;   // numel of the logical tensor (0: same as numel)
 };
 
 // FSDP unit: a flat parameter buffer sharded over `P` ranks with the
@@ -170,8 +171,54 @@ class Step {
   int layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& qb, int& ob);
   int layer_bwd(int l, Unit& u, float* grads);
   int head_fwd_bwd(Unit& u, float* grads);
+  // ---- MoE / expert parallelism (step_moe.cpp)
+  bool moe_ = false;
+  int E_ = 0, topk_ = 0, Fe_ = 0, El_ = 0, ep_ = 1, ep_i_ = 0, De_ = 1;
+  std::vector<int64_t> ep_members_;
+  ncclComm_t expert_comm_ = nullptr;
+  std::vector<Unit> expert_units_;  // [layer]; empty params for dense layers
+  bf16* eslot_ = nullptr;           // expert gather buffer (De > 1)
+  float* egrad_slot_ = nullptr;     // expert full-grad buffer (De > 1)
+  int64_t cap_rows_ = 0;            // receive-buffer rows (worst case)
+  size_t off_flags_ep_ = 0, off_counts_ = 0, off_xrecv_ = 0, off_yback_ = 0, off_dyrecv_ = 0,
+         off_dxback_ = 0;
+  uint32_t** d_ep_flags_ = nullptr;
+  int** d_count_tables_ = nullptr;
+  bf16** d_xrecv_peers_ = nullptr;
+  bf16** d_yback_peers_ = nullptr;
+  bf16** d_dyrecv_peers_ = nullptr;
+  bf16** d_dxback_peers_ = nullptr;
+  uint32_t epoch_ep_ = 0;
+  float *r_logits_ = nullptr, *r_wts_ = nullptr, *r_dw_ = nullptr;
+  int *r_idx_ = nullptr, *r_pos_ = nullptr, *r_pairat_ = nullptr, *r_cnt_ = nullptr,
+      *r_excl_ = nullptr, *r_hist_ = nullptr, *g_start_ = nullptr, *g_rows_ = nullptr,
+      *g_rows_pad_ = nullptr, *g_total_ = nullptr;
+  bf16 *gu_e_ = nullptr, *act_e_ = nullptr, *y_e_ = nullptr, *dact_e_ = nullptr, *dgu_e_ = nullptr,
+       *dx_e_ = nullptr, *dyp_ = nullptr, *dlogits_ = nullptr;
+  char* ep_peer(int j, size_t off) {
+    return (j == ep_i_ ? arena_ : peer_arena_[size_t(ep_members_[size_t(j)])]) + off;
+  }
+  int moe_setup_groups();      // in create(), before build_units
+  int moe_build_units();       // expert units
+  size_t moe_arena(size_t off);  // reserve arena regions, returns new offset
+  int moe_alloc();             // local scratch
+  int moe_import();            // peer tables after ipc import
+  int barrier_ep(cudaStream_t s);
+  int moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out);
+  int moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh2);
   int check(cudaError_t e, const char* what);
   int nccl(ncclResult_t r, const char* what);
 };
+
+template <class T>
+T* Step::alloc(size_t n, bool zero) {
+  void* p = nullptr;
+  const size_t bytes = (n * sizeof(T) > 256 ? n * sizeof(T) : 256);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  if (zero) cudaMemset(p, 0, bytes);
+  allocs_.push_back(p);
+  bytes_alloc_ += int64_t(bytes);
+  return static_cast<T*>(p);
+}
 
 }  // namespace opx

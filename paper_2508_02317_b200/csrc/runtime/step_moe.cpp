@@ -1,0 +1,350 @@
+// MoE / expert-parallel part of the step executor.
+//
+// Placement follows the reference plan API: EP groups are consecutive
+// ep-chunks of each (dp_shard x sp) group (ep_groups, plan.cpp:168-182); rank
+// e of an EP group owns experts [e*E/ep, (e+1)*E/ep) (Shard(0) of the stacked
+// expert weights), each FSDP-sharded over the strided group
+// of the (dp_shard*sp)/ep ranks with the same EP position
+// (resolve_expert_sharding, plan.cpp:85-93).  Per MoE layer the forward runs
+// router -> top-k -> stable permutation -> count exchange -> dispatch (peer
+// stores) -> grouped gate|up GEMM with SwiGLU epilogue -> grouped down GEMM ->
+// combine (peer stores) -> weighted unpermute + residual, the modeled
+// a2a_dispatch / experts / a2a_combine nodes of build_moe_block
+// (step_graph.cpp:253-293); the backward mirrors it (a2a_combine_grad,
+// experts, a2a_dispatch_grad) and adds the router gradient.
+#include <algorithm>
+#include <cstring>
+
+#include "common.h"
+#include "step.h"
+
+namespace opx {
+
+#define TRY(x)                     \
+  do {                             \
+    int rc_ = (x);                 \
+    if (rc_ != OPX_OK) return rc_; \
+  } while (0)
+#define CU(x) TRY(check((x), #x))
+#define NC(x) TRY(nccl((x), #x))
+
+namespace {
+int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+int Step::moe_setup_groups() {
+  const Moe& m = *a_.moe;
+  moe_ = true;
+  E_ = int(m.experts);
+  topk_ = int(m.top_k);
+  Fe_ = int(m.ffn);
+  ep_ = int(p_.ep);
+  El_ = E_ / ep_;
+  const int P = int(p_.shard_degree());
+  De_ = P / ep_;
+  if (Fe_ % 128 || E_ > 256 || topk_ > 16) {
+    set_error("MoE executor requires expert_ffn_dim % 128 == 0, num_experts <= 256, top_k <= 16");
+    return OPX_ERR_CONFIG;
+  }
+  if (ep_ > kMaxSp) {
+    set_error("ep > 8 is not supported (one NVSwitch domain)");
+    return OPX_ERR_CONFIG;
+  }
+  const int ms = shard_i_ * int(p_.sp) + sp_i_;  // index in the shard group
+  const int g = ms / ep_;
+  ep_i_ = ms % ep_;
+  ep_members_.clear();
+  for (int j = 0; j < ep_; ++j) ep_members_.push_back(shard_members_[size_t(g * ep_ + j)]);
+  if (world_comm_)
+    NC(ncclCommSplit(world_comm_, De_ > 1 ? rep_i_ * ep_ + ep_i_ : NCCL_SPLIT_NOCOLOR, rank_,
+                     &expert_comm_, nullptr));
+  return OPX_OK;
+}
+
+int Step::moe_build_units() {
+  const int64_t H = H_, Fe = Fe_, El = El_, E = E_;
+  const int ms = shard_i_ * int(p_.sp) + sp_i_;
+  expert_units_.assign(size_t(a_.layers), Unit{});
+  int64_t mx = 0;
+  for (int l = 0; l < a_.layers; ++l) {
+    if (!a_.is_moe_layer(l)) continue;
+    Unit& u = expert_units_[size_t(l)];
+    const std::string p = "model.layers." + std::to_string(l) + ".mlp.experts.";
+    u.name = "layer" + std::to_string(l) + ".experts";
+    Param gu;
+    gu.name = p + "gate_up_proj";
+    gu.shape = {El, 2 * Fe, H};
+    gu.numel = El * 2 * Fe * H;
+    gu.off = 0;
+    gu.interleave = 1;
+    gu.key_a = p + "gate_proj";
+    gu.key_b = p + "up_proj";
+    gu.rows_per_slab = 2 * Fe;
+    gu.cols = H;
+    gu.logical_offset = int64_t(ep_i_) * gu.numel;
+    gu.logical_numel = E * 2 * Fe * H;
+    Param dn;
+    dn.name = p + "down_proj";
+    dn.shape = {El, H, Fe};
+    dn.numel = El * H * Fe;
+    dn.off = rup(gu.numel, 128);
+    dn.key_a = dn.name;
+    dn.logical_offset = int64_t(ep_i_) * dn.numel;
+    dn.logical_numel = E * H * Fe;
+    u.params = {gu, dn};
+    u.numel = dn.off + rup(dn.numel, 128);
+    u.P = De_;
+    u.idx = ms / ep_;
+    u.comm = expert_comm_;
+    u.rep_comm = p_.dp_replicate > 1 ? rep_comm_ : nullptr;
+    u.padded = rup(u.numel, 64 * int64_t(De_));
+    u.shard = u.padded / De_;
+    u.master = alloc<float>(size_t(u.shard));
+    u.m = alloc<float>(size_t(u.shard));
+    u.v = alloc<float>(size_t(u.shard));
+    u.gshard = alloc<float>(size_t(u.shard));
+    u.pshard = alloc<bf16>(size_t(u.shard));
+    if (!u.master || !u.m || !u.v || !u.gshard || !u.pshard) {
+      set_error("out of device memory for expert shards");
+      return OPX_ERR_CUDA;
+    }
+    if (De_ == 1) {
+      u.full = u.pshard;
+      u.gfull = u.gshard;
+    }
+    mx = std::max(mx, u.padded);
+  }
+  if (De_ > 1 && mx > 0) {
+    eslot_ = alloc<bf16>(size_t(mx), false);
+    egrad_slot_ = alloc<float>(size_t(mx));
+    if (!eslot_ || !egrad_slot_) return cuda_fail(cudaErrorMemoryAllocation, "expert slots");
+  }
+  return OPX_OK;
+}
+
+size_t Step::moe_arena(size_t off) {
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += size_t(rup(int64_t(bytes), 256));
+    return o;
+  };
+  const size_t H = size_t(H_), P = size_t(T_) * size_t(topk_);
+  cap_rows_ = int64_t(P) * ep_ + int64_t(El_) * 128;
+  off_flags_ep_ = take(64 * sizeof(uint32_t));
+  off_counts_ = take(size_t(ep_) * size_t(E_) * sizeof(int));
+  off_xrecv_ = take(size_t(cap_rows_) * H * 2);
+  off_yback_ = take(P * H * 2);
+  off_dyrecv_ = take(size_t(cap_rows_) * H * 2);
+  off_dxback_ = take(P * H * 2);
+  return off;
+}
+
+int Step::moe_alloc() {
+  const size_t T = size_t(T_), P = T * size_t(topk_), cap = size_t(cap_rows_);
+  const size_t E = size_t(E_), H = size_t(H_), Fe = size_t(Fe_);
+  r_logits_ = alloc<float>(T * E, false);
+  r_wts_ = alloc<float>(P, false);
+  r_dw_ = alloc<float>(P, false);
+  r_idx_ = alloc<int>(P, false);
+  r_pos_ = alloc<int>(P, false);
+  r_pairat_ = alloc<int>(P, false);
+  r_cnt_ = alloc<int>(E);
+  r_excl_ = alloc<int>(E);
+  r_hist_ = alloc<int>(size_t(k_moe_sort_chunks(int(P))) * E);
+  g_start_ = alloc<int>(size_t(El_));
+  g_rows_ = alloc<int>(size_t(El_));
+  g_rows_pad_ = alloc<int>(size_t(El_));
+  g_total_ = alloc<int>(1);
+  gu_e_ = alloc<bf16>(cap * 2 * Fe, false);
+  act_e_ = alloc<bf16>(cap * Fe);
+  y_e_ = alloc<bf16>(cap * H, false);
+  dact_e_ = alloc<bf16>(cap * Fe, false);
+  dgu_e_ = alloc<bf16>(cap * 2 * Fe);
+  dx_e_ = alloc<bf16>(cap * H, false);
+  dyp_ = alloc<bf16>(P * H, false);
+  dlogits_ = alloc<bf16>(T * E, false);
+  d_ep_flags_ = alloc<uint32_t*>(kMaxSp);
+  d_count_tables_ = alloc<int*>(kMaxSp);
+  d_xrecv_peers_ = alloc<bf16*>(kMaxSp);
+  d_yback_peers_ = alloc<bf16*>(kMaxSp);
+  d_dyrecv_peers_ = alloc<bf16*>(kMaxSp);
+  d_dxback_peers_ = alloc<bf16*>(kMaxSp);
+  for (void* q : {(void*)gu_e_, (void*)act_e_, (void*)y_e_, (void*)dact_e_, (void*)dgu_e_,
+                  (void*)dx_e_, (void*)dyp_, (void*)d_dxback_peers_})
+    if (!q) return cuda_fail(cudaErrorMemoryAllocation, "MoE scratch");
+  if (ep_ == 1) TRY(moe_import());
+  return OPX_OK;
+}
+
+int Step::moe_import() {
+  std::vector<void*> fl(kMaxSp, nullptr), ct(kMaxSp, nullptr), xr(kMaxSp, nullptr),
+      yb(kMaxSp, nullptr), dy(kMaxSp, nullptr), dx(kMaxSp, nullptr);
+  for (int j = 0; j < ep_; ++j) {
+    fl[size_t(j)] = ep_peer(j, off_flags_ep_);
+    ct[size_t(j)] = ep_peer(j, off_counts_);
+    xr[size_t(j)] = ep_peer(j, off_xrecv_);
+    yb[size_t(j)] = ep_peer(j, off_yback_);
+    dy[size_t(j)] = ep_peer(j, off_dyrecv_);
+    dx[size_t(j)] = ep_peer(j, off_dxback_);
+  }
+  const size_t b = kMaxSp * sizeof(void*);
+  CU(cudaMemcpy(d_ep_flags_, fl.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_count_tables_, ct.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_xrecv_peers_, xr.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_yback_peers_, yb.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_dyrecv_peers_, dy.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_dxback_peers_, dx.data(), b, cudaMemcpyHostToDevice));
+  return OPX_OK;
+}
+
+int Step::barrier_ep(cudaStream_t s) {
+  if (ep_ == 1) return OPX_OK;
+  ++epoch_ep_;
+  CU(k_peer_barrier(d_ep_flags_, reinterpret_cast<uint32_t*>(arena_ + off_flags_ep_), ep_, ep_i_,
+                    epoch_ep_, d_timeout_, s));
+  return OPX_OK;
+}
+
+namespace {
+GemmDesc grouped(int M, int N, int K, const bf16* A, int64_t lda, bool amn, const bf16* B,
+                 int64_t ldb, bool bmn, int epi, void* D, int64_t ldd, int groups, int gk,
+                 const int* gs, const int* gr, int64_t rows_total, int64_t dstride) {
+  GemmDesc g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.A = A;
+  g.lda = lda;
+  g.a_mn = amn;
+  g.B = B;
+  g.ldb = ldb;
+  g.b_mn = bmn;
+  g.epi = epi;
+  g.D = D;
+  g.ldd = ldd;
+  g.groups = groups;
+  g.grouped_k = gk;
+  g.g_start = gs;
+  g.g_rows = gr;
+  g.rows_total = rows_total;
+  g.d_group_stride = dstride;
+  return g;
+}
+}  // namespace
+
+int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out) {
+  (void)l;
+  const int T = T_, H = H_, E = E_, k = topk_, Fe = Fe_, P = T_ * topk_;
+  const bf16* Wr = u.full + u.params[6].off;
+  const bf16* Wgu = eu.full + eu.params[0].off;
+  const bf16* Wd = eu.full + eu.params[1].off;
+  int* counts_all = reinterpret_cast<int*>(arena_ + off_counts_);
+  bf16* xrecv = reinterpret_cast<bf16*>(arena_ + off_xrecv_);
+  bf16* yback = reinterpret_cast<bf16*>(arena_ + off_yback_);
+  CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_));
+  CU(k_moe_topk(r_logits_, T, E, k, r_idx_, r_wts_, cs_));
+  CU(k_moe_sort(r_idx_, P, E, r_hist_, r_cnt_, r_excl_, r_pos_, r_pairat_, cs_));
+  CU(k_moe_publish_counts(r_cnt_, d_count_tables_, ep_, ep_i_, E, cs_));
+  TRY(barrier_ep(cs_));
+  CU(k_moe_groups(counts_all, ep_, E, ep_i_, g_start_, g_rows_, g_rows_pad_, g_total_, cs_));
+  CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                    d_xrecv_peers_, H, H, cs_));
+  TRY(barrier_ep(cs_));
+  CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
+  {
+    GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu, H, false, GEMM_EPI_SWIGLU, gu_e_,
+                         2 * Fe, El_, 0, g_start_, g_rows_, cap_rows_, 0);
+    g.D2 = act_e_;
+    g.ldd2 = Fe;
+    CU(gemm_run(g, cs_));
+  }
+  CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_, g_rows_, g_rows_pad_, El_, cs_));
+  CU(gemm_run(grouped(0, H, Fe, act_e_, Fe, false, Wd, Fe, false, GEMM_EPI_BF16, y_e_, H, El_, 0,
+                      g_start_, g_rows_, cap_rows_, 0),
+              cs_));
+  CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_yback_peers_, H, H,
+                   int(cap_rows_), cs_));
+  TRY(barrier_ep(cs_));
+  CU(k_moe_unpermute(yback, H, r_pos_, r_wts_, T, k, H, x2, x_out, cs_));
+  return OPX_OK;
+}
+
+int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh2) {
+  (void)l;
+  const int T = T_, H = H_, E = E_, k = topk_, Fe = Fe_, P = T_ * topk_;
+  const bf16* Wr = u.full + u.params[6].off;
+  const bf16* Wgu = eu.full + eu.params[0].off;
+  const bf16* Wd = eu.full + eu.params[1].off;
+  int* counts_all = reinterpret_cast<int*>(arena_ + off_counts_);
+  bf16* xrecv = reinterpret_cast<bf16*>(arena_ + off_xrecv_);
+  bf16* yback = reinterpret_cast<bf16*>(arena_ + off_yback_);
+  bf16* dyrecv = reinterpret_cast<bf16*>(arena_ + off_dyrecv_);
+  bf16* dxback = reinterpret_cast<bf16*>(arena_ + off_dxback_);
+  // weighted combine backward: per-pair output grads and router-weight grads
+  CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
+  // a2a_combine_grad: pair grads travel to the expert ranks (same layout as dispatch)
+  CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                    d_dyrecv_peers_, H, H, cs_));
+  TRY(barrier_ep(cs_));
+  CU(k_moe_zero_pad(dyrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
+  // experts backward (grouped GEMMs; wgrad K = 128-padded segment rows)
+  CU(gemm_run(grouped(0, Fe, H, dyrecv, H, false, Wd, Fe, true, GEMM_EPI_BF16, dact_e_, Fe, El_, 0,
+                      g_start_, g_rows_, cap_rows_, 0),
+              cs_));
+  CU(gemm_run(grouped(H, Fe, 0, dyrecv, H, true, act_e_, Fe, true, GEMM_EPI_F32,
+                      Ge + eu.params[1].off, Fe, El_, 1, g_start_, g_rows_pad_, cap_rows_,
+                      int64_t(H) * Fe),
+              cs_));
+  CU(k_moe_swiglu_bwd(dact_e_, gu_e_, dgu_e_, g_start_, g_rows_, g_rows_pad_, El_, Fe,
+                      int(cap_rows_), cs_));
+  CU(gemm_run(grouped(0, H, 2 * Fe, dgu_e_, 2 * Fe, false, Wgu, H, true, GEMM_EPI_BF16, dx_e_, H,
+                      El_, 0, g_start_, g_rows_, cap_rows_, 0),
+              cs_));
+  CU(gemm_run(grouped(2 * Fe, H, 0, dgu_e_, 2 * Fe, true, xrecv, H, true, GEMM_EPI_F32,
+                      Ge + eu.params[0].off, H, El_, 1, g_start_, g_rows_pad_, cap_rows_,
+                      int64_t(2) * Fe * H),
+              cs_));
+  // a2a_dispatch_grad: input grads travel back to the token owners
+  CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
+                   int(cap_rows_), cs_));
+  TRY(barrier_ep(cs_));
+  CU(k_moe_unpermute(dxback, H, r_pos_, nullptr, T, k, H, nullptr, dh2, cs_));
+  // router: renormalised-softmax backward, then dh2 += dlogits . Wr, dWr = dlogits^T h2
+  CU(k_moe_router_bwd(r_dw_, r_wts_, r_idx_, T, k, E, dlogits_, cs_));
+  {
+    GemmDesc g;
+    g.M = T;
+    g.N = H;
+    g.K = E;
+    g.A = dlogits_;
+    g.lda = E;
+    g.B = Wr;
+    g.ldb = H;
+    g.b_mn = true;
+    g.epi = GEMM_EPI_F32_RESID;
+    g.D = dh2;
+    g.ldd = H;
+    g.R = dh2;
+    g.ldr = H;
+    CU(gemm_run(g, cs_));
+  }
+  {
+    GemmDesc g;
+    g.M = E;
+    g.N = H;
+    g.K = T;
+    g.A = dlogits_;
+    g.lda = E;
+    g.a_mn = true;
+    g.B = h2_;
+    g.ldb = H;
+    g.b_mn = true;
+    g.epi = GEMM_EPI_F32;
+    g.D = G + u.params[6].off;
+    g.ldd = H;
+    CU(gemm_run(g, cs_));
+  }
+  return OPX_OK;
+}
+
+}  // namespace opx

@@ -14,6 +14,29 @@ def cluster(n):
     return c
 
 
+def tiny_moe(layers=2, hidden=256, heads=2, kv=2, ffn=768, vocab=2048, experts=64, top_k=4,
+             expert_ffn=256, stride=1):
+    m = tiny_dense(layers, hidden, heads, kv, ffn, vocab)
+    m["modules"][0]["arch"]["moe"] = {"num_experts": experts, "top_k": top_k,
+                                      "expert_ffn_dim": expert_ffn, "moe_layer_stride": stride}
+    return m
+
+
+def gpu_param_names(arch):
+    """Physical tensor names the executor exposes (gate|up stored interleaved)."""
+    out = []
+    for name, shape, _ in om.param_specs(arch):
+        if name.endswith("mlp.gate_proj.weight"):
+            out.append(name.replace("gate_proj", "gate_up_proj"))
+        elif name.endswith("mlp.experts.gate_proj"):
+            out.append(name.replace("gate_proj", "gate_up_proj"))
+        elif name.endswith("mlp.up_proj.weight") or name.endswith("mlp.experts.up_proj"):
+            continue
+        else:
+            out.append(name)
+    return out
+
+
 def tiny_dense(layers=2, hidden=256, heads=2, kv=2, ffn=768, vocab=2048):
     return {"param_dtype_bytes": 2, "modules": [{"name": "core", "kind": "foundation", "trainable": True,
             "arch": {"layers": layers, "hidden": hidden, "heads": heads, "kv_heads": kv,
@@ -56,6 +79,12 @@ def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
     got = {}
     for l in range(arch.layers):
         p = f"model.layers.{l}.mlp."
+        if arch.is_moe(l):
+            Fe, E = arch.expert_ffn, arch.experts
+            gu = gather_full(sessions, "grad", p + "experts.gate_up_proj").reshape(E, Fe // 128, 2, 128, H)
+            got[p + "experts.gate_proj"] = gu[:, :, 0].reshape(E, Fe, H)
+            got[p + "experts.up_proj"] = gu[:, :, 1].reshape(E, Fe, H)
+            continue
         gu = gather_full(sessions, "grad", p + "gate_up_proj.weight")
         g, u = om_deint(gu, F, H)
         got[p + "gate_proj.weight"] = g
@@ -74,7 +103,7 @@ def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
         P1 = om.adamw(P0, G, {}, 1, lr=EXEC["lr"], betas=tuple(EXEC["betas"]), eps=EXEC["eps"],
                       wd=EXEC["weight_decay"])
         for name, ref in P1.items():
-            if name.endswith("gate_proj.weight") or name.endswith("up_proj.weight"):
+            if name.endswith(("gate_proj.weight", "up_proj.weight", "experts.gate_proj", "experts.up_proj")):
                 continue
             x = gather_full(sessions, "master", name).reshape(ref.shape)
             d = np.abs(x - ref)

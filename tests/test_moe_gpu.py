@@ -1,0 +1,83 @@
+"""MoE on one B200: routing indices / permutation bit-exact against the CPU
+oracle given identical router inputs (north_star contract), and a full MoE
+step (router, top-k, permutation, dispatch/combine, grouped expert GEMMs with
+SwiGLU epilogue, weighted unpermute, router backward) against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import model as om
+
+gpu = pytest.mark.gpu
+if torch.cuda.is_available():
+    from tests.gpu_util import P, S, call
+
+
+@gpu
+@pytest.mark.parametrize("T,H,E,k", [(512, 256, 64, 4), (1000, 2048, 128, 8), (64, 512, 256, 16)])
+def test_router_topk_bit_exact(T, H, E, k):
+    torch.manual_seed(T + E)
+    h = (torch.randn(T, H, device="cuda")).to(torch.bfloat16)
+    w = (torch.randn(E, H, device="cuda") * 0.02).to(torch.bfloat16)
+    w[5] = w[3]  # an exact tie between experts 3 and 5 on every token
+    logits = torch.empty(T, E, device="cuda")
+    idx = torch.empty(T, k, device="cuda", dtype=torch.int32)
+    wts = torch.empty(T, k, device="cuda")
+    call("opx_moe_route", P(h), P(w), T, H, E, k, P(logits), P(idx), P(wts), S())
+    torch.cuda.synchronize()
+    ref = om.router_logits(h.float().cpu().numpy(), w.float().cpu().numpy())
+    assert np.array_equal(logits.cpu().numpy(), ref)
+    ridx, rw = om.topk_route(ref, k)
+    assert np.array_equal(idx.cpu().numpy(), ridx)
+    assert np.allclose(wts.cpu().numpy(), rw, rtol=1e-5, atol=1e-7)
+    sel = idx.cpu().numpy()
+    both = (sel == 3).any(1) & (sel == 5).any(1)
+    only5 = (sel == 5).any(1) & ~(sel == 3).any(1)
+    assert not only5.any()  # ties break towards the lower expert index
+    assert both.any() or (sel == 3).any()
+
+
+@gpu
+@pytest.mark.parametrize("T,k,E", [(300, 4, 64), (8192, 8, 128), (17, 1, 256)])
+def test_permutation_bit_exact(T, k, E):
+    rng = np.random.default_rng(T)
+    idx = np.stack([rng.choice(E, k, replace=False) for _ in range(T)]).astype(np.int32)
+    idx[::5] = idx[0]  # heavy collisions on a few experts
+    Pn = T * k
+    from paper_2508_02317_b200 import lib
+
+    nch = lib().opx_moe_sort_chunks(Pn)
+    d_idx = torch.from_numpy(idx).cuda()
+    hist = torch.empty(nch * E, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(E, dtype=torch.int32, device="cuda")
+    excl = torch.empty(E, dtype=torch.int32, device="cuda")
+    pos = torch.empty(Pn, dtype=torch.int32, device="cuda")
+    at = torch.empty(Pn, dtype=torch.int32, device="cuda")
+    call("opx_moe_sort", P(d_idx), Pn, E, P(hist), P(cnt), P(excl), P(pos), P(at), S())
+    torch.cuda.synchronize()
+    order, counts = om.permutation(idx, E)
+    assert np.array_equal(at.cpu().numpy(), order)
+    inv = np.empty_like(order)
+    inv[order] = np.arange(Pn)
+    assert np.array_equal(pos.cpu().numpy(), inv)
+    assert np.array_equal(cnt.cpu().numpy(), counts)
+    assert np.array_equal(excl.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)[:-1]]))
+
+
+@gpu
+def test_step_tiny_moe_matches_oracle():
+    from paper_2508_02317_b200.runtime import Session, synthetic_batch
+    from tests.step_common import EXEC, cluster, compare_step, tiny_moe
+
+    model = tiny_moe(layers=2, hidden=256, heads=2, kv=2, ffn=768, vocab=2048, experts=64, top_k=4,
+                     expert_ffn=256, stride=1)
+    S_ = 512
+    wl = {"seq_len": S_, "micro_batch": 1, "global_batch": 1}
+    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": 1}
+    s = Session(cluster(1), model, wl, plan, EXEC, rank=0, device=0)
+    s.init_weights(EXEC["seed"])
+    batch = synthetic_batch(2048, S_, 1, seed=2508)
+    s.load(batch)
+    r = s.run()
+    compare_step([s], model, batch, plan, r.loss)
+    s.close()

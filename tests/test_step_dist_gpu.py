@@ -29,14 +29,9 @@ def _run(world, model, plan, S, rows):
     from oracle import model as om
 
     arch = om.Arch.from_model_json(model)
-    names = []
-    for name, shape, _ in om.param_specs(arch):
-        if name.endswith("mlp.gate_proj.weight"):
-            names.append(name.replace("gate_proj", "gate_up_proj"))
-        elif name.endswith("mlp.up_proj.weight"):
-            continue
-        else:
-            names.append(name)
+    from tests.step_common import gpu_param_names
+
+    names = gpu_param_names(arch)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = random.randint(20000, 40000)
@@ -65,6 +60,31 @@ PLANS = [
     (4, {"dp_replicate": 2, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1}, 2),
     (4, {"dp_replicate": 1, "dp_shard": 1, "sp": 4, "ep": 1, "micro_batch": 1}, 1),
 ]
+
+
+MOE_PLANS = [
+    (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1}, 2),
+    (4, {"dp_replicate": 1, "dp_shard": 4, "sp": 1, "ep": 4, "micro_batch": 1}, 4),
+    (4, {"dp_replicate": 1, "dp_shard": 4, "sp": 1, "ep": 2, "micro_batch": 1}, 4),
+    (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 4, "micro_batch": 1}, 2),
+]
+
+
+@gpu
+@pytest.mark.parametrize("world,plan,rows", MOE_PLANS)
+def test_dist_moe_step_matches_oracle(world, plan, rows):
+    if NGPU < world:
+        pytest.skip(f"needs {world} GPUs")
+    from tests.step_common import tiny_moe
+
+    model = tiny_moe(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048, experts=64, top_k=4,
+                     expert_ffn=256)
+    S = 512
+    loss, sessions = _run(world, model, plan, S, rows)
+    from paper_2508_02317_b200.runtime import synthetic_batch
+
+    batch = synthetic_batch(2048, S, rows, seed=2508)
+    compare_step(sessions, model, batch, plan, loss)
 
 
 @gpu
