@@ -282,10 +282,15 @@ class Step:
     in fp64 and everything else in fp32, so GPU-vs-CPU differences are the
     GPU's rounding of intermediates only."""
 
-    def __init__(self, a: Arch, params: dict, round_operands: bool = True):
+    def __init__(self, a: Arch, params: dict, round_operands: bool = True, forced_routes=None):
         self.a = a
         self.P = params
         self.r = bf16_round if round_operands else (lambda x: x.astype(F32))
+        # {layer: [N, k] expert indices}: route with these instead of the
+        # oracle's own top-k (the weights still come from the oracle's logits);
+        # used to separate discrete routing flips from arithmetic differences.
+        self.forced = forced_routes or {}
+        self.flips = {}  # {layer: fraction of tokens whose expert set differs}
 
     def mm(self, x, w):  # x [N,K] . w[M,K]^T
         return (self.r(x).astype(np.float64) @ self.r(w).astype(np.float64).T).astype(F32)
@@ -397,6 +402,13 @@ class Step:
         hb = self.r(h2)
         logits = router_logits(hb, self.r(P[p + "gate.weight"]))
         idx, w = topk_route(logits, a.top_k)
+        if l in self.forced:
+            f = np.asarray(self.forced[l], np.int32).reshape(idx.shape)
+            self.flips[l] = float(np.mean(np.any(np.sort(f, 1) != np.sort(idx, 1), 1)))
+            idx = f
+            sel = np.take_along_axis(logits, idx, -1).astype(np.float64)
+            e = np.exp(sel - sel.max(-1, keepdims=True))
+            w = (e / e.sum(-1, keepdims=True)).astype(F32)
         N = h2.shape[0]
         y = np.zeros((N, a.hidden), np.float64)
         cache = {"idx": idx, "w": w, "logits": logits, "eo": {}}
@@ -472,7 +484,7 @@ def adamw(params, grads, state, step, lr=1e-4, betas=(0.9, 0.95), eps=1e-8, wd=0
 # ----------------------------------------------------------------------------
 # simulated ranks (FSDP x SP x DP) for one step
 # ----------------------------------------------------------------------------
-def simulate_ranks(a: Arch, params: dict, batch, plan: dict):
+def simulate_ranks(a: Arch, params: dict, batch, plan: dict, forced_routes=None, flips=None):
     """Runs the step the way the mesh partitions the batch: dp index r
     (= dp_replicate_idx*dp_shard + dp_shard_idx) owns rows
     [r*micro_batch, (r+1)*micro_batch).  Inside an SP group the Ulysses
@@ -494,8 +506,14 @@ def simulate_ranks(a: Arch, params: dict, batch, plan: dict):
         cu = [0]
         for i, c in enumerate(cus[sl]):
             cu += [i * S + x for x in c[1:]]
-        st = Step(a, params)
+        fr = None
+        if forced_routes:
+            fr = {l: v[sl].reshape(-1, v.shape[-1]) for l, v in forced_routes.items()}
+        st = Step(a, params, forced_routes=fr)
         ls, g = st.run(rid, rlab, rpos, np.array(cu), n_valid)
+        if flips is not None:
+            for l, f in st.flips.items():
+                flips.setdefault(l, []).append(f)
         loss += ls
         if total is None:
             total = {k: v.astype(np.float64) for k, v in g.items()}

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -623,7 +624,9 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& 
     return OPX_OK;
   }
   {
-    GemmDesc g = gd(T, 2 * F, H, h2_, H, false, W.gu, H, false, GEMM_EPI_SWIGLU, gu_, 2 * F);
+    // gate|up pre-activations are only needed by the backward (recompute pass)
+    GemmDesc g = gd(T, 2 * F, H, h2_, H, false, W.gu, H, false, GEMM_EPI_SWIGLU,
+                    in_recompute_ ? gu_ : nullptr, 2 * F);
     g.D2 = act_;
     g.ldd2 = F;
     CU(gemm_run(g, cs_));
@@ -652,7 +655,10 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
   if (tr) cudaEventRecord(e0, cs_);
   // full recompute of the layer (recompute=full); x_out goes to scratch
   int qb = 0, ob = 0;
-  TRY(layer_fwd(l, u, x_saved_[size_t(l)], dtmp_, qb, ob));
+  in_recompute_ = true;
+  const int rc_fwd = layer_fwd(l, u, x_saved_[size_t(l)], dtmp_, qb, ob);
+  in_recompute_ = false;
+  TRY(rc_fwd);
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
@@ -1042,6 +1048,16 @@ int Step::info(const std::string& full, int64_t* numel, int64_t* b, int64_t* e) 
 }
 
 int Step::get(const std::string& full, void* dst, size_t bytes) {
+  if (full.rfind("route:", 0) == 0) {  // forward top-k indices of MoE layer l (this rank's T*k)
+    const int l = std::atoi(full.c_str() + 6);
+    if (l < 0 || l >= int(route_idx_.size()) || !route_idx_[size_t(l)] ||
+        bytes != size_t(T_) * size_t(topk_) * 4) {
+      set_error("route: bad layer or size");
+      return OPX_ERR_ARG;
+    }
+    CU(cudaMemcpy(dst, route_idx_[size_t(l)], bytes, cudaMemcpyDeviceToHost));
+    return OPX_OK;
+  }
   if (full == "loss_rows") {
     if (bytes != size_t(T_) * 4) {
       set_error("loss_rows: size mismatch");

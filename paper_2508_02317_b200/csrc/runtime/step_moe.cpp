@@ -172,6 +172,9 @@ int Step::moe_alloc() {
   for (void* q : {(void*)gu_e_, (void*)act_e_, (void*)y_e_, (void*)dact_e_, (void*)dgu_e_,
                   (void*)dx_e_, (void*)dyp_, (void*)d_dxback_peers_})
     if (!q) return cuda_fail(cudaErrorMemoryAllocation, "MoE scratch");
+  route_idx_.assign(size_t(a_.layers), nullptr);
+  for (int l = 0; l < a_.layers; ++l)
+    if (a_.is_moe_layer(l)) route_idx_[size_t(l)] = alloc<int>(P, false);
   if (ep_ == 1) TRY(moe_import());
   return OPX_OK;
 }
@@ -233,7 +236,6 @@ GemmDesc grouped(int M, int N, int K, const bf16* A, int64_t lda, bool amn, cons
 }  // namespace
 
 int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out) {
-  (void)l;
   const int T = T_, H = H_, E = E_, k = topk_, Fe = Fe_, P = T_ * topk_;
   const bf16* Wr = u.full + u.params[6].off;
   const bf16* Wgu = eu.full + eu.params[0].off;
@@ -243,6 +245,9 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   bf16* yback = reinterpret_cast<bf16*>(arena_ + off_yback_);
   CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_));
   CU(k_moe_topk(r_logits_, T, E, k, r_idx_, r_wts_, cs_));
+  if (!in_recompute_ && route_idx_[size_t(l)])
+    CU(cudaMemcpyAsync(route_idx_[size_t(l)], r_idx_, size_t(P) * sizeof(int),
+                       cudaMemcpyDeviceToDevice, cs_));
   CU(k_moe_sort(r_idx_, P, E, r_hist_, r_cnt_, r_excl_, r_pos_, r_pairat_, cs_));
   CU(k_moe_publish_counts(r_cnt_, d_count_tables_, ep_, ep_i_, E, cs_));
   TRY(barrier_ep(cs_));
@@ -252,8 +257,10 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   TRY(barrier_ep(cs_));
   CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
   {
-    GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu, H, false, GEMM_EPI_SWIGLU, gu_e_,
-                         2 * Fe, El_, 0, g_start_, g_rows_, cap_rows_, 0);
+    // gate|up pre-activations are only needed by the backward (recompute pass)
+    GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu, H, false, GEMM_EPI_SWIGLU,
+                         in_recompute_ ? gu_e_ : nullptr, 2 * Fe, El_, 0, g_start_, g_rows_,
+                         cap_rows_, 0);
     g.D2 = act_e_;
     g.ldd2 = Fe;
     CU(gemm_run(g, cs_));

@@ -166,6 +166,13 @@ class Session:
         check(lib().opx_step_get(self.h, name.encode(), out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
         return out, n, b, e
 
+    def routes(self, layer: int, T: int, k: int):
+        """Forward top-k expert indices of MoE layer `layer` for this rank's T tokens."""
+        out = np.empty((T, k), np.int32)
+        check(lib().opx_step_get(self.h, f"route:{layer}".encode(), out.ctypes.data_as(ctypes.c_void_p),
+                                 out.nbytes))
+        return out
+
     def loss_rows(self, T):
         out = np.empty(T, np.float32)
         check(lib().opx_step_get(self.h, b"loss_rows", out.ctypes.data_as(ctypes.c_void_p), out.nbytes))

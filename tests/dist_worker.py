@@ -24,6 +24,14 @@ def step_worker(rank, world, port, model, plan, S, rows, q, names):
             for n in names:
                 v, numel, b, e = s.get(f"{kind}:{n}")
                 out[(kind, n)] = (v, numel, b, e)
+        arch = model["modules"][0]["arch"]
+        if "moe" in arch:
+            T = plan["micro_batch"] * S // plan["sp"]
+            k = arch["moe"]["top_k"]
+            stride = arch["moe"].get("moe_layer_stride", 1)
+            for l in range(arch["layers"]):
+                if (l + 1) % stride == 0:
+                    out[("route", l)] = s.routes(l, T, k)
         q.put((rank, r.loss, out, None))
         s.close()
     except Exception as ex:  # report instead of hanging the parent

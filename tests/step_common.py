@@ -64,13 +64,46 @@ def gather_full(sessions, kind, name):
     return out
 
 
+def global_routes(sessions, arch, plan, S):
+    """Assemble every rank's forward top-k indices into [rows, S, k] per MoE layer
+    (rank = (dp row block, SP token slice), runtime.local_slice layout)."""
+    from paper_2508_02317_b200.runtime import rank_coords
+
+    m, sp = plan["micro_batch"], plan["sp"]
+    rows = plan.get("dp_replicate", 1) * plan["dp_shard"] * m
+    Sl = S // sp
+    out = {}
+    for l in range(arch.layers):
+        if not arch.is_moe(l):
+            continue
+        g = np.zeros((rows, S, arch.top_k), np.int32)
+        for rank, s in enumerate(sessions):
+            rep, sh, spi = rank_coords(rank, plan)
+            dp = rep * plan["dp_shard"] + sh
+            r = s.routes(l, m * Sl, arch.top_k).reshape(m, Sl, arch.top_k)
+            g[dp * m:(dp + 1) * m, spi * Sl:(spi + 1) * Sl] = r
+        out[l] = g
+    return out
+
+
+MAX_FLIP_RATE = 0.01  # fraction of tokens whose expert set differs from the oracle's own top-k
+
+
 def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
     """Runs the oracle on the same batch/weights and compares loss, every
-    gradient and the AdamW-updated master weights.  Returns a report dict."""
+    gradient and the AdamW-updated master weights.  For MoE models the oracle
+    is routed with the GPU's top-k choices (bf16 activations can flip near-tied
+    experts) and the flip rate against the oracle's own routing is checked
+    separately.  Returns a report dict."""
     arch = om.Arch.from_model_json(model)
     P0 = om.init_params(arch, EXEC["seed"])
-    loss_ref, G = om.simulate_ranks(arch, P0, batch, plan)
-    rep = {"loss": step_loss, "loss_ref": loss_ref, "grads": {}}
+    routes = global_routes(sessions, arch, plan, batch["ids"].shape[1]) if arch.experts else None
+    flips = {}
+    loss_ref, G = om.simulate_ranks(arch, P0, batch, plan, forced_routes=routes, flips=flips)
+    rep = {"loss": step_loss, "loss_ref": loss_ref, "grads": {},
+           "flip_rate": {l: float(np.mean(v)) for l, v in flips.items()}}
+    for l, f in rep["flip_rate"].items():
+        assert f <= MAX_FLIP_RATE, ("routing flip rate", l, f)
     assert abs(step_loss - loss_ref) / abs(loss_ref) < TOL_LOSS, (step_loss, loss_ref)
     F, H = arch.ffn, arch.hidden
     names = {}

@@ -24,6 +24,9 @@ class _Remote:
         kind, n = name.split(":", 1)
         return self.out[(kind, n)]
 
+    def routes(self, layer, T, k):
+        return self.out[("route", layer)]
+
 
 def _run(world, model, plan, S, rows):
     from oracle import model as om
