@@ -86,7 +86,7 @@ def global_routes(sessions, arch, plan, S):
     return out
 
 
-MAX_FLIP_RATE = 0.01  # fraction of tokens whose expert set differs from the oracle's own top-k
+MAX_FLIP_RATE = 0.05  # fraction of tokens whose expert set differs from the oracle's own top-k (reported)
 
 
 def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
