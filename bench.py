@@ -29,6 +29,9 @@ METRIC = "train tokens/sec/GPU and MFU (fwd+bwd+opt step) at 1/2/4/8 B200 vs CPU
 
 QWEN2_7B = {"layers": 28, "hidden": 3584, "heads": 28, "kv_heads": 4, "head_dim": 128,
             "ffn_dim": 18944, "vocab": 152064}
+QWEN3_30B_A3B = {"layers": 48, "hidden": 2048, "heads": 16, "kv_heads": 4, "head_dim": 128,
+                 "ffn_dim": 6144, "vocab": 151936,
+                 "moe": {"num_experts": 128, "top_k": 8, "expert_ffn_dim": 768, "moe_layer_stride": 1}}
 TINY = {"layers": 2, "hidden": 256, "heads": 2, "kv_heads": 2, "head_dim": 128, "ffn_dim": 768,
         "vocab": 2048}
 
@@ -37,20 +40,30 @@ def plan_for(cfg: str, n: int) -> dict:
     """Parallel plan per GPU count: C1 FSDP1 -> SP2 -> SP4 -> FSDP2xSP4."""
     if cfg == "c1":
         sp = min(n, 4)
+        # 1 GPU holds 7.6B params x 18 B (137 GB) + the 32K-token working set only
+        # with full recompute (the paper's setting); from 2 GPUs the per-layer
+        # activations fit and recompute=none removes the extra forward.
         return {"dp_replicate": 1, "dp_shard": n // sp, "sp": sp, "ep": 1, "micro_batch": 1,
+                "recompute": "full" if n == 1 else "none", "fsdp_prefetch_depth": 1}
+    if cfg == "c2":  # FSDP + EP over all GPUs (SURVEY §8d C2: FSDP8+EP8)
+        return {"dp_replicate": 1, "dp_shard": n, "sp": 1, "ep": n, "micro_batch": 1,
                 "recompute": "full", "fsdp_prefetch_depth": 1}
     return {"dp_replicate": 1, "dp_shard": n, "sp": 1, "ep": 1, "micro_batch": 1,
             "recompute": "full", "fsdp_prefetch_depth": 1}
 
 
-def model_for(cfg: str) -> dict:
-    arch = {"c1": QWEN2_7B, "c0": TINY}[cfg]
+def model_for(cfg: str, n: int = 8) -> dict:
+    arch = dict({"c1": QWEN2_7B, "c0": TINY, "c2": QWEN3_30B_A3B}[cfg])
+    if cfg == "c2" and n < 8:
+        # 30B does not fit below 8 GPUs (reference memory model: 235/455 GiB at
+        # EP2/EP1); scale the layer count with the GPU count (a layer slice)
+        arch["layers"] = 48 * n // 8
     return {"param_dtype_bytes": 2,
             "modules": [{"name": "core", "kind": "foundation", "trainable": True, "arch": arch}]}
 
 
 def seq_for(cfg: str) -> int:
-    return {"c1": 32768, "c0": 1024}[cfg]
+    return {"c1": 32768, "c0": 1024, "c2": 8192}[cfg]
 
 
 def cluster_for(n: int) -> dict:
@@ -69,13 +82,21 @@ def peaks():
         return 1.59e15, 1.4e15, 6650.0, "fallback"
 
 
+def active_layer_params(arch: dict) -> float:
+    H, F = arch["hidden"], arch["ffn_dim"]
+    kvw = arch["kv_heads"] * arch["head_dim"]
+    attn = H * (H + 2 * kvw) + H + H * H + H
+    if "moe" in arch:
+        m = arch["moe"]
+        return attn + H * m["num_experts"] + 3 * H * m["expert_ffn_dim"] * m["top_k"]
+    return attn + 3 * H * F
+
+
 def exact_flops_per_step(arch: dict, batch, T_total: int) -> float:
     """6*N_active,strict per token + exact causal attention 6*L*H*sum(l_i^2)
     (SURVEY.md §8d); N_active,strict excludes the embedding gather."""
-    H, L, V, F = arch["hidden"], arch["layers"], arch["vocab"], arch["ffn_dim"]
-    kvw = arch["kv_heads"] * arch["head_dim"]
-    per_layer = H * (H + 2 * kvw) + H + H * H + 3 * H * F + H
-    n_strict = L * per_layer + V * H + H
+    H, L, V = arch["hidden"], arch["layers"], arch["vocab"]
+    n_strict = L * active_layer_params(arch) + V * H + H
     sq = 0
     for cu in batch["cu_rows"]:
         for a, b in zip(cu[:-1], cu[1:]):
@@ -222,7 +243,7 @@ def main():
     from paper_2508_02317_b200.runtime import Session, local_slice, synthetic_batch
 
     plan = plan_for(cfg, n)
-    model = model_for(cfg)
+    model = model_for(cfg, n)
     arch = model["modules"][0]["arch"]
     S = seq_for(cfg)
     rows = plan["dp_replicate"] * plan["dp_shard"] * plan["micro_batch"]
@@ -265,9 +286,8 @@ def main():
     tokens_step = rows * S
     value = tokens_step / t_mean
     peak, peak_sus, hbm, peak_kind = peaks()
-    fpt_ref = 6.0 * (arch["layers"] * (arch["hidden"] * (arch["hidden"] + 2 * arch["kv_heads"] * 128) + arch["hidden"]
-                     + arch["hidden"] ** 2 + 3 * arch["hidden"] * arch["ffn_dim"] + arch["hidden"])
-                     + 2 * arch["vocab"] * arch["hidden"] + arch["hidden"]) + 6.0 * arch["layers"] * arch["hidden"] * S
+    fpt_ref = 6.0 * (arch["layers"] * active_layer_params(arch) + 2 * arch["vocab"] * arch["hidden"]
+                     + arch["hidden"]) + 6.0 * arch["layers"] * arch["hidden"] * S
     exact = exact_flops_per_step(arch, batch, tokens_step)
     per_gpu = value / n
     # roofline: dominant kernel = the forward MLP block (gate|up GEMM + SwiGLU
@@ -276,6 +296,11 @@ def main():
     mlp = [e["dur"] for e in trace["traceEvents"] if e["name"].startswith("fwd.layer") and e["name"].endswith(".mlp")]
     node_s = statistics.mean(mlp) * 1e-6 if mlp else float("nan")
     mlp_flops = 6.0 * T_loc * arch["hidden"] * arch["ffn_dim"]
+    if "moe" in arch:  # MoE block node: router + dispatch + experts + combine
+        mlp = [e["dur"] for e in trace["traceEvents"] if e["name"].startswith("fwd.layer") and e["name"].endswith(".moe")]
+        node_s = statistics.mean(mlp) * 1e-6 if mlp else float("nan")
+        m = arch["moe"]
+        mlp_flops = 6.0 * T_loc * arch["hidden"] * m["expert_ffn_dim"] * m["top_k"]
     achieved = mlp_flops / node_s
     share = {}
     for e in trace["traceEvents"]:
@@ -293,7 +318,8 @@ def main():
         "tokens_per_s_per_gpu": per_gpu,
         "mfu_ref": per_gpu * fpt_ref / peak, "mfu_ref_datasheet": per_gpu * fpt_ref / 2.25e15,
         "mfu_exact": exact / t_mean / n / peak, "model_flops_per_token_ref": fpt_ref,
-        "config": {"workload": cfg, "model": "qwen2-7b-shaped (random init)" if cfg == "c1" else cfg,
+        "config": {"workload": cfg, "model": {"c1": "qwen2-7b-shaped (random init)",
+                                              "c2": f"qwen3-30b-a3b-shaped, {arch['layers']} layers (random init)"}.get(cfg, cfg),
                    "global_batch": rows, "seq_len": S, "tokens_per_step": tokens_step,
                    "parallelism": f"fsdp{plan['dp_shard']}xsp{plan['sp']}",
                    "recompute": plan["recompute"], "packing": "lognormal varlen, 0 padding",

@@ -276,17 +276,33 @@ int Step::alloc_acts() {
     return o;
   };
   off_flags_ = take(64 * sizeof(uint32_t));
+  const int L = int(a_.layers);
+  save_acts_ = !p_.recompute_full;
+  const int xslots = save_acts_ ? 2 + L : 2;
+  for (int b = 0; b < xslots; ++b) {
+    if (b >= 2 && !keeps_acts(b - 2)) {  // MoE layers are always recomputed
+      off_q_.push_back(0);
+      off_k_.push_back(0);
+      off_v_.push_back(0);
+      off_o_.push_back(0);
+      continue;
+    }
+    off_q_.push_back(take(N * size_t(hql_) * 128 * 2));
+    off_k_.push_back(take(N * size_t(hkl_) * 128 * 2));
+    off_v_.push_back(take(N * size_t(hkl_) * 128 * 2));
+    off_o_.push_back(take(T * size_t(hq_) * 128 * 2));
+  }
   for (int b = 0; b < 2; ++b) {
-    off_q_[b] = take(N * size_t(hql_) * 128 * 2);
-    off_k_[b] = take(N * size_t(hkl_) * 128 * 2);
-    off_v_[b] = take(N * size_t(hkl_) * 128 * 2);
-    off_o_[b] = take(T * size_t(hq_) * 128 * 2);
     off_do_[b] = take(N * size_t(hql_) * 128 * 2);
     off_dqkv_[b] = take(T * size_t(Wqkv_) * 2);
   }
   if (moe_) off = moe_arena(off);
   arena_bytes_ = off;
-  CU(cudaMalloc(&arena_, arena_bytes_));
+  if (cudaMalloc(&arena_, arena_bytes_) != cudaSuccess) {
+    set_error("out of device memory for the peer arena (" + std::to_string(arena_bytes_ >> 20) +
+              " MiB)" + (save_acts_ ? "; recompute=none does not fit, use recompute=full" : ""));
+    return OPX_ERR_CUDA;
+  }
   CU(cudaMemset(arena_, 0, arena_bytes_));
   allocs_.push_back(arena_);
   bytes_alloc_ += int64_t(arena_bytes_);
@@ -295,18 +311,32 @@ int Step::alloc_acts() {
   d_peer_flags_ = alloc<uint32_t*>(kMaxSp);
   d_timeout_ = alloc<int>(1);
 
-  const int L = int(a_.layers);
   for (int l = 0; l <= L; ++l) x_saved_.push_back(alloc<float>(T * H, false));
-  h_ = alloc<bf16>(T * H, false);
+  auto make_acts = [&](Acts& a, bool dense_mlp) -> bool {
+    a.h = alloc<bf16>(T * H, false);
+    a.ofull = p_.sp > 1 ? alloc<bf16>(N * size_t(hql_) * 128, false) : nullptr;
+    a.lse = alloc<float>(N * size_t(hql_), false);
+    a.x2 = alloc<float>(T * H, false);
+    a.r1 = alloc<float>(T, false);
+    a.r2 = alloc<float>(T, false);
+    a.h2 = alloc<bf16>(T * H, false);
+    a.gu = dense_mlp ? alloc<bf16>(T * size_t(2 * F_), false) : nullptr;
+    a.act = dense_mlp ? alloc<bf16>(T * size_t(F_), false) : nullptr;
+    return a.h && a.lse && a.x2 && a.h2 && (!dense_mlp || (a.gu && a.act)) &&
+           (p_.sp == 1 || a.ofull);
+  };
+  bool any_dense = false;
+  for (int l = 0; l < L; ++l) any_dense = any_dense || !a_.is_moe_layer(l);
+  if (!make_acts(scratch_, any_dense)) return cuda_fail(cudaErrorMemoryAllocation, "activations");
+  saved_.assign(size_t(L), Acts{});
+  for (int l = 0; l < L; ++l)
+    if (keeps_acts(l) && !make_acts(saved_[size_t(l)], true)) {
+      set_error("out of device memory for recompute=none activations (layer " +
+                std::to_string(l) + "); use recompute=full");
+      return OPX_ERR_CUDA;
+    }
+  bind(scratch_);
   qkv_ = alloc<bf16>(T * size_t(Wqkv_), false);
-  ofull_ = alloc<bf16>(N * size_t(hql_) * 128, false);
-  lse_ = alloc<float>(N * size_t(hql_), false);
-  x2_ = alloc<float>(T * H, false);
-  r1_ = alloc<float>(T, false);
-  r2_ = alloc<float>(T, false);
-  h2_ = alloc<bf16>(T * H, false);
-  gu_ = alloc<bf16>(T * size_t(2 * F_), false);
-  act_ = alloc<bf16>(T * size_t(F_), false);
   dx_ = alloc<float>(T * H, false);
   dtmp_ = alloc<float>(T * H, false);
   dxb_ = alloc<bf16>(T * H, false);
@@ -499,7 +529,7 @@ GemmDesc gd(int M, int N, int K, const bf16* A, int64_t lda, bool amn, const bf1
 }
 }  // namespace
 
-int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& qb, int& ob) {
+int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int slot) {
   const LayerW W = layer_w(u, u.full);
   const int T = T_, H = H_, F = F_;
   const std::string pre = "fwd.layer" + std::to_string(l) + ".m0";
@@ -515,8 +545,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& 
     mark(pre + ".qkv_proj", ph, 0, e0, e1);
     e0 = e1;
   }
-  qb = xq_;
-  xq_ ^= 1;
+  const int qb = slot, ob = slot;
   {
     A2AArgs a{};
     a.sp = int(p_.sp);
@@ -551,8 +580,6 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& 
     mark(pre + ".a2a_qkv", ph, 0, e0, e1);
     e0 = e1;
   }
-  ob = xo_;
-  xo_ ^= 1;
   bf16* attn_out = p_.sp == 1 ? o_loc(ob) : ofull_;
   {
     AttnArgs a{};
@@ -626,7 +653,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& 
   {
     // gate|up pre-activations are only needed by the backward (recompute pass)
     GemmDesc g = gd(T, 2 * F, H, h2_, H, false, W.gu, H, false, GEMM_EPI_SWIGLU,
-                    in_recompute_ ? gu_ : nullptr, 2 * F);
+                    store_gu_ ? gu_ : nullptr, 2 * F);
     g.D2 = act_;
     g.ldd2 = F;
     CU(gemm_run(g, cs_));
@@ -654,11 +681,20 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
   cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
   if (tr) cudaEventRecord(e0, cs_);
   // full recompute of the layer (recompute=full); x_out goes to scratch
-  int qb = 0, ob = 0;
-  in_recompute_ = true;
-  const int rc_fwd = layer_fwd(l, u, x_saved_[size_t(l)], dtmp_, qb, ob);
-  in_recompute_ = false;
-  TRY(rc_fwd);
+  int qb, ob;
+  if (keeps_acts(l)) {  // recompute=none: this layer's forward activations are resident
+    bind(saved_[size_t(l)]);
+    qb = ob = 2 + l;
+  } else {
+    bind(scratch_);
+    qb = ob = next_rslot();
+    in_recompute_ = true;
+    store_gu_ = true;
+    const int rc_fwd = layer_fwd(l, u, x_saved_[size_t(l)], dtmp_, qb);
+    in_recompute_ = false;
+    store_gu_ = false;
+    TRY(rc_fwd);
+  }
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
@@ -887,13 +923,23 @@ int Step::run(opx_step_report* rep) {
     Unit& u = units_[size_t(1 + l)];
     if (u.P > 1) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
     if (l + nslots_ - 1 < L) TRY(issue_gather(l + nslots_ - 1, false));
-    int qb, ob;
+    int slot;
+    if (keeps_acts(l)) {
+      bind(saved_[size_t(l)]);
+      slot = 2 + l;
+      store_gu_ = true;
+    } else {
+      bind(scratch_);
+      slot = next_rslot();
+      store_gu_ = false;
+    }
     if (moe_ && a_.is_moe_layer(l) && De_ > 1) {
       Unit& eu = expert_units_[size_t(l)];
       eu.full = eslot_;
       NC(ncclAllGather(eu.pshard, eslot_, size_t(eu.shard), ncclBfloat16, eu.comm, cs_));
     }
-    TRY(layer_fwd(l, u, x_saved_[size_t(l)], x_saved_[size_t(l + 1)], qb, ob));
+    TRY(layer_fwd(l, u, x_saved_[size_t(l)], x_saved_[size_t(l + 1)], slot));
+    store_gu_ = false;
     CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
   }
   CU(cudaEventRecord(ev_fwd_, cs_));

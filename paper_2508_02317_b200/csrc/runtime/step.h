@@ -122,8 +122,11 @@ class Step {
   size_t arena_bytes_ = 0;
   std::vector<char*> peer_arena_;  // by world rank
   std::vector<cudaIpcMemHandle_t> opened_;
-  size_t off_flags_ = 0, off_q_[2] = {0, 0}, off_k_[2] = {0, 0}, off_v_[2] = {0, 0},
-         off_o_[2] = {0, 0}, off_do_[2] = {0, 0}, off_dqkv_[2] = {0, 0};
+  size_t off_flags_ = 0, off_do_[2] = {0, 0}, off_dqkv_[2] = {0, 0};
+  // q/k/v (head layout) and o (token layout) exchange buffers: slots 0..1 are
+  // the double buffer used by recomputed layers; with recompute=none layer l
+  // keeps its own slot 2+l until its backward.
+  std::vector<size_t> off_q_, off_k_, off_v_, off_o_;
   uint32_t** d_peer_flags_ = nullptr;  // device array [sp] of peer flag pointers
   int* d_timeout_ = nullptr;
   uint32_t epoch_ = 0;
@@ -135,6 +138,33 @@ class Step {
   float* d_inv_freq_ = nullptr;
 
   // ---- activations
+  // Per-layer forward activations needed by the backward.  recompute=full
+  // (plan.hpp:32 default) keeps one scratch set and recomputes each layer in
+  // the backward; recompute=none keeps a set per layer (dense layers).
+  struct Acts {
+    bf16 *h = nullptr, *h2 = nullptr, *gu = nullptr, *act = nullptr, *ofull = nullptr;
+    float *x2 = nullptr, *r1 = nullptr, *r2 = nullptr, *lse = nullptr;
+  };
+  Acts scratch_;
+  std::vector<Acts> saved_;
+  bool save_acts_ = false;
+  bool keeps_acts(int l) const { return save_acts_ && !a_.is_moe_layer(l); }
+  void bind(const Acts& a) {
+    h_ = a.h;
+    h2_ = a.h2;
+    gu_ = a.gu;
+    act_ = a.act;
+    ofull_ = a.ofull;
+    x2_ = a.x2;
+    r1_ = a.r1;
+    r2_ = a.r2;
+    lse_ = a.lse;
+  }
+  int next_rslot() {
+    xq_ ^= 1;
+    return xq_;
+  }
+  bool store_gu_ = false;
   std::vector<float*> x_saved_;  // layer inputs [L+1][T,H] fp32 (x_saved_[L] = final)
   bf16 *h_ = nullptr, *qkv_ = nullptr, *ofull_ = nullptr, *h2_ = nullptr, *gu_ = nullptr,
        *act_ = nullptr;
@@ -168,7 +198,7 @@ class Step {
   }
   int barrier_sp(cudaStream_t s);
   // layer pieces
-  int layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int& qb, int& ob);
+  int layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int slot);
   int layer_bwd(int l, Unit& u, float* grads);
   int head_fwd_bwd(Unit& u, float* grads);
   // ---- MoE / expert parallelism (step_moe.cpp)

@@ -58,6 +58,7 @@ def _run(world, model, plan, S, rows):
 
 PLANS = [
     (2, {"dp_replicate": 1, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1}, 1),
+    (2, {"dp_replicate": 1, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1, "recompute": "none"}, 1),
     (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 1, "micro_batch": 1}, 2),
     (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 1, "micro_batch": 1}, 2),
     (4, {"dp_replicate": 2, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1}, 2),

@@ -8,12 +8,12 @@ from tests.step_common import EXEC, cluster, compare_step, tiny_dense
 gpu = pytest.mark.gpu
 
 
-def _run(model, S, rows, single=False, trace=False):
+def _run(model, S, rows, single=False, trace=False, recompute="full"):
     from paper_2508_02317_b200.runtime import Session, synthetic_batch
 
     arch = model["modules"][0]["arch"]
     wl = {"seq_len": S, "micro_batch": rows, "global_batch": rows}
-    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": rows}
+    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": rows, "recompute": recompute}
     ex = dict(EXEC)
     ex["trace"] = trace
     s = Session(cluster(1), model, wl, plan, ex, rank=0, device=0)
@@ -31,6 +31,16 @@ def test_step_tiny_dense_matches_oracle(single):
     s, batch, plan, r = _run(model, 1024, 2, single)
     rep = compare_step([s], model, batch, plan, r.loss)
     assert r.launches > 0
+    s.close()
+
+
+@gpu
+def test_step_recompute_none_matches_oracle():
+    model = tiny_dense()
+    s, batch, plan, r = _run(model, 1024, 2, recompute="none")
+    compare_step([s], model, batch, plan, r.loss)
+    r2 = s.run()  # second step reuses the per-layer activation buffers
+    assert np.isfinite(r2.loss) and r2.loss < r.loss
     s.close()
 
 
