@@ -16,6 +16,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../runtime/gemm_api.h"
@@ -413,6 +414,11 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const KParams& kp
 
 }  // namespace
 
+bool gemm_make_map(void* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                   uint32_t box_inner, uint32_t box_outer) {
+  return make_map(static_cast<CUtensorMap*>(map), base, inner, outer, ld, box_inner, box_outer);
+}
+
 int num_sms() {
   if (!g_num_sms) {
     int dev = 0;
@@ -468,6 +474,30 @@ cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s) {
   int tiles;
   const int nblk = (g.N + BN - 1) / BN;
   kp.band = 1;
+  static const bool force_1cta = getenv("OPX_GEMM_1CTA") != nullptr;
+  if (!grouped && !force_1cta) {
+    // 2-CTA path: same traffic model with 256-row pair tiles and 74 pairs per wave
+    const double a_bytes = double(g.M) * g.K * 2, b_blk = 256.0 * g.K * 2;
+    const int mblk2 = (g.M + 255) / 256;
+    const double budget = 80e6, wave = num_sms() / 2;
+    double best = 1e300;
+    int band = 1;
+    for (int nb = 1;; nb = nb * 2 > nblk ? nblk : nb * 2) {
+      const double bands = double((nblk + nb - 1) / nb);
+      double b_traffic = double(nblk) * b_blk;
+      if (nb * b_blk > budget) {
+        const double m_per_wave = wave / nb < 1 ? 1 : wave / nb;
+        b_traffic *= double(mblk2) / m_per_wave;
+      }
+      const double tot = a_bytes * bands + b_traffic;
+      if (tot < best * 0.999) {
+        best = tot;
+        band = nb;
+      }
+      if (nb == nblk) break;
+    }
+    return gemm2_run(g, band, s);
+  }
   if (!grouped) {
     // Pick the raster band minimising a DRAM-traffic estimate: inside a band
     // the (band x 256)-row B panel should stay L2-resident while every m-block

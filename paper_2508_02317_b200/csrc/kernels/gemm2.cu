@@ -1,0 +1,328 @@
+// 2-CTA bf16 GEMM on tcgen05 (cta_group::2), sm_100a.
+//
+// A cluster of two CTAs (one TPC) computes a 256 x 256 output tile with one
+// tcgen05.mma.cta_group::2 stream issued by the leader CTA: each CTA stages
+// its 128 rows of A and its 128 rows (output columns) of B, so every byte
+// loaded from L2 feeds twice the MMA work of the 1-CTA 128 x 256 tile
+// (128 vs 85 FLOP/B) -- the 1-CTA kernel was L2->SM bandwidth bound
+// (profiles/r1_c1_n1_summary.txt: 85 % L2 hit, ~14.6 TB/s L2 reads).
+// Each CTA's TMEM holds its 128 accumulator rows x 256 columns (double
+// buffered); its four epilogue warps drain them with the same fused
+// epilogues as kernels/gemm.cu.  Grouped (MoE) GEMMs stay on the 1-CTA kernel.
+#include <cuda.h>
+
+#include "../runtime/gemm_api.h"
+#include "../runtime/kernels_api.h"
+#include "ptx.cuh"
+
+namespace opx {
+namespace {
+
+constexpr int BM = 128;   // rows per CTA (256 per pair)
+constexpr int BNP = 256;  // output columns per pair tile
+constexpr int BNC = 128;  // B rows staged per CTA
+constexpr int BK = 64, STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BYTES = BNC * BK * 2;  // 16 KB
+constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+constexpr int THREADS = 256;
+
+struct P2 {
+  int M, N, K, epi, band;
+  void* D;
+  int64_t ldd;
+  const float* R;
+  int64_t ldr;
+  __nv_bfloat16* D2;
+  int64_t ldd2;
+  float scale;
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ void tile_coords(const P2& p, int t, int& mb, int& nb) {
+  const int mblk = (p.M + 2 * BM - 1) / (2 * BM);
+  const int nblk = (p.N + BNP - 1) / BNP;
+  const int per_band = p.band * mblk;
+  const int b = t / per_band, r = t % per_band;
+  const int bw = min(p.band, nblk - b * p.band);
+  mb = r / bw;
+  nb = b * p.band + r % bw;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const P2 p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 2 * 128);  // both CTAs' epilogue threads (leader's is used)
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_pair(tmem_slot, 512);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int mblk = (p.M + 2 * BM - 1) / (2 * BM);
+  const int nblk = (p.N + BNP - 1) / BNP;
+  const int ntiles = mblk * nblk;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  const int nk = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        int mb, nb;
+        tile_coords(p, t, mb, nb);
+        const int m0 = mb * 2 * BM + int(rank) * BM;
+        const int n0 = nb * BNP + int(rank) * BNC;
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) ptx::mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+          const uint32_t bar = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+          uint8_t* a = sA + stage * A_BYTES;
+          uint8_t* b = sB + stage * B_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            ptx::tma_load_2d_pair(&tmA, bar, a, k0, m0);
+          } else {
+            ptx::tma_load_2d_pair(&tmA, bar, a, m0, k0);
+            ptx::tma_load_2d_pair(&tmA, bar, a + 8192, m0 + 64, k0);
+          }
+          if (!B_MN) {
+            ptx::tma_load_2d_pair(&tmB, bar, b, k0, n0);
+          } else {
+            ptx::tma_load_2d_pair(&tmB, bar, b, n0, k0);
+            ptx::tma_load_2d_pair(&tmB, bar, b + 8192, n0 + 64, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BNP, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = cid; t < ntiles; t += ncl, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BNP;
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = ptx::smem_u32(sA + stage * A_BYTES);
+            const uint32_t b_addr = ptx::smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = A_MN ? ptx::umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
+                                       : ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bd = B_MN ? ptx::umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
+                                       : ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+              ptx::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
+            ptx::mma_commit_pair(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) ptx::mma_commit_pair(&tfull[acc], 0x3);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs, own 128 rows) ----------------
+    const int ew = warp - 4;
+    int local = 0;
+    const uint32_t tempty_leader[2] = {ptx::mapa(ptx::smem_u32(&tempty[0]), 0),
+                                       ptx::mapa(ptx::smem_u32(&tempty[1]), 0)};
+    for (int t = cid; t < ntiles; t += ncl, ++local) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int row = mb * 2 * BM + int(rank) * BM + ew * 32 + lane;
+      const bool row_ok = row < p.M;
+      const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + acc * BNP;
+      if (p.epi == GEMM_EPI_SWIGLU) {
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t g[32], u[32];
+          ptx::tmem_ld32(tbase + ch * 32, g);
+          ptx::tmem_ld32(tbase + 128 + ch * 32, u);
+          ptx::tmem_wait_ld();
+          const int f0 = nb * 128 + ch * 32;
+          if (row_ok && f0 < p.N / 2) {
+            __nv_bfloat16* act = p.D2 + int64_t(row) * p.ldd2 + f0;
+            __nv_bfloat16* gu = p.D ? reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd +
+                                          nb * BNP + ch * 32
+                                    : nullptr;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 va, vg, vu;
+              uint32_t* pa = reinterpret_cast<uint32_t*>(&va);
+              uint32_t* pg = reinterpret_cast<uint32_t*>(&vg);
+              uint32_t* pu = reinterpret_cast<uint32_t*>(&vu);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 gf = ptx::unpack_bf16(ptx::pack_bf16(
+                    __uint_as_float(g[q * 8 + 2 * e]), __uint_as_float(g[q * 8 + 2 * e + 1])));
+                const float2 uf = ptx::unpack_bf16(ptx::pack_bf16(
+                    __uint_as_float(u[q * 8 + 2 * e]), __uint_as_float(u[q * 8 + 2 * e + 1])));
+                pa[e] = ptx::pack_bf16(silu(gf.x) * uf.x, silu(gf.y) * uf.y);
+                pg[e] = ptx::pack_bf16(gf.x, gf.y);
+                pu[e] = ptx::pack_bf16(uf.x, uf.y);
+              }
+              *reinterpret_cast<uint4*>(act + q * 8) = va;
+              if (gu) {
+                *reinterpret_cast<uint4*>(gu + q * 8) = vg;
+                *reinterpret_cast<uint4*>(gu + 128 + q * 8) = vu;
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int ch = 0; ch < BNP / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + ch * 32, v);
+          ptx::tmem_wait_ld();
+          const int col0 = nb * BNP + ch * 32;
+          if (!row_ok || col0 >= p.N) continue;
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.scale;
+          const bool full_chunk = col0 + 32 <= p.N;
+          if (p.epi == GEMM_EPI_BF16) {
+            __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd + col0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (!full_chunk && col0 + q * 8 >= p.N) break;
+              uint4 o;
+              o.x = ptx::pack_bf16(f[q * 8 + 0], f[q * 8 + 1]);
+              o.y = ptx::pack_bf16(f[q * 8 + 2], f[q * 8 + 3]);
+              o.z = ptx::pack_bf16(f[q * 8 + 4], f[q * 8 + 5]);
+              o.w = ptx::pack_bf16(f[q * 8 + 6], f[q * 8 + 7]);
+              *reinterpret_cast<uint4*>(d + q * 8) = o;
+            }
+          } else {
+            float* d = reinterpret_cast<float*>(p.D) + int64_t(row) * p.ldd + col0;
+            const float* r = nullptr;
+            if (p.epi == GEMM_EPI_F32_RESID) r = p.R + int64_t(row) * p.ldr + col0;
+            if (p.epi == GEMM_EPI_F32_ACCUM) r = d;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (!full_chunk && col0 + q * 4 >= p.N) break;
+              float4 o = make_float4(f[q * 4 + 0], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
+              if (r) {
+                const float4 rv = *reinterpret_cast<const float4*>(r + q * 4);
+                o.x += rv.x;
+                o.y += rv.y;
+                o.z += rv.z;
+                o.w += rv.w;
+              }
+              *reinterpret_cast<float4*>(d + q * 4) = o;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive_cluster(tempty_leader[acc]);
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, 512);
+}
+
+template <bool A_MN, bool B_MN>
+cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, int grid,
+                    cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<A_MN, B_MN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  ++g_kernel_launches;
+  gemm_tc2_kernel<A_MN, B_MN><<<grid, THREADS, SMEM, s>>>(a, b, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
+  if (g.groups) return cudaErrorNotSupported;
+  CUtensorMap ma, mb;
+  bool ok = !g.a_mn ? gemm_make_map(&ma, g.A, uint64_t(g.K), uint64_t(g.M), g.lda, BK, BM)
+                    : gemm_make_map(&ma, g.A, uint64_t(g.M), uint64_t(g.K), g.lda, 64, BK);
+  ok = ok && (!g.b_mn ? gemm_make_map(&mb, g.B, uint64_t(g.K), uint64_t(g.N), g.ldb, BK, BNC)
+                      : gemm_make_map(&mb, g.B, uint64_t(g.N), uint64_t(g.K), g.ldb, 64, BK));
+  if (!ok) return cudaErrorInvalidValue;
+  P2 p;
+  p.M = g.M;
+  p.N = g.N;
+  p.K = g.K;
+  p.epi = g.epi;
+  p.band = band < 1 ? 1 : band;
+  p.D = g.D;
+  p.ldd = g.ldd;
+  p.R = g.R;
+  p.ldr = g.ldr;
+  p.D2 = g.D2;
+  p.ldd2 = g.ldd2;
+  p.scale = g.scale == 0.f ? 1.f : g.scale;
+  const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BNP - 1) / BNP);
+  int clusters = num_sms() / 2;
+  if (tiles < clusters) clusters = tiles;
+  const int grid = 2 * (clusters < 1 ? 1 : clusters);
+  if (!g.a_mn && !g.b_mn) return launch2<false, false>(ma, mb, p, grid, s);
+  if (!g.a_mn && g.b_mn) return launch2<false, true>(ma, mb, p, grid, s);
+  if (g.a_mn && !g.b_mn) return launch2<true, false>(ma, mb, p, grid, s);
+  return launch2<true, true>(ma, mb, p, grid, s);
+}
+
+}  // namespace opx

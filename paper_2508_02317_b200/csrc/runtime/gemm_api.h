@@ -49,6 +49,12 @@ struct GemmDesc {
 };
 
 cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s);
+// 2-CTA (cta_group::2, 256x256 per CTA pair) path for plain GEMMs; gemm_run
+// dispatches to it unless OPX_GEMM_1CTA is set.
+cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s);
+// 2-D bf16 TMA map (inner contiguous dim, outer dim, row stride in elements), SW128.
+bool gemm_make_map(void* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                   uint32_t box_inner, uint32_t box_outer);
 int num_sms();
 
 }  // namespace opx
