@@ -333,7 +333,8 @@ def main():
                      "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
                      "flops_per_launch": mlp_flops, "launch_ms": node_s * 1e3},
-        "phase_share": {k: round(v / tot, 4) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:12]},
+        "phase_share": {k: round(v / tot, 4) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:16]},
+        "node_ms": {k: round(v * 1e3, 2) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:24]},
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and n == 1:

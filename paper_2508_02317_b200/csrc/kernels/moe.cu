@@ -25,42 +25,57 @@ using bf16 = __nv_bfloat16;
 // router logits: logits[t, e] = sum_k h[t,k] * w[e,k], k ascending, fmul/fadd rn
 // block: 128 experts x 16 tokens; K staged through smem in chunks of 64
 // ---------------------------------------------------------------------------
-constexpr int RT = 16, RK = 64;
-__global__ void __launch_bounds__(128) router_kernel(const bf16* __restrict__ h,
+constexpr int RT = 64, RE = 128, RK = 32;  // block tile: 64 tokens x 128 experts, K chunks of 32
+// 256 threads; thread (ty, tx): tokens ty*4 .. +3, experts tx + 16*j (j < 8).
+__global__ void __launch_bounds__(256) router_kernel(const bf16* __restrict__ h,
                                                      const bf16* __restrict__ w,
                                                      float* __restrict__ logits, int T, int H,
                                                      int E) {
-  __shared__ float sh[RT][RK];
-  __shared__ float sw[128][RK + 1];
-  const int t0 = blockIdx.x * RT;
-  const int e0 = blockIdx.y * 128;
-  const int e = e0 + threadIdx.x;
-  float acc[RT];
+  __shared__ float sh[RK][RT + 4];
+  __shared__ float sw[RK][RE + 4];
+  const int t0 = blockIdx.x * RT, e0 = blockIdx.y * RE;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][8];
 #pragma unroll
-  for (int i = 0; i < RT; ++i) acc[i] = 0.f;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
   for (int k0 = 0; k0 < H; k0 += RK) {
-    for (int i = threadIdx.x; i < RT * RK; i += 128) {
+    for (int i = threadIdx.x; i < RT * RK; i += 256) {
       const int tt = i / RK, kk = i % RK;
       const int t = t0 + tt;
-      sh[tt][kk] = t < T ? __bfloat162float(h[int64_t(t) * H + k0 + kk]) : 0.f;
+      sh[kk][tt] = t < T ? __bfloat162float(h[int64_t(t) * H + k0 + kk]) : 0.f;
     }
-    for (int i = threadIdx.x; i < 128 * RK; i += 128) {
+    for (int i = threadIdx.x; i < RE * RK; i += 256) {
       const int ee = i / RK, kk = i % RK;
-      sw[ee][kk] = (e0 + ee) < E ? __bfloat162float(w[int64_t(e0 + ee) * H + k0 + kk]) : 0.f;
+      sw[kk][ee] = (e0 + ee) < E ? __bfloat162float(w[int64_t(e0 + ee) * H + k0 + kk]) : 0.f;
     }
     __syncthreads();
 #pragma unroll 4
     for (int kk = 0; kk < RK; ++kk) {
-      const float wv = sw[threadIdx.x][kk];
+      float hv[4], wv[8];
 #pragma unroll
-      for (int tt = 0; tt < RT; ++tt) acc[tt] = __fadd_rn(acc[tt], __fmul_rn(sh[tt][kk], wv));
+      for (int i = 0; i < 4; ++i) hv[i] = sh[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wv[j] = sw[kk][tx + 16 * j];
+      // k ascending, separately rounded multiply and add: the CPU oracle's order
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(hv[i], wv[j]));
     }
     __syncthreads();
   }
-  if (e < E)
 #pragma unroll
-    for (int tt = 0; tt < RT; ++tt)
-      if (t0 + tt < T) logits[int64_t(t0 + tt) * E + e] = acc[tt];
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + ty * 4 + i;
+    if (t >= T) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = e0 + tx + 16 * j;
+      if (e < E) logits[int64_t(t) * E + e] = acc[i][j];
+    }
+  }
 }
 
 // top-k per token (one warp per token), E <= 256, k <= 16
@@ -196,6 +211,21 @@ struct Layout {
   int ep, E, El;
 };
 
+// One warp copies a W-element bf16 row (W % 256 == 0 for the fast path): all
+// loads of the row are issued before the (possibly remote, NVLink) stores.
+__device__ __forceinline__ void copy_row(bf16* __restrict__ o, const bf16* __restrict__ s, int W,
+                                         int lane) {
+  int c = lane * 8;
+  for (; c + 7 * 256 < W; c += 8 * 256) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const uint4*>(s + c + u * 256);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) *reinterpret_cast<uint4*>(o + c + u * 256) = v[u];
+  }
+  for (; c < W; c += 256) *reinterpret_cast<uint4*>(o + c) = *reinterpret_cast<const uint4*>(s + c);
+}
+
 __device__ __forceinline__ int seg_len(const int* counts_all, const Layout& L, int e) {
   int n = 0;
   for (int s = 0; s < L.ep; ++s) n += counts_all[s * L.E + e];
@@ -279,8 +309,7 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
     const int row = st[d * (L.El + 1) + le] + before + (pos - excl[e]);
     const bf16* s = src + int64_t(per_pair ? pos : p / k) * ld_src;
     bf16* o = dst[d] + int64_t(row) * ld_dst;
-    for (int c = lane * 8; c < W; c += 256)
-      *reinterpret_cast<uint4*>(o + c) = *reinterpret_cast<const uint4*>(s + c);
+    copy_row(o, s, W, lane);
   }
 }
 
@@ -301,8 +330,7 @@ __global__ void combine_kernel(const bf16* __restrict__ src, int64_t ld_src,
     for (int e2 = 0; e2 < e; ++e2) excl_src += counts_all[s * L.E + e2];
     const bf16* a = src + int64_t(g_start[le] + r) * ld_src;
     bf16* o = dst[s] + int64_t(excl_src + off) * ld_dst;
-    for (int c = lane * 8; c < W; c += 256)
-      *reinterpret_cast<uint4*>(o + c) = *reinterpret_cast<const uint4*>(a + c);
+    copy_row(o, a, W, lane);
   }
 }
 
@@ -360,17 +388,31 @@ __global__ void combine_bwd_kernel(const float* __restrict__ dx, const bf16* __r
 
 // router backward (renormalised softmax over the selected experts):
 //   dsel_j = w_j (dw_j - sum_i w_i dw_i);  dlogits[t, idx_j] = dsel_j, else 0 (bf16)
+// one warp per token: coalesced zeroing of the row, then the k scattered values
 __global__ void router_bwd_kernel(const float* __restrict__ dw, const float* __restrict__ wts,
                                   const int* __restrict__ idx, int T, int k, int E,
                                   bf16* __restrict__ dlogits) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (t >= T) return;
   bf16* row = dlogits + int64_t(t) * E;
-  for (int e = 0; e < E; ++e) row[e] = __float2bfloat16_rn(0.f);
+  for (int e = lane * 2; e < E; e += 64) *reinterpret_cast<uint32_t*>(row + e) = 0u;
   float s = 0.f;
   for (int j = 0; j < k; ++j) s += wts[t * k + j] * dw[t * k + j];
-  for (int j = 0; j < k; ++j)
-    row[idx[t * k + j]] = __float2bfloat16_rn(wts[t * k + j] * (dw[t * k + j] - s));
+  __syncwarp();
+  if (lane < k)
+    row[idx[t * k + lane]] = __float2bfloat16_rn(wts[t * k + lane] * (dw[t * k + lane] - s));
+}
+
+// out[i] = sum_g part[g, i]  (fixed order)
+__global__ void sum_partials_kernel(const float* __restrict__ part, int G, int64_t n,
+                                    float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    for (int g = 0; g < G; ++g) acc += part[int64_t(g) * n + i];
+    out[i] = acc;
+  }
 }
 
 // every EP rank receives this rank's per-expert counts as row `me` of its table
@@ -430,9 +472,9 @@ __global__ void swiglu_bwd_grouped_kernel(const bf16* __restrict__ dact, const b
 cudaError_t k_moe_router(const __nv_bfloat16* h, const __nv_bfloat16* w, float* logits, int T,
                          int H, int E, cudaStream_t s) {
   if (H % RK) return cudaErrorInvalidValue;
-  dim3 grid((T + RT - 1) / RT, (E + 127) / 128);
+  dim3 grid((T + RT - 1) / RT, (E + RE - 1) / RE);
   ++g_kernel_launches;
-  router_kernel<<<grid, 128, 0, s>>>(h, w, logits, T, H, E);
+  router_kernel<<<grid, 256, 0, s>>>(h, w, logits, T, H, E);
   return cudaGetLastError();
 }
 
@@ -521,8 +563,17 @@ cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t l
 
 cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, int T, int k, int E,
                              __nv_bfloat16* dlogits, cudaStream_t s) {
+  if (k > 32 || E % 2) return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  router_bwd_kernel<<<(T + 127) / 128, 128, 0, s>>>(dw, wts, idx, T, k, E, dlogits);
+  router_bwd_kernel<<<(T * 32 + 255) / 256, 256, 0, s>>>(dw, wts, idx, T, k, E, dlogits);
+  return cudaGetLastError();
+}
+
+cudaError_t k_sum_partials(const float* part, int G, int64_t n, float* out, cudaStream_t s) {
+  int64_t b = (n + 255) / 256;
+  if (b > num_sms() * 8) b = num_sms() * 8;
+  ++g_kernel_launches;
+  sum_partials_kernel<<<int(b), 256, 0, s>>>(part, G, n, out);
   return cudaGetLastError();
 }
 

@@ -125,6 +125,7 @@ cudaError_t k_moe_publish_counts(const int* counts, int* const* tables, int ep, 
 cudaError_t k_moe_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __nv_bfloat16* dgu,
                              const int* g_start, const int* g_rows, const int* g_rows_pad, int El,
                              int F, int max_rows, cudaStream_t s);
+cudaError_t k_sum_partials(const float* part, int G, int64_t n, float* out, cudaStream_t s);
 cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, int T, int k, int E,
                              __nv_bfloat16* dlogits, cudaStream_t s);
 }  // namespace opx

@@ -225,6 +225,10 @@ class Step {
   int *r_idx_ = nullptr, *r_pos_ = nullptr, *r_pairat_ = nullptr, *r_cnt_ = nullptr,
       *r_excl_ = nullptr, *r_hist_ = nullptr, *g_start_ = nullptr, *g_rows_ = nullptr,
       *g_rows_pad_ = nullptr, *g_total_ = nullptr;
+  float* wr_part_ = nullptr;          // split-K partials of the router wgrad
+  int* wr_gs_ = nullptr;              // chunk starts / rows for the split
+  int* wr_gr_ = nullptr;
+  int wr_split_ = 1;
   bf16 *gu_e_ = nullptr, *act_e_ = nullptr, *y_e_ = nullptr, *dact_e_ = nullptr, *dgu_e_ = nullptr,
        *dx_e_ = nullptr, *dyp_ = nullptr, *dlogits_ = nullptr;
   char* ep_peer(int j, size_t off) {

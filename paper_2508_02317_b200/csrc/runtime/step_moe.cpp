@@ -172,6 +172,24 @@ int Step::moe_alloc() {
   for (void* q : {(void*)gu_e_, (void*)act_e_, (void*)y_e_, (void*)dact_e_, (void*)dgu_e_,
                   (void*)dx_e_, (void*)dyp_, (void*)d_dxback_peers_})
     if (!q) return cuda_fail(cudaErrorMemoryAllocation, "MoE scratch");
+  // router wgrad dWr[E, H] = dlogits^T h2 has only E x H / 256^2 output tiles
+  // and K = T: split K into chunks (grouped-K GEMM) and reduce the partials.
+  wr_split_ = 16;
+  while (wr_split_ > 1 && (T / size_t(wr_split_)) < 256) wr_split_ /= 2;
+  {
+    const int chunk = int((T + size_t(wr_split_) - 1) / size_t(wr_split_) + 63) / 64 * 64;
+    std::vector<int> gs(static_cast<size_t>(wr_split_)), gr(static_cast<size_t>(wr_split_));
+    for (int g = 0; g < wr_split_; ++g) {
+      gs[size_t(g)] = g * chunk;
+      gr[size_t(g)] = chunk;
+    }
+    wr_gs_ = alloc<int>(size_t(wr_split_));
+    wr_gr_ = alloc<int>(size_t(wr_split_));
+    wr_part_ = alloc<float>(size_t(wr_split_) * E * H, false);
+    if (!wr_gs_ || !wr_gr_ || !wr_part_) return cuda_fail(cudaErrorMemoryAllocation, "router split");
+    CU(cudaMemcpy(wr_gs_, gs.data(), gs.size() * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(wr_gr_, gr.data(), gr.size() * 4, cudaMemcpyHostToDevice));
+  }
   route_idx_.assign(size_t(a_.layers), nullptr);
   for (int l = 0; l < a_.layers; ++l)
     if (a_.is_moe_layer(l)) route_idx_[size_t(l)] = alloc<int>(P, false);
@@ -236,6 +254,17 @@ GemmDesc grouped(int M, int N, int K, const bf16* A, int64_t lda, bool amn, cons
 }  // namespace
 
 int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out) {
+  const std::string pre = std::string(in_recompute_ ? "bwd" : "fwd") + ".layer" + std::to_string(l) + ".m0.";
+  const std::string ph = std::string(in_recompute_ ? "bwd" : "fwd") + ".layer" + std::to_string(l);
+  cudaEvent_t e0 = nullptr;
+  auto mk = [&](const char* name) {
+    if (!ex_.trace) return;
+    cudaEvent_t e1 = ev();
+    cudaEventRecord(e1, cs_);
+    if (e0) mark(pre + name, ph, 0, e0, e1);
+    e0 = e1;
+  };
+  mk("");
   const int T = T_, H = H_, E = E_, k = topk_, Fe = Fe_, P = T_ * topk_;
   const bf16* Wr = u.full + u.params[6].off;
   const bf16* Wgu = eu.full + eu.params[0].off;
@@ -249,12 +278,14 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
     CU(cudaMemcpyAsync(route_idx_[size_t(l)], r_idx_, size_t(P) * sizeof(int),
                        cudaMemcpyDeviceToDevice, cs_));
   CU(k_moe_sort(r_idx_, P, E, r_hist_, r_cnt_, r_excl_, r_pos_, r_pairat_, cs_));
+  mk("router");
   CU(k_moe_publish_counts(r_cnt_, d_count_tables_, ep_, ep_i_, E, cs_));
   TRY(barrier_ep(cs_));
   CU(k_moe_groups(counts_all, ep_, E, ep_i_, g_start_, g_rows_, g_rows_pad_, g_total_, cs_));
   CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
                     d_xrecv_peers_, H, H, cs_));
   TRY(barrier_ep(cs_));
+  mk("a2a_dispatch");
   CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
   {
     // gate|up pre-activations are only needed by the backward (recompute pass)
@@ -269,15 +300,28 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   CU(gemm_run(grouped(0, H, Fe, act_e_, Fe, false, Wd, Fe, false, GEMM_EPI_BF16, y_e_, H, El_, 0,
                       g_start_, g_rows_, cap_rows_, 0),
               cs_));
+  mk("experts");
   CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_yback_peers_, H, H,
                    int(cap_rows_), cs_));
   TRY(barrier_ep(cs_));
+  mk("a2a_combine");
   CU(k_moe_unpermute(yback, H, r_pos_, r_wts_, T, k, H, x2, x_out, cs_));
+  mk("unpermute");
   return OPX_OK;
 }
 
 int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh2) {
-  (void)l;
+  const std::string pre = "bwd.layer" + std::to_string(l) + ".m0.";
+  const std::string ph = "bwd.layer" + std::to_string(l);
+  cudaEvent_t e0 = nullptr;
+  auto mk = [&](const char* name) {
+    if (!ex_.trace) return;
+    cudaEvent_t e1 = ev();
+    cudaEventRecord(e1, cs_);
+    if (e0) mark(pre + name, ph, 0, e0, e1);
+    e0 = e1;
+  };
+  mk("");
   const int T = T_, H = H_, E = E_, k = topk_, Fe = Fe_, P = T_ * topk_;
   const bf16* Wr = u.full + u.params[6].off;
   const bf16* Wgu = eu.full + eu.params[0].off;
@@ -293,6 +337,7 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
   CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
                     d_dyrecv_peers_, H, H, cs_));
   TRY(barrier_ep(cs_));
+  mk("a2a_combine_grad");
   CU(k_moe_zero_pad(dyrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
   // experts backward (grouped GEMMs; wgrad K = 128-padded segment rows)
   CU(gemm_run(grouped(0, Fe, H, dyrecv, H, false, Wd, Fe, true, GEMM_EPI_BF16, dact_e_, Fe, El_, 0,
@@ -312,9 +357,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
                       int64_t(2) * Fe * H),
               cs_));
   // a2a_dispatch_grad: input grads travel back to the token owners
+  mk("experts");
   CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
                    int(cap_rows_), cs_));
   TRY(barrier_ep(cs_));
+  mk("a2a_dispatch_grad");
   CU(k_moe_unpermute(dxback, H, r_pos_, nullptr, T, k, H, nullptr, dh2, cs_));
   // router: renormalised-softmax backward, then dh2 += dlogits . Wr, dWr = dlogits^T h2
   CU(k_moe_router_bwd(r_dw_, r_wts_, r_idx_, T, k, E, dlogits_, cs_));
@@ -335,22 +382,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
     g.ldr = H;
     CU(gemm_run(g, cs_));
   }
-  {
-    GemmDesc g;
-    g.M = E;
-    g.N = H;
-    g.K = T;
-    g.A = dlogits_;
-    g.lda = E;
-    g.a_mn = true;
-    g.B = h2_;
-    g.ldb = H;
-    g.b_mn = true;
-    g.epi = GEMM_EPI_F32;
-    g.D = G + u.params[6].off;
-    g.ldd = H;
-    CU(gemm_run(g, cs_));
-  }
+  CU(gemm_run(grouped(E, H, 0, dlogits_, E, true, h2_, H, true, GEMM_EPI_F32, wr_part_, H,
+                      wr_split_, 1, wr_gs_, wr_gr_, T, int64_t(E) * H),
+              cs_));
+  CU(k_sum_partials(wr_part_, wr_split_, int64_t(E) * H, G + u.params[6].off, cs_));
+  mk("router");
   return OPX_OK;
 }
 
