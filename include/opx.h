@@ -151,6 +151,14 @@ int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, 
                     const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
                     int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,
                     int N, int hq, int hk, float scale, void* stream);
+/* Same backward with fp32 dense [N, hk, 128] dK/dV outputs; each GQA group is
+ * split across kv_splits CTAs (0 = automatic) whose partials are summed by TMA
+ * bulk reduce-add.  This is the form the training step uses. */
+int opx_attn_bwd_tc_f32kv(const void* q, const void* k, const void* v, const void* o,
+                          const float* lse, const void* dout, float* dq_acc, float* dk_acc,
+                          float* dv_acc, float* delta, int64_t ld_q, int64_t ld_kv,
+                          const int32_t* seq_start, const int32_t* seq_end, int N, int hq, int hk,
+                          float scale, int kv_splits, void* stream);
 /* Single-rank Ulysses relayout (sp == 1 path) with RoPE, for testing. */
 int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void* v_full,
                   int hq, int hk, int rows, int S, const int32_t* pos, const float* inv_freq,

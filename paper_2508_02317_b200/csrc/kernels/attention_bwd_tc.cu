@@ -1,8 +1,12 @@
 // Causal packed-varlen GQA flash attention BACKWARD on tcgen05 (sm_100a).
 //
-// One CTA per (128-key tile, kv head).  K and V stay in smem; the CTA walks
-// the q heads of its GQA group and the 64-query tiles that can see its keys
+// One CTA per (128-key tile, kv head, head split).  K and V stay in smem; the
+// CTA walks its share of the q heads of the GQA group (all of them when
+// kv_splits == 1) and the 64-query tiles that can see its keys
 // (q in [k0, seq_end(last key))), with Q/dO double-buffered by TMA.
+// kv_splits > 1 shortens the CTAs (better tail balance when there are few key
+// tiles, e.g. one kv head per rank under Ulysses); the per-split dK/dV
+// partials are then summed by TMA bulk reduce-add into fp32 accumulators.
 //
 //   TMEM: S^T [0,64) | dP^T [64,128) | dQ^T [128,192) | dV [256,384) | dK [384,512)
 //   per q tile i (MMA warp, one elected lane):
@@ -18,8 +22,10 @@
 // The S^T/dP^T MMAs of tile i+1 overlap the dQ readout/reduction of tile i.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
+#include "../runtime/gemm_api.h"
 #include "../runtime/kernels_api.h"
 #include "attn_common.cuh"
 #include "ptx.cuh"
@@ -50,6 +56,8 @@ struct Params {
   int N, hq, hk;
   float scale, scale_log2;
   int skip_dq;  // debug: measure without the dQ reduction
+  int splits;   // q-head splits per kv head
+  int f32kv;    // dK/dV go to fp32 [N, hk, 128] through tdk/tdv (reduce-add if splits > 1)
 };
 
 __device__ __forceinline__ uint64_t kd(uint32_t base, int k, int blk) {
@@ -63,7 +71,8 @@ __device__ __forceinline__ void bar_sync_softmax() { asm volatile("bar.sync 1, 2
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
-                       const __grid_constant__ CUtensorMap tdq, const Params p) {
+                       const __grid_constant__ CUtensorMap tdq, const __grid_constant__ CUtensorMap tdk,
+                       const __grid_constant__ CUtensorMap tdv, const Params p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic on the __shared__ array keeps the
   // shared address space (no generic LD/ST on the hot path).
@@ -84,12 +93,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k0 = blockIdx.x * BK;
-  const int kh = blockIdx.y;
+  const int kh = blockIdx.y / p.splits, sidx = blockIdx.y % p.splits;
   const int G = p.hq / p.hk;
+  const int hbase = kh * G + (sidx * G) / p.splits;
+  const int nh = ((sidx + 1) * G) / p.splits - (sidx * G) / p.splits;
   const int klast = min(k0 + BK, p.N) - 1;
   const int qend = p.seq_end[klast];
   const int nq = (qend - k0 + BQ - 1) / BQ;
-  const int niter = G * nq;
+  const int niter = nh * nq;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tq);
@@ -125,7 +136,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tma_load_3d(&tv, kv_full, smem + OFF_V + 16384, 64, kh, k0);
       for (int it = 0; it < niter; ++it) {
         const int st = it & 1;
-        const int h = kh * G + it / nq;
+        const int h = hbase + it / nq;
         const int q0 = k0 + (it % nq) * BQ;
         if (it >= 2) ptx::mbar_wait(&qdo_empty[st], ((it >> 1) - 1) & 1);
         ptx::mbar_expect_tx(&qdo_full[st], 4 * 8192);
@@ -203,7 +214,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool issuer = threadIdx.x == 64;
     auto load_cols = [&](int it) {  // lse/delta/seq_start of tile it -> smem buffer it&1
       if (half == 0 && r < BQ) {
-        const int h = kh * G + it / nq;
+        const int h = hbase + it / nq;
         const int q = k0 + (it % nq) * BQ + r;
         const bool ok = q < p.N;
         const int buf = it & 1;
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
     // dQ^T(j) (thread: d row r, q columns c0..c0+31) -> fp32 staging [q][d] -> bulk reduce-add
     auto drain_dq = [&](int j) {
-      const int h = kh * G + j / nq;
+      const int h = hbase + j / nq;
       const int q0 = k0 + (j % nq) * BQ;
       ptx::mbar_wait(dq_full, j & 1);
       ptx::tc_fence_after();
@@ -305,6 +316,61 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (niter > 0) drain_dq(niter - 1);
     if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (p.f32kv) {
+      // ---- dK (scaled), dV -> fp32 SW128 staging [4 col chunks][128 rows][32]
+      // over the free Q/dO/P/S/stage buffers, then TMA store / reduce-add.
+      bar_sync_softmax();  // dQ staging reads done
+      uint8_t* stk = smem + OFF_Q;
+      uint8_t* stv = smem + OFF_Q + 65536;
+#pragma unroll 1
+      for (int c = half * 2; c < half * 2 + 2; ++c) {
+        uint32_t a[32], b[32];
+        ptx::tmem_ld32(TDK + lane_off + c * 32, a);
+        ptx::tmem_ld32(TDV + lane_off + c * 32, b);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t off = c * 16384 + r * 128 + (((q ^ (r & 7))) << 4);
+          *reinterpret_cast<float4*>(stk + off) =
+              make_float4(__uint_as_float(a[4 * q]) * p.scale, __uint_as_float(a[4 * q + 1]) * p.scale,
+                          __uint_as_float(a[4 * q + 2]) * p.scale, __uint_as_float(a[4 * q + 3]) * p.scale);
+          *reinterpret_cast<float4*>(stv + off) =
+              make_float4(__uint_as_float(b[4 * q]), __uint_as_float(b[4 * q + 1]),
+                          __uint_as_float(b[4 * q + 2]), __uint_as_float(b[4 * q + 3]));
+        }
+      }
+      ptx::fence_proxy_async();
+      bar_sync_softmax();
+      if (issuer) {
+        for (int c = 0; c < 4; ++c) {
+          if (p.splits > 1) {
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tdk)),
+                "r"(ptx::smem_u32(stk + c * 16384)), "r"(c * 32), "r"(kh), "r"(k0)
+                : "memory");
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tdv)),
+                "r"(ptx::smem_u32(stv + c * 16384)), "r"(c * 32), "r"(kh), "r"(k0)
+                : "memory");
+          } else {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tdk)),
+                "r"(ptx::smem_u32(stk + c * 16384)), "r"(c * 32), "r"(kh), "r"(k0)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tdv)),
+                "r"(ptx::smem_u32(stv + c * 16384)), "r"(c * 32), "r"(kh), "r"(k0)
+                : "memory");
+          }
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    } else {
     // ---- dK (scaled), dV rows -> bf16 (each thread: 64 of the 128 d columns)
     const bool ok = key < p.N;
     bf16* dkr = p.dk + int64_t(ok ? key : 0) * p.lddk + int64_t(kh) * D;
@@ -335,6 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -361,15 +428,36 @@ __global__ void delta_kernel(const bf16* __restrict__ dout, int64_t lddo, const 
 
 }  // namespace
 
-// dq_acc must be a dense [N, hq, 128] fp32 buffer (it is zeroed here).
+// dq_acc must be a dense [N, hq, 128] fp32 buffer (it is zeroed here).  With
+// dk_acc/dv_acc set, dK/dV are written as dense fp32 [N, hk, 128] (and dk/dv
+// are unused); kv_splits (0 = auto) then splits each GQA group across CTAs.
+int attn_bwd_kv_splits(int N, int hq, int hk) {
+  const int G = hq / hk;
+  if (const char* e = getenv("OPX_ATTN_KV_SPLITS")) return std::max(1, std::min(G, atoi(e)));
+  (void)N;
+  // One q head per CTA measured best on B200 for both C1 layouts (32K tokens,
+  // 7q/1kv: 437 -> 631 TFLOP/s; 28q/4kv: 600 -> 678): the causal tail of long
+  // early-key tiles dominates, and the extra fp32 reduce traffic stays in L2.
+  return G;
+}
+
 cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
   if (a.N <= 0) return cudaSuccess;
   if (a.hq % a.hk) return cudaErrorInvalidValue;
-  CUtensorMap mq, mk, mv, mdo, mdq;
+  const bool f32kv = a.dk_acc && a.dv_acc;
+  const int splits = f32kv ? (a.kv_splits > 0 ? std::min(a.kv_splits, a.hq / a.hk)
+                                              : attn_bwd_kv_splits(a.N, a.hq, a.hk))
+                           : 1;
+  CUtensorMap mq, mk, mv, mdo, mdq, mdk, mdv;
+  if (f32kv) {
+    if (!head_map_f32_sw(&mdk, a.dk_acc, a.N, a.hk, BK) || !head_map_f32_sw(&mdv, a.dv_acc, a.N, a.hk, BK))
+      return cudaErrorInvalidValue;
+  }
   if (!head_map(&mq, a.q, a.N, a.hq, a.ldq, BQ) || !head_map(&mk, a.k, a.N, a.hk, a.ldk, BK) ||
       !head_map(&mv, a.v, a.N, a.hk, a.ldv, BK) || !head_map(&mdo, a.dout, a.N, a.hq, a.lddo, BQ) ||
       !head_map_f32(&mdq, a.dq_acc, a.N, a.hq, BQ))
     return cudaErrorInvalidValue;
+  if (!f32kv) mdk = mdv = mdq;  // unused
   static bool cfg = false;
   if (!cfg) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -381,6 +469,10 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
   delta_kernel<<<int((warps * 32 + 255) / 256), 256, 0, s>>>(a.dout, a.lddo, a.o, a.ldo, a.delta, a.N, a.hq);
   cudaError_t e = cudaMemsetAsync(a.dq_acc, 0, size_t(a.N) * a.hq * D * sizeof(float), s);
   if (e != cudaSuccess) return e;
+  if (f32kv && splits > 1) {
+    if ((e = cudaMemsetAsync(a.dk_acc, 0, size_t(a.N) * a.hk * D * sizeof(float), s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(a.dv_acc, 0, size_t(a.N) * a.hk * D * sizeof(float), s)) != cudaSuccess) return e;
+  }
   Params p;
   p.lse = a.lse;
   p.delta = a.delta;
@@ -396,9 +488,11 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
   p.scale = a.scale;
   p.scale_log2 = a.scale * LOG2E;
   p.skip_dq = getenv("OPX_DEBUG_SKIP_DQ") != nullptr;
-  dim3 grid((a.N + BK - 1) / BK, a.hk);
+  p.splits = splits;
+  p.f32kv = f32kv;
+  dim3 grid((a.N + BK - 1) / BK, a.hk * splits);
   ++g_kernel_launches;
-  attn_bwd_tc_kernel<<<grid, THREADS, SMEM, s>>>(mq, mk, mv, mdo, mdq, p);
+  attn_bwd_tc_kernel<<<grid, THREADS, SMEM, s>>>(mq, mk, mv, mdo, mdq, mdk, mdv, p);
   return cudaGetLastError();
 }
 

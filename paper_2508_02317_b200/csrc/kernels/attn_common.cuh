@@ -71,5 +71,20 @@ static inline bool head_map_f32(CUtensorMap* m, const void* base, int N, int hea
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 [tokens, heads, 128] map with box {32, 1, rows}, SW128: the smem side is
+// [rows][32 floats] with 16-B chunks XOR-swizzled by (row & 7), so one thread
+// per row can write its 32 columns without bank conflicts (dK/dV partials).
+static inline bool head_map_f32_sw(CUtensorMap* m, const void* base, int N, int heads, int rows) {
+  auto enc = enc_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {128, cuuint64_t(heads), cuuint64_t(N)};
+  cuuint64_t strides[2] = {512, cuuint64_t(heads) * 512};
+  cuuint32_t box[3] = {32, 1, uint32_t(rows)};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace attn
 }  // namespace opx

@@ -404,6 +404,37 @@ int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, 
   OPX_CALL(k_attn_bwd_tc(a, static_cast<cudaStream_t>(stream)), "opx_attn_bwd_tc");
 }
 
+int opx_attn_bwd_tc_f32kv(const void* q, const void* k, const void* v, const void* o,
+                          const float* lse, const void* dout, float* dq_acc, float* dk_acc,
+                          float* dv_acc, float* delta, int64_t ld_q, int64_t ld_kv,
+                          const int32_t* seq_start, const int32_t* seq_end, int N, int hq, int hk,
+                          float scale, int kv_splits, void* stream) {
+  AttnArgs a{};
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.k = static_cast<const __nv_bfloat16*>(k);
+  a.v = static_cast<const __nv_bfloat16*>(v);
+  a.o = static_cast<__nv_bfloat16*>(const_cast<void*>(o));
+  a.lse = const_cast<float*>(lse);
+  a.ldq = ld_q;
+  a.ldk = ld_kv;
+  a.ldv = ld_kv;
+  a.ldo = ld_q;
+  a.seq_start = seq_start;
+  a.seq_end = seq_end;
+  a.N = N;
+  a.hq = hq;
+  a.hk = hk;
+  a.scale = scale;
+  a.dout = static_cast<const __nv_bfloat16*>(dout);
+  a.lddo = ld_q;
+  a.dq_acc = dq_acc;
+  a.dk_acc = dk_acc;
+  a.dv_acc = dv_acc;
+  a.kv_splits = kv_splits;
+  a.delta = delta;
+  OPX_CALL(k_attn_bwd_tc(a, static_cast<cudaStream_t>(stream)), "opx_attn_bwd_tc_f32kv");
+}
+
 int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void* v_full, int hq,
                   int hk, int rows, int S, const int32_t* pos, const float* inv_freq,
                   void* stream) {

@@ -58,12 +58,18 @@ struct AttnArgs {
   __nv_bfloat16* dv;
   int64_t lddk, lddv;
   float* delta;               // [hq, N] scratch
+  // tcgen05 backward only: fp32 dense [N, hk, 128] dK/dV outputs (replace dk/dv
+  // when both set) and the number of CTAs each GQA group is split across (0 = auto)
+  float* dk_acc = nullptr;
+  float* dv_acc = nullptr;
+  int kv_splits = 0;
 };
 cudaError_t k_attn_fwd(const AttnArgs& a, cudaStream_t s);
 cudaError_t k_attn_bwd(const AttnArgs& a, cudaStream_t s);
 // attention_tc.cu — the same forward on tcgen05/TMEM/TMA.
 cudaError_t k_attn_fwd_tc(const AttnArgs& a, cudaStream_t s);
 cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s);
+int attn_bwd_kv_splits(int N, int hq, int hk);
 
 // a2a.cu — Ulysses all-to-all over peer memory with fused RoPE.
 constexpr int kMaxSp = 8;

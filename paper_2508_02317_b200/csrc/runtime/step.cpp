@@ -343,8 +343,8 @@ int Step::alloc_acts() {
   dact_ = alloc<bf16>(T * size_t(F_), false);
   dgu_ = alloc<bf16>(T * size_t(2 * F_), false);
   dq_acc_ = alloc<float>(N * size_t(hql_) * 128, false);
-  dk_ = alloc<bf16>(N * size_t(hkl_) * 128, false);
-  dv_ = alloc<bf16>(N * size_t(hkl_) * 128, false);
+  dk_ = alloc<float>(N * size_t(hkl_) * 128, false);
+  dv_ = alloc<float>(N * size_t(hkl_) * 128, false);
   delta_ = alloc<float>(N * size_t(hql_), false);
   dw_part_ = alloc<float>(size_t(k_rmsnorm_bwd_parts(T_)) * H, false);
   hf_ = alloc<bf16>(T * H, false);
@@ -784,9 +784,8 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     a.dout = do_full(db);
     a.lddo = hql_ * 128;
     a.dq_acc = dq_acc_;
-    a.dk = dk_;
-    a.dv = dv_;
-    a.lddk = a.lddv = hkl_ * 128;
+    a.dk_acc = dk_;
+    a.dv_acc = dv_;
     a.delta = delta_;
     CU(k_attn_bwd_tc(a, cs_));
   }
@@ -807,8 +806,8 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     a.seq = S_;
     a.ngroups = 3;
     a.g[0] = A2AGroup{hq_, 0, 1, 1, {dq_acc_}};
-    a.g[1] = A2AGroup{hk_, hq_ * 128, 1, 0, {dk_}};
-    a.g[2] = A2AGroup{hk_, (hq_ + hk_) * 128, 0, 0, {dv_}};
+    a.g[1] = A2AGroup{hk_, hq_ * 128, 1, 1, {dk_}};
+    a.g[2] = A2AGroup{hk_, (hq_ + hk_) * 128, 0, 1, {dv_}};
     for (int j = 0; j < int(p_.sp); ++j) a.local[j] = peer(j, off_dqkv_[xb]);
     a.local_ld = Wqkv_;
     a.pos = d_pos_;

@@ -172,7 +172,8 @@ class Step {
   // backward scratch
   float *dx_ = nullptr, *dtmp_ = nullptr, *dq_acc_ = nullptr, *delta_ = nullptr,
         *dw_part_ = nullptr;
-  bf16 *dxb_ = nullptr, *dact_ = nullptr, *dgu_ = nullptr, *dk_ = nullptr, *dv_ = nullptr;
+  bf16 *dxb_ = nullptr, *dact_ = nullptr, *dgu_ = nullptr;
+  float *dk_ = nullptr, *dv_ = nullptr;  // fp32 dK/dV (split-GQA reduce-add)
   // head
   bf16 *hf_ = nullptr, *logits_ = nullptr;
   float *rf_ = nullptr, *dhf_ = nullptr, *loss_rows_ = nullptr, *loss_sum_ = nullptr;

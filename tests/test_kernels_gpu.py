@@ -389,3 +389,37 @@ def test_attention_bwd_tc(N, lens, hq, hk):
     for got, ref in ((dq, qr.grad), (dk, kr.grad), (dv, vr.grad)):
         assert rel_err(got, ref) < 3e-2, (rel_err(got, ref))
         assert cosine(got, ref) > 0.999
+
+
+@gpu
+@pytest.mark.parametrize("N,lens,hq,hk,splits", [(640, [100, 300, 64, 176], 4, 2, 1),
+                                                 (1024, [1000, 24], 7, 1, 2),
+                                                 (1024, [1000, 24], 7, 1, 7),
+                                                 (2048, [130, 1500, 418], 8, 2, 3),
+                                                 (1000, [1000], 4, 1, 0)])
+def test_attention_bwd_tc_f32kv_split(N, lens, hq, hk, splits):
+    """The step's form: fp32 dK/dV, GQA groups split across CTAs (partials
+    summed by TMA reduce-add), including a ragged last key tile."""
+    torch.manual_seed(N + 3)
+    q = bf(torch.randn(N, hq, 128, device=DEV))
+    k = bf(torch.randn(N, hk, 128, device=DEV))
+    v = bf(torch.randn(N, hk, 128, device=DEV))
+    st, en = _varlen(N, lens)
+    scale = 1 / math.sqrt(128)
+    qr, kr, vr = (t.float().clone().requires_grad_(True) for t in (q, k, v))
+    o_ref, lse_ref = _attn_ref(qr, kr, vr, st, hq, hk)
+    o = bf(o_ref.detach()).contiguous()
+    lse = lse_ref.detach().contiguous()
+    do = bf(torch.randn(N, hq, 128, device=DEV))
+    o_ref.backward(do.float())
+    dq = torch.empty(N, hq, 128, device=DEV)
+    dk = torch.full((N, hk, 128), float("nan"), device=DEV)  # must be fully overwritten
+    dv = torch.full_like(dk, float("nan"))
+    delta = torch.empty(hq, N, device=DEV)
+    call("opx_attn_bwd_tc_f32kv", P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv),
+         P(delta), hq * 128, hk * 128, P(st), P(en), N, hq, hk, scale, splits, S())
+    torch.cuda.synchronize()
+    for got, ref in ((dq, qr.grad), (dk, kr.grad), (dv, vr.grad)):
+        assert torch.isfinite(got).all()
+        assert rel_err(got, ref) < 3e-2, (rel_err(got, ref))
+        assert cosine(got, ref) > 0.999

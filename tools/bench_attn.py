@@ -37,11 +37,19 @@ def main():
         dk = torch.empty_like(k)
         dv = torch.empty_like(v)
         delta = torch.empty(hq, N, device="cuda")
+        dk32 = torch.empty(N, hk, 128, device="cuda")
+        dv32 = torch.empty_like(dk32)
         flops = 4 * 128 * hq * sq / 2  # causal fwd
         sc = 1 / math.sqrt(128)
-        for name in ("opx_attn_fwd", "opx_attn_fwd_tc", "opx_attn_bwd", "opx_attn_bwd_tc"):
+        names = ["opx_attn_fwd_tc", "opx_attn_bwd_tc"] + [f"split{sp}" for sp in range(0, hq // hk + 1)]
+        for name in names:
             def run():
-                if name.startswith("opx_attn_bwd"):
+                if name.startswith("split"):
+                    check(lib().opx_attn_bwd_tc_f32kv(P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk32),
+                                                      P(dv32), P(delta), hq * 128, hk * 128, P(st), P(en), N,
+                                                      hq, hk, ctypes.c_float(sc), int(name[5:]),
+                                                      ctypes.c_void_p(S)))
+                elif name.startswith("opx_attn_bwd"):
                     check(getattr(lib(), name)(P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv),
                                              P(delta), hq * 128, hk * 128, P(st), P(en), N, hq, hk, sc,
                                              ctypes.c_void_p(S)))
@@ -58,7 +66,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
-            f = flops * (2.5 if "bwd" in name else 1.0)
+            f = flops * (2.5 if ("bwd" in name or "split" in name) else 1.0)
             print(f"{name:18s} N={N} hq={hq} hk={hk}: {ms:8.3f} ms  {f / ms / 1e9:8.1f} TFLOP/s")
 
 
