@@ -71,6 +71,7 @@ typedef struct {
   double tokens;        /* tokens processed by this rank this step */
   double n_valid;       /* global count of supervised tokens */
   int64_t launches;     /* opx kernels launched during the step */
+  double enqueue_s;     /* host wall time spent enqueueing the step (launch-bound if ~step_time_s) */
 } opx_step_report;
 
 /* 128-byte NCCL unique id for the world communicator (rank 0 creates it). */

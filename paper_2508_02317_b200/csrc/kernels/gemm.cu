@@ -13,6 +13,10 @@
 // Grouped mode (MoE experts): per-group row segments (128-aligned) with a
 // per-group weight slab; either M varies per group (fwd/dgrad) or K does (wgrad).
 #include <cuda.h>
+
+#include <map>
+#include <string>
+#include <vector>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -428,7 +432,71 @@ int num_sms() {
   return g_num_sms;
 }
 
+static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s);
+
+// Diagnostics (OPX_GEMM_LOG=1): per-launch CUDA events around every GEMM,
+// aggregated by shape/layout/epilogue by gemm_log_dump().
+namespace {
+struct GemmLogEntry {
+  int M, N, K, a_mn, b_mn, epi, groups;
+  cudaEvent_t e0, e1;
+};
+std::vector<GemmLogEntry> g_gemm_log;
+}  // namespace
+
 cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s) {
+  static const bool log = getenv("OPX_GEMM_LOG") != nullptr;
+  if (!log) return gemm_run_impl(g, s);
+  GemmLogEntry e{g.M, g.N, g.K, g.a_mn, g.b_mn, g.epi, g.groups, nullptr, nullptr};
+  cudaEventCreate(&e.e0);
+  cudaEventCreate(&e.e1);
+  cudaEventRecord(e.e0, s);
+  const cudaError_t r = gemm_run_impl(g, s);
+  cudaEventRecord(e.e1, s);
+  g_gemm_log.push_back(e);
+  return r;
+}
+
+void gemm_log_dump(const char* tag) {
+  if (g_gemm_log.empty()) return;
+  struct Agg {
+    int n = 0;
+    double ms = 0, mn = 1e30, mx = 0;
+  };
+  std::map<std::string, Agg> agg;
+  static const bool each = getenv("OPX_GEMM_LOG")[0] == '2';
+  int idx = 0;
+  for (auto& e : g_gemm_log) {
+    cudaEventSynchronize(e.e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.e0, e.e1);
+    char key[128];
+    snprintf(key, sizeof key, "M=%d N=%d K=%d a_mn=%d b_mn=%d epi=%d groups=%d", e.M, e.N, e.K, e.a_mn,
+             e.b_mn, e.epi, e.groups);
+    Agg& a = agg[key];
+    ++a.n;
+    a.ms += ms;
+    a.mn = std::min(a.mn, double(ms));
+    a.mx = std::max(a.mx, double(ms));
+    if (each)
+      fprintf(stderr, "[gemm1 %s] #%d %s %.3f ms %.0f TF/s\n", tag, idx, key, ms,
+              2.0 * e.M * e.N * e.K / ms / 1e9);
+    ++idx;
+    cudaEventDestroy(e.e0);
+    cudaEventDestroy(e.e1);
+  }
+  g_gemm_log.clear();
+  for (auto& kv : agg) {
+    int M, N, K;
+    sscanf(kv.first.c_str(), "M=%d N=%d K=%d", &M, &N, &K);
+    const double mean = kv.second.ms / kv.second.n;
+    fprintf(stderr, "[gemm %s] %s n=%d mean=%.3f min=%.3f max=%.3f ms  %.0f TF/s(mean) %.0f(min)\n", tag,
+            kv.first.c_str(), kv.second.n, mean, kv.second.mn, kv.second.mx, 2.0 * M * N * K / mean / 1e9,
+            2.0 * M * N * K / kv.second.mn / 1e9);
+  }
+}
+
+static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   if ((g.groups == 0 || g.grouped_k) && g.M <= 0) return cudaSuccess;
   if (g.N <= 0) return cudaSuccess;
   if (g.N % 8 != 0 || (g.epi == GEMM_EPI_SWIGLU && g.N % 256 != 0)) return cudaErrorInvalidValue;

@@ -9,6 +9,14 @@
 // Each CTA's TMEM holds its 128 accumulator rows x 256 columns (double
 // buffered); its four epilogue warps drain them with the same fused
 // epilogues as kernels/gemm.cu.  Grouped (MoE) GEMMs stay on the 1-CTA kernel.
+//
+// Tiles are handed out dynamically: the leader's producer takes tickets from a
+// global counter and publishes each tile id through a small smem ring (with
+// mbarriers) to its MMA warp, both CTAs' epilogues and the peer producer.  A
+// static persistent schedule stalls the whole GEMM when some SMs are held by a
+// concurrent kernel (the FSDP all-gather / reduce-scatter on the comm stream):
+// the clusters that start late would still own 1/74 of the tiles each.  With
+// tickets, late clusters just find the work already taken.
 #include <cuda.h>
 
 #include "../runtime/gemm_api.h"
@@ -24,6 +32,8 @@ constexpr int BNC = 128;  // B rows staged per CTA
 constexpr int BK = 64, STAGES = 6;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BNC * BK * 2;  // 16 KB
+constexpr int QD = 4;                    // tile-id ring depth
+constexpr int Q_CONSUMERS = 1 + 1 + 4 + 4;  // peer producer, MMA, 2 x 4 epilogue warps
 constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
 constexpr int THREADS = 256;
 
@@ -36,6 +46,7 @@ struct P2 {
   __nv_bfloat16* D2;
   int64_t ldd2;
   float scale;
+  int* ctr;  // ticket counter (0 at launch; reset to 0 by the last ticket taker)
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -62,7 +73,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tq_full = tempty + 2;
+  uint64_t* tq_empty = tq_full + QD;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + QD);
+  int* tile_q = reinterpret_cast<int*>(tmem_slot + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -78,6 +92,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], 2 * 128);  // both CTAs' epilogue threads (leader's is used)
+    }
+    for (int s = 0; s < QD; ++s) {
+      ptx::mbar_init(&tq_full[s], 1);
+      ptx::mbar_init(&tq_empty[s], Q_CONSUMERS);  // leader's is used
     }
     ptx::fence_mbar_init();
   }
@@ -98,7 +116,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < ntiles; t += ncl) {
+      int qi = 0;
+      uint32_t qph = 0;
+      const uint32_t peer_tq = ptx::mapa(ptx::smem_u32(tile_q), 1);
+      const uint32_t peer_tqf = ptx::mapa(ptx::smem_u32(tq_full), 1);
+      const uint32_t leader_tqe = ptx::mapa(ptx::smem_u32(tq_empty), 0);
+      int t = cid;
+      if (leader) {  // publish the first tile
+        ptx::mbar_wait(&tq_empty[qi], qph ^ 1);
+        tile_q[qi] = t;
+        ptx::st_shared_cluster(peer_tq + 4 * qi, t);
+        ptx::mbar_arrive(&tq_full[qi]);
+        ptx::mbar_arrive_cluster(peer_tqf + 8 * qi);
+      } else {
+        ptx::mbar_wait_cluster(&tq_full[qi], qph);
+        t = tile_q[qi];
+        ptx::mbar_arrive_cluster(leader_tqe + 8 * qi);
+      }
+      if (++qi == QD) {
+        qi = 0;
+        qph ^= 1;
+      }
+      while (t < ntiles) {
+        // leader: take the next ticket now, publish it after this tile's loads
+        int v = 0;
+        if (leader) v = atomicAdd(p.ctr, 1);
         int mb, nb;
         tile_coords(p, t, mb, nb);
         const int m0 = mb * 2 * BM + int(rank) * BM;
@@ -127,6 +169,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             phase ^= 1;
           }
         }
+        if (leader) {
+          if (v == ntiles - 1) atomicExch(p.ctr, 0);  // last ticket overall: reset for reuse
+          t = ncl + v;
+          ptx::mbar_wait(&tq_empty[qi], qph ^ 1);
+          tile_q[qi] = t;
+          ptx::st_shared_cluster(peer_tq + 4 * qi, t);
+          ptx::mbar_arrive(&tq_full[qi]);
+          ptx::mbar_arrive_cluster(peer_tqf + 8 * qi);
+        } else {
+          ptx::mbar_wait_cluster(&tq_full[qi], qph);
+          t = tile_q[qi];
+          ptx::mbar_arrive_cluster(leader_tqe + 8 * qi);
+        }
+        if (++qi == QD) {
+          qi = 0;
+          qph ^= 1;
+        }
       }
     }
   } else if (warp == 1) {
@@ -136,7 +195,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = cid; t < ntiles; t += ncl, ++local) {
+      int qi = 0;
+      uint32_t qph = 0;
+      for (;; ++local) {
+        ptx::mbar_wait(&tq_full[qi], qph);
+        const int t = tile_q[qi];
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tq_empty[qi]);
+        if (++qi == QD) {
+          qi = 0;
+          qph ^= 1;
+        }
+        if (t >= ntiles) break;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -174,7 +244,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int local = 0;
     const uint32_t tempty_leader[2] = {ptx::mapa(ptx::smem_u32(&tempty[0]), 0),
                                        ptx::mapa(ptx::smem_u32(&tempty[1]), 0)};
-    for (int t = cid; t < ntiles; t += ncl, ++local) {
+    const uint32_t leader_tqe = ptx::mapa(ptx::smem_u32(tq_empty), 0);
+    int qi = 0;
+    uint32_t qph = 0;
+    for (;; ++local) {
+      if (leader) ptx::mbar_wait(&tq_full[qi], qph);
+      else ptx::mbar_wait_cluster(&tq_full[qi], qph);
+      const int t = tile_q[qi];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&tq_empty[qi]);
+        else ptx::mbar_arrive_cluster(leader_tqe + 8 * qi);
+      }
+      if (++qi == QD) {
+        qi = 0;
+        qph ^= 1;
+      }
+      if (t >= ntiles) break;
       int mb, nb;
       tile_coords(p, t, mb, nb);
       const int acc = local & 1;
@@ -294,6 +380,23 @@ cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, int
 
 }  // namespace
 
+// Pool of zeroed ticket counters (per device).  Each launch takes the next
+// slot; kernels leave their slot at 0, so a slot is reusable once its launch
+// has finished (1024 launches later).
+static int* ticket_counter() {
+  constexpr int kSlots = 1024;
+  static int* pool[64] = {};
+  static int next[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!pool[dev]) {
+    if (cudaMalloc(&pool[dev], kSlots * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(pool[dev], 0, kSlots * sizeof(int)) != cudaSuccess) return nullptr;
+  }
+  return pool[dev] + (next[dev]++ % kSlots);
+}
+
 cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   if (g.groups) return cudaErrorNotSupported;
   CUtensorMap ma, mb;
@@ -315,6 +418,8 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   p.D2 = g.D2;
   p.ldd2 = g.ldd2;
   p.scale = g.scale == 0.f ? 1.f : g.scale;
+  p.ctr = ticket_counter();
+  if (!p.ctr) return cudaErrorMemoryAllocation;
   const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BNP - 1) / BNP);
   int clusters = num_sms() / 2;
   if (tiles < clusters) clusters = tiles;

@@ -49,6 +49,8 @@ struct GemmDesc {
 };
 
 cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s);
+// OPX_GEMM_LOG diagnostics: print per-shape GEMM times recorded since the last dump.
+void gemm_log_dump(const char* tag);
 // 2-CTA (cta_group::2, 256x256 per CTA pair) path for plain GEMMs; gemm_run
 // dispatches to it unless OPX_GEMM_1CTA is set.
 cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s);

@@ -14,6 +14,7 @@
 //   opt:  fused AdamW on the local fp32 shard (:392-409).
 // Node names and phases follow step_graph.cpp so measured traces line up with
 // the simulated ones.
+#include <chrono>
 #include "step.h"
 
 #include <algorithm>
@@ -78,6 +79,7 @@ Step::~Step() {
   if (expert_comm_) ncclCommDestroy(expert_comm_);
   if (rep_comm_) ncclCommDestroy(rep_comm_);
   if (shard_comm_) ncclCommDestroy(shard_comm_);
+  if (shard_comm_head_) ncclCommDestroy(shard_comm_head_);
   if (world_comm_) ncclCommDestroy(world_comm_);
   if (cs_) cudaStreamDestroy(cs_);
   if (ms_) cudaStreamDestroy(ms_);
@@ -129,12 +131,29 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
   if (world_ > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
+    // Per-layer FSDP/HSDP/EP collectives run on the comm stream beside the
+    // compute kernels: cap the SMs NCCL takes (OPX_NCCL_MAX_CTAS, default 8) so
+    // the overlapped GEMMs (dynamic tile tickets) keep most of the GPU.
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    {
+      const char* e = getenv("OPX_NCCL_MAX_CTAS");
+      const int mx = e ? atoi(e) : 8;
+      if (mx > 0) {
+        cfg.maxCTAs = mx;
+        cfg.minCTAs = std::min(mx, 4);
+      }
+    }
+    // The head unit's gather (first in the step) and reduce-scatter (last)
+    // are exposed, so they use an uncapped communicator.
     NC(ncclCommInitRank(&world_comm_, world_, id, rank_));
-    if (sh * sp > 1) NC(ncclCommSplit(world_comm_, rep_i_, rank_, &shard_comm_, nullptr));
+    if (sh * sp > 1) {
+      NC(ncclCommSplit(world_comm_, rep_i_, rank_, &shard_comm_, &cfg));
+      NC(ncclCommSplit(world_comm_, rep_i_, rank_, &shard_comm_head_, nullptr));
+    }
     if (p.dp_replicate > 1)
-      NC(ncclCommSplit(world_comm_, shard_i_ * sp + sp_i_, rank_, &rep_comm_, nullptr));
+      NC(ncclCommSplit(world_comm_, shard_i_ * sp + sp_i_, rank_, &rep_comm_, &cfg));
     else
-      NC(ncclCommSplit(world_comm_, NCCL_SPLIT_NOCOLOR, rank_, &rep_comm_, nullptr));
+      NC(ncclCommSplit(world_comm_, NCCL_SPLIT_NOCOLOR, rank_, &rep_comm_, &cfg));
   }
 
   rows_ = int(p.micro_batch);
@@ -160,6 +179,7 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
     TRY(moe_setup_groups());
   }
   TRY(build_units());
+  if (shard_comm_head_) units_[0].comm = shard_comm_head_;
   TRY(alloc_acts());
   return OPX_OK;
 }
@@ -497,6 +517,11 @@ int Step::barrier_sp(cudaStream_t s) {
 // one layer
 // ---------------------------------------------------------------------------
 namespace {
+// timing experiments only: OPX_DEBUG_NO_A2A skips the Ulysses exchanges (wrong numerics)
+bool dbg_no_a2a() {
+  static const bool v = getenv("OPX_DEBUG_NO_A2A") != nullptr;
+  return v;
+}
 struct LayerW {
   const bf16 *ln1, *qkv, *o, *ln2, *gu, *down;
 };
@@ -571,7 +596,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.local_ld = Wqkv_;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
-    CU(k_a2a_seq2head(a, cs_));
+    if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
     TRY(barrier_sp(cs_));
   }
   if (tr) {
@@ -618,7 +643,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.local_ld = hq_ * 128;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
-    CU(k_a2a_head2seq(a, cs_));
+    if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
     TRY(barrier_sp(cs_));
     if (tr) {
       e1 = ev();
@@ -714,18 +739,33 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     TRY(moe_bwd(l, u, eu, G, eu.gfull, dtmp_));
     CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
   } else {
-  CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
-  CU(gemm_run(gd(T, F, H, dxb_, H, false, W.down, F, true, GEMM_EPI_BF16, dact_, F), cs_));
-  CU(gemm_run(gd(H, F, T, dxb_, H, true, act_, F, true, GEMM_EPI_F32, g_down, F), cs_));
-  CU(k_swiglu_bwd(dact_, gu_, dgu_, T, F, cs_));
-  CU(gemm_run(gd(T, H, 2 * F, dgu_, 2 * F, false, W.gu, H, true, GEMM_EPI_F32, dtmp_, H), cs_));
-  CU(gemm_run(gd(2 * F, H, T, dgu_, 2 * F, true, h2_, H, true, GEMM_EPI_F32, g_gu, H), cs_));
-  CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
+    // per-GEMM sub-nodes when tracing (mlp.*), so the profile separates the
+    // dgrad/wgrad GEMMs from the elementwise work
+    auto sub = [&](const char* name) {
+      if (!tr) return;
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".mlp." + name, ph, 0, e0, e1);
+      e0 = e1;
+    };
+    CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
+    CU(gemm_run(gd(T, F, H, dxb_, H, false, W.down, F, true, GEMM_EPI_BF16, dact_, F), cs_));
+    sub("dgrad_down");
+    CU(gemm_run(gd(H, F, T, dxb_, H, true, act_, F, true, GEMM_EPI_F32, g_down, F), cs_));
+    sub("wgrad_down");
+    CU(k_swiglu_bwd(dact_, gu_, dgu_, T, F, cs_));
+    sub("swiglu_bwd");
+    CU(gemm_run(gd(T, H, 2 * F, dgu_, 2 * F, false, W.gu, H, true, GEMM_EPI_F32, dtmp_, H), cs_));
+    sub("dgrad_gu");
+    CU(gemm_run(gd(2 * F, H, T, dgu_, 2 * F, true, h2_, H, true, GEMM_EPI_F32, g_gu, H), cs_));
+    sub("wgrad_gu");
+    CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
+    sub("rmsnorm_bwd");
   }
-  if (tr) {
+  if (tr && a_.is_moe_layer(l)) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
-    mark(pre + (a_.is_moe_layer(l) ? ".moe" : ".mlp"), ph, 0, e0, e1);
+    mark(pre + ".moe", ph, 0, e0, e1);
     e0 = e1;
   }
   // ---- attention output projection
@@ -755,7 +795,7 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     a.local_ld = Q;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
-    CU(k_a2a_seq2head(a, cs_));
+    if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
     TRY(barrier_sp(cs_));
   }
   if (tr) {
@@ -812,7 +852,7 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     a.local_ld = Wqkv_;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
-    CU(k_a2a_head2seq(a, cs_));
+    if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
     TRY(barrier_sp(cs_));
   }
   if (tr) {
@@ -879,6 +919,7 @@ int Step::run(opx_step_report* rep) {
   ev_next_ = 0;
   ++step_count_;
   const int64_t launches0 = g_kernel_launches;
+  const auto host_t0 = std::chrono::steady_clock::now();
   CU(cudaMemsetAsync(d_timeout_, 0, sizeof(int), cs_));
   CU(cudaEventRecord(ev_start_, cs_));
   CU(cudaStreamWaitEvent(ms_, ev_start_, 0));
@@ -1038,11 +1079,14 @@ int Step::run(opx_step_report* rep) {
   // loss: local sum -> world all-reduce (reporting only, off the timed path)
   CU(k_sum(loss_rows_, T_, loss_sum_, cs_));
   if (world_comm_) NC(ncclAllReduce(loss_sum_, loss_sum_, 1, ncclFloat, ncclSum, world_comm_, cs_));
+  const double enqueue_s =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
   float loss = 0.f;
   int timeout = 0;
   CU(cudaMemcpyAsync(&loss, loss_sum_, 4, cudaMemcpyDeviceToHost, cs_));
   CU(cudaMemcpyAsync(&timeout, d_timeout_, 4, cudaMemcpyDeviceToHost, cs_));
   CU(cudaStreamSynchronize(cs_));
+  if (getenv("OPX_GEMM_LOG")) gemm_log_dump(("rank" + std::to_string(rank_)).c_str());
   if (timeout) {
     set_error("peer barrier timed out (a peer rank stalled)");
     return OPX_ERR_TIMEOUT;
@@ -1062,6 +1106,7 @@ int Step::run(opx_step_report* rep) {
     rep->tokens = double(T_);
     rep->n_valid = double(n_valid_);
     rep->launches = g_kernel_launches - launches0 - 1;  // minus the loss reduction
+    rep->enqueue_s = enqueue_s;
   }
   return OPX_OK;
 }

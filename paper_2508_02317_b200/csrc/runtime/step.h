@@ -103,7 +103,8 @@ class Step {
 
   // ---- streams, comms, events
   cudaStream_t cs_ = nullptr, ms_ = nullptr;
-  ncclComm_t world_comm_ = nullptr, shard_comm_ = nullptr, rep_comm_ = nullptr;
+  ncclComm_t world_comm_ = nullptr, shard_comm_ = nullptr, rep_comm_ = nullptr,
+             shard_comm_head_ = nullptr;
   cudaEvent_t ev_start_ = nullptr, ev_fwd_ = nullptr, ev_bwd_ = nullptr, ev_end_ = nullptr;
   std::vector<cudaEvent_t> ev_ag_, ev_use_done_, ev_grad_done_, ev_rs_done_;
   cudaEvent_t ev_head_ag_ = nullptr, ev_head_rs_ = nullptr;
