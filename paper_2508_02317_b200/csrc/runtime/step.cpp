@@ -300,7 +300,7 @@ int Step::alloc_acts() {
   save_acts_ = !p_.recompute_full;
   const int xslots = save_acts_ ? 2 + L : 2;
   for (int b = 0; b < xslots; ++b) {
-    if (b >= 2 && !keeps_acts(b - 2)) {  // MoE layers are always recomputed
+    if (b >= 2 && !keeps_acts(b - 2)) {
       off_q_.push_back(0);
       off_k_.push_back(0);
       off_v_.push_back(0);
@@ -350,7 +350,7 @@ int Step::alloc_acts() {
   if (!make_acts(scratch_, any_dense)) return cuda_fail(cudaErrorMemoryAllocation, "activations");
   saved_.assign(size_t(L), Acts{});
   for (int l = 0; l < L; ++l)
-    if (keeps_acts(l) && !make_acts(saved_[size_t(l)], true)) {
+    if (keeps_acts(l) && !make_acts(saved_[size_t(l)], !a_.is_moe_layer(l))) {
       set_error("out of device memory for recompute=none activations (layer " +
                 std::to_string(l) + "); use recompute=full");
       return OPX_ERR_CUDA;

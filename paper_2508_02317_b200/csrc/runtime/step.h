@@ -149,7 +149,10 @@ class Step {
   Acts scratch_;
   std::vector<Acts> saved_;
   bool save_acts_ = false;
-  bool keeps_acts(int l) const { return save_acts_ && !a_.is_moe_layer(l); }
+  // recompute=none keeps every layer's forward activations; MoE layers keep
+  // the attention activations, their routing and the combined expert outputs
+  // and only re-run dispatch + gate|up in the backward (moe_bwd).
+  bool keeps_acts(int l) const { return save_acts_; }
   void bind(const Acts& a) {
     h_ = a.h;
     h2_ = a.h2;
@@ -212,8 +215,23 @@ class Step {
   bf16* eslot_ = nullptr;           // expert gather buffer (De > 1)
   float* egrad_slot_ = nullptr;     // expert full-grad buffer (De > 1)
   int64_t cap_rows_ = 0;            // receive-buffer rows (worst case)
-  size_t off_flags_ep_ = 0, off_counts_ = 0, off_xrecv_ = 0, off_yback_ = 0, off_dyrecv_ = 0,
-         off_dxback_ = 0;
+  size_t off_flags_ep_ = 0, off_xrecv_ = 0, off_dyrecv_ = 0, off_dxback_ = 0;
+  // routing state + the peer-written count table and combine buffer: slot 0 is
+  // scratch (recomputed layers), slot 1 + l belongs to MoE layer l under recompute=none
+  struct MoeRoute {
+    float* wts = nullptr;
+    int *idx = nullptr, *pos = nullptr, *pairat = nullptr, *cnt = nullptr, *excl = nullptr,
+        *g_start = nullptr, *g_rows = nullptr, *g_rows_pad = nullptr, *g_total = nullptr;
+  };
+  std::vector<MoeRoute> routes_;        // [slot]
+  std::vector<size_t> off_counts_s_;    // [slot]
+  std::vector<size_t> off_yback_s_;     // [slot]
+  int rslot_ = 0;
+  void moe_bind(int l);                 // select slot 1+l (l >= 0) or scratch (l < 0)
+  int* counts_cur() { return reinterpret_cast<int*>(arena_ + off_counts_s_[size_t(rslot_)]); }
+  bf16* yback_cur() { return reinterpret_cast<bf16*>(arena_ + off_yback_s_[size_t(rslot_)]); }
+  int** count_tab_cur() { return d_count_tables_ + size_t(rslot_) * kMaxSp; }
+  bf16** yback_tab_cur() { return d_yback_peers_ + size_t(rslot_) * kMaxSp; }
   uint32_t** d_ep_flags_ = nullptr;
   int** d_count_tables_ = nullptr;
   bf16** d_xrecv_peers_ = nullptr;

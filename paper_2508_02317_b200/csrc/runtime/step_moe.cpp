@@ -131,9 +131,16 @@ size_t Step::moe_arena(size_t off) {
   const size_t H = size_t(H_), P = size_t(T_) * size_t(topk_);
   cap_rows_ = int64_t(P) * ep_ + int64_t(El_) * 128;
   off_flags_ep_ = take(64 * sizeof(uint32_t));
-  off_counts_ = take(size_t(ep_) * size_t(E_) * sizeof(int));
+  const int L = int(a_.layers);
+  const int nslots = save_acts_ ? 1 + L : 1;
+  off_counts_s_.assign(size_t(nslots), 0);
+  off_yback_s_.assign(size_t(nslots), 0);
+  for (int sl = 0; sl < nslots; ++sl) {
+    if (sl > 0 && !a_.is_moe_layer(sl - 1)) continue;
+    off_counts_s_[size_t(sl)] = take(size_t(ep_) * size_t(E_) * sizeof(int));
+    off_yback_s_[size_t(sl)] = take(P * H * 2);
+  }
   off_xrecv_ = take(size_t(cap_rows_) * H * 2);
-  off_yback_ = take(P * H * 2);
   off_dyrecv_ = take(size_t(cap_rows_) * H * 2);
   off_dxback_ = take(P * H * 2);
   return off;
@@ -143,18 +150,27 @@ int Step::moe_alloc() {
   const size_t T = size_t(T_), P = T * size_t(topk_), cap = size_t(cap_rows_);
   const size_t E = size_t(E_), H = size_t(H_), Fe = size_t(Fe_);
   r_logits_ = alloc<float>(T * E, false);
-  r_wts_ = alloc<float>(P, false);
   r_dw_ = alloc<float>(P, false);
-  r_idx_ = alloc<int>(P, false);
-  r_pos_ = alloc<int>(P, false);
-  r_pairat_ = alloc<int>(P, false);
-  r_cnt_ = alloc<int>(E);
-  r_excl_ = alloc<int>(E);
   r_hist_ = alloc<int>(size_t(k_moe_sort_chunks(int(P))) * E);
-  g_start_ = alloc<int>(size_t(El_));
-  g_rows_ = alloc<int>(size_t(El_));
-  g_rows_pad_ = alloc<int>(size_t(El_));
-  g_total_ = alloc<int>(1);
+  routes_.assign(off_counts_s_.size(), MoeRoute{});
+  for (size_t sl = 0; sl < routes_.size(); ++sl) {
+    if (sl > 0 && !a_.is_moe_layer(int(sl) - 1)) continue;
+    MoeRoute& r = routes_[sl];
+    r.wts = alloc<float>(P, false);
+    r.idx = alloc<int>(P, false);
+    r.pos = alloc<int>(P, false);
+    r.pairat = alloc<int>(P, false);
+    r.cnt = alloc<int>(E);
+    r.excl = alloc<int>(E);
+    r.g_start = alloc<int>(size_t(El_));
+    r.g_rows = alloc<int>(size_t(El_));
+    r.g_rows_pad = alloc<int>(size_t(El_));
+    r.g_total = alloc<int>(1);
+    if (!r.wts || !r.idx || !r.pos || !r.pairat || !r.cnt || !r.excl || !r.g_start || !r.g_rows ||
+        !r.g_rows_pad || !r.g_total)
+      return cuda_fail(cudaErrorMemoryAllocation, "MoE routing state");
+  }
+  moe_bind(-1);
   gu_e_ = alloc<bf16>(cap * 2 * Fe, false);
   act_e_ = alloc<bf16>(cap * Fe);
   y_e_ = alloc<bf16>(cap * H, false);
@@ -164,9 +180,9 @@ int Step::moe_alloc() {
   dyp_ = alloc<bf16>(P * H, false);
   dlogits_ = alloc<bf16>(T * E, false);
   d_ep_flags_ = alloc<uint32_t*>(kMaxSp);
-  d_count_tables_ = alloc<int*>(kMaxSp);
+  d_count_tables_ = alloc<int*>(kMaxSp * routes_.size());
   d_xrecv_peers_ = alloc<bf16*>(kMaxSp);
-  d_yback_peers_ = alloc<bf16*>(kMaxSp);
+  d_yback_peers_ = alloc<bf16*>(kMaxSp * routes_.size());
   d_dyrecv_peers_ = alloc<bf16*>(kMaxSp);
   d_dxback_peers_ = alloc<bf16*>(kMaxSp);
   for (void* q : {(void*)gu_e_, (void*)act_e_, (void*)y_e_, (void*)dact_e_, (void*)dgu_e_,
@@ -197,22 +213,40 @@ int Step::moe_alloc() {
   return OPX_OK;
 }
 
+void Step::moe_bind(int l) {
+  rslot_ = l >= 0 ? 1 + l : 0;
+  const MoeRoute& r = routes_[size_t(rslot_)];
+  r_wts_ = r.wts;
+  r_idx_ = r.idx;
+  r_pos_ = r.pos;
+  r_pairat_ = r.pairat;
+  r_cnt_ = r.cnt;
+  r_excl_ = r.excl;
+  g_start_ = r.g_start;
+  g_rows_ = r.g_rows;
+  g_rows_pad_ = r.g_rows_pad;
+  g_total_ = r.g_total;
+}
+
 int Step::moe_import() {
-  std::vector<void*> fl(kMaxSp, nullptr), ct(kMaxSp, nullptr), xr(kMaxSp, nullptr),
-      yb(kMaxSp, nullptr), dy(kMaxSp, nullptr), dx(kMaxSp, nullptr);
+  const size_t ns = routes_.size();
+  std::vector<void*> fl(kMaxSp, nullptr), ct(kMaxSp * ns, nullptr), xr(kMaxSp, nullptr),
+      yb(kMaxSp * ns, nullptr), dy(kMaxSp, nullptr), dx(kMaxSp, nullptr);
   for (int j = 0; j < ep_; ++j) {
     fl[size_t(j)] = ep_peer(j, off_flags_ep_);
-    ct[size_t(j)] = ep_peer(j, off_counts_);
+    for (size_t sl = 0; sl < ns; ++sl) {
+      ct[sl * kMaxSp + size_t(j)] = ep_peer(j, off_counts_s_[sl]);
+      yb[sl * kMaxSp + size_t(j)] = ep_peer(j, off_yback_s_[sl]);
+    }
     xr[size_t(j)] = ep_peer(j, off_xrecv_);
-    yb[size_t(j)] = ep_peer(j, off_yback_);
     dy[size_t(j)] = ep_peer(j, off_dyrecv_);
     dx[size_t(j)] = ep_peer(j, off_dxback_);
   }
   const size_t b = kMaxSp * sizeof(void*);
   CU(cudaMemcpy(d_ep_flags_, fl.data(), b, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_count_tables_, ct.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_count_tables_, ct.data(), b * ns, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_xrecv_peers_, xr.data(), b, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_yback_peers_, yb.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_yback_peers_, yb.data(), b * ns, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_dyrecv_peers_, dy.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_dxback_peers_, dx.data(), b, cudaMemcpyHostToDevice));
   return OPX_OK;
@@ -265,13 +299,14 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
     e0 = e1;
   };
   mk("");
+  moe_bind(keeps_acts(l) ? l : -1);
   const int T = T_, H = H_, E = E_, k = topk_, Fe = Fe_, P = T_ * topk_;
   const bf16* Wr = u.full + u.params[6].off;
   const bf16* Wgu = eu.full + eu.params[0].off;
   const bf16* Wd = eu.full + eu.params[1].off;
-  int* counts_all = reinterpret_cast<int*>(arena_ + off_counts_);
+  int* counts_all = counts_cur();
   bf16* xrecv = reinterpret_cast<bf16*>(arena_ + off_xrecv_);
-  bf16* yback = reinterpret_cast<bf16*>(arena_ + off_yback_);
+  bf16* yback = yback_cur();
   CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_));
   CU(k_moe_topk(r_logits_, T, E, k, r_idx_, r_wts_, cs_));
   if (!in_recompute_ && route_idx_[size_t(l)])
@@ -279,13 +314,15 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
                        cudaMemcpyDeviceToDevice, cs_));
   CU(k_moe_sort(r_idx_, P, E, r_hist_, r_cnt_, r_excl_, r_pos_, r_pairat_, cs_));
   mk("router");
-  CU(k_moe_publish_counts(r_cnt_, d_count_tables_, ep_, ep_i_, E, cs_));
+  CU(k_moe_publish_counts(r_cnt_, count_tab_cur(), ep_, ep_i_, E, cs_));
   TRY(barrier_ep(cs_));
   CU(k_moe_groups(counts_all, ep_, E, ep_i_, g_start_, g_rows_, g_rows_pad_, g_total_, cs_));
+  mk("a2a_counts");
   CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
                     d_xrecv_peers_, H, H, cs_));
-  TRY(barrier_ep(cs_));
   mk("a2a_dispatch");
+  TRY(barrier_ep(cs_));
+  mk("a2a_wait");
   CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
   {
     // gate|up pre-activations are only needed by the backward (recompute pass)
@@ -301,10 +338,11 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
                       g_start_, g_rows_, cap_rows_, 0),
               cs_));
   mk("experts");
-  CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_yback_peers_, H, H,
+  CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
                    int(cap_rows_), cs_));
-  TRY(barrier_ep(cs_));
   mk("a2a_combine");
+  TRY(barrier_ep(cs_));
+  mk("a2a_wait");
   CU(k_moe_unpermute(yback, H, r_pos_, r_wts_, T, k, H, x2, x_out, cs_));
   mk("unpermute");
   return OPX_OK;
@@ -322,22 +360,44 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
     e0 = e1;
   };
   mk("");
+  const bool kept = keeps_acts(l);
+  moe_bind(kept ? l : -1);
   const int T = T_, H = H_, E = E_, k = topk_, Fe = Fe_, P = T_ * topk_;
   const bf16* Wr = u.full + u.params[6].off;
   const bf16* Wgu = eu.full + eu.params[0].off;
   const bf16* Wd = eu.full + eu.params[1].off;
-  int* counts_all = reinterpret_cast<int*>(arena_ + off_counts_);
+  int* counts_all = counts_cur();
   bf16* xrecv = reinterpret_cast<bf16*>(arena_ + off_xrecv_);
-  bf16* yback = reinterpret_cast<bf16*>(arena_ + off_yback_);
+  bf16* yback = yback_cur();
   bf16* dyrecv = reinterpret_cast<bf16*>(arena_ + off_dyrecv_);
   bf16* dxback = reinterpret_cast<bf16*>(arena_ + off_dxback_);
+  if (kept) {
+    // selective recompute: routing and combined outputs are resident; re-send
+    // the tokens (the expert-side receive buffer is shared scratch) and redo
+    // gate|up, storing the pre-activations for the SwiGLU backward
+    CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                      d_xrecv_peers_, H, H, cs_));
+    mk("a2a_redispatch");
+    TRY(barrier_ep(cs_));
+    mk("a2a_wait");
+    CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
+    GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu, H, false, GEMM_EPI_SWIGLU, gu_e_,
+                         2 * Fe, El_, 0, g_start_, g_rows_, cap_rows_, 0);
+    g.D2 = act_e_;
+    g.ldd2 = Fe;
+    CU(gemm_run(g, cs_));
+    CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_, g_rows_, g_rows_pad_, El_, cs_));
+    mk("gate_up_recompute");
+  }
   // weighted combine backward: per-pair output grads and router-weight grads
   CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
   // a2a_combine_grad: pair grads travel to the expert ranks (same layout as dispatch)
+  mk("combine_bwd");
   CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
                     d_dyrecv_peers_, H, H, cs_));
-  TRY(barrier_ep(cs_));
   mk("a2a_combine_grad");
+  TRY(barrier_ep(cs_));
+  mk("a2a_wait");
   CU(k_moe_zero_pad(dyrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
   // experts backward (grouped GEMMs; wgrad K = 128-padded segment rows)
   CU(gemm_run(grouped(0, Fe, H, dyrecv, H, false, Wd, Fe, true, GEMM_EPI_BF16, dact_e_, Fe, El_, 0,
@@ -360,8 +420,9 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
   mk("experts");
   CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
                    int(cap_rows_), cs_));
-  TRY(barrier_ep(cs_));
   mk("a2a_dispatch_grad");
+  TRY(barrier_ep(cs_));
+  mk("a2a_wait");
   CU(k_moe_unpermute(dxback, H, r_pos_, nullptr, T, k, H, nullptr, dh2, cs_));
   // router: renormalised-softmax backward, then dh2 += dlogits . Wr, dWr = dlogits^T h2
   CU(k_moe_router_bwd(r_dw_, r_wts_, r_idx_, T, k, E, dlogits_, cs_));

@@ -71,6 +71,8 @@ MOE_PLANS = [
     (4, {"dp_replicate": 1, "dp_shard": 4, "sp": 1, "ep": 4, "micro_batch": 1}, 4),
     (4, {"dp_replicate": 1, "dp_shard": 4, "sp": 1, "ep": 2, "micro_batch": 1}, 4),
     (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 4, "micro_batch": 1}, 2),
+    (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "recompute": "none"}, 2),
+    (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 4, "micro_batch": 1, "recompute": "none"}, 2),
 ]
 
 
