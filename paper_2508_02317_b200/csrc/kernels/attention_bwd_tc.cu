@@ -8,7 +8,7 @@
 // tiles, e.g. one kv head per rank under Ulysses); the per-split dK/dV
 // partials are then summed by TMA bulk reduce-add into fp32 accumulators.
 //
-//   TMEM: S^T [0,64) | dP^T [64,128) | dQ^T [128,192) | dV [256,384) | dK [384,512)
+//   TMEM: S^T [0,64) | dP^T [64,128) | dQ^T x2 [128,256) | dV [256,384) | dK [384,512)
 //   per q tile i (MMA warp, one elected lane):
 //     S^T  = K  Q_i^T    (M=128 keys, N=64 q, K=128 d)            -> s_full
 //     dP^T = V  dO_i^T
@@ -19,7 +19,10 @@
 //     dQ^T = K^T  dS^T   (M=128 d, N=64 q, K=128 keys)            -> dq_full
 //     -- softmax warps: dQ^T rows (one d per thread) -> fp32 smem [q][d]
 //        -> one TMA bulk reduce-add into the fp32 dQ accumulator
-// The S^T/dP^T MMAs of tile i+1 overlap the dQ readout/reduction of tile i.
+// The S^T/dP^T MMAs of tile i+1 are issued as soon as the softmax warps have
+// pulled S^T/dP^T(i) into registers (s_free), so they overlap the softmax of
+// tile i; dQ^T is double buffered in TMEM so the gradient MMAs of tile i+1 do
+// not wait for the readout of tile i.
 #include <cuda.h>
 
 #include <algorithm>
@@ -44,6 +47,7 @@ constexpr int OFF_K = 0, OFF_V = 32768, OFF_Q = 65536 /*[2] x 16K*/, OFF_O = 983
               OFF_P = 131072, OFF_S = 147456, OFF_STAGE = 163840 /*32K fp32*/,
               OFF_MISC = 196608;
 constexpr int SMEM = 1024 + OFF_MISC + 3 * 2 * BQ * 4 + 256;
+static_assert(3 * 2 * BQ * 4 + 13 * 8 + 8 <= 3 * 2 * BQ * 4 + 256, "misc region");
 
 struct Params {
   const float* lse;
@@ -86,9 +90,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* qdo_empty = bars + 3;  // [2]
   uint64_t* s_full = bars + 5;
   uint64_t* p_ready = bars + 6;
-  uint64_t* dq_full = bars + 7;
-  uint64_t* dqt_free = bars + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* dq_full = bars + 7;    // [2]
+  uint64_t* dqt_free = bars + 9;   // [2]
+  uint64_t* s_free = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   float* stage = reinterpret_cast<float*>(smem + OFF_STAGE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -115,8 +120,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(p_ready, NSM);
-    ptx::mbar_init(dq_full, 1);
-    ptx::mbar_init(dqt_free, NSM);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&dq_full[i], 1);
+      ptx::mbar_init(&dqt_free[i], NSM);
+    }
+    ptx::mbar_init(s_free, NSM);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
@@ -124,7 +132,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t TST = tmem, TDP = tmem + 64, TDQ = tmem + 128, TDV = tmem + 256, TDK = tmem + 384;
+  const uint32_t TST = tmem, TDP = tmem + 64, TDQ = tmem + 128 /* + 64 * (it & 1) */,
+                 TDV = tmem + 256, TDK = tmem + 384;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -138,7 +147,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = it & 1;
         const int h = hbase + it / nq;
         const int q0 = k0 + (it % nq) * BQ;
-        if (it >= 2) ptx::mbar_wait(&qdo_empty[st], ((it >> 1) - 1) & 1);
+        if (it >= 2) ptx::mbar_wait_sleep(&qdo_empty[st], ((it >> 1) - 1) & 1);
         ptx::mbar_expect_tx(&qdo_full[st], 4 * 8192);
         uint8_t* q = smem + OFF_Q + st * 16384;
         uint8_t* o = smem + OFF_O + st * 16384;
@@ -155,14 +164,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, BQ, true, true);     // dQ^T
     const uint32_t ak = ptx::smem_u32(smem + OFF_K), av = ptx::smem_u32(smem + OFF_V),
                    ap = ptx::smem_u32(smem + OFF_P), as = ptx::smem_u32(smem + OFF_S);
-    ptx::mbar_wait(kv_full, 0);
+    ptx::mbar_wait_sleep(kv_full, 0);
     // issue order: S/dP(i+1) right after P(i) is ready, then dV/dK/dQ(i), so
     // the softmax of tile i+1 overlaps the gradient MMAs of tile i.
     auto issue_sdp = [&](int it) {
       const int st = it & 1;
       const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
       const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
-      ptx::mbar_wait(&qdo_full[st], (it >> 1) & 1);
+      ptx::mbar_wait_sleep(&qdo_full[st], (it >> 1) & 1);
       ptx::tc_fence_after();
       if (lane == 0) {
 #pragma unroll
@@ -180,9 +189,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int st = it & 1;
       const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
       const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
-      ptx::mbar_wait(p_ready, it & 1);   // P/dS(it) in smem; S^T/dP^T(it) consumed
-      if (it + 1 < niter) issue_sdp(it + 1);
-      if (it > 0) ptx::mbar_wait(dqt_free, (it - 1) & 1);  // dQ^T(it-1) read out
+      if (it + 1 < niter) {
+        ptx::mbar_wait_sleep(s_free, it & 1);  // S^T/dP^T(it) are in the softmax registers
+        issue_sdp(it + 1);
+      }
+      ptx::mbar_wait_sleep(p_ready, it & 1);   // P/dS(it) in smem
+      if (it >= 2) ptx::mbar_wait_sleep(&dqt_free[st], ((it >> 1) - 1) & 1);  // dQ^T(it-2) read out
       ptx::tc_fence_after();
       if (lane == 0) {
 #pragma unroll
@@ -193,8 +205,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           ptx::mma_bf16_ss(TDK, kd(as, k, 0), md(aq, k, 8192), id_kv, (it | k) != 0);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
-          ptx::mma_bf16_ss(TDQ, md(ak, k, 16384), md(as, k, 8192), id_q, k != 0);
-        ptx::mma_commit(dq_full);
+          ptx::mma_bf16_ss(TDQ + 64 * st, md(ak, k, 16384), md(as, k, 8192), id_q, k != 0);
+        ptx::mma_commit(&dq_full[st]);
         ptx::mma_commit(&qdo_empty[st]);
       }
       __syncwarp();
@@ -227,13 +239,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto drain_dq = [&](int j) {
       const int h = hbase + j / nq;
       const int q0 = k0 + (j % nq) * BQ;
-      ptx::mbar_wait(dq_full, j & 1);
+      ptx::mbar_wait_sleep(&dq_full[j & 1], (j >> 1) & 1);
       ptx::tc_fence_after();
       uint32_t qv[32];
-      ptx::tmem_ld32(TDQ + lane_off + c0, qv);
+      ptx::tmem_ld32(TDQ + 64 * (j & 1) + lane_off + c0, qv);
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(dqt_free);
+      ptx::mbar_arrive(&dqt_free[j & 1]);
       if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       bar_sync_softmax();  // staging buffer free
 #pragma unroll
@@ -265,12 +277,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       const int* sst = s_sst + buf * BQ;
       const bool full_vis = key <= q0 + c0 && q0 + c0 + 31 < p.N && sst[c0 + 31] <= key;
-      ptx::mbar_wait(s_full, it & 1);
+      ptx::mbar_wait_sleep(s_full, it & 1);
       ptx::tc_fence_after();
       uint32_t sv[32], dv[32];
       ptx::tmem_ld32(TST + lane_off + c0, sv);
       ptx::tmem_ld32(TDP + lane_off + c0, dv);
       ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(s_free);  // the MMA warp may overwrite S^T/dP^T now
       uint32_t pw[16], dw[16];
       if (full_vis) {
 #pragma unroll

@@ -127,18 +127,35 @@ __global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const float* __restrict
 
 // dx_out = dres + rstd * (g - xhat * mean(g * xhat)),  g = dy * w,  xhat = x * rstd
 // dw partial over the block's rows -> dw_part[blockIdx.x, H]
+// V = float4s per thread (H <= NT*4*V), so registers scale with H; the next
+// row's x/dy loads are issued before the current row's block reduction, which
+// keeps HBM busy across the __syncthreads (the kernel was latency bound).
 constexpr int BWD_ROWS = 16;
+template <int V>
 __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
     const float* __restrict__ dy, const float* __restrict__ x, const bf16* __restrict__ w,
     const float* __restrict__ rstd, const float* dres, float* dx_out,
     float* __restrict__ dw_part, int T, int H) {
-  __shared__ float red[NT / 32];
+  __shared__ float red[2][NT / 32];
   const int nv = H / 4;
-  float4 dwacc[MAXV];
-  float4 wv[MAXV];
+  float4 dwacc[V], wv[V], xn[V], dn[V];
   const uint2* wr = reinterpret_cast<const uint2*>(w);
+  const int r0 = blockIdx.x * BWD_ROWS;
+  const int rows = min(BWD_ROWS, T - r0);
+  auto load = [&](int64_t row) {
+    const float4* xr = reinterpret_cast<const float4*>(x + row * H);
+    const float4* gr = reinterpret_cast<const float4*>(dy + row * H);
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
+    for (int i = 0; i < V; ++i) {
+      const int idx = threadIdx.x + i * NT;
+      if (idx < nv) {
+        xn[i] = xr[idx];
+        dn[i] = gr[idx];
+      }
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
     dwacc[i] = make_float4(0, 0, 0, 0);
     const int idx = threadIdx.x + i * NT;
     if (idx < nv) {
@@ -147,20 +164,17 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
       wv[i] = make_float4(a.x, a.y, b.x, b.y);
     }
   }
-  const int r0 = blockIdx.x * BWD_ROWS;
-  for (int rr = 0; rr < BWD_ROWS; ++rr) {
+  if (rows > 0) load(r0);
+  for (int rr = 0; rr < rows; ++rr) {
     const int64_t row = r0 + rr;
-    if (row >= T) break;
     const float rs = rstd[row];
-    const float4* xr = reinterpret_cast<const float4*>(x + row * H);
-    const float4* gr = reinterpret_cast<const float4*>(dy + row * H);
-    float4 xh[MAXV], g[MAXV];
+    float4 xh[V], g[V];
     float dot = 0.f;
 #pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
+    for (int i = 0; i < V; ++i) {
       const int idx = threadIdx.x + i * NT;
       if (idx < nv) {
-        const float4 xv = xr[idx], dv = gr[idx];
+        const float4 xv = xn[i], dv = dn[i];
         xh[i] = make_float4(xv.x * rs, xv.y * rs, xv.z * rs, xv.w * rs);
         g[i] = make_float4(dv.x * wv[i].x, dv.y * wv[i].y, dv.z * wv[i].z, dv.w * wv[i].w);
         dot += g[i].x * xh[i].x + g[i].y * xh[i].y + g[i].z * xh[i].z + g[i].w * xh[i].w;
@@ -170,11 +184,20 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
         dwacc[i].w += dv.w * xh[i].w;
       }
     }
-    const float mean = block_sum(dot, red) / float(H);
+    if (rr + 1 < rows) load(row + 1);  // in flight during the reduction
+    // block reduction (double-buffered scratch: one barrier per row)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if ((threadIdx.x & 31) == 0) red[rr & 1][threadIdx.x / 32] = dot;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) tot += red[rr & 1][i];
+    const float mean = tot / float(H);
     const float4* rr4 = dres ? reinterpret_cast<const float4*>(dres + row * H) : nullptr;
     float4* o4 = reinterpret_cast<float4*>(dx_out + row * H);
 #pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
+    for (int i = 0; i < V; ++i) {
       const int idx = threadIdx.x + i * NT;
       if (idx < nv) {
         float4 o = make_float4(rs * (g[i].x - xh[i].x * mean), rs * (g[i].y - xh[i].y * mean),
@@ -192,13 +215,12 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
   }
   float4* dp = reinterpret_cast<float4*>(dw_part + int64_t(blockIdx.x) * H);
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
+  for (int i = 0; i < V; ++i) {
     const int idx = threadIdx.x + i * NT;
     if (idx < nv) dp[idx] = dwacc[i];
   }
 }
 
-// out[c] (+)= sum_r part[r, c]  (fixed order -> deterministic)
 __global__ void colsum_kernel(const float* __restrict__ part, int rows, int cols,
                               float* __restrict__ out, int accumulate) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -446,7 +468,14 @@ cudaError_t k_rmsnorm_bwd(const float* dy, const float* x, const __nv_bfloat16* 
   if (T <= 0) return cudaSuccess;
   const int nb = k_rmsnorm_bwd_parts(T);
   ++g_kernel_launches;
-  rmsnorm_bwd_kernel<<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
+  if (H <= NT * 4)
+    rmsnorm_bwd_kernel<1><<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
+  else if (H <= NT * 8)
+    rmsnorm_bwd_kernel<2><<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
+  else if (H <= NT * 16)
+    rmsnorm_bwd_kernel<4><<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
+  else
+    rmsnorm_bwd_kernel<8><<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
   ++g_kernel_launches;
   colsum_kernel<<<(H + 127) / 128, 128, 0, s>>>(dw_part, nb, H, dw, accumulate_dw);
   return cudaGetLastError();

@@ -68,6 +68,7 @@ void Step::mark(const std::string& name, const std::string& phase, int tid, cuda
 Step::~Step() {
   if (cs_) cudaStreamSynchronize(cs_);
   if (ms_) cudaStreamSynchronize(ms_);
+  if (os_) cudaStreamSynchronize(os_);
   for (size_t r = 0; r < peer_arena_.size(); ++r)
     if (peer_arena_[r] && peer_arena_[r] != arena_) cudaIpcCloseMemHandle(peer_arena_[r]);
   for (void* p : allocs_) cudaFree(p);
@@ -83,6 +84,22 @@ Step::~Step() {
   if (world_comm_) ncclCommDestroy(world_comm_);
   if (cs_) cudaStreamDestroy(cs_);
   if (ms_) cudaStreamDestroy(ms_);
+  if (os_) cudaStreamDestroy(os_);
+}
+
+int Step::opt_unit(Unit& u, cudaStream_t after, const std::string& name) {
+  if (u.params.empty()) return OPX_OK;
+  cudaEvent_t ready = ev();
+  CU(cudaEventRecord(ready, after));
+  CU(cudaStreamWaitEvent(os_, ready, 0));
+  CU(k_adamw(u.master, u.m, u.v, u.gshard, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps,
+             ex_.wd, step_count_, os_));
+  if (ex_.trace) {
+    cudaEvent_t done = ev();
+    CU(cudaEventRecord(done, os_));
+    mark(name, "optimizer", 2, ready, done);
+  }
+  return OPX_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -115,6 +132,7 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
   CU(cudaSetDevice(device));
   CU(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&os_, cudaStreamNonBlocking));
   for (cudaEvent_t* e : {&ev_start_, &ev_fwd_, &ev_bwd_, &ev_end_, &ev_head_ag_, &ev_head_rs_})
     CU(cudaEventCreate(e));
 
@@ -1023,6 +1041,7 @@ int Step::run(opx_step_report* rep) {
       if (eu.rep_comm)
         NC(ncclAllReduce(eu.gshard, eu.gshard, size_t(eu.shard), ncclFloat, ncclSum,
                          eu.rep_comm, cs_));
+      TRY(opt_unit(eu, cs_, "opt.experts.layer" + std::to_string(l)));
     }
     CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
     if (u.P > 1 || u.rep_comm) {
@@ -1043,6 +1062,9 @@ int Step::run(opx_step_report* rep) {
       if (tr)
         mark("bwd.rs.layer" + std::to_string(l) + ".m0", "bwd.layer" + std::to_string(l), 1, a,
              ev_rs_done_[size_t(l)]);
+      TRY(opt_unit(u, ms_, "opt.layer" + std::to_string(l)));
+    } else {
+      TRY(opt_unit(u, cs_, "opt.layer" + std::to_string(l)));
     }
   }
   CU(k_embed_bwd(d_ids_, dx_, hu.gfull + hu.params[0].off, T_, H_, cs_));
@@ -1058,6 +1080,9 @@ int Step::run(opx_step_report* rep) {
     if (hu.rep_comm)
       NC(ncclAllReduce(hu.gshard, hu.gshard, size_t(hu.shard), ncclFloat, ncclSum, hu.rep_comm,
                        ms_));
+    TRY(opt_unit(hu, ms_, "opt.head"));
+  } else {
+    TRY(opt_unit(hu, cs_, "opt.head"));
   }
   // join the comm stream
   cudaEvent_t join = ev();
@@ -1066,13 +1091,12 @@ int Step::run(opx_step_report* rep) {
   CU(cudaEventRecord(ev_bwd_, cs_));
 
   // ---------------- optimizer ----------------
-  for (Unit& u : units_)
-    CU(k_adamw(u.master, u.m, u.v, u.gshard, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps,
-               ex_.wd, step_count_, cs_));
-  for (Unit& u : expert_units_)
-    if (!u.params.empty())
-      CU(k_adamw(u.master, u.m, u.v, u.gshard, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2,
-                 ex_.eps, ex_.wd, step_count_, cs_));
+  // every unit's AdamW was issued on os_ as soon as its gradient was final;
+  // the step ends when the last one (the head, whose embedding gradient
+  // completes last) is done
+  cudaEvent_t opt_join = ev();
+  CU(cudaEventRecord(opt_join, os_));
+  CU(cudaStreamWaitEvent(cs_, opt_join, 0));
   CU(cudaEventRecord(ev_end_, cs_));
   if (tr) mark("optimizer", "optimizer", 0, ev_bwd_, ev_end_);
 

@@ -103,6 +103,10 @@ class Step {
 
   // ---- streams, comms, events
   cudaStream_t cs_ = nullptr, ms_ = nullptr;
+  // optimizer stream: each unit's AdamW runs as soon as its gradient is final
+  // (after its reduce-scatter), overlapping the rest of the backward
+  cudaStream_t os_ = nullptr;
+  int opt_unit(Unit& u, cudaStream_t after, const std::string& name);
   ncclComm_t world_comm_ = nullptr, shard_comm_ = nullptr, rep_comm_ = nullptr,
              shard_comm_head_ = nullptr;
   cudaEvent_t ev_start_ = nullptr, ev_fwd_ = nullptr, ev_bwd_ = nullptr, ev_end_ = nullptr;

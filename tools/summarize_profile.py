@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 
-def launch_shares(path, last_fraction=0.5):
+def launch_shares(path, last_fraction=0.5, last_n=None):
     rows = list(csv.reader(open(path)))
     hdr = None
     data = []
@@ -16,7 +16,7 @@ def launch_shares(path, last_fraction=0.5):
             continue
         if hdr and len(r) == len(hdr):
             data.append(dict(zip(hdr, r)))
-    data = data[int(len(data) * (1 - last_fraction)):]
+    data = data[-last_n:] if last_n else data[int(len(data) * (1 - last_fraction)):]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for d in data:
         name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
@@ -26,7 +26,8 @@ def launch_shares(path, last_fraction=0.5):
         agg[name][0] += 1
         agg[name][1] += v
     tot = sum(v[1] for v in agg.values())
-    out = [f"launch list (ncu gpu__time_duration.sum, --clock-control none; last {int(last_fraction*100)}% of launches = one step)",
+    what = f"last {last_n} launches" if last_n else f"last {int(last_fraction*100)}% of launches"
+    out = [f"launch list (ncu gpu__time_duration.sum, --clock-control none; {what} = one step)",
            f"{'kernel':58s} {'launches':>8s} {'ms':>10s} {'share':>7s}"]
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:20]:
         out.append(f"{k[:58]:58s} {v[0]:8d} {v[1] / 1e6:10.2f} {100 * v[1] / tot:6.2f}%")
@@ -61,7 +62,11 @@ def report_metrics(path):
 
 
 if __name__ == "__main__":
-    print(launch_shares(sys.argv[1]))
-    for p in sys.argv[2:]:
+    args = sys.argv[1:]
+    last_n = None
+    if args and args[0].startswith("--last="):
+        last_n = int(args.pop(0).split("=")[1])
+    print(launch_shares(args[0], last_n=last_n))
+    for p in args[1:]:
         print()
         print(report_metrics(p))
