@@ -130,9 +130,13 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
     return OPX_ERR_CONFIG;
   }
   CU(cudaSetDevice(device));
-  CU(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
-  CU(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
-  CU(cudaStreamCreateWithFlags(&os_, cudaStreamNonBlocking));
+  // compute and comm streams at the highest priority, the optimizer stream at
+  // the lowest: its HBM-bound AdamW blocks only fill SMs the step leaves idle
+  int prio_lo = 0, prio_hi = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CU(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, prio_hi));
+  CU(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, prio_hi));
+  CU(cudaStreamCreateWithPriority(&os_, cudaStreamNonBlocking, prio_lo));
   for (cudaEvent_t* e : {&ev_start_, &ev_fwd_, &ev_bwd_, &ev_end_, &ev_head_ag_, &ev_head_rs_})
     CU(cudaEventCreate(e));
 
