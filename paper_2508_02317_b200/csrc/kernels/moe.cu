@@ -11,6 +11,7 @@
 // buffers (CUDA-IPC mappings), laid out as per-local-expert segments padded to
 // 128 rows (so grouped-GEMM M tiles never straddle experts and wgrad K blocks
 // read zeros), ordered by source rank then by the source's pair order.
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "../runtime/kernels_api.h"
@@ -522,8 +523,9 @@ cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pai
                            int64_t ld_dst, int W, cudaStream_t s) {
   Layout L{ep, E, E / ep};
   const int smem = ep * (L.El + 1) * int(sizeof(int));
+  static const int max_blocks = getenv("OPX_A2A_BLOCKS") ? atoi(getenv("OPX_A2A_BLOCKS")) : num_sms() * 8;
   int blocks = (P * 32 + 255) / 256;
-  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
   ++g_kernel_launches;
   dispatch_kernel<<<blocks, 256, smem, s>>>(src, ld_src, per_pair, pair_at, P, k, counts_all,
@@ -535,8 +537,9 @@ cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* c
                           int E, int me, const int* g_start, __nv_bfloat16* const* dst,
                           int64_t ld_dst, int W, int max_rows, cudaStream_t s) {
   Layout L{ep, E, E / ep};
+  static const int max_bx = getenv("OPX_COMBINE_BX") ? atoi(getenv("OPX_COMBINE_BX")) : 64;
   int bx = (max_rows * 32 + 255) / 256 / L.El + 1;
-  if (bx > 64) bx = 64;
+  if (bx > max_bx) bx = max_bx;
   dim3 grid(bx, L.El);
   ++g_kernel_launches;
   combine_kernel<<<grid, 256, 0, s>>>(src, ld_src, counts_all, L, me, g_start, dst, ld_dst, W);

@@ -69,6 +69,7 @@ Step::~Step() {
   if (cs_) cudaStreamSynchronize(cs_);
   if (ms_) cudaStreamSynchronize(ms_);
   if (os_) cudaStreamSynchronize(os_);
+  if (xs_) cudaStreamSynchronize(xs_);
   for (size_t r = 0; r < peer_arena_.size(); ++r)
     if (peer_arena_[r] && peer_arena_[r] != arena_) cudaIpcCloseMemHandle(peer_arena_[r]);
   for (void* p : allocs_) cudaFree(p);
@@ -85,6 +86,9 @@ Step::~Step() {
   if (cs_) cudaStreamDestroy(cs_);
   if (ms_) cudaStreamDestroy(ms_);
   if (os_) cudaStreamDestroy(os_);
+  if (xs_) cudaStreamDestroy(xs_);
+  for (auto e : ev_redisp_)
+    if (e) cudaEventDestroy(e);
 }
 
 int Step::opt_unit(Unit& u, cudaStream_t after, const std::string& name) {
@@ -1006,6 +1010,18 @@ int Step::run(opx_step_report* rep) {
   }
   CU(cudaEventRecord(ev_fwd_, cs_));
 
+  if (moe_ && save_acts_) {
+    // the top MoE layer's token re-send can start now, overlapping the head:
+    // every peer passed that layer's forward combine barrier, so its expert
+    // GEMMs no longer read the receive buffer
+    const int lt = next_moe_below(L);
+    if (lt >= 0) {
+      cudaEvent_t e = ev();
+      CU(cudaEventRecord(e, cs_));
+      CU(cudaStreamWaitEvent(xs_, e, 0));
+      TRY(moe_redispatch(lt));
+    }
+  }
   // ---------------- head (fwd + CE + bwd) ----------------
   TRY(head_fwd_bwd(hu, hu.gfull));
 
@@ -1101,6 +1117,11 @@ int Step::run(opx_step_report* rep) {
   cudaEvent_t opt_join = ev();
   CU(cudaEventRecord(opt_join, os_));
   CU(cudaStreamWaitEvent(cs_, opt_join, 0));
+  if (xs_) {
+    cudaEvent_t xj = ev();
+    CU(cudaEventRecord(xj, xs_));
+    CU(cudaStreamWaitEvent(cs_, xj, 0));
+  }
   CU(cudaEventRecord(ev_end_, cs_));
   if (tr) mark("optimizer", "optimizer", 0, ev_bwd_, ev_end_);
 

@@ -237,6 +237,19 @@ class Step {
   int** count_tab_cur() { return d_count_tables_ + size_t(rslot_) * kMaxSp; }
   bf16** yback_tab_cur() { return d_yback_peers_ + size_t(rslot_) * kMaxSp; }
   uint32_t** d_ep_flags_ = nullptr;
+  // recompute=none MoE backward: the token re-send of layer l runs on xs_ with
+  // its own barrier flags while the compute stream finishes the layer above
+  cudaStream_t xs_ = nullptr;
+  size_t off_flags_ep2_ = 0;
+  uint32_t** d_ep_flags2_ = nullptr;
+  uint32_t epoch_ep2_ = 0;
+  std::vector<cudaEvent_t> ev_redisp_;  // [layer]
+  int moe_redispatch(int l);            // issue on xs_ after the caller's cs_ point
+  int next_moe_below(int l) const {
+    for (int j = l - 1; j >= 0; --j)
+      if (a_.is_moe_layer(j)) return j;
+    return -1;
+  }
   int** d_count_tables_ = nullptr;
   bf16** d_xrecv_peers_ = nullptr;
   bf16** d_yback_peers_ = nullptr;

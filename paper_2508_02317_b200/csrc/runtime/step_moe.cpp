@@ -131,6 +131,7 @@ size_t Step::moe_arena(size_t off) {
   const size_t H = size_t(H_), P = size_t(T_) * size_t(topk_);
   cap_rows_ = int64_t(P) * ep_ + int64_t(El_) * 128;
   off_flags_ep_ = take(64 * sizeof(uint32_t));
+  off_flags_ep2_ = take(64 * sizeof(uint32_t));
   const int L = int(a_.layers);
   const int nslots = save_acts_ ? 1 + L : 1;
   off_counts_s_.assign(size_t(nslots), 0);
@@ -180,6 +181,14 @@ int Step::moe_alloc() {
   dyp_ = alloc<bf16>(P * H, false);
   dlogits_ = alloc<bf16>(T * E, false);
   d_ep_flags_ = alloc<uint32_t*>(kMaxSp);
+  d_ep_flags2_ = alloc<uint32_t*>(kMaxSp);
+  if (save_acts_) {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&xs_, cudaStreamNonBlocking, hi));
+    ev_redisp_.assign(size_t(a_.layers), nullptr);
+    for (auto& e : ev_redisp_) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   d_count_tables_ = alloc<int*>(kMaxSp * routes_.size());
   d_xrecv_peers_ = alloc<bf16*>(kMaxSp);
   d_yback_peers_ = alloc<bf16*>(kMaxSp * routes_.size());
@@ -230,10 +239,12 @@ void Step::moe_bind(int l) {
 
 int Step::moe_import() {
   const size_t ns = routes_.size();
-  std::vector<void*> fl(kMaxSp, nullptr), ct(kMaxSp * ns, nullptr), xr(kMaxSp, nullptr),
+  std::vector<void*> fl(kMaxSp, nullptr), fl2(kMaxSp, nullptr), ct(kMaxSp * ns, nullptr),
+      xr(kMaxSp, nullptr),
       yb(kMaxSp * ns, nullptr), dy(kMaxSp, nullptr), dx(kMaxSp, nullptr);
   for (int j = 0; j < ep_; ++j) {
     fl[size_t(j)] = ep_peer(j, off_flags_ep_);
+    fl2[size_t(j)] = ep_peer(j, off_flags_ep2_);
     for (size_t sl = 0; sl < ns; ++sl) {
       ct[sl * kMaxSp + size_t(j)] = ep_peer(j, off_counts_s_[sl]);
       yb[sl * kMaxSp + size_t(j)] = ep_peer(j, off_yback_s_[sl]);
@@ -244,11 +255,36 @@ int Step::moe_import() {
   }
   const size_t b = kMaxSp * sizeof(void*);
   CU(cudaMemcpy(d_ep_flags_, fl.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_ep_flags2_, fl2.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_count_tables_, ct.data(), b * ns, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_xrecv_peers_, xr.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_yback_peers_, yb.data(), b * ns, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_dyrecv_peers_, dy.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_dxback_peers_, dx.data(), b, cudaMemcpyHostToDevice));
+  return OPX_OK;
+}
+
+int Step::moe_redispatch(int l) {
+  if (l < 0 || !xs_ || !keeps_acts(l) || !a_.is_moe_layer(l)) return OPX_OK;
+  const MoeRoute& r = routes_[size_t(1 + l)];
+  const int* counts = reinterpret_cast<const int*>(arena_ + off_counts_s_[size_t(1 + l)]);
+  const int P = T_ * topk_;
+  cudaEvent_t a = ex_.trace ? ev() : nullptr;
+  if (a) cudaEventRecord(a, xs_);
+  CU(k_moe_dispatch(saved_[size_t(l)].h2, H_, 0, r.pairat, P, topk_, counts, r.excl, ep_, E_,
+                    ep_i_, d_xrecv_peers_, H_, H_, xs_));
+  if (ep_ > 1) {
+    ++epoch_ep2_;
+    CU(k_peer_barrier(d_ep_flags2_, reinterpret_cast<uint32_t*>(arena_ + off_flags_ep2_), ep_, ep_i_,
+                      epoch_ep2_, d_timeout_, xs_));
+  }
+  CU(cudaEventRecord(ev_redisp_[size_t(l)], xs_));
+  if (a) {
+    cudaEvent_t b = ev();
+    cudaEventRecord(b, xs_);
+    mark("bwd.layer" + std::to_string(l) + ".m0.a2a_redispatch", "bwd.layer" + std::to_string(l), 3,
+         a, b);
+  }
   return OPX_OK;
 }
 
@@ -372,14 +408,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
   bf16* dyrecv = reinterpret_cast<bf16*>(arena_ + off_dyrecv_);
   bf16* dxback = reinterpret_cast<bf16*>(arena_ + off_dxback_);
   if (kept) {
-    // selective recompute: routing and combined outputs are resident; re-send
-    // the tokens (the expert-side receive buffer is shared scratch) and redo
-    // gate|up, storing the pre-activations for the SwiGLU backward
-    CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                      d_xrecv_peers_, H, H, cs_));
-    mk("a2a_redispatch");
-    TRY(barrier_ep(cs_));
-    mk("a2a_wait");
+    // selective recompute: routing and combined outputs are resident; the
+    // tokens were re-sent on xs_ (moe_redispatch, overlapping the layer above);
+    // redo gate|up, storing the pre-activations for the SwiGLU backward
+    CU(cudaStreamWaitEvent(cs_, ev_redisp_[size_t(l)], 0));
+    mk("a2a_redispatch_wait");
     CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
     GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu, H, false, GEMM_EPI_SWIGLU, gu_e_,
                          2 * Fe, El_, 0, g_start_, g_rows_, cap_rows_, 0);
@@ -448,6 +481,17 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
               cs_));
   CU(k_sum_partials(wr_part_, wr_split_, int64_t(E) * H, G + u.params[6].off, cs_));
   mk("router");
+  if (kept) {
+    // every peer passed the dispatch_grad barrier above, so all of them are done
+    // with their receive buffers for this layer: re-send the next MoE layer's tokens
+    const int ln = next_moe_below(l);
+    if (ln >= 0) {
+      cudaEvent_t e = ev();
+      CU(cudaEventRecord(e, cs_));
+      CU(cudaStreamWaitEvent(xs_, e, 0));
+      TRY(moe_redispatch(ln));
+    }
+  }
   return OPX_OK;
 }
 
