@@ -95,6 +95,15 @@ int opx_step_load_batch(opx_step* st, const int32_t* ids, const int32_t* labels,
                         const int32_t* positions, const int32_t* cu_seqlens, int n_cu,
                         int64_t n_valid_global);
 int opx_step_run(opx_step* st, opx_step_report* rep);
+/* FSDP flat-shard checkpoint: every unit's fp32 master /
+ * exp_avg / exp_avg_sq shards in the executor's chunked layout plus a
+ * manifest; replaces the reference's on-disk step state that `omniplan
+ * reshard` plans move between world sizes (reshard.cpp:20-56, cli.cpp:422-496).
+ * Collective in spirit: every rank calls it; synchronise ranks around it. */
+int opx_step_save(opx_step* st, const char* dir);
+/* Loads a checkpoint saved with the same shard counts (reshard it first with
+ * paper_2508_02317_b200/checkpoint.py otherwise); bf16 params = round(master). */
+int opx_step_load(opx_step* st, const char* dir);
 /* Copies a named tensor to host. Names: "param:<name>", "grad:<name>",
  * "master:<name>", "exp_avg:<name>", "exp_avg_sq:<name>", "loss_rows".
  * <name> follows HF naming ("model.layers.0.self_attn.q_proj.weight"). Only
@@ -160,6 +169,14 @@ int opx_attn_bwd_tc_f32kv(const void* q, const void* k, const void* v, const voi
                           float* dv_acc, float* delta, int64_t ld_q, int64_t ld_kv,
                           const int32_t* seq_start, const int32_t* seq_end, int N, int hq, int hk,
                           float scale, int kv_splits, void* stream);
+/* Reshard copy plan for one flat parameter (reshard.cpp:20-56 make_plan):
+ * rank r of a layout owns [min(r*c, numel), min((r+1)*c, numel)) with
+ * c = ceil(numel/parts) when align == 0 (the reference) or
+ * c = round_up(numel, align*parts)/parts (the executor's FSDP units, align 64).
+ * Writes {"numel","src_chunk","dst_chunk","ops":[[src_rank,src_off,dst_rank,dst_off,len],..]}
+ * ordered by (dst_rank, dst_offset); verified like reshard.cpp:58-110. */
+int opx_reshard_plan(int64_t numel, int64_t src_parts, int64_t src_align, int64_t dst_parts,
+                     int64_t dst_align, char* out_json, size_t cap);
 /* Single-rank Ulysses relayout (sp == 1 path) with RoPE, for testing. */
 int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void* v_full,
                   int hq, int hk, int rows, int S, const int32_t* pos, const float* inv_freq,

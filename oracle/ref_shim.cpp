@@ -11,6 +11,7 @@
 #include "omniplan/comm.hpp"
 #include "omniplan/config_io.hpp"
 #include "omniplan/plan.hpp"
+#include "omniplan/reshard.hpp"
 #include "omniplan/simulator.hpp"
 #include "omniplan/step_graph.hpp"
 
@@ -138,6 +139,20 @@ int ref_simulate(const char* cj, const char* mj, const char* wj, const char* pj,
     json names = json::array();
     for (auto& n : g.nodes) names.push_back(n.name);
     r["node_names"] = names;
+    return out(r.dump(), buf, cap);
+  } catch (const std::exception& e) {
+    return out(std::string("{\"error\": ") + json(e.what()).dump() + "}", buf, cap) ? 9 : 2;
+  }
+}
+
+// The reference's reshard copy plan (reshard.cpp:20-56) for ceil-chunk layouts.
+int ref_reshard_plan(long long numel, long long src_parts, long long dst_parts, char* buf,
+                     size_t cap) {
+  try {
+    ReshardPlan p = make_plan(ShardLayout{"p", numel, src_parts}, ShardLayout{"p", numel, dst_parts});
+    json ops = json::array();
+    for (auto& o : p.ops) ops.push_back({o.src_rank, o.src_offset, o.dst_rank, o.dst_offset, o.len});
+    json r{{"numel", p.numel}, {"ops", ops}, {"violations", verify(p, numel)}};
     return out(r.dump(), buf, cap);
   } catch (const std::exception& e) {
     return out(std::string("{\"error\": ") + json(e.what()).dump() + "}", buf, cap) ? 9 : 2;

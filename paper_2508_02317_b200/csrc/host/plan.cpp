@@ -324,6 +324,63 @@ Interval owned_interval(i64 n, i64 parts, i64 r) {
   return {std::min(r * c, n), std::min((r + 1) * c, n)};
 }
 
+i64 layout_chunk(i64 n, i64 parts, i64 align) {
+  if (parts <= 0) throw std::invalid_argument("parts must be positive");
+  if (align <= 0) return (n + parts - 1) / parts;
+  const i64 q = align * parts;
+  return (n + q - 1) / q * q / parts;
+}
+
+Interval chunk_interval(i64 n, i64 c, i64 r) { return {std::min(r * c, n), std::min((r + 1) * c, n)}; }
+
+// Interval intersection of every destination shard with every source shard,
+// ordered by (dst_rank, dst_offset) like make_plan (reshard.cpp:20-56).
+std::vector<CopyOp> reshard_plan(i64 n, i64 sp, i64 sc, i64 dp, i64 dc) {
+  if (sp <= 0 || dp <= 0) throw std::invalid_argument("parts must be positive");
+  if (sc * sp < n || dc * dp < n) throw std::invalid_argument("layout does not cover numel");
+  std::vector<CopyOp> ops;
+  for (i64 d = 0; d < dp; ++d) {
+    const Interval di = chunk_interval(n, dc, d);
+    if (di.end <= di.begin) continue;
+    for (i64 s = 0; s < sp; ++s) {
+      const Interval si = chunk_interval(n, sc, s);
+      const i64 lo = std::max(di.begin, si.begin), hi = std::min(di.end, si.end);
+      if (lo < hi) ops.push_back({s, lo - si.begin, d, lo - di.begin, hi - lo});
+    }
+  }
+  return ops;
+}
+
+// Same checks as verify (reshard.cpp:58-110): positive lengths, total == numel,
+// every destination rank written contiguously from 0 with no gap or overlap.
+std::vector<std::string> reshard_verify(const std::vector<CopyOp>& ops, i64 n) {
+  std::vector<std::string> v;
+  i64 total = 0, max_dst = -1;
+  for (auto& o : ops) {
+    total += o.len;
+    max_dst = std::max(max_dst, o.dst_rank);
+    if (o.len <= 0) v.push_back("non-positive copy length in op for dst rank " + std::to_string(o.dst_rank));
+  }
+  if (total != n) v.push_back("copy lengths sum to " + std::to_string(total) + ", expected " + std::to_string(n));
+  std::vector<std::vector<Interval>> per(size_t(max_dst + 1));
+  for (auto& o : ops)
+    if (o.len > 0) per[size_t(o.dst_rank)].push_back({o.dst_offset, o.dst_offset + o.len});
+  i64 covered = 0;
+  for (size_t d = 0; d < per.size(); ++d) {
+    auto& iv = per[d];
+    std::sort(iv.begin(), iv.end(), [](const Interval& a, const Interval& b) { return a.begin < b.begin; });
+    i64 cur = 0;
+    for (auto& i : iv) {
+      if (i.begin < cur) v.push_back("overlapping writes on dst rank " + std::to_string(d));
+      else if (i.begin > cur) v.push_back("coverage gap on dst rank " + std::to_string(d));
+      cur = std::max(cur, i.end);
+    }
+    covered += cur;
+  }
+  if (covered != n && total == n) v.push_back("destination coverage is " + std::to_string(covered));
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // JSON configs: same field names as config_io.cpp:52-151.
 // ---------------------------------------------------------------------------

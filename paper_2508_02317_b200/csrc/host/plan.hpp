@@ -166,6 +166,21 @@ struct Interval {
 };
 Interval owned_interval(i64 numel, i64 parts, i64 rank);
 
+// ---- reshard copy plans (reshard.cpp:20-56 make_plan, :58-110 verify) -------
+// Rank r of a layout owns [min(r*c, n), min((r+1)*c, n)).  chunk = 0 means the
+// reference's c = ceil(n / parts); the executor's FSDP units use
+// c = round_up(n, align*parts) / parts (flat buffers padded for aligned
+// collectives), so a checkpoint shard is "chunk c of the logical numel" and
+// the same interval-intersection plan moves it between world sizes.
+struct CopyOp {
+  i64 src_rank = 0, src_offset = 0, dst_rank = 0, dst_offset = 0, len = 0;
+};
+i64 layout_chunk(i64 numel, i64 parts, i64 align);  // align 0 -> ceil(n/parts)
+Interval chunk_interval(i64 numel, i64 chunk, i64 rank);
+std::vector<CopyOp> reshard_plan(i64 numel, i64 src_parts, i64 src_chunk, i64 dst_parts,
+                                 i64 dst_chunk);
+std::vector<std::string> reshard_verify(const std::vector<CopyOp>& ops, i64 numel);
+
 // ---- JSON config I/O (config_io.cpp:52-151, 248-262) -----------------------
 // All parse functions throw opx::ConfigError with a path-qualified message.
 struct ConfigError : std::exception {

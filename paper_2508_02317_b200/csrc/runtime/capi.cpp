@@ -404,6 +404,38 @@ int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, 
   OPX_CALL(k_attn_bwd_tc(a, static_cast<cudaStream_t>(stream)), "opx_attn_bwd_tc");
 }
 
+int opx_reshard_plan(int64_t numel, int64_t src_parts, int64_t src_align, int64_t dst_parts,
+                     int64_t dst_align, char* out_json, size_t cap) {
+  try {
+    const int64_t sc = opx::layout_chunk(numel, src_parts, src_align);
+    const int64_t dc = opx::layout_chunk(numel, dst_parts, dst_align);
+    const auto ops = opx::reshard_plan(numel, src_parts, sc, dst_parts, dc);
+    const auto bad = opx::reshard_verify(ops, numel);
+    if (!bad.empty()) {
+      opx::set_error("reshard plan invalid: " + bad[0]);
+      return OPX_ERR_ARG;
+    }
+    std::string s = "{\"numel\":" + std::to_string(numel) + ",\"src_chunk\":" + std::to_string(sc) +
+                    ",\"dst_chunk\":" + std::to_string(dc) + ",\"ops\":[";
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const auto& o = ops[i];
+      s += (i ? ",[" : "[") + std::to_string(o.src_rank) + "," + std::to_string(o.src_offset) + "," +
+           std::to_string(o.dst_rank) + "," + std::to_string(o.dst_offset) + "," +
+           std::to_string(o.len) + "]";
+    }
+    s += "]}";
+    if (s.size() + 1 > cap) {
+      opx::set_error("reshard plan buffer too small");
+      return OPX_ERR_ARG;
+    }
+    std::memcpy(out_json, s.c_str(), s.size() + 1);
+    return OPX_OK;
+  } catch (const std::exception& e) {
+    opx::set_error(e.what());
+    return OPX_ERR_ARG;
+  }
+}
+
 int opx_attn_bwd_tc_f32kv(const void* q, const void* k, const void* v, const void* o,
                           const float* lse, const void* dout, float* dq_acc, float* dk_acc,
                           float* dv_acc, float* delta, int64_t ld_q, int64_t ld_kv,

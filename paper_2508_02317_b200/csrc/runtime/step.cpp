@@ -1358,6 +1358,8 @@ int opx_step_load_batch(opx_step* st, const int32_t* ids, const int32_t* labels,
   return st->impl.load_batch(ids, labels, positions, cu, n_cu, n_valid);
 }
 int opx_step_run(opx_step* st, opx_step_report* rep) { return st->impl.run(rep); }
+int opx_step_save(opx_step* st, const char* dir) { return st->impl.save(dir ? dir : ""); }
+int opx_step_load(opx_step* st, const char* dir) { return st->impl.load(dir ? dir : ""); }
 int opx_step_get(opx_step* st, const char* name, void* dst, size_t bytes) {
   return st->impl.get(name, dst, bytes);
 }

@@ -80,6 +80,8 @@ class Step {
   int load_batch(const int32_t* ids, const int32_t* labels, const int32_t* pos, const int32_t* cu,
                  int n_cu, int64_t n_valid);
   int run(opx_step_report* rep);
+  int save(const std::string& dir);  // checkpoint.cpp
+  int load(const std::string& dir);
   int get(const std::string& name, void* dst, size_t bytes);
   int info(const std::string& name, int64_t* numel, int64_t* b, int64_t* e);
   std::string trace_json();
@@ -279,6 +281,11 @@ class Step {
   int barrier_ep(cudaStream_t s);
   int moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out);
   int moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh2);
+  struct CkptUnit {
+    std::string name;
+    Unit* u;
+  };
+  std::vector<CkptUnit> ckpt_units();
   int check(cudaError_t e, const char* what);
   int nccl(ncclResult_t r, const char* what);
 };

@@ -178,6 +178,20 @@ class Session:
         check(lib().opx_step_get(self.h, b"loss_rows", out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
         return out
 
+    def save(self, path: str):
+        """FSDP flat-shard checkpoint (opx_step_save); every rank calls it."""
+        if self.dist is not None and self.world > 1:
+            self.dist.barrier()
+        check(lib().opx_step_save(self.h, os.fspath(path).encode()))
+        if self.dist is not None and self.world > 1:
+            self.dist.barrier()
+
+    def load_checkpoint(self, path: str):
+        """Loads a checkpoint with this plan's shard counts (see checkpoint.reshard)."""
+        if self.dist is not None and self.world > 1:
+            self.dist.barrier()
+        check(lib().opx_step_load(self.h, os.fspath(path).encode()))
+
     def trace(self) -> dict:
         cap = 1 << 24
         buf = ctypes.create_string_buffer(cap)

@@ -40,3 +40,34 @@ def step_worker(rank, world, port, model, plan, S, rows, q, names):
         q.put((rank, None, None, traceback.format_exc()))
     finally:
         td.destroy_process_group()
+
+
+def ckpt_worker(rank, world, port, model, plan, S, rows, q, names, path):
+    """One step, save a checkpoint, then a second step; returns the masters at
+    the checkpoint and the second step's loss."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import torch.distributed as td
+
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_02317_b200.runtime import Session, synthetic_batch
+        from tests.step_common import EXEC, cluster
+
+        wl = {"seq_len": S, "micro_batch": plan["micro_batch"], "global_batch": rows}
+        s = Session(cluster(world), model, wl, plan, EXEC, rank=rank, device=rank, dist=td)
+        s.init_weights(EXEC["seed"])
+        batch = synthetic_batch(model["modules"][0]["arch"]["vocab"], S, rows, seed=2508)
+        s.load(batch)
+        s.run()
+        s.save(path)
+        out = {n: s.get(f"master:{n}") for n in names}
+        r2 = s.run()
+        q.put((rank, r2.loss, out, None))
+        s.close()
+    except Exception:
+        import traceback
+
+        q.put((rank, None, None, traceback.format_exc()))
+    finally:
+        td.destroy_process_group()

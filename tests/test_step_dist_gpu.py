@@ -105,3 +105,55 @@ def test_dist_step_matches_oracle(world, plan, rows):
 
     batch = synthetic_batch(2048, S, rows, seed=2508)
     compare_step(sessions, model, batch, plan, loss)
+
+
+@gpu
+def test_checkpoint_reshard_fsdp2_to_1(tmp_path):
+    """f3: save FSDP2 shards after one step, reshard 2 -> 1 with the reference's
+    copy plan, load on one GPU: masters are bit-identical and the next step's
+    loss matches the FSDP2 run's."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    from oracle import model as om
+    from paper_2508_02317_b200 import checkpoint
+    from paper_2508_02317_b200.runtime import Session, synthetic_batch
+    from tests.dist_worker import ckpt_worker
+    from tests.step_common import EXEC, cluster, gpu_param_names
+
+    model = tiny_dense(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048)
+    arch = om.Arch.from_model_json(model)
+    names = gpu_param_names(arch)
+    S, rows = 512, 2
+    plan2 = {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 1, "micro_batch": 1}
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    a = str(tmp_path / "fsdp2")
+    ps = [ctx.Process(target=ckpt_worker, args=(r, 2, port, model, plan2, S, rows, q, names, a))
+          for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(2):
+        rank, loss, out, err = q.get(timeout=600)
+        assert err is None, err
+        res[rank] = (loss, out)
+    for p in ps:
+        p.join(60)
+    b = str(tmp_path / "fsdp1")
+    checkpoint.reshard(a, b, dp_shard=1, sp=1)
+
+    plan1 = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": rows}
+    wl = {"seq_len": S, "micro_batch": rows, "global_batch": rows}
+    s = Session(cluster(1), model, wl, plan1, EXEC, rank=0, device=0)
+    s.load_checkpoint(b)
+    for n in names:
+        full, numel, b0, e0 = s.get(f"master:{n}")
+        parts = sorted((res[r][1][n] for r in range(2)), key=lambda t: t[2])
+        cat = np.concatenate([p[0] for p in parts if p[3] > p[2]])
+        assert cat.size == numel and full.size == numel
+        assert np.array_equal(full, cat), n
+    s.load(synthetic_batch(2048, S, rows, seed=2508))
+    r2 = s.run()
+    assert abs(r2.loss - res[0][0]) <= 1e-3 * abs(res[0][0]), (r2.loss, res[0][0])
+    s.close()
