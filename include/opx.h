@@ -169,6 +169,13 @@ int opx_attn_bwd_tc_f32kv(const void* q, const void* k, const void* v, const voi
                           float* dv_acc, float* delta, int64_t ld_q, int64_t ld_kv,
                           const int32_t* seq_start, const int32_t* seq_end, int N, int hq, int hk,
                           float scale, int kv_splits, void* stream);
+/* Sequence packing (packing.cpp:10-83 pack + padding_ratio): first fit of
+ * samples (ids may be NULL -> 0..n-1) toward `target` tokens; policy 0 = first
+ * fit decreasing (ties by ascending id), 1 = arrival order.  Writes
+ * {"rows":[{"capacity","entries":[[id,offset,length],..],"boundaries":[..]}],
+ *  "padding_ratio":x}; an over-length sample returns 2 (PackError's message). */
+int opx_pack(const int64_t* ids, const int64_t* lengths, int64_t n, int64_t target, int policy,
+             char* out_json, size_t cap);
 /* Reshard copy plan for one flat parameter (reshard.cpp:20-56 make_plan):
  * rank r of a layout owns [min(r*c, numel), min((r+1)*c, numel)) with
  * c = ceil(numel/parts) when align == 0 (the reference) or

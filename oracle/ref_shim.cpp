@@ -10,6 +10,7 @@
 #include "json.hpp"
 #include "omniplan/comm.hpp"
 #include "omniplan/config_io.hpp"
+#include "omniplan/packing.hpp"
 #include "omniplan/plan.hpp"
 #include "omniplan/reshard.hpp"
 #include "omniplan/simulator.hpp"
@@ -140,6 +141,29 @@ int ref_simulate(const char* cj, const char* mj, const char* wj, const char* pj,
     for (auto& n : g.nodes) names.push_back(n.name);
     r["node_names"] = names;
     return out(r.dump(), buf, cap);
+  } catch (const std::exception& e) {
+    return out(std::string("{\"error\": ") + json(e.what()).dump() + "}", buf, cap) ? 9 : 2;
+  }
+}
+
+// The reference's packer (packing.cpp:10-50): policy 0 FFD, 1 arrival.
+int ref_pack(const long long* lengths, long long n, long long target, int policy, char* buf,
+             size_t cap) {
+  try {
+    std::vector<Sample> v;
+    for (long long i = 0; i < n; ++i) v.push_back(Sample{i, lengths[i]});
+    auto rows = pack(v, target, policy == 1 ? PackPolicy::first_fit_arrival
+                                            : PackPolicy::first_fit_decreasing);
+    json rj = json::array();
+    for (auto& r : rows) {
+      json e = json::array();
+      for (auto& x : r.entries) e.push_back({x.id, x.offset, x.length});
+      rj.push_back({{"capacity", r.capacity}, {"entries", e}, {"boundaries", r.boundaries}});
+    }
+    return out(json{{"rows", rj}, {"padding_ratio", padding_ratio(rows)}}.dump(), buf, cap);
+  } catch (const PackError& e) {
+    return out(std::string("{\"error\": ") + json(e.what()).dump() + ", \"sample\": " +
+                   std::to_string(e.sample_id) + "}", buf, cap) ? 9 : 2;
   } catch (const std::exception& e) {
     return out(std::string("{\"error\": ") + json(e.what()).dump() + "}", buf, cap) ? 9 : 2;
   }

@@ -4,6 +4,7 @@
 #include <sstream>
 #include <string>
 
+#include "../host/packing.hpp"
 #include "../host/plan.hpp"
 #include "common.h"
 #include "json.hpp"
@@ -402,6 +403,38 @@ int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, 
   a.lddv = ld_kv;
   a.delta = delta;
   OPX_CALL(k_attn_bwd_tc(a, static_cast<cudaStream_t>(stream)), "opx_attn_bwd_tc");
+}
+
+int opx_pack(const int64_t* ids, const int64_t* lengths, int64_t n, int64_t target, int policy,
+             char* out_json, size_t cap) {
+  try {
+    std::vector<opx::PackSample> v(size_t(n > 0 ? n : 0));
+    for (int64_t i = 0; i < n; ++i) v[size_t(i)] = {ids ? ids[i] : i, lengths[i]};
+    const auto rows = opx::pack(v, target, policy == 1 ? opx::PackPolicy::first_fit_arrival
+                                                       : opx::PackPolicy::first_fit_decreasing);
+    nlohmann::json j;
+    nlohmann::json rj = nlohmann::json::array();
+    for (const auto& r : rows) {
+      nlohmann::json e = nlohmann::json::array();
+      for (const auto& x : r.entries) e.push_back({x.id, x.offset, x.length});
+      rj.push_back({{"capacity", r.capacity}, {"entries", e}, {"boundaries", r.boundaries}});
+    }
+    j["rows"] = rj;
+    j["padding_ratio"] = opx::padding_ratio(rows);
+    const std::string s = j.dump();
+    if (s.size() + 1 > cap) {
+      opx::set_error("pack output buffer too small (need " + std::to_string(s.size() + 1) + ")");
+      return OPX_ERR_ARG;
+    }
+    std::memcpy(out_json, s.c_str(), s.size() + 1);
+    return OPX_OK;
+  } catch (const opx::PackError& e) {
+    opx::set_error(e.what());
+    return OPX_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    opx::set_error(e.what());
+    return OPX_ERR_ARG;
+  }
 }
 
 int opx_reshard_plan(int64_t numel, int64_t src_parts, int64_t src_align, int64_t dst_parts,

@@ -74,3 +74,26 @@ def test_step_deterministic_loss_and_second_step():
     assert r1b.loss == r1.loss
     s.close()
     s2.close()
+
+
+@gpu
+def test_step_ffd_packed_batch_with_padding():
+    """f1: a batch produced by the first-fit-decreasing packer (short rows get
+    a trailing padding segment with ignored labels) through the full step."""
+    from paper_2508_02317_b200 import packing as pk
+    from paper_2508_02317_b200.runtime import Session
+
+    model = tiny_dense()
+    arch = model["modules"][0]["arch"]
+    rng = np.random.default_rng(5)
+    samples = [rng.integers(0, arch["vocab"], n) for n in (700, 250, 600, 180, 90, 77)]
+    batch, rep = pk.packed_batch(samples, 1024, rows=2)
+    assert rep["padding_ratio"] > 0
+    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": 2, "recompute": "full"}
+    wl = {"seq_len": 1024, "micro_batch": 2, "global_batch": 2}
+    s = Session(cluster(1), model, wl, plan, EXEC, rank=0, device=0)
+    s.init_weights(EXEC["seed"])
+    s.load(batch)
+    r = s.run()
+    compare_step([s], model, batch, plan, r.loss)
+    s.close()
