@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the fwd+bwd+AdamW training step (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c0] [--impl opx|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c4|c0] [--impl opx|reference]
 
 N > 1 is launched by the driver under torchrun (one rank per GPU).  Rank 0
 prints ONE JSON line.  `value` is whole-job tokens/s from device time (CUDA
@@ -29,6 +29,9 @@ METRIC = "train tokens/sec/GPU and MFU (fwd+bwd+opt step) at 1/2/4/8 B200 vs CPU
 
 QWEN2_7B = {"layers": 28, "hidden": 3584, "heads": 28, "kv_heads": 4, "head_dim": 128,
             "ffn_dim": 18944, "vocab": 152064}
+# C4: Qwen2-72B-shaped 8-layer slice, the long-context HBM-sizing stress
+QWEN2_72B_SLICE = {"layers": 8, "hidden": 8192, "heads": 64, "kv_heads": 8, "head_dim": 128,
+                   "ffn_dim": 29568, "vocab": 152064}
 QWEN3_30B_A3B = {"layers": 48, "hidden": 2048, "heads": 16, "kv_heads": 4, "head_dim": 128,
                  "ffn_dim": 6144, "vocab": 151936,
                  "moe": {"num_experts": 128, "top_k": 8, "expert_ffn_dim": 768, "moe_layer_stride": 1}}
@@ -45,6 +48,11 @@ def plan_for(cfg: str, n: int) -> dict:
         # activations fit and recompute=none removes the extra forward.
         return {"dp_replicate": 1, "dp_shard": n // sp, "sp": sp, "ep": 1, "micro_batch": 1,
                 "recompute": "full" if n == 1 else "none", "fsdp_prefetch_depth": 1}
+    if cfg == "c4":  # SP over all GPUs (SP8, shard 1); 128K tokens, one row
+        # per-layer activations at 128K/sp tokens (~10 GB at SP4, ~5 GB at SP8):
+        # keep them from 8 GPUs, recompute below
+        return {"dp_replicate": 1, "dp_shard": 1, "sp": n, "ep": 1, "micro_batch": 1,
+                "recompute": "none" if n >= 8 else "full", "fsdp_prefetch_depth": 1}
     if cfg == "c2":  # FSDP + EP over all GPUs (FSDP8+EP8)
         # recompute=none keeps attention activations, routing and combined expert
         # outputs (~0.6 GB/layer at 8K tokens); the backward re-sends tokens and
@@ -56,7 +64,7 @@ def plan_for(cfg: str, n: int) -> dict:
 
 
 def model_for(cfg: str, n: int = 8) -> dict:
-    arch = dict({"c1": QWEN2_7B, "c0": TINY, "c2": QWEN3_30B_A3B}[cfg])
+    arch = dict({"c1": QWEN2_7B, "c0": TINY, "c2": QWEN3_30B_A3B, "c4": QWEN2_72B_SLICE}[cfg])
     if cfg == "c2" and n < 8:
         # 30B does not fit below 8 GPUs (reference memory model: 235/455 GiB at
         # EP2/EP1); scale the layer count with the GPU count (a layer slice)
@@ -66,7 +74,7 @@ def model_for(cfg: str, n: int = 8) -> dict:
 
 
 def seq_for(cfg: str) -> int:
-    return {"c1": 32768, "c0": 1024, "c2": 8192}[cfg]
+    return {"c1": 32768, "c0": 1024, "c2": 8192, "c4": 131072}[cfg]
 
 
 def cluster_for(n: int) -> dict:
@@ -329,7 +337,8 @@ def main():
         "mfu_ref": per_gpu * fpt_ref / peak, "mfu_ref_datasheet": per_gpu * fpt_ref / 2.25e15,
         "mfu_exact": exact / t_mean / n / peak, "model_flops_per_token_ref": fpt_ref,
         "config": {"workload": cfg, "model": {"c1": "qwen2-7b-shaped (random init)",
-                                              "c2": f"qwen3-30b-a3b-shaped, {arch['layers']} layers (random init)"}.get(cfg, cfg),
+                                              "c2": f"qwen3-30b-a3b-shaped, {arch['layers']} layers (random init)",
+                                              "c4": "qwen2-72b-shaped 8-layer slice (random init)"}.get(cfg, cfg),
                    "global_batch": rows, "seq_len": S, "tokens_per_step": tokens_step,
                    "parallelism": f"fsdp{plan['dp_shard']}xsp{plan['sp']}",
                    "recompute": plan["recompute"], "packing": "lognormal varlen, 0 padding",
