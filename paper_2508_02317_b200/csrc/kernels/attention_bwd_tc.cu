@@ -61,6 +61,8 @@ struct Params {
   float scale, scale_log2;
   int skip_dq;  // debug: measure without the dQ reduction
   int splits;   // q-head splits per kv head
+  float* dq_acc;  // [N, hq, 128] fp32 (direct reductions when dq_red)
+  int dq_red;     // 1: dQ by red.global.add from registers, 0: TMA bulk reduce via smem
   int f32kv;    // dK/dV go to fp32 [N, hk, 128] through tdk/tdv (reduce-add if splits > 1)
 };
 
@@ -246,6 +248,19 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&dqt_free[j & 1]);
+      if (p.dq_red) {
+        // lanes hold consecutive d: every red below is one coalesced 128-B
+        // reduction; no staging, no block barriers on the critical path
+        float* dst = p.dq_acc + (int64_t(q0 + c0) * p.hq + h) * D + r;
+        const int64_t qstride = int64_t(p.hq) * D;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q0 + c0 + q < p.N)
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + q * qstride),
+                         "f"(__uint_as_float(qv[q]) * p.scale)
+                         : "memory");
+        return;
+      }
       if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       bar_sync_softmax();  // staging buffer free
 #pragma unroll
@@ -289,8 +304,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (full_vis) {
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const float p0 = exp2f(fmaf(__uint_as_float(sv[i]), p.scale_log2, -lv[i]));
-          const float p1 = exp2f(fmaf(__uint_as_float(sv[i + 1]), p.scale_log2, -lv[i + 1]));
+          // 1 in 4 exponentials on the FMA pipe (SFU and tensor pipe are co-critical)
+          const float x0 = fmaf(__uint_as_float(sv[i]), p.scale_log2, -lv[i]);
+          const float p0 = (i & 7) == 6 ? exp2_fma(x0) : ex2(x0);
+          const float p1 = ex2(fmaf(__uint_as_float(sv[i + 1]), p.scale_log2, -lv[i + 1]));
           pw[i / 2] = ptx::pack_bf16(p0, p1);
           dw[i / 2] = ptx::pack_bf16(p0 * (__uint_as_float(dv[i]) - dl[i]),
                                      p1 * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
@@ -303,7 +320,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int e = 0; e < 2; ++e) {
             const int q = q0 + c0 + i + e;
             const bool ok = (key <= q) & (key >= sst[c0 + i + e]) & (key < p.N);
-            const float x = exp2f(fmaf(__uint_as_float(sv[i + e]), p.scale_log2, -lv[i + e]));
+            const float x = ex2(fmaf(__uint_as_float(sv[i + e]), p.scale_log2, -lv[i + e]));
             pp[e] = ok ? x : 0.f;
           }
           pw[i / 2] = ptx::pack_bf16(pp[0], pp[1]);
@@ -503,6 +520,8 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
   p.scale_log2 = a.scale * LOG2E;
   p.skip_dq = getenv("OPX_DEBUG_SKIP_DQ") != nullptr;
   p.splits = splits;
+  p.dq_acc = a.dq_acc;
+  p.dq_red = getenv("OPX_ATTN_DQ_RED") ? atoi(getenv("OPX_ATTN_DQ_RED")) : 0;
   p.f32kv = f32kv;
   dim3 grid((a.N + BK - 1) / BK, a.hk * splits);
   ++g_kernel_launches;

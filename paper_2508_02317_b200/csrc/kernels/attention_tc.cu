@@ -45,14 +45,6 @@ struct FwdParams {
   float scale_log2;
 };
 
-// 2^x on the FMA/ALU pipes: 2^floor(x) * p(frac), p degree 3 (rel. err 8.6e-5)
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -126.f);
-  const float fi = floorf(x);
-  const float f = x - fi;
-  const float p = fmaf(fmaf(fmaf(0.07705827f, f, 0.2276545f), f, 0.69511473f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (int(fi) << 23));
-}
 
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -235,8 +227,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < 128; i += 2) {
-        const float a0 = (i & 7) == 6 ? exp2_fma(s[i] - base) : exp2f(s[i] - base);
-        const float a1 = exp2f(s[i + 1] - base);
+        const float a0 = (i & 7) == 6 ? exp2_fma(s[i] - base) : ex2(s[i] - base);
+        const float a1 = ex2(s[i + 1] - base);
         sum += a0 + a1;
         s[i / 2] = __uint_as_float(ptx::pack_bf16(a0, a1));
       }

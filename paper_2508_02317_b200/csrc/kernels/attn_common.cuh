@@ -20,6 +20,22 @@ static __device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) {
   // MN-major SW128 operand: K rows of 128 B, the two 64-element MN chunks 16 KB apart
   return ptx::umma_desc_sw128(base + k * 2048, 16384, 1024);
 }
+// 2^x on the SFU, flush-to-zero (exp2f adds a denormal-range fixup per call)
+static __device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x on the FMA/ALU pipes: 2^floor(x) * p(frac), p degree 3 (rel. err 8.6e-5);
+// used for a fraction of the softmax exponentials to unload the SFU
+static __device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float fi = floorf(x);
+  const float f = x - fi;
+  const float p = fmaf(fmaf(fmaf(0.07705827f, f, 0.2276545f), f, 0.69511473f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (int(fi) << 23));
+}
+
 // byte offset of 16-B chunk c (0..15) of row r in a [128][128] bf16 SW128 tile
 static __device__ __forceinline__ uint32_t sw_off(int r, int c) {
   return (c >> 3) * 16384 + r * 128 + (((c & 7) ^ (r & 7)) << 4);
