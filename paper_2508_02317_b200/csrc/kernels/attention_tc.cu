@@ -35,6 +35,13 @@ constexpr int FWD_THREADS = 320;
 constexpr int FWD_SMEM = 1024 + TILE_BYTES * 7 + 256;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESH = 8.0f;
+// 1/POLY_SHARE of the exponentials go to the FMA-pipe polynomial (0: none).
+// Measured on B200 (C1 shapes): 1/4 -> 844 TF/s, 1/2 -> 675 TF/s: the softmax
+// warps are issue-bound, not MUFU-bound, so only a small share is moved.
+#ifndef OPX_FWD_POLY_SHARE
+#define OPX_FWD_POLY_SHARE 4
+#endif
+constexpr int POLY_SHARE = OPX_FWD_POLY_SHARE;
 
 struct FwdParams {
   bf16* o;
@@ -203,35 +210,39 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       ptx::mbar_arrive(&s_empty[t]);
       const int kbase = kv0 + j * BN;
       const bool full_vis = kbase >= sst && kbase + BN - 1 <= row;
-      float mx = -INFINITY;
-      if (full_vis) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          s[i] *= p.scale_log2;
-          mx = fmaxf(mx, s[i]);
-        }
-      } else {
+      // row max of the raw scores (scale > 0), 3-input max
+      float mr = -INFINITY;
+      if (!full_vis) {
 #pragma unroll
         for (int i = 0; i < 128; ++i) {
           const int key = kbase + i;
-          s[i] = (key >= sst && key <= row) ? s[i] * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s[i]);
+          s[i] = (key >= sst && key <= row) ? s[i] : -INFINITY;
         }
       }
+#pragma unroll
+      for (int i = 0; i < 128; i += 2) mr = fmax3(mr, s[i], s[i + 1]);
+      const float mx = mr * p.scale_log2;
       const bool need = mx > m_used + RESCALE_THRESH || (m_used == -INFINITY && mx > -INFINITY);
       const float m_new = need ? mx : m_used;
       const float alpha = (need && m_used != -INFINITY) ? exp2f(m_used - m_new) : 1.f;
       const float base = m_new == -INFINITY ? 0.f : m_new;
-      // exponentials before waiting for the previous PV (overlap with the MMA)
-      // packed bf16 P is written in place over s[0..63] (slot i/2 <= i)
-      float sum = 0.f;
+      // exponentials before waiting for the previous PV (overlap with the MMA);
+      // x = s*scale - base and the row sum as packed fp32x2 ops.  Packed bf16 P
+      // is written in place over s[0..63] (slot i/2 <= i)
+      const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2), nb2 = f2pack(-base, -base);
+      uint64_t sum2 = f2pack(0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < 128; i += 2) {
-        const float a0 = (i & 7) == 6 ? exp2_fma(s[i] - base) : ex2(s[i] - base);
-        const float a1 = ex2(s[i + 1] - base);
-        sum += a0 + a1;
+        float x0, x1;
+        f2unpack(ffma2(f2pack(s[i], s[i + 1]), sc2, nb2), x0, x1);
+        const float a0 = (POLY_SHARE == 2 || (POLY_SHARE == 4 && (i & 7) == 6)) ? exp2_fma(x0) : ex2(x0);
+        const float a1 = ex2(x1);
+        sum2 = fadd2(sum2, f2pack(a0, a1));
         s[i / 2] = __uint_as_float(ptx::pack_bf16(a0, a1));
       }
+      float sum_lo, sum_hi;
+      f2unpack(sum2, sum_lo, sum_hi);
+      const float sum = sum_lo + sum_hi;
       if (j > 0) ptx::mbar_wait(&o_done[t], (j - 1) & 1);  // PV(j-1) done: O stable, P free
       ptx::tc_fence_after();
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {

@@ -20,6 +20,37 @@ static __device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) {
   // MN-major SW128 operand: K rows of 128 B, the two 64-element MN chunks 16 KB apart
   return ptx::umma_desc_sw128(base + k * 2048, 16384, 1024);
 }
+// Packed fp32x2 ops (FFMA2 / FADD2 / FMUL2 on sm_100) and the 3-input max
+// (FMNMX3): the softmax warps are issue-bound, these halve their FP work.
+static __device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t u;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(u) : "f"(a), "f"(b));
+  return u;
+}
+static __device__ __forceinline__ void f2unpack(uint64_t u, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(u));
+}
+static __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+static __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+static __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+static __device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 // 2^x on the SFU, flush-to-zero (exp2f adds a denormal-range fixup per call)
 static __device__ __forceinline__ float ex2(float x) {
   float y;
