@@ -26,6 +26,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "../runtime/gemm_api.h"
@@ -45,7 +46,7 @@ constexpr float LOG2E = 1.4426950408889634f;
 // smem map (bytes, 1024-aligned base)
 constexpr int OFF_K = 0, OFF_V = 32768, OFF_Q = 65536 /*[2] x 16K*/, OFF_O = 98304 /*[2] x 16K*/,
               OFF_P = 131072, OFF_S = 147456, OFF_STAGE = 163840 /*32K fp32*/,
-              OFF_MISC = 196608;
+              OFF_P2 = 196608, OFF_S2 = 212992 /* P/dS double buffer */, OFF_MISC = 229376;
 constexpr int SMEM = 1024 + OFF_MISC + 3 * 2 * BQ * 4 + 256;
 static_assert(3 * 2 * BQ * 4 + 13 * 8 + 8 <= 3 * 2 * BQ * 4 + 256, "misc region");
 
@@ -60,9 +61,9 @@ struct Params {
   int N, hq, hk;
   float scale, scale_log2;
   int skip_dq;  // debug: measure without the dQ reduction
+  long long* prof;  // debug (OPX_ATTN_PROF=<cta>): clock64 stamps [64 iters][16] of one CTA
+  int prof_cta;
   int splits;   // q-head splits per kv head
-  float* dq_acc;  // [N, hq, 128] fp32 (direct reductions when dq_red)
-  int dq_red;     // 1: dQ by red.global.add from registers, 0: TMA bulk reduce via smem
   int f32kv;    // dK/dV go to fp32 [N, hk, 128] through tdk/tdv (reduce-add if splits > 1)
 };
 
@@ -72,6 +73,22 @@ __device__ __forceinline__ uint64_t kd(uint32_t base, int k, int blk) {
 __device__ __forceinline__ uint64_t md(uint32_t base, int k, int lbo) {
   return ptx::umma_desc_sw128(base + k * 2048, lbo, 1024);
 }
+// Phase stamps for tools/prof_attn_phases.py: build with -DOPX_ATTN_PROF_BUILD=1
+// and run with OPX_ATTN_PROF=<cta>; compiled out otherwise.
+#ifndef OPX_ATTN_PROF_BUILD
+#define OPX_ATTN_PROF_BUILD 0
+#endif
+#if OPX_ATTN_PROF_BUILD
+#define PROF(it, k)                                                                        \
+  do {                                                                                     \
+    if (p.prof && int(blockIdx.x + gridDim.x * blockIdx.y) == p.prof_cta && (it) < 64)     \
+      p.prof[(it) * 16 + (k)] = clock64();                                                 \
+  } while (0)
+#else
+#define PROF(it, k) \
+  do {              \
+  } while (0)
+#endif
 __device__ __forceinline__ void bar_sync_softmax() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -165,7 +182,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t id_kv = ptx::idesc_bf16_f32(128, D, false, true);    // dV, dK
     constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, BQ, true, true);     // dQ^T
     const uint32_t ak = ptx::smem_u32(smem + OFF_K), av = ptx::smem_u32(smem + OFF_V),
-                   ap = ptx::smem_u32(smem + OFF_P), as = ptx::smem_u32(smem + OFF_S);
+                   ap0 = ptx::smem_u32(smem + OFF_P), as0 = ptx::smem_u32(smem + OFF_S),
+                   ap1 = ptx::smem_u32(smem + OFF_P2), as1 = ptx::smem_u32(smem + OFF_S2);
     ptx::mbar_wait_sleep(kv_full, 0);
     // issue order: S/dP(i+1) right after P(i) is ready, then dV/dK/dQ(i), so
     // the softmax of tile i+1 overlaps the gradient MMAs of tile i.
@@ -193,11 +211,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
       if (it + 1 < niter) {
         ptx::mbar_wait_sleep(s_free, it & 1);  // S^T/dP^T(it) are in the softmax registers
+        if (lane == 0) PROF(it, 0);
         issue_sdp(it + 1);
       }
       ptx::mbar_wait_sleep(p_ready, it & 1);   // P/dS(it) in smem
+      if (lane == 0) PROF(it, 1);
       if (it >= 2) ptx::mbar_wait_sleep(&dqt_free[st], ((it >> 1) - 1) & 1);  // dQ^T(it-2) read out
+      if (lane == 0) PROF(it, 2);
       ptx::tc_fence_after();
+      const uint32_t ap = st ? ap1 : ap0, as = st ? as1 : as0;  // P/dS(it) buffer
       if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k)
@@ -223,9 +245,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int c0 = half * 32;        // first of this thread's 32 q columns
     const int key = k0 + r;
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
-    uint8_t* sP = smem + OFF_P;
-    uint8_t* sS = smem + OFF_S;
     const bool issuer = threadIdx.x == 64;
+    const bool pt = issuer;  // debug stamps
     auto load_cols = [&](int it) {  // lse/delta/seq_start of tile it -> smem buffer it&1
       if (half == 0 && r < BQ) {
         const int h = hbase + it / nq;
@@ -242,25 +263,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int h = hbase + j / nq;
       const int q0 = k0 + (j % nq) * BQ;
       ptx::mbar_wait_sleep(&dq_full[j & 1], (j >> 1) & 1);
+      if (pt) PROF(j + 1, 8);
       ptx::tc_fence_after();
       uint32_t qv[32];
       ptx::tmem_ld32(TDQ + 64 * (j & 1) + lane_off + c0, qv);
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&dqt_free[j & 1]);
-      if (p.dq_red) {
-        // lanes hold consecutive d: every red below is one coalesced 128-B
-        // reduction; no staging, no block barriers on the critical path
-        float* dst = p.dq_acc + (int64_t(q0 + c0) * p.hq + h) * D + r;
-        const int64_t qstride = int64_t(p.hq) * D;
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q0 + c0 + q < p.N)
-            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + q * qstride),
-                         "f"(__uint_as_float(qv[q]) * p.scale)
-                         : "memory");
-        return;
-      }
       if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       bar_sync_softmax();  // staging buffer free
 #pragma unroll
@@ -279,6 +288,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (niter > 0) load_cols(0);
     bar_sync_softmax();
     for (int it = 0; it < niter; ++it) {
+      if (pt) PROF(it, 4);
       const int q0 = k0 + (it % nq) * BQ;
       const int buf = it & 1;
       // broadcast vector loads of this thread's 32 columns
@@ -293,6 +303,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int* sst = s_sst + buf * BQ;
       const bool full_vis = key <= q0 + c0 && q0 + c0 + 31 < p.N && sst[c0 + 31] <= key;
       ptx::mbar_wait_sleep(s_full, it & 1);
+      if (pt) PROF(it, 5);
       ptx::tc_fence_after();
       uint32_t sv[32], dv[32];
       ptx::tmem_ld32(TST + lane_off + c0, sv);
@@ -302,15 +313,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::mbar_arrive(s_free);  // the MMA warp may overwrite S^T/dP^T now
       uint32_t pw[16], dw[16];
       if (full_vis) {
+        // packed fp32x2: x = s*scale - lse, dS = P (dP - delta); 1 in 4
+        // exponentials on the FMA pipe
+        const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2);
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          // 1 in 4 exponentials on the FMA pipe (SFU and tensor pipe are co-critical)
-          const float x0 = fmaf(__uint_as_float(sv[i]), p.scale_log2, -lv[i]);
+          float x0, x1;
+          f2unpack(ffma2(f2pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sc2,
+                         f2pack(-lv[i], -lv[i + 1])),
+                   x0, x1);
           const float p0 = (i & 7) == 6 ? exp2_fma(x0) : ex2(x0);
-          const float p1 = ex2(fmaf(__uint_as_float(sv[i + 1]), p.scale_log2, -lv[i + 1]));
+          const float p1 = ex2(x1);
+          const uint64_t pp = f2pack(p0, p1);
+          const uint64_t dd = fadd2(f2pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
+                                    f2pack(-dl[i], -dl[i + 1]));
+          float d0, d1;
+          f2unpack(fmul2(pp, dd), d0, d1);
           pw[i / 2] = ptx::pack_bf16(p0, p1);
-          dw[i / 2] = ptx::pack_bf16(p0 * (__uint_as_float(dv[i]) - dl[i]),
-                                     p1 * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
+          dw[i / 2] = ptx::pack_bf16(d0, d1);
         }
       } else {
 #pragma unroll
@@ -328,9 +348,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      pp[1] * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
         }
       }
-      // the gradient MMAs of tile it-1 read sP/sS: wait for them, drain their
-      // dQ^T, then publish P/dS(it)
-      if (it > 0) drain_dq(it - 1);
+      // publish P/dS(it) into buffer it&1: the gradient MMAs of tile it-2, the
+      // last readers of that buffer, completed before dQ^T(it-2) was drained
+      // (previous iteration); then drain dQ^T(it-1) off the MMA critical path
+      if (pt) PROF(it, 6);
+      uint8_t* sP = smem + ((it & 1) ? OFF_P2 : OFF_P);
+      uint8_t* sS = smem + ((it & 1) ? OFF_S2 : OFF_S);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         const int chunk = half * 4 + cc;
@@ -342,8 +365,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::fence_proxy_async();
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_ready);
+      if (pt) PROF(it, 7);
+      if (it > 0) drain_dq(it - 1);
+      if (pt) PROF(it, 9);
       if (it + 1 < niter) load_cols(it + 1);
       bar_sync_softmax();  // next tile's column data visible
+      if (pt) PROF(it, 10);
     }
     if (niter > 0) drain_dq(niter - 1);
     if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -519,13 +546,45 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
   p.scale = a.scale;
   p.scale_log2 = a.scale * LOG2E;
   p.skip_dq = getenv("OPX_DEBUG_SKIP_DQ") != nullptr;
+  static long long* prof = nullptr;
+  p.prof = nullptr;
+  p.prof_cta = getenv("OPX_ATTN_PROF") ? atoi(getenv("OPX_ATTN_PROF")) : -1;
+  if (p.prof_cta >= 0) {
+    if (!prof) cudaMalloc(&prof, 64 * 16 * sizeof(long long));
+    cudaMemsetAsync(prof, 0, 64 * 16 * sizeof(long long), s);
+    p.prof = prof;
+  }
   p.splits = splits;
-  p.dq_acc = a.dq_acc;
-  p.dq_red = getenv("OPX_ATTN_DQ_RED") ? atoi(getenv("OPX_ATTN_DQ_RED")) : 0;
   p.f32kv = f32kv;
   dim3 grid((a.N + BK - 1) / BK, a.hk * splits);
   ++g_kernel_launches;
   attn_bwd_tc_kernel<<<grid, THREADS, SMEM, s>>>(mq, mk, mv, mdo, mdq, mdk, mdv, p);
+  if (p.prof) {  // debug: per-iteration phase durations (cycles) of one CTA
+    long long h[64 * 16];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, p.prof, sizeof h, cudaMemcpyDeviceToHost);
+    double acc[16] = {};
+    int n = 0;
+    for (int it = 4; it < 60 && h[(it + 1) * 16 + 4]; ++it, ++n) {
+      const long long* a = h + it * 16;
+      const long long* b = h + (it + 1) * 16;
+      acc[0] += double(b[4] - a[4]);   // iteration
+      acc[1] += double(a[5] - a[4]);   // wait S
+      acc[2] += double(a[6] - a[5]);   // ld + compute
+      acc[3] += double(a[7] - a[6]);   // STS P/dS + arrive
+      acc[4] += double(b[8] - a[7]);   // wait dQ(it)... (stamp 8 of it+1 = wait dq(it) done)
+      acc[5] += double(a[9] - b[8] > 0 ? a[9] - a[7] : 0);
+      acc[6] += double(a[10] - a[9]);  // load_cols + bar
+      acc[7] += double(a[1] - a[0]);   // MMA: s_free -> p_ready
+      acc[8] += double(a[2] - a[1]);   // MMA: wait dqt_free
+    }
+    if (n)
+      fprintf(stderr,
+              "[attn_bwd prof cta %d, %d iters] iter %.0f | wait_S %.0f ld+math %.0f publish %.0f "
+              "drain(wait dq %.0f, total %.0f) cols+bar %.0f | mma: s_free->p_ready %.0f wait_dqt %.0f\n",
+              p.prof_cta, n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n,
+              acc[6] / n, acc[7] / n, acc[8] / n);
+  }
   return cudaGetLastError();
 }
 
