@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = it & 1;
         const int h = hbase + it / nq;
         const int q0 = k0 + (it % nq) * BQ;
-        if (it >= 2) ptx::mbar_wait_sleep(&qdo_empty[st], ((it >> 1) - 1) & 1);
+        if (it >= 2) ptx::mbar_wait(&qdo_empty[st], ((it >> 1) - 1) & 1);
         ptx::mbar_expect_tx(&qdo_full[st], 4 * 8192);
         uint8_t* q = smem + OFF_Q + st * 16384;
         uint8_t* o = smem + OFF_O + st * 16384;
@@ -184,14 +184,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t ak = ptx::smem_u32(smem + OFF_K), av = ptx::smem_u32(smem + OFF_V),
                    ap0 = ptx::smem_u32(smem + OFF_P), as0 = ptx::smem_u32(smem + OFF_S),
                    ap1 = ptx::smem_u32(smem + OFF_P2), as1 = ptx::smem_u32(smem + OFF_S2);
-    ptx::mbar_wait_sleep(kv_full, 0);
+    ptx::mbar_wait(kv_full, 0);
     // issue order: S/dP(i+1) right after P(i) is ready, then dV/dK/dQ(i), so
     // the softmax of tile i+1 overlaps the gradient MMAs of tile i.
     auto issue_sdp = [&](int it) {
       const int st = it & 1;
       const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
       const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
-      ptx::mbar_wait_sleep(&qdo_full[st], (it >> 1) & 1);
+      ptx::mbar_wait(&qdo_full[st], (it >> 1) & 1);
       ptx::tc_fence_after();
       if (lane == 0) {
 #pragma unroll
@@ -210,13 +210,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
       const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
       if (it + 1 < niter) {
-        ptx::mbar_wait_sleep(s_free, it & 1);  // S^T/dP^T(it) are in the softmax registers
+        ptx::mbar_wait(s_free, it & 1);  // S^T/dP^T(it) are in the softmax registers
         if (lane == 0) PROF(it, 0);
         issue_sdp(it + 1);
       }
-      ptx::mbar_wait_sleep(p_ready, it & 1);   // P/dS(it) in smem
+      ptx::mbar_wait(p_ready, it & 1);   // P/dS(it) in smem
       if (lane == 0) PROF(it, 1);
-      if (it >= 2) ptx::mbar_wait_sleep(&dqt_free[st], ((it >> 1) - 1) & 1);  // dQ^T(it-2) read out
+      if (it >= 2) ptx::mbar_wait(&dqt_free[st], ((it >> 1) - 1) & 1);  // dQ^T(it-2) read out
       if (lane == 0) PROF(it, 2);
       ptx::tc_fence_after();
       const uint32_t ap = st ? ap1 : ap0, as = st ? as1 : as0;  // P/dS(it) buffer
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto drain_dq = [&](int j) {
       const int h = hbase + j / nq;
       const int q0 = k0 + (j % nq) * BQ;
-      ptx::mbar_wait_sleep(&dq_full[j & 1], (j >> 1) & 1);
+      ptx::mbar_wait(&dq_full[j & 1], (j >> 1) & 1);
       if (pt) PROF(j + 1, 8);
       ptx::tc_fence_after();
       uint32_t qv[32];
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       const int* sst = s_sst + buf * BQ;
       const bool full_vis = key <= q0 + c0 && q0 + c0 + 31 < p.N && sst[c0 + 31] <= key;
-      ptx::mbar_wait_sleep(s_full, it & 1);
+      ptx::mbar_wait(s_full, it & 1);
       if (pt) PROF(it, 5);
       ptx::tc_fence_after();
       uint32_t sv[32], dv[32];
