@@ -278,6 +278,7 @@ def main():
     if dist:
         dist.barrier()
     times, walls, launches, losses, enq = [], [], 0, [], []
+    kept = 0
     with Clocks(local) as clk:
         for _ in range(args.steps):
             t0 = time.perf_counter()
@@ -287,6 +288,7 @@ def main():
             times.append(r.step_time_s)
             launches += r.launches
             enq.append(r.enqueue_s)
+            kept = int(r.kept_layers)
             losses.append(r.loss)
     trace = sess.trace()
     if dist:
@@ -341,7 +343,8 @@ def main():
                                               "c4": "qwen2-72b-shaped 8-layer slice (random init)"}.get(cfg, cfg),
                    "global_batch": rows, "seq_len": S, "tokens_per_step": tokens_step,
                    "parallelism": f"fsdp{plan['dp_shard']}xsp{plan['sp']}",
-                   "recompute": plan["recompute"], "packing": "lognormal varlen, 0 padding",
+                   "recompute": plan["recompute"], "kept_layers": kept,
+                   "packing": "lognormal varlen, 0 padding",
                    "l2": "inputs+weights >> 126 MB L2 (no flush needed)",
                    "peak_kind": peak_kind},
         "loss": losses[-1],

@@ -72,6 +72,7 @@ typedef struct {
   double n_valid;       /* global count of supervised tokens */
   int64_t launches;     /* opx kernels launched during the step */
   double enqueue_s;     /* host wall time spent enqueueing the step (launch-bound if ~step_time_s) */
+  int64_t kept_layers;  /* layers whose activations stay resident (no full recompute) */
 } opx_step_report;
 
 /* 128-byte NCCL unique id for the world communicator (rank 0 creates it). */

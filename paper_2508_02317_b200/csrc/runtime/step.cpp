@@ -324,7 +324,33 @@ int Step::alloc_acts() {
   off_flags_ = take(64 * sizeof(uint32_t));
   const int L = int(a_.layers);
   save_acts_ = !p_.recompute_full;
-  const int xslots = save_acts_ ? 2 + L : 2;
+  keep_mode_.assign(size_t(L), save_acts_ ? 2 : 0);
+  if (!save_acts_ && ex_.selective_recompute && !moe_) {
+    // bytes one attention-kept layer adds: its q/k/v/o exchange slot + h, the
+    // sp>1 head-layout output, lse, x2, h2 and the norm statistics
+    const size_t per_layer =
+        round_up(int64_t(N * size_t(hql_) * 256), 256) + 2 * round_up(int64_t(N * size_t(hkl_) * 256), 256) +
+        round_up(int64_t(T * size_t(hq_) * 256), 256) + T * H * 2 + (p_.sp > 1 ? N * size_t(hql_) * 256 : 0) +
+        N * size_t(hql_) * 4 + T * H * 4 + T * 8 + T * H * 2;
+    // everything else this function and the step still allocate
+    const size_t F = size_t(F_), V = size_t(V_);
+    const size_t chunk = size_t(std::min<int64_t>(ex_.ce_chunk, T_));
+    const size_t fixed =
+        2 * (N * size_t(hql_) * 256 + 2 * N * size_t(hkl_) * 256 + T * size_t(hq_) * 256) +  // 2 slots
+        2 * (N * size_t(hql_) * 256 + T * size_t(Wqkv_) * 2) +                               // dO, dqkv
+        size_t(L + 1) * T * H * 4 +                                                           // x_saved
+        per_layer + T * 2 * F * 2 + T * F * 2 +                                               // scratch acts
+        T * size_t(Wqkv_) * 2 + 2 * T * H * 4 + T * H * 2 + T * F * 2 + T * 2 * F * 2 +    // qkv, dx, dtmp, dxb, dact, dgu
+        N * size_t(hql_) * 128 * 4 + 2 * N * size_t(hkl_) * 128 * 4 + N * size_t(hql_) * 4 +  // dq, dk, dv, delta
+        size_t(k_rmsnorm_bwd_parts(T_)) * H * 4 + T * H * 2 + T * H * 4 + chunk * V * 2;    // dw_part, hf, dhf, logits
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    const size_t margin = size_t(6) << 30;  // NCCL, CUDA context growth, allocator slack
+    int K = 0;
+    if (free_b > fixed + margin) K = int(std::min<size_t>(size_t(L), (free_b - fixed - margin) / per_layer));
+    for (int l = L - K; l < L; ++l) keep_mode_[size_t(l)] = 1;  // the backward starts at the top
+  }
+  const int xslots = 2 + L;
   for (int b = 0; b < xslots; ++b) {
     if (b >= 2 && !keeps_acts(b - 2)) {
       off_q_.push_back(0);
@@ -376,7 +402,7 @@ int Step::alloc_acts() {
   if (!make_acts(scratch_, any_dense)) return cuda_fail(cudaErrorMemoryAllocation, "activations");
   saved_.assign(size_t(L), Acts{});
   for (int l = 0; l < L; ++l)
-    if (keeps_acts(l) && !make_acts(saved_[size_t(l)], !a_.is_moe_layer(l))) {
+    if (keeps_acts(l) && !make_acts(saved_[size_t(l)], keeps_mlp(l) && !a_.is_moe_layer(l))) {
       set_error("out of device memory for recompute=none activations (layer " +
                 std::to_string(l) + "); use recompute=full");
       return OPX_ERR_CUDA;
@@ -733,9 +759,16 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
   if (tr) cudaEventRecord(e0, cs_);
   // full recompute of the layer (recompute=full); x_out goes to scratch
   int qb, ob;
-  if (keeps_acts(l)) {  // recompute=none: this layer's forward activations are resident
-    bind(saved_[size_t(l)]);
+  if (keeps_acts(l)) {  // this layer's forward activations are resident
+    bind_layer(l);
     qb = ob = 2 + l;
+    if (!keeps_mlp(l) && !a_.is_moe_layer(l)) {
+      // attention-kept layer: recompute only gate|up (+ SwiGLU) from the saved h2
+      GemmDesc g = gd(T, 2 * F, H, h2_, H, false, W.gu, H, false, GEMM_EPI_SWIGLU, gu_, 2 * F);
+      g.D2 = act_;
+      g.ldd2 = F;
+      CU(gemm_run(g, cs_));
+    }
   } else {
     bind(scratch_);
     qb = ob = next_rslot();
@@ -991,9 +1024,9 @@ int Step::run(opx_step_report* rep) {
     if (l + nslots_ - 1 < L) TRY(issue_gather(l + nslots_ - 1, false));
     int slot;
     if (keeps_acts(l)) {
-      bind(saved_[size_t(l)]);
+      bind_layer(l);
       slot = 2 + l;
-      store_gu_ = true;
+      store_gu_ = keeps_mlp(l);
     } else {
       bind(scratch_);
       slot = next_rslot();
@@ -1156,6 +1189,8 @@ int Step::run(opx_step_report* rep) {
     rep->n_valid = double(n_valid_);
     rep->launches = g_kernel_launches - launches0 - 1;  // minus the loss reduction
     rep->enqueue_s = enqueue_s;
+    rep->kept_layers = 0;
+    for (int m : keep_mode_) rep->kept_layers += m >= 1;
   }
   return OPX_OK;
 }
@@ -1320,6 +1355,7 @@ int opx_step_create(const char* cj, const char* mj, const char* wj, const char* 
     ex.rms_eps = e.value("rms_eps", ex.rms_eps);
     ex.ce_chunk = e.value("ce_chunk", ex.ce_chunk);
     ex.trace = e.value("trace", false);
+    ex.selective_recompute = e.value("selective_recompute", true);
   } catch (const std::exception& e) {
     set_error(e.what());
     return OPX_ERR_CONFIG;

@@ -25,6 +25,9 @@ struct ExecCfg {
   float rms_eps = 1e-6f;
   int64_t ce_chunk = 8192;
   bool trace = false;
+  // recompute=full: keep the attention activations of as many dense layers as
+  // free HBM allows (their backward recomputes only gate|up)
+  bool selective_recompute = true;
 };
 
 // One parameter inside an FSDP flat unit.  `phys_name` is the name exposed by
@@ -158,7 +161,18 @@ class Step {
   // recompute=none keeps every layer's forward activations; MoE layers keep
   // the attention activations, their routing and the combined expert outputs
   // and only re-run dispatch + gate|up in the backward (moe_bwd).
-  bool keeps_acts(int l) const { return save_acts_; }
+  // per-layer: 0 = recompute the whole layer, 1 = attention activations kept
+  // (the backward recomputes only the gate|up GEMM), 2 = everything kept
+  std::vector<int> keep_mode_;
+  bool keeps_acts(int l) const { return keep_mode_[size_t(l)] >= 1; }
+  bool keeps_mlp(int l) const { return keep_mode_[size_t(l)] == 2; }
+  void bind_layer(int l) {  // saved activations of layer l (scratch MLP buffers for mode 1)
+    bind(saved_[size_t(l)]);
+    if (!keeps_mlp(l)) {
+      gu_ = scratch_.gu;
+      act_ = scratch_.act;
+    }
+  }
   void bind(const Acts& a) {
     h_ = a.h;
     h2_ = a.h2;

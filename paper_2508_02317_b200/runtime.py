@@ -23,7 +23,8 @@ class StepReport(ctypes.Structure):
                 ("bwd_s", ctypes.c_double), ("opt_s", ctypes.c_double),
                 ("comm_wait_s", ctypes.c_double), ("loss", ctypes.c_double),
                 ("tokens", ctypes.c_double), ("n_valid", ctypes.c_double),
-                ("launches", ctypes.c_int64), ("enqueue_s", ctypes.c_double)]
+                ("launches", ctypes.c_int64), ("enqueue_s", ctypes.c_double),
+                ("kept_layers", ctypes.c_int64)]
 
 
 def _s(x) -> bytes:

@@ -8,7 +8,7 @@ from tests.step_common import EXEC, cluster, compare_step, tiny_dense
 gpu = pytest.mark.gpu
 
 
-def _run(model, S, rows, single=False, trace=False, recompute="full"):
+def _run(model, S, rows, single=False, trace=False, recompute="full", selective=True):
     from paper_2508_02317_b200.runtime import Session, synthetic_batch
 
     arch = model["modules"][0]["arch"]
@@ -16,6 +16,7 @@ def _run(model, S, rows, single=False, trace=False, recompute="full"):
     plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": rows, "recompute": recompute}
     ex = dict(EXEC)
     ex["trace"] = trace
+    ex["selective_recompute"] = selective
     s = Session(cluster(1), model, wl, plan, ex, rank=0, device=0)
     s.init_weights(EXEC["seed"])
     batch = synthetic_batch(arch["vocab"], S, rows, seed=2508, single_sample=single)
@@ -29,8 +30,19 @@ def _run(model, S, rows, single=False, trace=False, recompute="full"):
 def test_step_tiny_dense_matches_oracle(single):
     model = tiny_dense()
     s, batch, plan, r = _run(model, 1024, 2, single)
+    assert r.kept_layers == model["modules"][0]["arch"]["layers"]  # attention-kept (selective)
     rep = compare_step([s], model, batch, plan, r.loss)
     assert r.launches > 0
+    s.close()
+
+
+@gpu
+def test_step_pure_full_recompute_matches_oracle():
+    """recompute=full with selective keeping off: every layer recomputed."""
+    model = tiny_dense()
+    s, batch, plan, r = _run(model, 1024, 2, selective=False)
+    assert r.kept_layers == 0
+    compare_step([s], model, batch, plan, r.loss)
     s.close()
 
 
