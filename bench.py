@@ -83,6 +83,20 @@ def cluster_for(n: int) -> dict:
                      "inter_latency": 2e-5}}
 
 
+def mlp_traffic(cfg: str, T_loc: int):
+    """DRAM bytes of one forward MLP node (gate|up + down GEMM) from the committed
+    ncu capture at 32768 tokens, scaled linearly to this rank's tokens; None when
+    there is no capture for this config."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+    except Exception:
+        return None
+    if cfg != "c1":
+        return None
+    return t["mlp_node_dram_bytes"] * T_loc / t["tokens"]
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -355,7 +369,8 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "fwd MLP block (tcgen05 gate|up GEMM+SwiGLU, down GEMM)",
                      "achieved": achieved / 1e12, "peak": peak_sus / 1e12, "unit": "TFLOP/s",
                      "frac": achieved / peak_sus, "peak_kind": f"{peak_kind} sustained",
-                     "traffic": None,
+                     "traffic": mlp_traffic(cfg, T_loc),
+                     "traffic_unit": "bytes per node (ncu dram__bytes_read+write, profiles/ncu_traffic.json)",
                      "flops_per_launch": mlp_flops, "launch_ms": node_s * 1e3},
         "phase_share": {k: round(v / tot, 4) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:16]},
         "node_ms": {k: round(v * 1e3, 2) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:24]},
