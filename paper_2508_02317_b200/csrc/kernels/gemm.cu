@@ -547,7 +547,9 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
     // 2-CTA path: same traffic model with 256-row pair tiles and 74 pairs per wave
     const double a_bytes = double(g.M) * g.K * 2, b_blk = 256.0 * g.K * 2;
     const int mblk2 = (g.M + 255) / 256;
-    const double budget = 80e6, wave = num_sms() / 2;
+    // L2 budget for the resident B panel (OPX_GEMM_BUDGET_MB overrides, read per call)
+    const char* be = getenv("OPX_GEMM_BUDGET_MB");
+    const double budget = be ? atof(be) * 1e6 : 40e6, wave = num_sms() / 2;
     double best = 1e300;
     int band = 1;
     for (int nb = 1;; nb = nb * 2 > nblk ? nblk : nb * 2) {
