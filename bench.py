@@ -97,6 +97,21 @@ def mlp_traffic(cfg: str, T_loc: int):
     return t["mlp_node_dram_bytes"] * T_loc / t["tokens"]
 
 
+def calibration(trace, plan, model, wl, n, step_s):
+    """the reference simulator's constants (compute_efficiency,
+    intra-node bandwidth) fitted to this run's trace (paper_2508_02317_b200.calibrate)."""
+    try:
+        from paper_2508_02317_b200 import calibrate as cal
+
+        c = cal.calibrate(trace, plan, model, wl, cluster_for(n), step_s)
+        keep = ("compute_efficiency", "intra_node_bw", "unmodelled_s", "modelled_compute_s")
+        out = {k: c[k] for k in keep}
+        out["per_kind_efficiency"] = {k: round(v, 3) for k, v in c["per_kind_efficiency"].items()}
+        return out
+    except Exception as e:  # reporting only
+        return {"error": str(e)}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -375,6 +390,7 @@ def main():
         "phase_share": {k: round(v / tot, 4) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:16]},
         "node_ms": {k: round(v * 1e3, 2) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:24]},
         "clocks": clk.summary(),
+        "calibration": calibration(trace, plan, model, wl, n, t_mean),
         "host_enqueue_ms": statistics.mean(enq) * 1e3, "host_cpus": os.cpu_count(),
         "hbm_free_gb": torch.cuda.mem_get_info(local)[0] / 1e9,
     }

@@ -125,7 +125,9 @@ int ref_simulate(const char* cj, const char* mj, const char* wj, const char* pj,
     WorkloadSpec w = parse_workload(json::parse(wj));
     ParallelPlan p = plan_from(json::parse(pj), c.world_size());
     StepGraph g = build_step_graph(p, m, c, w);
-    Timeline tl = simulate(g, p, c);
+    SimOptions so;
+    so.compute_efficiency = json::parse(pj).value("compute_efficiency", so.compute_efficiency);
+    Timeline tl = simulate(g, p, c, so);
     StepReport rep = report(tl, g, p, m, c, w);
     json r{{"step_time_s", rep.step_time},
            {"throughput_tokens_per_s_per_gpu", rep.throughput},
@@ -138,8 +140,16 @@ int ref_simulate(const char* cj, const char* mj, const char* wj, const char* pj,
            {"reduce_scatter", g.collective_count(CollectiveKind::reduce_scatter)},
            {"all_reduce", g.collective_count(CollectiveKind::all_reduce)}};
     json names = json::array();
-    for (auto& n : g.nodes) names.push_back(n.name);
+    json nodes = json::array();
+    for (auto& n : g.nodes) {
+      names.push_back(n.name);
+      nodes.push_back({{"name", n.name},
+                       {"kind", n.kind == NodeKind::compute ? "compute" : "collective"},
+                       {"flops", n.flops},
+                       {"bytes", n.bytes}});
+    }
     r["node_names"] = names;
+    r["nodes"] = nodes;
     return out(r.dump(), buf, cap);
   } catch (const std::exception& e) {
     return out(std::string("{\"error\": ") + json(e.what()).dump() + "}", buf, cap) ? 9 : 2;
