@@ -44,9 +44,12 @@ constexpr int THREADS = 320;  // TMA, MMA, 8 softmax/dQ warps (2 per TMEM lane q
 constexpr int NSM = 256;       // softmax threads
 constexpr float LOG2E = 1.4426950408889634f;
 // smem map (bytes, 1024-aligned base)
-constexpr int OFF_K = 0, OFF_V = 32768, OFF_Q = 65536 /*[2] x 16K*/, OFF_O = 98304 /*[2] x 16K*/,
-              OFF_P = 131072, OFF_S = 147456, OFF_STAGE = 163840 /*32K fp32*/,
-              OFF_P2 = 196608, OFF_S2 = 212992 /* P/dS double buffer */, OFF_MISC = 229376;
+// Q/dO: 3-stage ring (a stage is released only when the gradient MMAs of its
+// tile complete, and the TMA refill takes ~1-2 us, so two stages starved the
+// S/dP MMAs of the next tile)
+constexpr int QSTAGES = 3;
+constexpr int OFF_K = 0, OFF_V = 32768, OFF_Q = 65536 /*[3] x 16K*/, OFF_O = 114688 /*[3] x 16K*/,
+              OFF_P = 163840, OFF_S = 180224, OFF_STAGE = 196608 /*32K fp32*/, OFF_MISC = 229376;
 constexpr int SMEM = 1024 + OFF_MISC + 3 * 2 * BQ * 4 + 256;
 static_assert(3 * 2 * BQ * 4 + 13 * 8 + 8 <= 3 * 2 * BQ * 4 + 256, "misc region");
 
@@ -105,14 +108,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   int* s_sst = reinterpret_cast<int*>(s_dlt + 2 * BQ);
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_sst + 2 * BQ);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qdo_full = bars + 1;   // [2]
-  uint64_t* qdo_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_ready = bars + 6;
-  uint64_t* dq_full = bars + 7;    // [2]
-  uint64_t* dqt_free = bars + 9;   // [2]
-  uint64_t* s_free = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* qdo_full = bars + 1;   // [3]
+  uint64_t* qdo_empty = bars + 4;  // [3]
+  uint64_t* s_full = bars + 7;
+  uint64_t* p_ready = bars + 8;
+  uint64_t* dq_full = bars + 9;    // [2]
+  uint64_t* dqt_free = bars + 11;  // [2]
+  uint64_t* s_free = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   float* stage = reinterpret_cast<float*>(smem + OFF_STAGE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     ptx::tma_prefetch(&tdo);
     ptx::tma_prefetch(&tdq);
     ptx::mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QSTAGES; ++i) {
       ptx::mbar_init(&qdo_full[i], 1);
       ptx::mbar_init(&qdo_empty[i], 1);
     }
@@ -163,10 +166,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tma_load_3d(&tv, kv_full, smem + OFF_V, 0, kh, k0);
       ptx::tma_load_3d(&tv, kv_full, smem + OFF_V + 16384, 64, kh, k0);
       for (int it = 0; it < niter; ++it) {
-        const int st = it & 1;
+        const int st = it % QSTAGES;
         const int h = hbase + it / nq;
         const int q0 = k0 + (it % nq) * BQ;
-        if (it >= 2) ptx::mbar_wait(&qdo_empty[st], ((it >> 1) - 1) & 1);
+        if (it >= QSTAGES) ptx::mbar_wait(&qdo_empty[st], ((it / QSTAGES) - 1) & 1);
         ptx::mbar_expect_tx(&qdo_full[st], 4 * 8192);
         uint8_t* q = smem + OFF_Q + st * 16384;
         uint8_t* o = smem + OFF_O + st * 16384;
@@ -182,16 +185,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t id_kv = ptx::idesc_bf16_f32(128, D, false, true);    // dV, dK
     constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, BQ, true, true);     // dQ^T
     const uint32_t ak = ptx::smem_u32(smem + OFF_K), av = ptx::smem_u32(smem + OFF_V),
-                   ap0 = ptx::smem_u32(smem + OFF_P), as0 = ptx::smem_u32(smem + OFF_S),
-                   ap1 = ptx::smem_u32(smem + OFF_P2), as1 = ptx::smem_u32(smem + OFF_S2);
+                   ap = ptx::smem_u32(smem + OFF_P), as = ptx::smem_u32(smem + OFF_S);
     ptx::mbar_wait(kv_full, 0);
     // issue order: S/dP(i+1) right after P(i) is ready, then dV/dK/dQ(i), so
     // the softmax of tile i+1 overlaps the gradient MMAs of tile i.
     auto issue_sdp = [&](int it) {
-      const int st = it & 1;
+      const int st = it % QSTAGES;
       const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
       const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
-      ptx::mbar_wait(&qdo_full[st], (it >> 1) & 1);
+      ptx::mbar_wait(&qdo_full[st], (it / QSTAGES) & 1);
       ptx::tc_fence_after();
       if (lane == 0) {
 #pragma unroll
@@ -206,9 +208,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
     if (niter > 0) issue_sdp(0);
     for (int it = 0; it < niter; ++it) {
-      const int st = it & 1;
-      const uint32_t aq = ptx::smem_u32(smem + OFF_Q + st * 16384);
-      const uint32_t ao = ptx::smem_u32(smem + OFF_O + st * 16384);
+      const int st = it & 1;                // dQ^T TMEM buffer
+      const int qs = it % QSTAGES;          // Q/dO stage
+      const uint32_t aq = ptx::smem_u32(smem + OFF_Q + qs * 16384);
+      const uint32_t ao = ptx::smem_u32(smem + OFF_O + qs * 16384);
       if (it + 1 < niter) {
         ptx::mbar_wait(s_free, it & 1);  // S^T/dP^T(it) are in the softmax registers
         if (lane == 0) PROF(it, 0);
@@ -219,7 +222,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (it >= 2) ptx::mbar_wait(&dqt_free[st], ((it >> 1) - 1) & 1);  // dQ^T(it-2) read out
       if (lane == 0) PROF(it, 2);
       ptx::tc_fence_after();
-      const uint32_t ap = st ? ap1 : ap0, as = st ? as1 : as0;  // P/dS(it) buffer
       if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k)
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < BK / 16; ++k)
           ptx::mma_bf16_ss(TDQ + 64 * st, md(ak, k, 16384), md(as, k, 8192), id_q, k != 0);
         ptx::mma_commit(&dq_full[st]);
-        ptx::mma_commit(&qdo_empty[st]);
+        ptx::mma_commit(&qdo_empty[qs]);
       }
       __syncwarp();
     }
@@ -348,12 +350,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      pp[1] * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
         }
       }
-      // publish P/dS(it) into buffer it&1: the gradient MMAs of tile it-2, the
-      // last readers of that buffer, completed before dQ^T(it-2) was drained
-      // (previous iteration); then drain dQ^T(it-1) off the MMA critical path
+      // the gradient MMAs of tile it-1 read sP/sS: wait for them (dQ^T(it-1)
+      // drain), then publish P/dS(it)
       if (pt) PROF(it, 6);
-      uint8_t* sP = smem + ((it & 1) ? OFF_P2 : OFF_P);
-      uint8_t* sS = smem + ((it & 1) ? OFF_S2 : OFF_S);
+      if (it > 0) drain_dq(it - 1);
+      if (pt) PROF(it, 9);
+      uint8_t* sP = smem + OFF_P;
+      uint8_t* sS = smem + OFF_S;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         const int chunk = half * 4 + cc;
@@ -366,8 +369,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_ready);
       if (pt) PROF(it, 7);
-      if (it > 0) drain_dq(it - 1);
-      if (pt) PROF(it, 9);
       if (it + 1 < niter) load_cols(it + 1);
       bar_sync_softmax();  // next tile's column data visible
       if (pt) PROF(it, 10);
