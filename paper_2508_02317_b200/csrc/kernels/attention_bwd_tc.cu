@@ -3,7 +3,7 @@
 // One CTA per (128-key tile, kv head, head split).  K and V stay in smem; the
 // CTA walks its share of the q heads of the GQA group (all of them when
 // kv_splits == 1) and the 64-query tiles that can see its keys
-// (q in [k0, seq_end(last key))), with Q/dO double-buffered by TMA.
+// (q in [k0, seq_end(last key))), with Q/dO in a 3-stage TMA ring.
 // kv_splits > 1 shortens the CTAs (better tail balance when there are few key
 // tiles, e.g. one kv head per rank under Ulysses); the per-split dK/dV
 // partials are then summed by TMA bulk reduce-add into fp32 accumulators.
