@@ -24,52 +24,88 @@ using bf16 = __nv_bfloat16;
 
 // ---------------------------------------------------------------------------
 // router logits: logits[t, e] = sum_k h[t,k] * w[e,k], k ascending, fmul/fadd rn
-// block: 128 experts x 16 tokens; K staged through smem in chunks of 64
-// ---------------------------------------------------------------------------
-constexpr int RT = 64, RE = 128, RK = 32;  // block tile: 64 tokens x 128 experts, K chunks of 32
-// 256 threads; thread (ty, tx): tokens ty*4 .. +3, experts tx + 16*j (j < 8).
-__global__ void __launch_bounds__(256) router_kernel(const bf16* __restrict__ h,
-                                                     const bf16* __restrict__ w,
-                                                     float* __restrict__ logits, int T, int H,
-                                                     int E) {
+// (the CPU oracle's sequential order, so routing is bit-exact).  Block tile:
+// 32 tokens x 128 experts (256 blocks at T = 8192, two per SM), K in chunks of
+// 32 staged through smem with 16-B loads; the next chunk is fetched into
+// registers while the current one is consumed.
+constexpr int RT = 32, RE = 128, RK = 32;
+// 256 threads; thread (ty, tx): tokens ty*2 .. +1, experts tx + 16*j (j < 8).
+__global__ void __launch_bounds__(256, 2) router_kernel(const bf16* __restrict__ h,
+                                                        const bf16* __restrict__ w,
+                                                        float* __restrict__ logits, int T, int H,
+                                                        int E) {
   __shared__ float sh[RK][RT + 4];
   __shared__ float sw[RK][RE + 4];
   const int t0 = blockIdx.x * RT, e0 = blockIdx.y * RE;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][8];
+  // staging: h chunk = 32 tok x 32 k = 128 x 16 B (threads 0..127),
+  //          w chunk = 128 exp x 32 k = 512 x 16 B (2 per thread)
+  const int hr = threadIdx.x >> 2, hc = (threadIdx.x & 3) * 8;   // h: token row, k offset
+  uint4 hq = make_uint4(0, 0, 0, 0), wq[2];
+  auto fetch = [&](int k0) {
+    if (threadIdx.x < RT * 4) {
+      const int t = t0 + hr;
+      hq = t < T ? *reinterpret_cast<const uint4*>(h + int64_t(t) * H + k0 + hc) : make_uint4(0, 0, 0, 0);
+    }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int u = 0; u < 2; ++u) {
+      const int idx = threadIdx.x + u * 256;
+      const int e = e0 + (idx >> 2);
+      wq[u] = e < E ? *reinterpret_cast<const uint4*>(w + int64_t(e) * H + k0 + (idx & 3) * 8)
+                    : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto stash = [&]() {
+    if (threadIdx.x < RT * 4) {
+      const uint32_t v[4] = {hq.x, hq.y, hq.z, hq.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = ptx::unpack_bf16(v[q]);
+        sh[hc + 2 * q][hr] = f.x;
+        sh[hc + 2 * q + 1][hr] = f.y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int idx = threadIdx.x + u * 256;
+      const int ee = idx >> 2, kc = (idx & 3) * 8;
+      const uint32_t v[4] = {wq[u].x, wq[u].y, wq[u].z, wq[u].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = ptx::unpack_bf16(v[q]);
+        sw[kc + 2 * q][ee] = f.x;
+        sw[kc + 2 * q + 1][ee] = f.y;
+      }
+    }
+  };
+  float acc[2][8];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  fetch(0);
   for (int k0 = 0; k0 < H; k0 += RK) {
-    for (int i = threadIdx.x; i < RT * RK; i += 256) {
-      const int tt = i / RK, kk = i % RK;
-      const int t = t0 + tt;
-      sh[kk][tt] = t < T ? __bfloat162float(h[int64_t(t) * H + k0 + kk]) : 0.f;
-    }
-    for (int i = threadIdx.x; i < RE * RK; i += 256) {
-      const int ee = i / RK, kk = i % RK;
-      sw[kk][ee] = (e0 + ee) < E ? __bfloat162float(w[int64_t(e0 + ee) * H + k0 + kk]) : 0.f;
-    }
+    stash();
     __syncthreads();
+    if (k0 + RK < H) fetch(k0 + RK);  // in flight during the FMAs below
 #pragma unroll 4
     for (int kk = 0; kk < RK; ++kk) {
-      float hv[4], wv[8];
+      float hv[2], wv[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) hv[i] = sh[kk][ty * 4 + i];
+      for (int i = 0; i < 2; ++i) hv[i] = sh[kk][ty * 2 + i];
 #pragma unroll
       for (int j = 0; j < 8; ++j) wv[j] = sw[kk][tx + 16 * j];
       // k ascending, separately rounded multiply and add: the CPU oracle's order
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(hv[i], wv[j]));
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int t = t0 + ty * 4 + i;
+  for (int i = 0; i < 2; ++i) {
+    const int t = t0 + ty * 2 + i;
     if (t >= T) continue;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -472,7 +508,7 @@ __global__ void swiglu_bwd_grouped_kernel(const bf16* __restrict__ dact, const b
 
 cudaError_t k_moe_router(const __nv_bfloat16* h, const __nv_bfloat16* w, float* logits, int T,
                          int H, int E, cudaStream_t s) {
-  if (H % RK) return cudaErrorInvalidValue;
+  if (H % RK || H % 8) return cudaErrorInvalidValue;
   dim3 grid((T + RT - 1) / RT, (E + RE - 1) / RE);
   ++g_kernel_launches;
   router_kernel<<<grid, 256, 0, s>>>(h, w, logits, T, H, E);
