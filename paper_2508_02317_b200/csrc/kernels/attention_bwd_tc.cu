@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::mbar_wait(s_free, it & 1);  // S^T/dP^T(it) are in the softmax registers
         if (lane == 0) PROF(it, 0);
         issue_sdp(it + 1);
+        if (lane == 0) PROF(it, 3);
       }
       ptx::mbar_wait(p_ready, it & 1);   // P/dS(it) in smem
       if (lane == 0) PROF(it, 1);
@@ -229,11 +230,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k)
           ptx::mma_bf16_ss(TDK, kd(as, k, 0), md(aq, k, 8192), id_kv, (it | k) != 0);
+        ptx::mma_commit(&qdo_empty[qs]);  // release the Q/dO stage early: dQ^T does not read it
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
           ptx::mma_bf16_ss(TDQ + 64 * st, md(ak, k, 16384), md(as, k, 8192), id_q, k != 0);
         ptx::mma_commit(&dq_full[st]);
-        ptx::mma_commit(&qdo_empty[qs]);
       }
       __syncwarp();
     }
@@ -578,13 +579,17 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
       acc[6] += double(a[10] - a[9]);  // load_cols + bar
       acc[7] += double(a[1] - a[0]);   // MMA: s_free -> p_ready
       acc[8] += double(a[2] - a[1]);   // MMA: wait dqt_free
+      acc[9] += double(a[3] - a[0]);   // MMA: S/dP issue incl. qdo_full wait
+      acc[10] += double(a[0] - a[5]);  // s_free seen by MMA - s_full seen by softmax (same it)
+      acc[11] += double(b[5] - a[3]);  // S(it+1) issued -> softmax sees s_full(it+1)
     }
     if (n)
       fprintf(stderr,
               "[attn_bwd prof cta %d, %d iters] iter %.0f | wait_S %.0f ld+math %.0f publish %.0f "
-              "drain(wait dq %.0f, total %.0f) cols+bar %.0f | mma: s_free->p_ready %.0f wait_dqt %.0f\n",
+              "drain(wait dq %.0f, total %.0f) cols+bar %.0f | mma: s_free->p_ready %.0f wait_dqt %.0f "
+              "issue_S %.0f sfull->sfree %.0f S_issue->S_seen %.0f\n",
               p.prof_cta, n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n,
-              acc[6] / n, acc[7] / n, acc[8] / n);
+              acc[6] / n, acc[7] / n, acc[8] / n, acc[9] / n, acc[10] / n, acc[11] / n);
   }
   return cudaGetLastError();
 }
