@@ -222,12 +222,18 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
 }
 
 __global__ void colsum_kernel(const float* __restrict__ part, int rows, int cols,
-                              float* __restrict__ out, int accumulate) {
+                              void* __restrict__ out, int accumulate, int out_bf16) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   float s = 0.f;
   for (int r = 0; r < rows; ++r) s += part[int64_t(r) * cols + c];
-  out[c] = accumulate ? out[c] + s : s;
+  if (out_bf16) {
+    bf16* o = static_cast<bf16*>(out);
+    o[c] = __float2bfloat16(accumulate ? __bfloat162float(o[c]) + s : s);
+  } else {
+    float* o = static_cast<float*>(out);
+    o[c] = accumulate ? o[c] + s : s;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -375,8 +381,9 @@ __global__ void swiglu_bwd_kernel(const bf16* __restrict__ dact, const bf16* __r
 // ---------------------------------------------------------------------------
 // AdamW (torch.optim.AdamW semantics), fp32 master/m/v/grad, bf16 param copy.
 // ---------------------------------------------------------------------------
+template <typename G>
 __global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                             const float* __restrict__ g, bf16* __restrict__ pb, int64_t n,
+                             const G* __restrict__ g, bf16* __restrict__ pb, int64_t n,
                              float lr, float b1, float b2, float eps, float wd, float bc1,
                              float bc2_sqrt) {
   const int64_t n4 = n / 4;
@@ -387,7 +394,14 @@ __global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float
     float4 pv = reinterpret_cast<float4*>(p)[i];
     float4 mv = reinterpret_cast<float4*>(m)[i];
     float4 vv = reinterpret_cast<float4*>(v)[i];
-    const float4 gv = reinterpret_cast<const float4*>(g)[i];
+    float4 gv;
+    if constexpr (sizeof(G) == 4) {
+      gv = reinterpret_cast<const float4*>(g)[i];
+    } else {  // bf16 gradients (layer / expert units)
+      const uint2 q = reinterpret_cast<const uint2*>(g)[i];
+      const float2 a = ptx::unpack_bf16(q.x), b = ptx::unpack_bf16(q.y);
+      gv = make_float4(a.x, a.y, b.x, b.y);
+    }
     float* pp = &pv.x;
     float* mp = &mv.x;
     float* vp = &vv.x;
@@ -463,7 +477,7 @@ int k_rmsnorm_bwd_parts(int T) { return (T + BWD_ROWS - 1) / BWD_ROWS; }
 
 cudaError_t k_rmsnorm_bwd(const float* dy, const float* x, const __nv_bfloat16* w,
                           const float* rstd, const float* dres, float* dx, float* dw_part,
-                          float* dw, int accumulate_dw, int T, int H, cudaStream_t s) {
+                          void* dw, int accumulate_dw, int T, int H, cudaStream_t s, int dw_bf16) {
   if (H % 4 || H > NT * 4 * MAXV) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
   const int nb = k_rmsnorm_bwd_parts(T);
@@ -477,7 +491,7 @@ cudaError_t k_rmsnorm_bwd(const float* dy, const float* x, const __nv_bfloat16* 
   else
     rmsnorm_bwd_kernel<8><<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
   ++g_kernel_launches;
-  colsum_kernel<<<(H + 127) / 128, 128, 0, s>>>(dw_part, nb, H, dw, accumulate_dw);
+  colsum_kernel<<<(H + 127) / 128, 128, 0, s>>>(dw_part, nb, H, dw, accumulate_dw, dw_bf16);
   return cudaGetLastError();
 }
 
@@ -516,15 +530,21 @@ cudaError_t k_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __n
   return cudaGetLastError();
 }
 
-cudaError_t k_adamw(float* p, float* m, float* v, const float* g, __nv_bfloat16* pb, int64_t n,
-                    float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t s) {
+cudaError_t k_adamw(float* p, float* m, float* v, const void* g, int g_bf16, __nv_bfloat16* pb,
+                    int64_t n, float lr, float b1, float b2, float eps, float wd, int step,
+                    cudaStream_t s) {
   if (n % 4) return cudaErrorInvalidValue;
   if (n <= 0) return cudaSuccess;
   const double bc1 = 1.0 - std::pow(double(b1), step);
   const double bc2 = 1.0 - std::pow(double(b2), step);
   ++g_kernel_launches;
-  adamw_kernel<<<grid_for(n / 4), NT, 0, s>>>(p, m, v, g, pb, n, lr, b1, b2, eps, wd, float(bc1),
-                                               float(std::sqrt(bc2)));
+  if (g_bf16)
+    adamw_kernel<bf16><<<grid_for(n / 4), NT, 0, s>>>(p, m, v, static_cast<const bf16*>(g), pb, n, lr,
+                                                      b1, b2, eps, wd, float(bc1), float(std::sqrt(bc2)));
+  else
+    adamw_kernel<float><<<grid_for(n / 4), NT, 0, s>>>(p, m, v, static_cast<const float*>(g), pb, n,
+                                                       lr, b1, b2, eps, wd, float(bc1),
+                                                       float(std::sqrt(bc2)));
   return cudaGetLastError();
 }
 

@@ -443,12 +443,13 @@ __global__ void router_bwd_kernel(const float* __restrict__ dw, const float* __r
 
 // out[i] = sum_g part[g, i]  (fixed order)
 __global__ void sum_partials_kernel(const float* __restrict__ part, int G, int64_t n,
-                                    float* __restrict__ out) {
+                                    void* __restrict__ out, int out_bf16) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     float acc = 0.f;
     for (int g = 0; g < G; ++g) acc += part[int64_t(g) * n + i];
-    out[i] = acc;
+    if (out_bf16) static_cast<bf16*>(out)[i] = __float2bfloat16(acc);
+    else static_cast<float*>(out)[i] = acc;
   }
 }
 
@@ -608,11 +609,11 @@ cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, 
   return cudaGetLastError();
 }
 
-cudaError_t k_sum_partials(const float* part, int G, int64_t n, float* out, cudaStream_t s) {
+cudaError_t k_sum_partials(const float* part, int G, int64_t n, void* out, cudaStream_t s, int out_bf16) {
   int64_t b = (n + 255) / 256;
   if (b > num_sms() * 8) b = num_sms() * 8;
   ++g_kernel_launches;
-  sum_partials_kernel<<<int(b), 256, 0, s>>>(part, G, n, out);
+  sum_partials_kernel<<<int(b), 256, 0, s>>>(part, G, n, out, out_bf16);
   return cudaGetLastError();
 }
 

@@ -277,7 +277,7 @@ int opx_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t T, int F
 }
 int opx_adamw(float* p, float* m, float* v, const float* g, void* pb, int64_t n, float lr,
               float b1, float b2, float eps, float wd, int step, void* stream) {
-  OPX_CALL(k_adamw(p, m, v, g, static_cast<__nv_bfloat16*>(pb), n, lr, b1, b2, eps, wd, step,
+  OPX_CALL(k_adamw(p, m, v, g, 0, static_cast<__nv_bfloat16*>(pb), n, lr, b1, b2, eps, wd, step,
                    static_cast<cudaStream_t>(stream)),
            "opx_adamw");
 }

@@ -23,7 +23,8 @@ cudaError_t k_rmsnorm_fwd(const float* x, const __nv_bfloat16* w, __nv_bfloat16*
 int k_rmsnorm_bwd_parts(int T);
 cudaError_t k_rmsnorm_bwd(const float* dy, const float* x, const __nv_bfloat16* w,
                           const float* rstd, const float* dres, float* dx, float* dw_part,
-                          float* dw, int accumulate_dw, int T, int H, cudaStream_t s);
+                          void* dw, int accumulate_dw, int T, int H, cudaStream_t s,
+                          int dw_bf16 = 0);
 cudaError_t k_embed_fwd(const int* ids, const __nv_bfloat16* E, float* x, int T, int H,
                         cudaStream_t s);
 cudaError_t k_embed_bwd(const int* ids, const float* dx, float* dE, int T, int H, cudaStream_t s);
@@ -31,8 +32,10 @@ cudaError_t k_ce_fwd_bwd(__nv_bfloat16* logits, int64_t ldl, const int* labels, 
                          int V, float inv_n, cudaStream_t s);
 cudaError_t k_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __nv_bfloat16* dgu,
                          int64_t T, int F, cudaStream_t s);
-cudaError_t k_adamw(float* p, float* m, float* v, const float* g, __nv_bfloat16* pb, int64_t n,
-                    float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t s);
+// g: fp32 or (g_bf16) bf16 gradients
+cudaError_t k_adamw(float* p, float* m, float* v, const void* g, int g_bf16, __nv_bfloat16* pb,
+                    int64_t n, float lr, float b1, float b2, float eps, float wd, int step,
+                    cudaStream_t s);
 cudaError_t k_cast_f32_bf16(const float* x, __nv_bfloat16* y, int64_t n, cudaStream_t s);
 cudaError_t k_sum(const float* x, int64_t n, float* out, cudaStream_t s);
 
@@ -131,7 +134,8 @@ cudaError_t k_moe_publish_counts(const int* counts, int* const* tables, int ep, 
 cudaError_t k_moe_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __nv_bfloat16* dgu,
                              const int* g_start, const int* g_rows, const int* g_rows_pad, int El,
                              int F, int max_rows, cudaStream_t s);
-cudaError_t k_sum_partials(const float* part, int G, int64_t n, float* out, cudaStream_t s);
+cudaError_t k_sum_partials(const float* part, int G, int64_t n, void* out, cudaStream_t s,
+                           int out_bf16 = 0);
 cudaError_t k_moe_router_bwd(const float* dw, const float* wts, const int* idx, int T, int k, int E,
                              __nv_bfloat16* dlogits, cudaStream_t s);
 }  // namespace opx

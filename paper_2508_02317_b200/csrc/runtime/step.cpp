@@ -96,8 +96,8 @@ int Step::opt_unit(Unit& u, cudaStream_t after, const std::string& name) {
   cudaEvent_t ready = ev();
   CU(cudaEventRecord(ready, after));
   CU(cudaStreamWaitEvent(os_, ready, 0));
-  CU(k_adamw(u.master, u.m, u.v, u.gshard, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps,
-             ex_.wd, step_count_, os_));
+  CU(k_adamw(u.master, u.m, u.v, u.gshard, u.gbf, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2,
+             ex_.eps, ex_.wd, step_count_, os_));
   if (ex_.trace) {
     cudaEvent_t done = ev();
     CU(cudaEventRecord(done, os_));
@@ -223,7 +223,8 @@ int Step::build_units() {
     u.master = alloc<float>(size_t(u.shard));
     u.m = alloc<float>(size_t(u.shard));
     u.v = alloc<float>(size_t(u.shard));
-    u.gshard = alloc<float>(size_t(u.shard));
+    u.gshard = u.gbf ? static_cast<void*>(alloc<bf16>(size_t(u.shard)))
+                     : static_cast<void*>(alloc<float>(size_t(u.shard)));
     u.pshard = alloc<bf16>(size_t(u.shard));
     if (!u.master || !u.m || !u.v || !u.gshard || !u.pshard) {
       set_error("out of device memory for parameter shards");
@@ -269,6 +270,7 @@ int Step::build_units() {
     Unit u;
     const std::string p = "model.layers." + std::to_string(l) + ".";
     u.name = "layer" + std::to_string(l);
+    u.gbf = ex_.bf16_grads;
     add(u, p + "input_layernorm.weight", {H}, true);
     add(u, p + "self_attn.q_proj.weight", {int64_t(hq_) * 128, H}, false);
     add(u, p + "self_attn.k_proj.weight", {int64_t(hk_) * 128, H}, false);
@@ -293,7 +295,8 @@ int Step::build_units() {
       if (!gslot_.back()) return cuda_fail(cudaErrorMemoryAllocation, "gather slots");
     }
     for (int s = 0; s < 2; ++s) {
-      gradslot_.push_back(alloc<float>(size_t(mx)));
+      gradslot_.push_back(ex_.bf16_grads ? static_cast<void*>(alloc<bf16>(size_t(mx)))
+                                         : static_cast<void*>(alloc<float>(size_t(mx))));
       if (!gradslot_.back()) return cuda_fail(cudaErrorMemoryAllocation, "grad slots");
     }
     Unit& hu = units_[0];
@@ -498,7 +501,7 @@ int Step::init_weights(uint64_t seed) {
     CU(cudaMemsetAsync(u.pshard, 0, size_t(u.shard) * 2, cs_));
     CU(cudaMemsetAsync(u.m, 0, size_t(u.shard) * 4, cs_));
     CU(cudaMemsetAsync(u.v, 0, size_t(u.shard) * 4, cs_));
-    CU(cudaMemsetAsync(u.gshard, 0, size_t(u.shard) * 4, cs_));
+    CU(cudaMemsetAsync(u.gshard, 0, size_t(u.shard) * u.gbytes(), cs_));
     for (const Param& q : u.params) {
       const int64_t lo = std::max(sb, q.off), hi = std::min(se, q.off + q.numel);
       if (hi <= lo) continue;
@@ -749,7 +752,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
   return OPX_OK;
 }
 
-int Step::layer_bwd(int l, Unit& u, float* G) {
+int Step::layer_bwd(int l, Unit& u, void* G) {
   const int T = T_, H = H_, F = F_, Q = hq_ * 128;
   const LayerW W = layer_w(u, u.full);
   const bool tr = ex_.trace;
@@ -785,18 +788,19 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     mark(pre + ".recompute", ph, 0, e0, e1);
     e0 = e1;
   }
-  float* g_ln1 = G + u.params[0].off;
-  float* g_qkv = G + u.params[1].off;
-  float* g_o = G + u.params[4].off;
-  float* g_ln2 = G + u.params[5].off;
-  float* g_gu = u.params.size() > 7 ? G + u.params[6].off : nullptr;
-  float* g_down = u.params.size() > 7 ? G + u.params[7].off : nullptr;
+  void* g_ln1 = u.gat(G, u.params[0].off);
+  void* g_qkv = u.gat(G, u.params[1].off);
+  void* g_o = u.gat(G, u.params[4].off);
+  void* g_ln2 = u.gat(G, u.params[5].off);
+  void* g_gu = u.params.size() > 7 ? u.gat(G, u.params[6].off) : nullptr;
+  void* g_down = u.params.size() > 7 ? u.gat(G, u.params[7].off) : nullptr;
+  const int EPI_G = u.gbf ? GEMM_EPI_BF16 : GEMM_EPI_F32;  // weight-gradient epilogue
 
   // ---- MLP (dense) or MoE block
   if (a_.is_moe_layer(l)) {
     Unit& eu = expert_units_[size_t(l)];
     TRY(moe_bwd(l, u, eu, G, eu.gfull, dtmp_));
-    CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
+    CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_, u.gbf));
   } else {
     // per-GEMM sub-nodes when tracing (mlp.*), so the profile separates the
     // dgrad/wgrad GEMMs from the elementwise work
@@ -810,15 +814,15 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
     CU(gemm_run(gd(T, F, H, dxb_, H, false, W.down, F, true, GEMM_EPI_BF16, dact_, F), cs_));
     sub("dgrad_down");
-    CU(gemm_run(gd(H, F, T, dxb_, H, true, act_, F, true, GEMM_EPI_F32, g_down, F), cs_));
+    CU(gemm_run(gd(H, F, T, dxb_, H, true, act_, F, true, EPI_G, g_down, F), cs_));
     sub("wgrad_down");
     CU(k_swiglu_bwd(dact_, gu_, dgu_, T, F, cs_));
     sub("swiglu_bwd");
     CU(gemm_run(gd(T, H, 2 * F, dgu_, 2 * F, false, W.gu, H, true, GEMM_EPI_F32, dtmp_, H), cs_));
     sub("dgrad_gu");
-    CU(gemm_run(gd(2 * F, H, T, dgu_, 2 * F, true, h2_, H, true, GEMM_EPI_F32, g_gu, H), cs_));
+    CU(gemm_run(gd(2 * F, H, T, dgu_, 2 * F, true, h2_, H, true, EPI_G, g_gu, H), cs_));
     sub("wgrad_gu");
-    CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_));
+    CU(k_rmsnorm_bwd(dtmp_, x2_, W.ln2, r2_, dx_, dx_, dw_part_, g_ln2, 0, T, H, cs_, u.gbf));
     sub("rmsnorm_bwd");
   }
   if (tr && a_.is_moe_layer(l)) {
@@ -840,7 +844,7 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
     do_loc = do_scratch;
   }
   CU(gemm_run(gd(T, Q, H, dxb_, H, false, W.o, Q, true, GEMM_EPI_BF16, do_loc, Q), cs_));
-  CU(gemm_run(gd(H, Q, T, dxb_, H, true, o_loc(ob), Q, true, GEMM_EPI_F32, g_o, Q), cs_));
+  CU(gemm_run(gd(H, Q, T, dxb_, H, true, o_loc(ob), Q, true, EPI_G, g_o, Q), cs_));
   if (p_.sp > 1) {
     A2AArgs a{};
     a.sp = int(p_.sp);
@@ -922,9 +926,9 @@ int Step::layer_bwd(int l, Unit& u, float* G) {
   }
   bf16* dqkv = dqkv_loc(xb);
   CU(gemm_run(gd(T, H, Wqkv_, dqkv, Wqkv_, false, W.qkv, H, true, GEMM_EPI_F32, dtmp_, H), cs_));
-  CU(gemm_run(gd(Wqkv_, H, T, dqkv, Wqkv_, true, h_, H, true, GEMM_EPI_F32, g_qkv, H), cs_));
+  CU(gemm_run(gd(Wqkv_, H, T, dqkv, Wqkv_, true, h_, H, true, EPI_G, g_qkv, H), cs_));
   CU(k_rmsnorm_bwd(dtmp_, x_saved_[size_t(l)], W.ln1, r1_, dx_, dx_, dw_part_, g_ln1, 0, T, H,
-                   cs_));
+                   cs_, u.gbf));
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
@@ -995,7 +999,7 @@ int Step::run(opx_step_report* rep) {
     CU(cudaStreamWaitEvent(cs_, ev_head_ag_, 0));
   }
   // embedding grad region is scatter-added: zero it
-  CU(cudaMemsetAsync(hu.gfull + hu.params[0].off, 0, size_t(hu.params[0].numel) * 4, cs_));
+  CU(cudaMemsetAsync(hu.gat(hu.gfull, hu.params[0].off), 0, size_t(hu.params[0].numel) * 4, cs_));
   CU(k_embed_fwd(d_ids_, hu.full + hu.params[0].off, x_saved_[0], T_, H_, cs_));
 
   auto issue_gather = [&](int l, bool bwd) -> int {
@@ -1056,7 +1060,7 @@ int Step::run(opx_step_report* rep) {
     }
   }
   // ---------------- head (fwd + CE + bwd) ----------------
-  TRY(head_fwd_bwd(hu, hu.gfull));
+  TRY(head_fwd_bwd(hu, static_cast<float*>(hu.gfull)));  // the head keeps fp32 grads
 
   // ---------------- backward ----------------
   // layers L-nslots .. L-1 are still resident in their slots from the forward
@@ -1087,12 +1091,15 @@ int Step::run(opx_step_report* rep) {
       Unit& eu = expert_units_[size_t(l)];
       if (eu.P > 1) {
         if (eu.padded > eu.numel)
-          CU(cudaMemsetAsync(eu.gfull + eu.numel, 0, size_t(eu.padded - eu.numel) * 4, cs_));
-        NC(ncclReduceScatter(eu.gfull, eu.gshard, size_t(eu.shard), ncclFloat, ncclSum, eu.comm,
+          CU(cudaMemsetAsync(eu.gat(eu.gfull, eu.numel), 0, size_t(eu.padded - eu.numel) * eu.gbytes(),
+                             cs_));
+        NC(ncclReduceScatter(eu.gfull, eu.gshard, size_t(eu.shard), eu.gbf ? ncclBfloat16 : ncclFloat,
+                             ncclSum, eu.comm,
                              cs_));
       }
       if (eu.rep_comm)
-        NC(ncclAllReduce(eu.gshard, eu.gshard, size_t(eu.shard), ncclFloat, ncclSum,
+        NC(ncclAllReduce(eu.gshard, eu.gshard, size_t(eu.shard), eu.gbf ? ncclBfloat16 : ncclFloat,
+                         ncclSum,
                          eu.rep_comm, cs_));
       TRY(opt_unit(eu, cs_, "opt.experts.layer" + std::to_string(l)));
     }
@@ -1104,13 +1111,14 @@ int Step::run(opx_step_report* rep) {
       if (tr) cudaEventRecord(a, ms_);
       if (u.P > 1) {
         if (u.padded > u.numel)
-          CU(cudaMemsetAsync(u.gfull + u.numel, 0, size_t(u.padded - u.numel) * 4, ms_));
-        NC(ncclReduceScatter(u.gfull, u.gshard, size_t(u.shard), ncclFloat, ncclSum, u.comm,
+          CU(cudaMemsetAsync(u.gat(u.gfull, u.numel), 0, size_t(u.padded - u.numel) * u.gbytes(),
                              ms_));
+        NC(ncclReduceScatter(u.gfull, u.gshard, size_t(u.shard), u.gbf ? ncclBfloat16 : ncclFloat,
+                             ncclSum, u.comm, ms_));
       }
       if (u.rep_comm)
-        NC(ncclAllReduce(u.gshard, u.gshard, size_t(u.shard), ncclFloat, ncclSum, u.rep_comm,
-                         ms_));
+        NC(ncclAllReduce(u.gshard, u.gshard, size_t(u.shard), u.gbf ? ncclBfloat16 : ncclFloat,
+                         ncclSum, u.rep_comm, ms_));
       CU(cudaEventRecord(ev_rs_done_[size_t(l)], ms_));
       if (tr)
         mark("bwd.rs.layer" + std::to_string(l) + ".m0", "bwd.layer" + std::to_string(l), 1, a,
@@ -1120,13 +1128,13 @@ int Step::run(opx_step_report* rep) {
       TRY(opt_unit(u, cs_, "opt.layer" + std::to_string(l)));
     }
   }
-  CU(k_embed_bwd(d_ids_, dx_, hu.gfull + hu.params[0].off, T_, H_, cs_));
+  CU(k_embed_bwd(d_ids_, dx_, static_cast<float*>(hu.gfull) + hu.params[0].off, T_, H_, cs_));
   if (P > 1 || hu.rep_comm) {
     CU(cudaEventRecord(ev_head_rs_, cs_));
     CU(cudaStreamWaitEvent(ms_, ev_head_rs_, 0));
     if (P > 1) {
       if (hu.padded > hu.numel)
-        CU(cudaMemsetAsync(hu.gfull + hu.numel, 0, size_t(hu.padded - hu.numel) * 4, ms_));
+        CU(cudaMemsetAsync(hu.gat(hu.gfull, hu.numel), 0, size_t(hu.padded - hu.numel) * 4, ms_));
       NC(ncclReduceScatter(hu.gfull, hu.gshard, size_t(hu.shard), ncclFloat, ncclSum, hu.comm,
                            ms_));
     }
@@ -1265,17 +1273,28 @@ int Step::get(const std::string& full, void* dst, size_t bytes) {
       if (cnt) CU(cudaMemcpy(dst, u.pshard + src0, bytes, cudaMemcpyDeviceToHost));
       return OPX_OK;
     }
+    if (bytes != size_t(cnt) * 4) {
+      set_error("size mismatch for " + full);
+      return OPX_ERR_ARG;
+    }
+    if (kind == "grad" && u.gbf) {  // bf16 gradients are returned widened to fp32
+      std::vector<uint16_t> h(static_cast<size_t>(cnt));
+      if (cnt) CU(cudaMemcpy(h.data(), static_cast<const bf16*>(u.gshard) + src0, size_t(cnt) * 2,
+                             cudaMemcpyDeviceToHost));
+      float* o = static_cast<float*>(dst);
+      for (int64_t i = 0; i < cnt; ++i) {
+        const uint32_t w = uint32_t(h[size_t(i)]) << 16;
+        std::memcpy(&o[i], &w, 4);
+      }
+      return OPX_OK;
+    }
     const float* src = kind == "master" ? u.master
-                       : kind == "grad" ? u.gshard
+                       : kind == "grad" ? static_cast<const float*>(u.gshard)
                        : kind == "exp_avg" ? u.m
                        : kind == "exp_avg_sq" ? u.v
                                               : nullptr;
     if (!src) {
       set_error("unknown tensor kind '" + kind + "'");
-      return OPX_ERR_ARG;
-    }
-    if (bytes != size_t(cnt) * 4) {
-      set_error("size mismatch for " + full);
       return OPX_ERR_ARG;
     }
     if (cnt) CU(cudaMemcpy(dst, src + src0, bytes, cudaMemcpyDeviceToHost));
@@ -1356,6 +1375,7 @@ int opx_step_create(const char* cj, const char* mj, const char* wj, const char* 
     ex.ce_chunk = e.value("ce_chunk", ex.ce_chunk);
     ex.trace = e.value("trace", false);
     ex.selective_recompute = e.value("selective_recompute", true);
+    ex.bf16_grads = e.value("bf16_grads", true);
   } catch (const std::exception& e) {
     set_error(e.what());
     return OPX_ERR_CONFIG;

@@ -28,6 +28,9 @@ struct ExecCfg {
   // recompute=full: keep the attention activations of as many dense layers as
   // free HBM allows (their backward recomputes only gate|up)
   bool selective_recompute = true;
+  // bf16 gradients for layer / expert units (the reference's memory model,
+  // memory.cpp; halves gradient HBM and reduce-scatter bytes)
+  bool bf16_grads = true;
 };
 
 // One parameter inside an FSDP flat unit.  `phys_name` is the name exposed by
@@ -55,10 +58,17 @@ struct Unit {
   int P = 1, idx = 0;          // shard-group size and this rank's index in it
   ncclComm_t comm = nullptr;   // shard group
   ncclComm_t rep_comm = nullptr;  // HSDP replicate group (nullptr if none)
-  float *master = nullptr, *m = nullptr, *v = nullptr, *gshard = nullptr;
+  float *master = nullptr, *m = nullptr, *v = nullptr;
+  // gradients: fp32, or bf16 when gbf (layer and expert units: halves their
+  // memory and reduce-scatter bytes; the head keeps fp32 for its scatter-add
+  // embedding gradient and chunk-accumulated LM-head gradient)
+  void* gshard = nullptr;
+  bool gbf = false;
+  size_t gbytes() const { return gbf ? 2 : 4; }
+  void* gat(void* base, int64_t off) const { return static_cast<char*>(base) + off * int64_t(gbytes()); }
   bf16* pshard = nullptr;
   bf16* full = nullptr;        // gathered params (alias of pshard when P == 1)
-  float* gfull = nullptr;      // full-layout grads (alias of gshard when P == 1)
+  void* gfull = nullptr;       // full-layout grads (alias of gshard when P == 1)
   const Param* find(const std::string& n) const {
     for (auto& p : params)
       if (p.name == n) return &p;
@@ -124,7 +134,7 @@ class Step {
   // ---- parameters
   std::vector<Unit> units_;  // [0] head, [1+l] layer l
   std::vector<bf16*> gslot_;     // gathered-param slots (P > 1)
-  std::vector<float*> gradslot_; // full-grad slots (P > 1)
+  std::vector<void*> gradslot_;  // full-grad slots (P > 1; bf16 when ExecCfg::bf16_grads)
   int nslots_ = 2;
 
   // ---- peer-visible arena (Ulysses exchanges)
@@ -224,7 +234,7 @@ class Step {
   int barrier_sp(cudaStream_t s);
   // layer pieces
   int layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int slot);
-  int layer_bwd(int l, Unit& u, float* grads);
+  int layer_bwd(int l, Unit& u, void* grads);
   int head_fwd_bwd(Unit& u, float* grads);
   // ---- MoE / expert parallelism (step_moe.cpp)
   bool moe_ = false;
@@ -233,7 +243,7 @@ class Step {
   ncclComm_t expert_comm_ = nullptr;
   std::vector<Unit> expert_units_;  // [layer]; empty params for dense layers
   bf16* eslot_ = nullptr;           // expert gather buffer (De > 1)
-  float* egrad_slot_ = nullptr;     // expert full-grad buffer (De > 1)
+  void* egrad_slot_ = nullptr;      // expert full-grad buffer (De > 1)
   int64_t cap_rows_ = 0;            // receive-buffer rows (worst case)
   size_t off_flags_ep_ = 0, off_xrecv_ = 0, off_dyrecv_ = 0, off_dxback_ = 0;
   // routing state + the peer-written count table and combine buffer: slot 0 is
@@ -294,7 +304,7 @@ class Step {
   int moe_import();            // peer tables after ipc import
   int barrier_ep(cudaStream_t s);
   int moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out);
-  int moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh2);
+  int moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2);
   struct CkptUnit {
     std::string name;
     Unit* u;

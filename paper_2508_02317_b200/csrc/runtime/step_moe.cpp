@@ -102,7 +102,9 @@ int Step::moe_build_units() {
     u.master = alloc<float>(size_t(u.shard));
     u.m = alloc<float>(size_t(u.shard));
     u.v = alloc<float>(size_t(u.shard));
-    u.gshard = alloc<float>(size_t(u.shard));
+    u.gbf = ex_.bf16_grads;
+    u.gshard = u.gbf ? static_cast<void*>(alloc<bf16>(size_t(u.shard)))
+                     : static_cast<void*>(alloc<float>(size_t(u.shard)));
     u.pshard = alloc<bf16>(size_t(u.shard));
     if (!u.master || !u.m || !u.v || !u.gshard || !u.pshard) {
       set_error("out of device memory for expert shards");
@@ -116,7 +118,8 @@ int Step::moe_build_units() {
   }
   if (De_ > 1 && mx > 0) {
     eslot_ = alloc<bf16>(size_t(mx), false);
-    egrad_slot_ = alloc<float>(size_t(mx));
+    egrad_slot_ = ex_.bf16_grads ? static_cast<void*>(alloc<bf16>(size_t(mx)))
+                                 : static_cast<void*>(alloc<float>(size_t(mx)));
     if (!eslot_ || !egrad_slot_) return cuda_fail(cudaErrorMemoryAllocation, "expert slots");
   }
   return OPX_OK;
@@ -384,7 +387,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   return OPX_OK;
 }
 
-int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh2) {
+int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2) {
   const std::string pre = "bwd.layer" + std::to_string(l) + ".m0.";
   const std::string ph = "bwd.layer" + std::to_string(l);
   cudaEvent_t e0 = nullptr;
@@ -436,8 +439,8 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
   CU(gemm_run(grouped(0, Fe, H, dyrecv, H, false, Wd, Fe, true, GEMM_EPI_BF16, dact_e_, Fe, El_, 0,
                       g_start_, g_rows_, cap_rows_, 0),
               cs_));
-  CU(gemm_run(grouped(H, Fe, 0, dyrecv, H, true, act_e_, Fe, true, GEMM_EPI_F32,
-                      Ge + eu.params[1].off, Fe, El_, 1, g_start_, g_rows_pad_, cap_rows_,
+  CU(gemm_run(grouped(H, Fe, 0, dyrecv, H, true, act_e_, Fe, true, eu.gbf ? GEMM_EPI_BF16 : GEMM_EPI_F32,
+                      eu.gat(Ge, eu.params[1].off), Fe, El_, 1, g_start_, g_rows_pad_, cap_rows_,
                       int64_t(H) * Fe),
               cs_));
   CU(k_moe_swiglu_bwd(dact_e_, gu_e_, dgu_e_, g_start_, g_rows_, g_rows_pad_, El_, Fe,
@@ -445,8 +448,8 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
   CU(gemm_run(grouped(0, H, 2 * Fe, dgu_e_, 2 * Fe, false, Wgu, H, true, GEMM_EPI_BF16, dx_e_, H,
                       El_, 0, g_start_, g_rows_, cap_rows_, 0),
               cs_));
-  CU(gemm_run(grouped(2 * Fe, H, 0, dgu_e_, 2 * Fe, true, xrecv, H, true, GEMM_EPI_F32,
-                      Ge + eu.params[0].off, H, El_, 1, g_start_, g_rows_pad_, cap_rows_,
+  CU(gemm_run(grouped(2 * Fe, H, 0, dgu_e_, 2 * Fe, true, xrecv, H, true,
+                      eu.gbf ? GEMM_EPI_BF16 : GEMM_EPI_F32, eu.gat(Ge, eu.params[0].off), H, El_, 1, g_start_, g_rows_pad_, cap_rows_,
                       int64_t(2) * Fe * H),
               cs_));
   // a2a_dispatch_grad: input grads travel back to the token owners
@@ -479,7 +482,7 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, float* G, float* Ge, float* dh
   CU(gemm_run(grouped(E, H, 0, dlogits_, E, true, h2_, H, true, GEMM_EPI_F32, wr_part_, H,
                       wr_split_, 1, wr_gs_, wr_gr_, T, int64_t(E) * H),
               cs_));
-  CU(k_sum_partials(wr_part_, wr_split_, int64_t(E) * H, G + u.params[6].off, cs_));
+  CU(k_sum_partials(wr_part_, wr_split_, int64_t(E) * H, u.gat(G, u.params[6].off), cs_, u.gbf));
   mk("router");
   if (kept) {
     // every peer passed the dispatch_grad barrier above, so all of them are done
