@@ -329,12 +329,12 @@ int Step::alloc_acts() {
   save_acts_ = !p_.recompute_full;
   keep_mode_.assign(size_t(L), save_acts_ ? 2 : 0);
   if (!save_acts_ && ex_.selective_recompute && !moe_) {
-    // bytes one attention-kept layer adds: its q/k/v/o exchange slot + h, the
-    // sp>1 head-layout output, lse, x2, h2 and the norm statistics
+    // bytes one attention-kept layer adds: its q/k/v/o exchange slot, the
+    // sp>1 head-layout output and lse
     const size_t per_layer =
         round_up(int64_t(N * size_t(hql_) * 256), 256) + 2 * round_up(int64_t(N * size_t(hkl_) * 256), 256) +
-        round_up(int64_t(T * size_t(hq_) * 256), 256) + T * H * 2 + (p_.sp > 1 ? N * size_t(hql_) * 256 : 0) +
-        N * size_t(hql_) * 4 + T * H * 4 + T * 8 + T * H * 2;
+        round_up(int64_t(T * size_t(hq_) * 256), 256) + (p_.sp > 1 ? N * size_t(hql_) * 256 : 0) +
+        N * size_t(hql_) * 4 + 4 * 256;
     // everything else this function and the step still allocate
     const size_t F = size_t(F_), V = size_t(V_);
     const size_t chunk = size_t(std::min<int64_t>(ex_.ce_chunk, T_));
@@ -342,7 +342,7 @@ int Step::alloc_acts() {
         2 * (N * size_t(hql_) * 256 + 2 * N * size_t(hkl_) * 256 + T * size_t(hq_) * 256) +  // 2 slots
         2 * (N * size_t(hql_) * 256 + T * size_t(Wqkv_) * 2) +                               // dO, dqkv
         size_t(L + 1) * T * H * 4 +                                                           // x_saved
-        per_layer + T * 2 * F * 2 + T * F * 2 +                                               // scratch acts
+        per_layer + T * H * 12 + T * 8 + T * 2 * F * 2 + T * F * 2 +                         // scratch acts
         T * size_t(Wqkv_) * 2 + 2 * T * H * 4 + T * H * 2 + T * F * 2 + T * 2 * F * 2 +    // qkv, dx, dtmp, dxb, dact, dgu
         N * size_t(hql_) * 128 * 4 + 2 * N * size_t(hkl_) * 128 * 4 + N * size_t(hql_) * 4 +  // dq, dk, dv, delta
         size_t(k_rmsnorm_bwd_parts(T_)) * H * 4 + T * H * 2 + T * H * 4 + chunk * V * 2;    // dw_part, hf, dhf, logits
@@ -350,8 +350,16 @@ int Step::alloc_acts() {
     CU(cudaMemGetInfo(&free_b, &total_b));
     const size_t margin = size_t(6) << 30;  // NCCL, CUDA context growth, allocator slack
     int K = 0;
-    if (free_b > fixed + margin) K = int(std::min<size_t>(size_t(L), (free_b - fixed - margin) / per_layer));
+    size_t budget = free_b > fixed + margin ? free_b - fixed - margin : 0;
+    K = int(std::min<size_t>(size_t(L), budget / per_layer));
     for (int l = L - K; l < L; ++l) keep_mode_[size_t(l)] = 1;  // the backward starts at the top
+    budget -= size_t(K) * per_layer;
+    // what is left upgrades layers to keeping everything (no gate|up recompute)
+    const size_t mlp_extra = T * H * 8 + T * 8 + T * size_t(2 * F_) * 2 + T * size_t(F_) * 2 + 8 * 256;
+    for (int l = L - 1; l >= L - K && budget >= mlp_extra; --l) {
+      keep_mode_[size_t(l)] = 2;
+      budget -= mlp_extra;
+    }
   }
   const int xslots = 2 + L;
   for (int b = 0; b < xslots; ++b) {
@@ -387,7 +395,12 @@ int Step::alloc_acts() {
   d_timeout_ = alloc<int>(1);
 
   for (int l = 0; l <= L; ++l) x_saved_.push_back(alloc<float>(T * H, false));
-  auto make_acts = [&](Acts& a, bool dense_mlp) -> bool {
+  auto make_acts = [&](Acts& a, bool dense_mlp, bool lean = false) -> bool {
+    if (lean) {  // mode 1: attention state only
+      a.ofull = p_.sp > 1 ? alloc<bf16>(N * size_t(hql_) * 128, false) : nullptr;
+      a.lse = alloc<float>(N * size_t(hql_), false);
+      return a.lse && (p_.sp == 1 || a.ofull);
+    }
     a.h = alloc<bf16>(T * H, false);
     a.ofull = p_.sp > 1 ? alloc<bf16>(N * size_t(hql_) * 128, false) : nullptr;
     a.lse = alloc<float>(N * size_t(hql_), false);
@@ -405,7 +418,8 @@ int Step::alloc_acts() {
   if (!make_acts(scratch_, any_dense)) return cuda_fail(cudaErrorMemoryAllocation, "activations");
   saved_.assign(size_t(L), Acts{});
   for (int l = 0; l < L; ++l)
-    if (keeps_acts(l) && !make_acts(saved_[size_t(l)], keeps_mlp(l) && !a_.is_moe_layer(l))) {
+    if (keeps_acts(l) && !make_acts(saved_[size_t(l)], keeps_mlp(l) && !a_.is_moe_layer(l),
+                                    keep_mode_[size_t(l)] == 1)) {
       set_error("out of device memory for recompute=none activations (layer " +
                 std::to_string(l) + "); use recompute=full");
       return OPX_ERR_CUDA;
@@ -766,7 +780,17 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     bind_layer(l);
     qb = ob = 2 + l;
     if (!keeps_mlp(l) && !a_.is_moe_layer(l)) {
-      // attention-kept layer: recompute only gate|up (+ SwiGLU) from the saved h2
+      // attention-kept layer: recompute ln1 (h, for the qkv weight gradient),
+      // the output projection + residual (x2), ln2 (h2) and gate|up + SwiGLU
+      CU(k_rmsnorm_fwd(x_saved_[size_t(l)], W.ln1, h_, r1_, T, H, ex_.rms_eps, cs_));
+      {
+        GemmDesc g = gd(T, H, hq_ * 128, o_loc(ob), hq_ * 128, false, W.o, hq_ * 128, false,
+                        GEMM_EPI_F32_RESID, x2_, H);
+        g.R = x_saved_[size_t(l)];
+        g.ldr = H;
+        CU(gemm_run(g, cs_));
+      }
+      CU(k_rmsnorm_fwd(x2_, W.ln2, h2_, r2_, T, H, ex_.rms_eps, cs_));
       GemmDesc g = gd(T, 2 * F, H, h2_, H, false, W.gu, H, false, GEMM_EPI_SWIGLU, gu_, 2 * F);
       g.D2 = act_;
       g.ldd2 = F;

@@ -171,14 +171,23 @@ class Step {
   // recompute=none keeps every layer's forward activations; MoE layers keep
   // the attention activations, their routing and the combined expert outputs
   // and only re-run dispatch + gate|up in the backward (moe_bwd).
-  // per-layer: 0 = recompute the whole layer, 1 = attention activations kept
-  // (the backward recomputes only the gate|up GEMM), 2 = everything kept
+  // per-layer: 0 = recompute the whole layer, 1 = attention state kept (the
+  // backward recomputes the norms, the output projection and gate|up, not
+  // q/k/v nor attention), 2 = everything kept
   std::vector<int> keep_mode_;
   bool keeps_acts(int l) const { return keep_mode_[size_t(l)] >= 1; }
   bool keeps_mlp(int l) const { return keep_mode_[size_t(l)] == 2; }
-  void bind_layer(int l) {  // saved activations of layer l (scratch MLP buffers for mode 1)
+  // saved activations of layer l; a mode-1 layer keeps only its attention
+  // state (q/k/v/o slot, lse, head-layout output) and borrows the scratch
+  // buffers for everything its backward recomputes
+  void bind_layer(int l) {
     bind(saved_[size_t(l)]);
     if (!keeps_mlp(l)) {
+      h_ = scratch_.h;
+      h2_ = scratch_.h2;
+      x2_ = scratch_.x2;
+      r1_ = scratch_.r1;
+      r2_ = scratch_.r2;
       gu_ = scratch_.gu;
       act_ = scratch_.act;
     }
