@@ -395,27 +395,45 @@ __global__ void unpermute_kernel(const bf16* __restrict__ Y, int64_t ldy, const 
   }
 }
 
-// backward of the weighted combine:
+// backward of the weighted combine (one warp per token):
 //   dYp[pos(t,j)] = bf16(w[t,j] * dx[t]);  dw[t,j] = <dx[t], Y[pos(t,j)]>
+// dx[t] stays in registers (MAXC chunks of 256 columns, 8 per lane, 16-B accesses)
+template <int MAXC>
 __global__ void combine_bwd_kernel(const float* __restrict__ dx, const bf16* __restrict__ Y, int64_t ldy,
                                    const int* __restrict__ pos_of_pair, const float* __restrict__ wts,
                                    int T, int k, int H, bf16* __restrict__ dYp, float* __restrict__ dw) {
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
+  const int nc = H / 256;
+  float g[MAXC][8];
+#pragma unroll
+  for (int i = 0; i < MAXC; ++i) {
+    if (i >= nc) break;
+    const float* src = dx + int64_t(t) * H + i * 256 + lane * 8;
+    const float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
+    g[i][0] = a.x; g[i][1] = a.y; g[i][2] = a.z; g[i][3] = a.w;
+    g[i][4] = b.x; g[i][5] = b.y; g[i][6] = b.z; g[i][7] = b.w;
+  }
   for (int j = 0; j < k; ++j) {
     const int pos = pos_of_pair[t * k + j];
     const float wj = wts[t * k + j];
+    const bf16* yr = Y + int64_t(pos) * ldy + lane * 8;
+    bf16* dr = dYp + int64_t(pos) * ldy + lane * 8;
     float dot = 0.f;
-    for (int c = lane * 4; c < H; c += 128) {
-      const float4 g = *reinterpret_cast<const float4*>(dx + int64_t(t) * H + c);
-      const uint2 q = *reinterpret_cast<const uint2*>(Y + int64_t(pos) * ldy + c);
-      const float2 a = ptx::unpack_bf16(q.x), b = ptx::unpack_bf16(q.y);
-      dot += g.x * a.x + g.y * a.y + g.z * b.x + g.w * b.y;
-      uint2 o;
-      o.x = ptx::pack_bf16(wj * g.x, wj * g.y);
-      o.y = ptx::pack_bf16(wj * g.z, wj * g.w);
-      *reinterpret_cast<uint2*>(dYp + int64_t(pos) * ldy + c) = o;
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      if (i >= nc) break;
+      const uint4 q = *reinterpret_cast<const uint4*>(yr + i * 256);
+      const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 a = ptx::unpack_bf16(v[e]);
+        dot += g[i][2 * e] * a.x + g[i][2 * e + 1] * a.y;
+        o[e] = ptx::pack_bf16(wj * g[i][2 * e], wj * g[i][2 * e + 1]);
+      }
+      *reinterpret_cast<uint4*>(dr + i * 256) = make_uint4(o[0], o[1], o[2], o[3]);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
@@ -595,9 +613,15 @@ cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_
 cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t ldy,
                               const int* pos_of_pair, const float* wts, int T, int k, int H,
                               __nv_bfloat16* dYp, float* dw, cudaStream_t s) {
-  if (H % 128) return cudaErrorInvalidValue;
+  if (H % 256 || H > 4096) return cudaErrorInvalidValue;
   ++g_kernel_launches;
-  combine_bwd_kernel<<<(T * 32 + 255) / 256, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
+  const int blocks = (T * 32 + 255) / 256;
+  if (H <= 1024)
+    combine_bwd_kernel<4><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
+  else if (H <= 2048)
+    combine_bwd_kernel<8><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
+  else
+    combine_bwd_kernel<16><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
   return cudaGetLastError();
 }
 
