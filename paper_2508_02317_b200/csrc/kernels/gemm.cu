@@ -543,6 +543,11 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   const int nblk = (g.N + BN - 1) / BN;
   kp.band = 1;
   static const bool force_1cta = getenv("OPX_GEMM_1CTA") != nullptr;
+  // grouped-M (expert fwd / dgrad) on the 2-CTA kernel (device-side tile
+  // lists) is opt-in: on the C2 expert shapes it measured equal (dgrad, down)
+  // or slower (gate|up + SwiGLU: 0.54 vs 0.36 ms) than the 1-CTA kernel
+  static const bool grouped_2cta = getenv("OPX_GEMM_GROUPED_2CTA") != nullptr;
+  if (gm && grouped_2cta && !force_1cta && g.K % BK == 0) return gemm2_run(g, 1, s);
   if (!grouped && !force_1cta) {
     // 2-CTA path: same traffic model with 256-row pair tiles and 74 pairs per wave
     const double a_bytes = double(g.M) * g.K * 2, b_blk = 256.0 * g.K * 2;

@@ -47,10 +47,37 @@ struct P2 {
   int64_t ldd2;
   float scale;
   int* ctr;  // ticket counter (0 at launch; reset to 0 by the last ticket taker)
+  // grouped-M (MoE experts): A/D rows of group g are g_start[g] .. +g_rows[g]
+  // (128-aligned segments; a 256-row pair tile may run into the next segment,
+  // those rows are computed and masked), B is slab g of a [groups*N, K]
+  // (K-major) or [groups*K, N] (MN-major) stack
+  int groups;
+  const int* g_start;
+  const int* g_rows;
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
+__device__ __forceinline__ int ntiles_of(const P2& p) {
+  const int nblk = (p.N + BNP - 1) / BNP;
+  if (!p.groups) return ((p.M + 2 * BM - 1) / (2 * BM)) * nblk;
+  int n = 0;
+  for (int g = 0; g < p.groups; ++g) n += ((p.g_rows[g] + 2 * BM - 1) / (2 * BM)) * nblk;
+  return n;
+}
+// grouped tile t -> group, first A/D row of the pair tile, n-block
+__device__ __forceinline__ void gtile_coords(const P2& p, int t, int& g, int& row0, int& nb) {
+  const int nblk = (p.N + BNP - 1) / BNP;
+  for (g = 0; g < p.groups; ++g) {
+    const int mblk = (p.g_rows[g] + 2 * BM - 1) / (2 * BM);
+    if (t < mblk * nblk) {
+      row0 = p.g_start[g] + (t % mblk) * 2 * BM;
+      nb = t / mblk;
+      return;
+    }
+    t -= mblk * nblk;
+  }
+}
 __device__ __forceinline__ void tile_coords(const P2& p, int t, int& mb, int& nb) {
   const int mblk = (p.M + 2 * BM - 1) / (2 * BM);
   const int nblk = (p.N + BNP - 1) / BNP;
@@ -105,9 +132,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int mblk = (p.M + 2 * BM - 1) / (2 * BM);
-  const int nblk = (p.N + BNP - 1) / BNP;
-  const int ntiles = mblk * nblk;
+  const int ntiles = ntiles_of(p);
   const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
   const int nk = (p.K + BK - 1) / BK;
 
@@ -141,10 +166,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // leader: take the next ticket now, publish it after this tile's loads
         int v = 0;
         if (leader) v = atomicAdd(p.ctr, 1);
-        int mb, nb;
-        tile_coords(p, t, mb, nb);
-        const int m0 = mb * 2 * BM + int(rank) * BM;
-        const int n0 = nb * BNP + int(rank) * BNC;
+        int mb = 0, nb = 0, g = 0, row0 = 0;
+        if (p.groups) gtile_coords(p, t, g, row0, nb);
+        else tile_coords(p, t, mb, nb), row0 = mb * 2 * BM;
+        const int m0 = row0 + int(rank) * BM;
+        // grouped: B slab g sits g*N rows (K-major) / g*K k-rows (MN-major) down
+        const int n0 = nb * BNP + int(rank) * BNC + (p.groups && !B_MN ? g * p.N : 0);
+        const int kofs = p.groups && B_MN ? g * p.K : 0;
         for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
@@ -161,8 +189,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (!B_MN) {
             ptx::tma_load_2d_pair(&tmB, bar, b, k0, n0);
           } else {
-            ptx::tma_load_2d_pair(&tmB, bar, b, n0, k0);
-            ptx::tma_load_2d_pair(&tmB, bar, b + 8192, n0 + 64, k0);
+            ptx::tma_load_2d_pair(&tmB, bar, b, n0, kofs + k0);
+            ptx::tma_load_2d_pair(&tmB, bar, b + 8192, n0 + 64, kofs + k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -261,14 +289,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         qph ^= 1;
       }
       if (t >= ntiles) break;
-      int mb, nb;
-      tile_coords(p, t, mb, nb);
+      int mb = 0, nb = 0, g = 0, row0 = 0;
+      if (p.groups) gtile_coords(p, t, g, row0, nb);
+      else tile_coords(p, t, mb, nb), row0 = mb * 2 * BM;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row = mb * 2 * BM + int(rank) * BM + ew * 32 + lane;
-      const bool row_ok = row < p.M;
+      const int row = row0 + int(rank) * BM + ew * 32 + lane;
+      const bool row_ok = p.groups ? (row - p.g_start[g]) < p.g_rows[g] : row < p.M;
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + acc * BNP;
       if (p.epi == GEMM_EPI_SWIGLU) {
 #pragma unroll 1
@@ -398,12 +427,15 @@ static int* ticket_counter() {
 }
 
 cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
-  if (g.groups) return cudaErrorNotSupported;
+  const bool gm = g.groups > 0;
+  if (gm && (g.grouped_k || g.a_mn)) return cudaErrorNotSupported;
   CUtensorMap ma, mb;
-  bool ok = !g.a_mn ? gemm_make_map(&ma, g.A, uint64_t(g.K), uint64_t(g.M), g.lda, BK, BM)
+  const uint64_t a_rows = gm ? uint64_t(g.rows_total) : uint64_t(g.M);
+  bool ok = !g.a_mn ? gemm_make_map(&ma, g.A, uint64_t(g.K), a_rows, g.lda, BK, BM)
                     : gemm_make_map(&ma, g.A, uint64_t(g.M), uint64_t(g.K), g.lda, 64, BK);
-  ok = ok && (!g.b_mn ? gemm_make_map(&mb, g.B, uint64_t(g.K), uint64_t(g.N), g.ldb, BK, BNC)
-                      : gemm_make_map(&mb, g.B, uint64_t(g.N), uint64_t(g.K), g.ldb, 64, BK));
+  const uint64_t nst = gm ? uint64_t(g.groups) : 1;
+  ok = ok && (!g.b_mn ? gemm_make_map(&mb, g.B, uint64_t(g.K), nst * uint64_t(g.N), g.ldb, BK, BNC)
+                      : gemm_make_map(&mb, g.B, uint64_t(g.N), nst * uint64_t(g.K), g.ldb, 64, BK));
   if (!ok) return cudaErrorInvalidValue;
   P2 p;
   p.M = g.M;
@@ -420,7 +452,11 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   p.scale = g.scale == 0.f ? 1.f : g.scale;
   p.ctr = ticket_counter();
   if (!p.ctr) return cudaErrorMemoryAllocation;
-  const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BNP - 1) / BNP);
+  p.groups = g.groups;
+  p.g_start = g.g_start;
+  p.g_rows = g.g_rows;
+  // grouped: the tile count lives in device memory; idle clusters exit at once
+  const int tiles = gm ? num_sms() / 2 : ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BNP - 1) / BNP);
   int clusters = num_sms() / 2;
   if (tiles < clusters) clusters = tiles;
   const int grid = 2 * (clusters < 1 ? 1 : clusters);
