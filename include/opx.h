@@ -121,7 +121,9 @@ int opx_step_destroy(opx_step* st);
 /* ------------------------------------------------------------------------
  * Kernel-level entry points (device pointers, cudaStream_t as void*).
  * ------------------------------------------------------------------------ */
-/* D = A . B^T (see csrc/runtime/gemm_api.h for layouts and epilogues). */
+/* D = A . B^T (see csrc/runtime/gemm_api.h for layouts and epilogues).
+ * epi 5 (SwiGLU backward): acc = dact [M, N]; D2/ldd2 pass the forward's bf16
+ * gate|up [M, 2N] (input); D receives d(gate)|d(up) [M, 2N] in the same layout. */
 int opx_gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
              int64_t ldb, int b_mn, int epi, void* D, int64_t ldd, const float* R, int64_t ldr,
              void* D2, int64_t ldd2, float scale, void* stream);

@@ -25,6 +25,7 @@
 
 #include "../runtime/gemm_api.h"
 #include "../runtime/kernels_api.h"
+#include "epilogue.cuh"
 #include "ptx.cuh"
 
 namespace opx {
@@ -45,6 +46,8 @@ struct KParams {
   int64_t ldr;
   __nv_bfloat16* D2;
   int64_t ldd2;
+  const __nv_bfloat16* G2;  // GEMM_EPI_SWIGLU_BWD: forward gate|up
+  int64_t ldg2;
   float scale;
   // grouped
   int groups;          // 0 = plain GEMM
@@ -270,7 +273,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
       const bool empty_k = c.nk == 0;
 
-      if (p.epi == GEMM_EPI_SWIGLU) {
+      if (p.epi == GEMM_EPI_SWIGLU_BWD) {
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + ch * 32, v);
+          ptx::tmem_wait_ld();
+          const int f0 = c.nb * BN + ch * 32;
+          if (row_ok && f0 < p.N)
+            epi::swiglu_bwd32(v, p.G2 + int64_t(row) * p.ldg2,
+                              reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd, f0);
+        }
+      } else if (p.epi == GEMM_EPI_SWIGLU) {
         // Columns [0,128) of the tile are gate, [128,256) up, for features
         // nb*128 + [0,128).
 #pragma unroll 1
@@ -500,6 +514,7 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   if ((g.groups == 0 || g.grouped_k) && g.M <= 0) return cudaSuccess;
   if (g.N <= 0) return cudaSuccess;
   if (g.N % 8 != 0 || (g.epi == GEMM_EPI_SWIGLU && g.N % 256 != 0)) return cudaErrorInvalidValue;
+  if (g.epi == GEMM_EPI_SWIGLU_BWD && (g.N % 128 != 0 || !g.G2 || g.groups)) return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
   const bool grouped = g.groups > 0;
   const bool gm = grouped && !g.grouped_k;  // rows of A vary per group
@@ -531,6 +546,8 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   kp.ldr = g.ldr;
   kp.D2 = g.D2;
   kp.ldd2 = g.ldd2;
+  kp.G2 = g.G2;
+  kp.ldg2 = g.ldg2;
   kp.scale = g.scale == 0.f ? 1.f : g.scale;
   kp.groups = g.groups;
   kp.grouped_k = g.grouped_k;

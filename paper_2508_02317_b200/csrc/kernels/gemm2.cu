@@ -21,6 +21,7 @@
 
 #include "../runtime/gemm_api.h"
 #include "../runtime/kernels_api.h"
+#include "epilogue.cuh"
 #include "ptx.cuh"
 
 namespace opx {
@@ -45,6 +46,8 @@ struct P2 {
   int64_t ldr;
   __nv_bfloat16* D2;
   int64_t ldd2;
+  const __nv_bfloat16* G2;
+  int64_t ldg2;
   float scale;
   int* ctr;  // ticket counter (0 at launch; reset to 0 by the last ticket taker)
   // grouped-M (MoE experts): A/D rows of group g are g_start[g] .. +g_rows[g]
@@ -299,7 +302,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int row = row0 + int(rank) * BM + ew * 32 + lane;
       const bool row_ok = p.groups ? (row - p.g_start[g]) < p.g_rows[g] : row < p.M;
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + acc * BNP;
-      if (p.epi == GEMM_EPI_SWIGLU) {
+      if (p.epi == GEMM_EPI_SWIGLU_BWD) {
+#pragma unroll 1
+        for (int ch = 0; ch < BNP / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + ch * 32, v);
+          ptx::tmem_wait_ld();
+          const int f0 = nb * BNP + ch * 32;
+          if (row_ok && f0 < p.N)
+            epi::swiglu_bwd32(v, p.G2 + int64_t(row) * p.ldg2,
+                              reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd, f0);
+        }
+      } else if (p.epi == GEMM_EPI_SWIGLU) {
 #pragma unroll 1
         for (int ch = 0; ch < 4; ++ch) {
           uint32_t g[32], u[32];
@@ -449,6 +463,8 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   p.ldr = g.ldr;
   p.D2 = g.D2;
   p.ldd2 = g.ldd2;
+  p.G2 = g.G2;
+  p.ldg2 = g.ldg2;
   p.scale = g.scale == 0.f ? 1.f : g.scale;
   p.ctr = ticket_counter();
   if (!p.ctr) return cudaErrorMemoryAllocation;

@@ -206,8 +206,13 @@ int opx_gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const vo
   g.ldd = ldd;
   g.R = R;
   g.ldr = ldr;
-  g.D2 = static_cast<__nv_bfloat16*>(D2);
-  g.ldd2 = ldd2;
+  if (epi == GEMM_EPI_SWIGLU_BWD) {  // D2/ldd2 carry the forward gate|up (an input)
+    g.G2 = static_cast<const __nv_bfloat16*>(D2);
+    g.ldg2 = ldd2;
+  } else {
+    g.D2 = static_cast<__nv_bfloat16*>(D2);
+    g.ldd2 = ldd2;
+  }
   g.scale = scale;
   cudaError_t e = gemm_run(g, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? OPX_OK : cuda_fail(e, "opx_gemm");

@@ -12,6 +12,9 @@ enum GemmEpi : int {
   GEMM_EPI_F32_RESID = 2,  // D(f32)  = R + acc*scale   (R may alias D)
   GEMM_EPI_F32_ACCUM = 3,  // D(f32) += acc*scale
   GEMM_EPI_SWIGLU = 4,     // D2(bf16)[., N/2] = silu(gate)*up; D (optional) = bf16 gate|up
+  // acc = dact[., N] (N = F); G2 = the forward's bf16 gate|up [., 2N] (128-col
+  // interleave); D(bf16)[., 2N] = d(gate)|d(up) of silu(gate)*up, same layout
+  GEMM_EPI_SWIGLU_BWD = 5,
 };
 
 // D[M,N] = A . B^T with
@@ -39,6 +42,8 @@ struct GemmDesc {
   int64_t ldr = 0;
   __nv_bfloat16* D2 = nullptr;
   int64_t ldd2 = 0;
+  const __nv_bfloat16* G2 = nullptr;  // GEMM_EPI_SWIGLU_BWD input
+  int64_t ldg2 = 0;
   float scale = 1.f;
   int groups = 0;
   int grouped_k = 0;

@@ -836,6 +836,9 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
       e0 = e1;
     };
     CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
+    // (GEMM_EPI_SWIGLU_BWD fuses the next kernel into this GEMM's epilogue, but
+    // its sigmoid/expf work made the epilogue outlast the mainloop: 172 ms vs
+    // 89 + 32 ms unfused per C1 step on one GPU, so the step keeps them apart)
     CU(gemm_run(gd(T, F, H, dxb_, H, false, W.down, F, true, GEMM_EPI_BF16, dact_, F), cs_));
     sub("dgrad_down");
     CU(gemm_run(gd(H, F, T, dxb_, H, true, act_, F, true, EPI_G, g_down, F), cs_));

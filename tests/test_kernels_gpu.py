@@ -185,6 +185,25 @@ def test_swiglu_bwd():
     assert rel_err(dv[:, :, 1].reshape(T, F), u.grad) < 1e-2
 
 
+@gpu
+def test_gemm_swiglu_bwd_epilogue():
+    """dact = dY . Wd with the SwiGLU backward fused in the epilogue matches the
+    unfused kernel applied to a torch-computed dact (up to accumulation order)."""
+    torch.manual_seed(4)
+    T, F, H = 384, 512, 256
+    dy = bf(torch.randn(T, H, device=DEV))
+    wd = bf(torch.randn(H, F, device=DEV) * 0.05)   # [K=H rows, N=F cols]: B MN-major
+    gu = bf(torch.randn(T, 2 * F, device=DEV))
+    dgu = torch.empty_like(gu)
+    call("opx_gemm", T, F, H, P(dy), H, 0, P(wd), F, 1, 5, P(dgu), 2 * F, None, 0, P(gu), 2 * F, 1.0, S())
+    dact = bf(dy.float() @ wd.float())
+    ref = torch.empty_like(gu)
+    call("opx_swiglu_bwd", P(dact), P(gu), P(ref), T, F, S())
+    torch.cuda.synchronize()
+    assert rel_err(dgu, ref) < 1e-2
+    assert (dgu.float() - ref.float()).abs().max().item() <= 0.02 * ref.float().abs().max().item()
+
+
 # ---------------------------------------------------------------- AdamW
 @gpu
 def test_adamw():
