@@ -35,7 +35,8 @@ QWEN2_72B_SLICE = {"layers": 8, "hidden": 8192, "heads": 64, "kv_heads": 8, "hea
 QWEN3_30B_A3B = {"layers": 48, "hidden": 2048, "heads": 16, "kv_heads": 4, "head_dim": 128,
                  "ffn_dim": 6144, "vocab": 151936,
                  "moe": {"num_experts": 128, "top_k": 8, "expert_ffn_dim": 768, "moe_layer_stride": 1}}
-TINY = {"layers": 2, "hidden": 256, "heads": 2, "kv_heads": 2, "head_dim": 128, "ffn_dim": 768,
+# C0: 2 layers, H=256, 4 heads of 64, 2 kv heads, ffn 768, V=2048, S=1024
+TINY = {"layers": 2, "hidden": 256, "heads": 4, "kv_heads": 2, "head_dim": 64, "ffn_dim": 768,
         "vocab": 2048}
 
 
@@ -59,7 +60,8 @@ def plan_for(cfg: str, n: int) -> dict:
         # redoes gate|up only
         return {"dp_replicate": 1, "dp_shard": n, "sp": 1, "ep": n, "micro_batch": 1,
                 "recompute": "none", "fsdp_prefetch_depth": 1}
-    return {"dp_replicate": 1, "dp_shard": n, "sp": 1, "ep": 1, "micro_batch": 1,
+    sp = 2 if n % 2 == 0 else 1  # C0: FSDP2 x SP2 at 4 GPUs
+    return {"dp_replicate": 1, "dp_shard": n // sp, "sp": sp, "ep": 1, "micro_batch": 1,
             "recompute": "full", "fsdp_prefetch_depth": 1}
 
 

@@ -23,12 +23,17 @@ namespace opx {
 namespace {
 
 using bf16 = __nv_bfloat16;
-constexpr int D = 128, HALF = 64;
+// The head layout always has 128-element head vectors; a model head_dim hd < 128
+// (multiple of 16) occupies the first hd elements and the rest stays zero (the
+// buffers are zeroed once and never written there), so the attention kernels
+// run unchanged at d = 128 with the softmax scale of hd.
+constexpr int D = 128;
 
 // Each thread moves 8 elements of the first half and the matching 8 of the
 // second half of one head vector (so RoPE pairs stay in one thread).
 __global__ void seq2head_kernel(const A2AArgs a) {
-  const int per_tok = 8;  // threads per head vector
+  const int hd = a.hd ? a.hd : D, HALF = hd / 2;
+  const int per_tok = hd / 16;  // threads per head vector
   int heads = 0;
   for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total;
   const int T = a.rows * (a.seq / a.sp);
@@ -48,7 +53,7 @@ __global__ void seq2head_kernel(const A2AArgs a) {
     const int b = r / S_loc, p = r % S_loc;
     const int64_t gtok = int64_t(b) * a.seq + int64_t(a.rank) * S_loc + p;
 
-    const bf16* s = src + int64_t(r) * a.local_ld + G.col0 + hh * D + c8 * 8;
+    const bf16* s = src + int64_t(r) * a.local_ld + G.col0 + hh * hd + c8 * 8;
     uint4 lo = *reinterpret_cast<const uint4*>(s);
     uint4 hi = *reinterpret_cast<const uint4*>(s + HALF);
     if (G.rope) {
@@ -72,7 +77,8 @@ __global__ void seq2head_kernel(const A2AArgs a) {
 }
 
 __global__ void head2seq_kernel(const A2AArgs a) {
-  const int per_tok = 8;
+  const int hd = a.hd ? a.hd : D, HALF = hd / 2;
+  const int per_tok = hd / 16;
   int heads_loc = 0;  // heads held by this rank across groups
   for (int i = 0; i < a.ngroups; ++i) heads_loc += a.g[i].heads_total / a.sp;
   const int64_t Ntok = int64_t(a.rows) * a.seq;
@@ -133,7 +139,7 @@ __global__ void head2seq_kernel(const A2AArgs a) {
     }
     const int hglob = a.rank * per_rank + hh;  // head index within the group
     bf16* d = reinterpret_cast<bf16*>(a.local[dst_rank]) + int64_t(r) * a.local_ld + G.col0 +
-              hglob * D + c8 * 8;
+              hglob * hd + c8 * 8;
     *reinterpret_cast<uint4*>(d) = lo;
     *reinterpret_cast<uint4*>(d + HALF) = hi;
   }

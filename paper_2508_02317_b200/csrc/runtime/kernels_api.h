@@ -93,7 +93,8 @@ struct A2AArgs {
                                    // head->seq: per-rank destination [rows*S/sp, width]
   int64_t local_ld;                // row stride (elements) of the local [tokens, width] buffers
   const int* pos;                  // [rows*S] position ids (global token index)
-  const float* inv_freq;           // [64]
+  const float* inv_freq;           // [hd/2]
+  int hd = 0;                      // model head_dim (0 = 128); <= 128, multiple of 16
 };
 cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s);
 cudaError_t k_a2a_head2seq(const A2AArgs& a, cudaStream_t s);

@@ -125,10 +125,14 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
     return OPX_ERR_CONFIG;
   }
   a_ = *f->arch;
-  if (a_.head_dim != 128 || a_.hidden % 128 || a_.ffn % 128) {
-    set_error("executor requires head_dim == 128 and hidden, ffn multiples of 128");
+  if (a_.head_dim > 128 || a_.head_dim % 16 || a_.hidden % 128 || a_.ffn % 128) {
+    set_error("executor requires head_dim <= 128 (multiple of 16) and hidden, ffn multiples of 128");
     return OPX_ERR_CONFIG;
   }
+  d_ = int(a_.head_dim);
+  // attention runs on 128-wide zero-padded head vectors; a relayout between the
+  // local [T, heads*d] rows and the head layout is needed for SP or d < 128
+  relay_ = p.sp > 1 || d_ != 128;
   if (p.sp > kMaxSp) {
     set_error("sp > 8 is not supported (one NVSwitch domain)");
     return OPX_ERR_CONFIG;
@@ -192,7 +196,7 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
   hk_ = int(a_.kv_heads);
   hql_ = hq_ / sp;
   hkl_ = hk_ / sp;
-  Wqkv_ = (hq_ + 2 * hk_) * 128;
+  Wqkv_ = (hq_ + 2 * hk_) * d_;
   F_ = int(a_.ffn);
   V_ = int(a_.vocab);
   nslots_ = int(std::max<int64_t>(p.prefetch_depth, 0)) + 1;
@@ -272,10 +276,10 @@ int Step::build_units() {
     u.name = "layer" + std::to_string(l);
     u.gbf = ex_.bf16_grads;
     add(u, p + "input_layernorm.weight", {H}, true);
-    add(u, p + "self_attn.q_proj.weight", {int64_t(hq_) * 128, H}, false);
-    add(u, p + "self_attn.k_proj.weight", {int64_t(hk_) * 128, H}, false);
-    add(u, p + "self_attn.v_proj.weight", {int64_t(hk_) * 128, H}, false);
-    add(u, p + "self_attn.o_proj.weight", {H, int64_t(hq_) * 128}, false);
+    add(u, p + "self_attn.q_proj.weight", {int64_t(hq_) * d_, H}, false);
+    add(u, p + "self_attn.k_proj.weight", {int64_t(hk_) * d_, H}, false);
+    add(u, p + "self_attn.v_proj.weight", {int64_t(hk_) * d_, H}, false);
+    add(u, p + "self_attn.o_proj.weight", {H, int64_t(hq_) * d_}, false);
     add(u, p + "post_attention_layernorm.weight", {H}, true);
     if (a_.is_moe_layer(l)) {
       add(u, p + "mlp.gate.weight", {int64_t(a_.moe->experts), H}, false);
@@ -333,7 +337,7 @@ int Step::alloc_acts() {
     // sp>1 head-layout output and lse
     const size_t per_layer =
         round_up(int64_t(N * size_t(hql_) * 256), 256) + 2 * round_up(int64_t(N * size_t(hkl_) * 256), 256) +
-        round_up(int64_t(T * size_t(hq_) * 256), 256) + (p_.sp > 1 ? N * size_t(hql_) * 256 : 0) +
+        round_up(int64_t(T * size_t(hq_) * 256), 256) + (relay_ ? N * size_t(hql_) * 256 : 0) +
         N * size_t(hql_) * 4 + 4 * 256;
     // everything else this function and the step still allocate
     const size_t F = size_t(F_), V = size_t(V_);
@@ -397,12 +401,12 @@ int Step::alloc_acts() {
   for (int l = 0; l <= L; ++l) x_saved_.push_back(alloc<float>(T * H, false));
   auto make_acts = [&](Acts& a, bool dense_mlp, bool lean = false) -> bool {
     if (lean) {  // mode 1: attention state only
-      a.ofull = p_.sp > 1 ? alloc<bf16>(N * size_t(hql_) * 128, false) : nullptr;
+      a.ofull = relay_ ? alloc<bf16>(N * size_t(hql_) * 128, false) : nullptr;
       a.lse = alloc<float>(N * size_t(hql_), false);
-      return a.lse && (p_.sp == 1 || a.ofull);
+      return a.lse && (!relay_ || a.ofull);
     }
     a.h = alloc<bf16>(T * H, false);
-    a.ofull = p_.sp > 1 ? alloc<bf16>(N * size_t(hql_) * 128, false) : nullptr;
+    a.ofull = relay_ ? alloc<bf16>(N * size_t(hql_) * 128, false) : nullptr;
     a.lse = alloc<float>(N * size_t(hql_), false);
     a.x2 = alloc<float>(T * H, false);
     a.r1 = alloc<float>(T, false);
@@ -411,7 +415,7 @@ int Step::alloc_acts() {
     a.gu = dense_mlp ? alloc<bf16>(T * size_t(2 * F_), false) : nullptr;
     a.act = dense_mlp ? alloc<bf16>(T * size_t(F_), false) : nullptr;
     return a.h && a.lse && a.x2 && a.h2 && (!dense_mlp || (a.gu && a.act)) &&
-           (p_.sp == 1 || a.ofull);
+           (!relay_ || a.ofull);
   };
   bool any_dense = false;
   for (int l = 0; l < L; ++l) any_dense = any_dense || !a_.is_moe_layer(l);
@@ -452,8 +456,8 @@ int Step::alloc_acts() {
   for (void* q : {(void*)h_, (void*)logits_, (void*)dq_acc_, (void*)d_inv_freq_, (void*)x2_})
     if (!q) return cuda_fail(cudaErrorMemoryAllocation, "activations");
   std::vector<float> inv(64);
-  for (int i = 0; i < 64; ++i)
-    inv[size_t(i)] = float(1.0 / std::pow(ex_.rope_theta, double(2 * i) / 128.0));
+  for (int i = 0; i < 64; ++i)  // RoPE over head_dim d: theta^(-2i/d), i < d/2
+    inv[size_t(i)] = i < d_ / 2 ? float(1.0 / std::pow(ex_.rope_theta, double(2 * i) / double(d_))) : 0.f;
   CU(cudaMemcpy(d_inv_freq_, inv.data(), 64 * sizeof(float), cudaMemcpyHostToDevice));
   if (moe_) TRY(moe_alloc());
   if (p_.sp == 1) {  // no peers: flags point at ourselves
@@ -651,10 +655,10 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.g[0].col0 = 0;
     a.g[0].rope = 1;
     a.g[1].heads_total = hk_;
-    a.g[1].col0 = hq_ * 128;
+    a.g[1].col0 = hq_ * d_;
     a.g[1].rope = 1;
     a.g[2].heads_total = hk_;
-    a.g[2].col0 = (hq_ + hk_) * 128;
+    a.g[2].col0 = (hq_ + hk_) * d_;
     a.g[2].rope = 0;
     for (int j = 0; j < int(p_.sp); ++j) {
       a.g[0].full[j] = peer(j, off_q_[qb]);
@@ -665,6 +669,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.local_ld = Wqkv_;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
+    a.hd = d_;
     if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
     TRY(barrier_sp(cs_));
   }
@@ -674,7 +679,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     mark(pre + ".a2a_qkv", ph, 0, e0, e1);
     e0 = e1;
   }
-  bf16* attn_out = p_.sp == 1 ? o_loc(ob) : ofull_;
+  bf16* attn_out = relay_ ? ofull_ : o_loc(ob);
   {
     AttnArgs a{};
     a.q = q_full(qb);
@@ -690,7 +695,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.N = Ntok_;
     a.hq = hql_;
     a.hk = hkl_;
-    a.scale = 1.0f / std::sqrt(128.0f);
+    a.scale = 1.0f / std::sqrt(float(d_));
     CU(k_attn_fwd_tc(a, cs_));
   }
   if (tr) {
@@ -699,7 +704,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     mark(pre + ".attn_core", ph, 0, e0, e1);
     e0 = e1;
   }
-  if (p_.sp > 1) {
+  if (relay_) {
     A2AArgs a{};
     a.sp = int(p_.sp);
     a.rank = sp_i_;
@@ -709,9 +714,10 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.g[0].heads_total = hq_;
     a.g[0].full[0] = ofull_;
     for (int j = 0; j < int(p_.sp); ++j) a.local[j] = peer(j, off_o_[ob]);
-    a.local_ld = hq_ * 128;
+    a.local_ld = hq_ * d_;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
+    a.hd = d_;
     if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
     TRY(barrier_sp(cs_));
     if (tr) {
@@ -722,7 +728,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     }
   }
   {
-    GemmDesc g = gd(T, H, hq_ * 128, o_loc(ob), hq_ * 128, false, W.o, hq_ * 128, false,
+    GemmDesc g = gd(T, H, hq_ * d_, o_loc(ob), hq_ * d_, false, W.o, hq_ * d_, false,
                     GEMM_EPI_F32_RESID, x2_, H);
     g.R = x_in;
     g.ldr = H;
@@ -767,7 +773,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
 }
 
 int Step::layer_bwd(int l, Unit& u, void* G) {
-  const int T = T_, H = H_, F = F_, Q = hq_ * 128;
+  const int T = T_, H = H_, F = F_, Q = hq_ * d_;
   const LayerW W = layer_w(u, u.full);
   const bool tr = ex_.trace;
   const std::string pre = "bwd.layer" + std::to_string(l) + ".m0";
@@ -784,7 +790,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
       // the output projection + residual (x2), ln2 (h2) and gate|up + SwiGLU
       CU(k_rmsnorm_fwd(x_saved_[size_t(l)], W.ln1, h_, r1_, T, H, ex_.rms_eps, cs_));
       {
-        GemmDesc g = gd(T, H, hq_ * 128, o_loc(ob), hq_ * 128, false, W.o, hq_ * 128, false,
+        GemmDesc g = gd(T, H, hq_ * d_, o_loc(ob), hq_ * d_, false, W.o, hq_ * d_, false,
                         GEMM_EPI_F32_RESID, x2_, H);
         g.R = x_saved_[size_t(l)];
         g.ldr = H;
@@ -862,9 +868,9 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
   CU(k_cast_f32_bf16(dx_, dxb_, int64_t(T) * H, cs_));
   const int db = xdo_;
   xdo_ ^= 1;
-  bf16* do_loc = p_.sp == 1 ? do_full(db) : ofull_ + 0;  // see below for sp > 1
+  bf16* do_loc = relay_ ? ofull_ + 0 : do_full(db);  // see below when relaying
   bf16* do_scratch = nullptr;
-  if (p_.sp > 1) {
+  if (relay_) {
     // ofull_ still holds the attention output needed by attn_bwd: use dact_
     // (dead after the MLP backward, >= T*hq*128 elements) as the local dO.
     do_scratch = dact_;
@@ -872,7 +878,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
   }
   CU(gemm_run(gd(T, Q, H, dxb_, H, false, W.o, Q, true, GEMM_EPI_BF16, do_loc, Q), cs_));
   CU(gemm_run(gd(H, Q, T, dxb_, H, true, o_loc(ob), Q, true, EPI_G, g_o, Q), cs_));
-  if (p_.sp > 1) {
+  if (relay_) {
     A2AArgs a{};
     a.sp = int(p_.sp);
     a.rank = sp_i_;
@@ -885,6 +891,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.local_ld = Q;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
+    a.hd = d_;
     if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
     TRY(barrier_sp(cs_));
   }
@@ -900,7 +907,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.q = q_full(qb);
     a.k = k_full(qb);
     a.v = v_full(qb);
-    a.o = p_.sp == 1 ? o_loc(ob) : ofull_;
+    a.o = relay_ ? ofull_ : o_loc(ob);
     a.lse = lse_;
     a.ldq = hql_ * 128;
     a.ldk = a.ldv = hkl_ * 128;
@@ -910,7 +917,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.N = Ntok_;
     a.hq = hql_;
     a.hk = hkl_;
-    a.scale = 1.0f / std::sqrt(128.0f);
+    a.scale = 1.0f / std::sqrt(float(d_));
     a.dout = do_full(db);
     a.lddo = hql_ * 128;
     a.dq_acc = dq_acc_;
@@ -936,12 +943,13 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.seq = S_;
     a.ngroups = 3;
     a.g[0] = A2AGroup{hq_, 0, 1, 1, {dq_acc_}};
-    a.g[1] = A2AGroup{hk_, hq_ * 128, 1, 1, {dk_}};
-    a.g[2] = A2AGroup{hk_, (hq_ + hk_) * 128, 0, 1, {dv_}};
+    a.g[1] = A2AGroup{hk_, hq_ * d_, 1, 1, {dk_}};
+    a.g[2] = A2AGroup{hk_, (hq_ + hk_) * d_, 0, 1, {dv_}};
     for (int j = 0; j < int(p_.sp); ++j) a.local[j] = peer(j, off_dqkv_[xb]);
     a.local_ld = Wqkv_;
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
+    a.hd = d_;
     if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
     TRY(barrier_sp(cs_));
   }

@@ -111,6 +111,7 @@ class Step {
   int rep_i_ = 0, shard_i_ = 0, sp_i_ = 0;
   std::vector<int64_t> sp_members_, shard_members_, rep_members_;
   int rows_ = 1, S_ = 1, S_loc_ = 1, T_ = 1, Ntok_ = 1;
+  bool relay_ = false;  // head-layout relayout needed (sp > 1 or head_dim < 128)
   int H_ = 0, d_ = 128, hq_ = 0, hk_ = 0, hql_ = 0, hkl_ = 0, Wqkv_ = 0, F_ = 0, V_ = 0;
   int step_count_ = 0;
   int64_t n_valid_ = 1;

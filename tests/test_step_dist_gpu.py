@@ -94,6 +94,21 @@ def test_dist_moe_step_matches_oracle(world, plan, rows):
 
 
 @gpu
+def test_dist_c0_fsdp2_sp2_head_dim_64():
+    """BASELINE C0 as specified: 2 layers, H=256, 4 heads of 64 (2 kv),
+    ffn 768, V=2048, S=1024, FSDP2 x SP2 on 4 GPUs, global batch 2."""
+    if NGPU < 4:
+        pytest.skip("needs 4 GPUs")
+    model = tiny_dense(layers=2, hidden=256, heads=4, kv=2, ffn=768, vocab=2048)
+    plan = {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 1, "micro_batch": 1}
+    loss, sessions = _run(4, model, plan, 1024, 2)
+    from paper_2508_02317_b200.runtime import synthetic_batch
+
+    batch = synthetic_batch(2048, 1024, 2, seed=2508)
+    compare_step(sessions, model, batch, plan, loss)
+
+
+@gpu
 @pytest.mark.parametrize("world,plan,rows", PLANS)
 def test_dist_step_matches_oracle(world, plan, rows):
     if NGPU < world:

@@ -109,3 +109,15 @@ def test_step_ffd_packed_batch_with_padding():
     r = s.run()
     compare_step([s], model, batch, plan, r.loss)
     s.close()
+
+
+@gpu
+@pytest.mark.parametrize("hidden,heads,kv", [(256, 4, 2), (640, 8, 2)])
+def test_step_head_dim_below_128(hidden, heads, kv):
+    """head_dim 64 (the SURVEY C0 shape: H=256, 4 heads, 2 kv heads) and 80
+    (the omni-modal ViT's): attention runs on zero-padded 128-wide head vectors
+    with the 1/sqrt(d) scale; RoPE rotates over d."""
+    model = tiny_dense(layers=2, hidden=hidden, heads=heads, kv=kv, ffn=768, vocab=2048)
+    s, batch, plan, r = _run(model, 1024, 2)
+    compare_step([s], model, batch, plan, r.loss)
+    s.close()
