@@ -59,7 +59,8 @@ def plan_for(cfg: str, n: int) -> dict:
         # outputs (~0.6 GB/layer at 8K tokens); the backward re-sends tokens and
         # redoes gate|up only
         return {"dp_replicate": 1, "dp_shard": n, "sp": 1, "ep": n, "micro_batch": 1,
-                "recompute": "none", "fsdp_prefetch_depth": 1}
+                "recompute": "none", "fsdp_prefetch_depth": 1,
+                "moe_overlap": os.environ.get("OPX_BENCH_MOE_OVERLAP", "1") == "1"}
     sp = 2 if n % 2 == 0 else 1  # C0: FSDP2 x SP2 at 4 GPUs
     return {"dp_replicate": 1, "dp_shard": n // sp, "sp": sp, "ep": 1, "micro_batch": 1,
             "recompute": "full", "fsdp_prefetch_depth": 1}

@@ -317,7 +317,7 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
                                 const int* __restrict__ pair_at, int P, int k,
                                 const int* __restrict__ counts_all, const int* __restrict__ excl,
                                 Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst,
-                                int W) {
+                                int W, int le_lo, int le_hi) {
   extern __shared__ int st[];  // [ep][El+1] segment starts of every destination rank
   if (threadIdx.x < L.ep) {
     const int d = threadIdx.x;
@@ -341,6 +341,7 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
     }
     const int e = lo;
     const int d = e / L.El, le = e % L.El;
+    if (le < le_lo || le >= le_hi) continue;  // another phase's experts (moe_overlap)
     int before = 0;
     for (int s = 0; s < me; ++s) before += counts_all[s * L.E + e];
     const int row = st[d * (L.El + 1) + le] + before + (pos - excl[e]);
@@ -355,9 +356,9 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
 __global__ void combine_kernel(const bf16* __restrict__ src, int64_t ld_src,
                                const int* __restrict__ counts_all, Layout L, int me,
                                const int* __restrict__ g_start, bf16* const* __restrict__ dst,
-                               int64_t ld_dst, int W) {
+                               int64_t ld_dst, int W, int le_lo) {
   const int lane = threadIdx.x & 31;
-  const int le = blockIdx.y;
+  const int le = le_lo + blockIdx.y;
   const int e = me * L.El + le;
   const int n = seg_len(counts_all, L, e);
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
@@ -575,8 +576,9 @@ cudaError_t k_moe_zero_pad(__nv_bfloat16* buf, int64_t ld, int W, const int* g_s
 cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pair,
                            const int* pair_at, int P, int k, const int* counts_all,
                            const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
-                           int64_t ld_dst, int W, cudaStream_t s) {
+                           int64_t ld_dst, int W, cudaStream_t s, int le_lo, int le_hi) {
   Layout L{ep, E, E / ep};
+  if (le_hi < 0) le_hi = L.El;
   const int smem = ep * (L.El + 1) * int(sizeof(int));
   static const int max_blocks = getenv("OPX_A2A_BLOCKS") ? atoi(getenv("OPX_A2A_BLOCKS")) : num_sms() * 8;
   int blocks = (P * 32 + 255) / 256;
@@ -584,20 +586,24 @@ cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pai
   if (blocks < 1) blocks = 1;
   ++g_kernel_launches;
   dispatch_kernel<<<blocks, 256, smem, s>>>(src, ld_src, per_pair, pair_at, P, k, counts_all,
-                                            excl, L, me, dst, ld_dst, W);
+                                            excl, L, me, dst, ld_dst, W, le_lo, le_hi);
   return cudaGetLastError();
 }
 
 cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* counts_all, int ep,
                           int E, int me, const int* g_start, __nv_bfloat16* const* dst,
-                          int64_t ld_dst, int W, int max_rows, cudaStream_t s) {
+                          int64_t ld_dst, int W, int max_rows, cudaStream_t s, int le_lo,
+                          int le_n) {
   Layout L{ep, E, E / ep};
   static const int max_bx = getenv("OPX_COMBINE_BX") ? atoi(getenv("OPX_COMBINE_BX")) : 64;
   int bx = (max_rows * 32 + 255) / 256 / L.El + 1;
   if (bx > max_bx) bx = max_bx;
-  dim3 grid(bx, L.El);
+  if (le_n < 0) le_n = L.El - le_lo;
+  if (le_n <= 0) return cudaSuccess;
+  dim3 grid(bx, le_n);
   ++g_kernel_launches;
-  combine_kernel<<<grid, 256, 0, s>>>(src, ld_src, counts_all, L, me, g_start, dst, ld_dst, W);
+  combine_kernel<<<grid, 256, 0, s>>>(src, ld_src, counts_all, L, me, g_start, dst, ld_dst, W,
+                                      le_lo);
   return cudaGetLastError();
 }
 

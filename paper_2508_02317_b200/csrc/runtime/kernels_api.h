@@ -120,10 +120,11 @@ cudaError_t k_moe_zero_pad(__nv_bfloat16* buf, int64_t ld, int W, const int* g_s
 cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pair,
                            const int* pair_at, int P, int k, const int* counts_all,
                            const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
-                           int64_t ld_dst, int W, cudaStream_t s);
+                           int64_t ld_dst, int W, cudaStream_t s, int le_lo = 0, int le_hi = -1);
 cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* counts_all, int ep,
                           int E, int me, const int* g_start, __nv_bfloat16* const* dst,
-                          int64_t ld_dst, int W, int max_rows, cudaStream_t s);
+                          int64_t ld_dst, int W, int max_rows, cudaStream_t s, int le_lo = 0,
+                          int le_n = -1);
 cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_of_pair,
                             const float* wts, int T, int k, int H, const float* resid, float* out,
                             cudaStream_t s);

@@ -70,6 +70,7 @@ Step::~Step() {
   if (ms_) cudaStreamSynchronize(ms_);
   if (os_) cudaStreamSynchronize(os_);
   if (xs_) cudaStreamSynchronize(xs_);
+  if (xs2_) cudaStreamSynchronize(xs2_);
   for (size_t r = 0; r < peer_arena_.size(); ++r)
     if (peer_arena_[r] && peer_arena_[r] != arena_) cudaIpcCloseMemHandle(peer_arena_[r]);
   for (void* p : allocs_) cudaFree(p);
@@ -87,6 +88,7 @@ Step::~Step() {
   if (ms_) cudaStreamDestroy(ms_);
   if (os_) cudaStreamDestroy(os_);
   if (xs_) cudaStreamDestroy(xs_);
+  if (xs2_) cudaStreamDestroy(xs2_);
   for (auto e : ev_redisp_)
     if (e) cudaEventDestroy(e);
 }

@@ -279,6 +279,13 @@ class Step {
   size_t off_flags_ep2_ = 0;
   uint32_t** d_ep_flags2_ = nullptr;
   uint32_t epoch_ep2_ = 0;
+  // moe_overlap: the second expert half of the forward runs on xs2_ with its own
+  // barrier flag set
+  cudaStream_t xs2_ = nullptr;
+  size_t off_flags_ep3_ = 0;
+  uint32_t** d_ep_flags3_ = nullptr;
+  uint32_t epoch_ep3_ = 0;
+  int barrier_ep3(cudaStream_t s);
   std::vector<cudaEvent_t> ev_redisp_;  // [layer]
   int moe_redispatch(int l);            // issue on xs_ after the caller's cs_ point
   int next_moe_below(int l) const {

@@ -135,6 +135,7 @@ size_t Step::moe_arena(size_t off) {
   cap_rows_ = int64_t(P) * ep_ + int64_t(El_) * 128;
   off_flags_ep_ = take(64 * sizeof(uint32_t));
   off_flags_ep2_ = take(64 * sizeof(uint32_t));
+  off_flags_ep3_ = take(64 * sizeof(uint32_t));
   const int L = int(a_.layers);
   const int nslots = save_acts_ ? 1 + L : 1;
   off_counts_s_.assign(size_t(nslots), 0);
@@ -185,6 +186,12 @@ int Step::moe_alloc() {
   dlogits_ = alloc<bf16>(T * E, false);
   d_ep_flags_ = alloc<uint32_t*>(kMaxSp);
   d_ep_flags2_ = alloc<uint32_t*>(kMaxSp);
+  d_ep_flags3_ = alloc<uint32_t*>(kMaxSp);
+  if (p_.moe_overlap && ep_ > 1) {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&xs2_, cudaStreamNonBlocking, hi));
+  }
   if (save_acts_) {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -242,12 +249,14 @@ void Step::moe_bind(int l) {
 
 int Step::moe_import() {
   const size_t ns = routes_.size();
-  std::vector<void*> fl(kMaxSp, nullptr), fl2(kMaxSp, nullptr), ct(kMaxSp * ns, nullptr),
+  std::vector<void*> fl(kMaxSp, nullptr), fl2(kMaxSp, nullptr), fl3(kMaxSp, nullptr),
+      ct(kMaxSp * ns, nullptr),
       xr(kMaxSp, nullptr),
       yb(kMaxSp * ns, nullptr), dy(kMaxSp, nullptr), dx(kMaxSp, nullptr);
   for (int j = 0; j < ep_; ++j) {
     fl[size_t(j)] = ep_peer(j, off_flags_ep_);
     fl2[size_t(j)] = ep_peer(j, off_flags_ep2_);
+    fl3[size_t(j)] = ep_peer(j, off_flags_ep3_);
     for (size_t sl = 0; sl < ns; ++sl) {
       ct[sl * kMaxSp + size_t(j)] = ep_peer(j, off_counts_s_[sl]);
       yb[sl * kMaxSp + size_t(j)] = ep_peer(j, off_yback_s_[sl]);
@@ -259,6 +268,7 @@ int Step::moe_import() {
   const size_t b = kMaxSp * sizeof(void*);
   CU(cudaMemcpy(d_ep_flags_, fl.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_ep_flags2_, fl2.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_ep_flags3_, fl3.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_count_tables_, ct.data(), b * ns, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_xrecv_peers_, xr.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_yback_peers_, yb.data(), b * ns, cudaMemcpyHostToDevice));
@@ -288,6 +298,14 @@ int Step::moe_redispatch(int l) {
     mark("bwd.layer" + std::to_string(l) + ".m0.a2a_redispatch", "bwd.layer" + std::to_string(l), 3,
          a, b);
   }
+  return OPX_OK;
+}
+
+int Step::barrier_ep3(cudaStream_t s) {
+  if (ep_ == 1) return OPX_OK;
+  ++epoch_ep3_;
+  CU(k_peer_barrier(d_ep_flags3_, reinterpret_cast<uint32_t*>(arena_ + off_flags_ep3_), ep_, ep_i_,
+                    epoch_ep3_, d_timeout_, s));
   return OPX_OK;
 }
 
@@ -357,31 +375,89 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   TRY(barrier_ep(cs_));
   CU(k_moe_groups(counts_all, ep_, E, ep_i_, g_start_, g_rows_, g_rows_pad_, g_total_, cs_));
   mk("a2a_counts");
-  CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                    d_xrecv_peers_, H, H, cs_));
-  mk("a2a_dispatch");
-  TRY(barrier_ep(cs_));
-  mk("a2a_wait");
-  CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
-  {
-    // gate|up pre-activations are only needed by the backward (recompute pass)
-    GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu, H, false, GEMM_EPI_SWIGLU,
-                         in_recompute_ ? gu_e_ : nullptr, 2 * Fe, El_, 0, g_start_, g_rows_,
-                         cap_rows_, 0);
-    g.D2 = act_e_;
-    g.ldd2 = Fe;
-    CU(gemm_run(g, cs_));
+  // experts [lo, hi) of every rank: dispatch -> barrier -> gate|up + SwiGLU ->
+  // down -> combine -> barrier, on stream st with barrier flag set `fs`
+  auto phase = [&](int lo, int hi, cudaStream_t st, int fs, bool marks) -> int {
+    CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                      d_xrecv_peers_, H, H, st, lo, hi));
+    if (marks) mk("a2a_dispatch");
+    TRY(fs ? barrier_ep3(st) : barrier_ep(st));
+    if (marks) mk("a2a_wait");
+    const int n = hi - lo;
+    CU(k_moe_zero_pad(xrecv, H, H, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
+    {
+      // gate|up pre-activations are only needed by the backward (recompute pass)
+      GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu + int64_t(lo) * 2 * Fe * H, H, false,
+                           GEMM_EPI_SWIGLU, in_recompute_ ? gu_e_ : nullptr, 2 * Fe, n, 0,
+                           g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
+      g.D2 = act_e_;
+      g.ldd2 = Fe;
+      CU(gemm_run(g, st));
+    }
+    CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
+    CU(gemm_run(grouped(0, H, Fe, act_e_, Fe, false, Wd + int64_t(lo) * H * Fe, Fe, false,
+                        GEMM_EPI_BF16, y_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0),
+                st));
+    if (marks) mk("experts");
+    CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
+                     int(cap_rows_), st, lo, n));
+    if (marks) mk("a2a_combine");
+    TRY(fs ? barrier_ep3(st) : barrier_ep(st));
+    if (marks) mk("a2a_wait");
+    return OPX_OK;
+  };
+  if (p_.moe_overlap && ep_ > 1 && El_ >= 2 && xs2_) {
+    // moe_overlap (plan.hpp): two expert halves pipelined on two streams so the
+    // second half's dispatch overlaps the first half's GEMMs and the first
+    // half's combine overlaps the second half's GEMMs (expert GEMMs of the two
+    // halves are serialised with an event)
+    const int h = El_ / 2;
+    cudaEvent_t ready = ev(), gemm_a = ev(), done_b = ev();
+    CU(cudaEventRecord(ready, cs_));
+    CU(cudaStreamWaitEvent(xs2_, ready, 0));
+    // half B: dispatch, then its GEMMs after half A's
+    CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                      d_xrecv_peers_, H, H, xs2_, h, El_));
+    TRY(barrier_ep3(xs2_));
+    // half A on the compute stream
+    CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                      d_xrecv_peers_, H, H, cs_, 0, h));
+    mk("a2a_dispatch");
+    TRY(barrier_ep(cs_));
+    mk("a2a_wait");
+    auto experts = [&](int lo, int hi, cudaStream_t st) -> int {
+      const int n = hi - lo;
+      CU(k_moe_zero_pad(xrecv, H, H, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
+      GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu + int64_t(lo) * 2 * Fe * H, H, false,
+                           GEMM_EPI_SWIGLU, in_recompute_ ? gu_e_ : nullptr, 2 * Fe, n, 0,
+                           g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
+      g.D2 = act_e_;
+      g.ldd2 = Fe;
+      CU(gemm_run(g, st));
+      CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
+      CU(gemm_run(grouped(0, H, Fe, act_e_, Fe, false, Wd + int64_t(lo) * H * Fe, Fe, false,
+                          GEMM_EPI_BF16, y_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0),
+                  st));
+      return OPX_OK;
+    };
+    TRY(experts(0, h, cs_));
+    CU(cudaEventRecord(gemm_a, cs_));
+    mk("experts");
+    CU(cudaStreamWaitEvent(xs2_, gemm_a, 0));
+    TRY(experts(h, El_, xs2_));
+    CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
+                     int(cap_rows_), xs2_, h, El_ - h));
+    TRY(barrier_ep3(xs2_));
+    CU(cudaEventRecord(done_b, xs2_));
+    CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
+                     int(cap_rows_), cs_, 0, h));
+    mk("a2a_combine");
+    TRY(barrier_ep(cs_));
+    CU(cudaStreamWaitEvent(cs_, done_b, 0));
+    mk("a2a_wait");
+  } else {
+    TRY(phase(0, El_, cs_, 0, true));
   }
-  CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_, g_rows_, g_rows_pad_, El_, cs_));
-  CU(gemm_run(grouped(0, H, Fe, act_e_, Fe, false, Wd, Fe, false, GEMM_EPI_BF16, y_e_, H, El_, 0,
-                      g_start_, g_rows_, cap_rows_, 0),
-              cs_));
-  mk("experts");
-  CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
-                   int(cap_rows_), cs_));
-  mk("a2a_combine");
-  TRY(barrier_ep(cs_));
-  mk("a2a_wait");
   CU(k_moe_unpermute(yback, H, r_pos_, r_wts_, T, k, H, x2, x_out, cs_));
   mk("unpermute");
   return OPX_OK;

@@ -43,6 +43,15 @@ def tiny_dense(layers=2, hidden=256, heads=2, kv=2, ffn=768, vocab=2048):
                      "head_dim": hidden // heads, "ffn_dim": ffn, "vocab": vocab}}]}
 
 
+def free_port() -> int:
+    """A TCP port nothing listens on right now (the OS picks it)."""
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 EXEC = {"seed": 2508, "lr": 1e-4, "betas": [0.9, 0.95], "eps": 1e-8, "weight_decay": 0.1}
 
 TOL_LOSS = 1e-3   # relative, north_star

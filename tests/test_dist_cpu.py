@@ -6,6 +6,8 @@ import multiprocessing as mp
 import os
 import random
 
+from tests.step_common import free_port
+
 import numpy as np
 
 from paper_2508_02317_b200.plan import resolve
@@ -61,7 +63,7 @@ def _worker(rank, world, port, q):
 def test_gloo_world2_host_logic():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = random.randint(30000, 45000)
+    port = free_port()
     ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in ps:
         p.start()

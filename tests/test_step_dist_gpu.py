@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.step_common import compare_step, tiny_dense
+from tests.step_common import compare_step, free_port, tiny_dense
 
 gpu = pytest.mark.gpu
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
@@ -28,6 +28,32 @@ class _Remote:
         return self.out[("route", layer)]
 
 
+def _collect(q, ps, world, timeout=600):
+    """Gather every worker's result; fail fast if a worker dies without one
+    (a dead rank would otherwise leave its peers waiting in a collective)."""
+    import queue
+    import time
+
+    res, t0 = {}, time.time()
+    while len(res) < world:
+        try:
+            rank, loss, out, err = q.get(timeout=5)
+        except queue.Empty:
+            dead = [p.exitcode for p in ps if p.exitcode not in (None, 0)]
+            if dead:
+                for p in ps:
+                    if p.is_alive():
+                        p.kill()
+                raise AssertionError(f"worker exited with {dead} before reporting")
+            assert time.time() - t0 < timeout, "workers timed out"
+            continue
+        assert err is None, err
+        res[rank] = (loss, out)
+    for p in ps:
+        p.join(60)
+    return res
+
+
 def _run(world, model, plan, S, rows):
     from oracle import model as om
 
@@ -37,20 +63,14 @@ def _run(world, model, plan, S, rows):
     names = gpu_param_names(arch)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = random.randint(20000, 40000)
+    port = free_port()
     from tests.dist_worker import step_worker
 
     ps = [ctx.Process(target=step_worker, args=(r, world, port, model, plan, S, rows, q, names))
           for r in range(world)]
     for p in ps:
         p.start()
-    res = {}
-    for _ in range(world):
-        rank, loss, out, err = q.get(timeout=600)
-        assert err is None, err
-        res[rank] = (loss, out)
-    for p in ps:
-        p.join(60)
+    res = _collect(q, ps, world)
     losses = {round(v[0], 6) for v in res.values()}
     assert len(losses) == 1, losses  # every rank reports the same global loss
     return res[0][0], [_Remote(res[r][1]) for r in range(world)]
@@ -73,6 +93,9 @@ MOE_PLANS = [
     (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 4, "micro_batch": 1}, 2),
     (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "recompute": "none"}, 2),
     (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 4, "micro_batch": 1, "recompute": "none"}, 2),
+    (4, {"dp_replicate": 1, "dp_shard": 4, "sp": 1, "ep": 4, "micro_batch": 1, "recompute": "none",
+         "moe_overlap": True}, 4),
+    (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "moe_overlap": True}, 2),
 ]
 
 
@@ -142,19 +165,13 @@ def test_checkpoint_reshard_fsdp2_to_1(tmp_path):
     plan2 = {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 1, "micro_batch": 1}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = random.randint(20000, 40000)
+    port = free_port()
     a = str(tmp_path / "fsdp2")
     ps = [ctx.Process(target=ckpt_worker, args=(r, 2, port, model, plan2, S, rows, q, names, a))
           for r in range(2)]
     for p in ps:
         p.start()
-    res = {}
-    for _ in range(2):
-        rank, loss, out, err = q.get(timeout=600)
-        assert err is None, err
-        res[rank] = (loss, out)
-    for p in ps:
-        p.join(60)
+    res = _collect(q, ps, 2)
     b = str(tmp_path / "fsdp1")
     checkpoint.reshard(a, b, dp_shard=1, sp=1)
 
