@@ -100,6 +100,35 @@ def mlp_traffic(cfg: str, T_loc: int):
     return t["mlp_node_dram_bytes"] * T_loc / t["tokens"]
 
 
+def nvlink_rates(trace, plan, arch, S):
+    """Achieved per-GPU NVLink bytes/s of the all-to-all kernels (bytes that
+    leave the rank, (P-1)/P of the payload, comm.cpp:8-22) over their traced
+    device time, against 900 GB/s per direction."""
+    T = plan["micro_batch"] * S // plan["sp"]
+    H, kvw = arch["hidden"], arch["kv_heads"] * arch["head_dim"]
+    out = {"peak_GBps_per_direction": 900.0}
+    nodes = {}
+    for e in trace["traceEvents"]:
+        if e.get("tid", 0) != 0 or ".m0." not in e["name"]:
+            continue
+        key = e["name"].split(".", 1)[0] + "." + e["name"].split(".m0.")[-1]
+        nodes.setdefault(key, []).append(e["dur"] * 1e-6)
+    sp, ep = plan["sp"], plan.get("ep", 1)
+    if sp > 1:
+        frac = (sp - 1) / sp
+        qkv = T * (H + 2 * kvw) * 2 * frac
+        for key, b in (("fwd.a2a_qkv", qkv), ("fwd.a2a_out", T * H * 2 * frac)):
+            if key in nodes:
+                out[key.split(".")[1] + "_GBps"] = round(b * len(nodes[key]) / sum(nodes[key]) / 1e9, 1)
+    if ep > 1 and "moe" in arch:
+        frac = (ep - 1) / ep
+        b = T * arch["moe"]["top_k"] * H * 2 * frac
+        for key in ("fwd.a2a_dispatch", "fwd.a2a_combine", "bwd.a2a_combine_grad", "bwd.a2a_dispatch_grad"):
+            if key in nodes:
+                out[key.split(".")[1] + "_GBps"] = round(b * len(nodes[key]) / sum(nodes[key]) / 1e9, 1)
+    return out
+
+
 def calibration(trace, plan, model, wl, n, step_s):
     """the reference simulator's constants (compute_efficiency,
     intra-node bandwidth) fitted to this run's trace (paper_2508_02317_b200.calibrate)."""
@@ -394,6 +423,7 @@ def main():
         "node_ms": {k: round(v * 1e3, 2) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:24]},
         "clocks": clk.summary(),
         "calibration": calibration(trace, plan, model, wl, n, t_mean),
+        "nvlink": nvlink_rates(trace, plan, arch, S),
         "host_enqueue_ms": statistics.mean(enq) * 1e3, "host_cpus": os.cpu_count(),
         "hbm_free_gb": torch.cuda.mem_get_info(local)[0] / 1e9,
     }
