@@ -64,8 +64,14 @@ __global__ void seq2head_kernel(const A2AArgs a) {
       for (int e = 0; e < 4; ++e) {
         const float2 x1 = ptx::unpack_bf16(l[e]), x2 = ptx::unpack_bf16(h[e]);
         float sn0, cs0, sn1, cs1;
-        sincosf(pos * a.inv_freq[c8 * 8 + 2 * e], &sn0, &cs0);
-        sincosf(pos * a.inv_freq[c8 * 8 + 2 * e + 1], &sn1, &cs1);
+        if (a.rope_tab) {  // precomputed sincosf(pos * inv_freq[i]) (identical values)
+          const float2* t = a.rope_tab + int64_t(a.pos[gtok]) * HALF + c8 * 8 + 2 * e;
+          const float4 v = *reinterpret_cast<const float4*>(t);
+          sn0 = v.x; cs0 = v.y; sn1 = v.z; cs1 = v.w;
+        } else {
+          sincosf(pos * a.inv_freq[c8 * 8 + 2 * e], &sn0, &cs0);
+          sincosf(pos * a.inv_freq[c8 * 8 + 2 * e + 1], &sn1, &cs1);
+        }
         l[e] = ptx::pack_bf16(x1.x * cs0 - x2.x * sn0, x1.y * cs1 - x2.y * sn1);
         h[e] = ptx::pack_bf16(x2.x * cs0 + x1.x * sn0, x2.y * cs1 + x1.y * sn1);
       }
@@ -122,7 +128,13 @@ __global__ void head2seq_kernel(const A2AArgs a) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         float sn, cs;
-        sincosf(pos * a.inv_freq[c8 * 8 + e], &sn, &cs);
+        if (a.rope_tab) {
+          const float2 v = a.rope_tab[int64_t(a.pos[gtok]) * HALF + c8 * 8 + e];
+          sn = v.x;
+          cs = v.y;
+        } else {
+          sincosf(pos * a.inv_freq[c8 * 8 + e], &sn, &cs);
+        }
         const float y1 = x1[e] * cs + x2[e] * sn;
         const float y2 = x2[e] * cs - x1[e] * sn;
         x1[e] = y1;
@@ -161,7 +173,25 @@ __global__ void peer_barrier_kernel(uint32_t* const* peer_flags, uint32_t* my_fl
   __threadfence_system();
 }
 
+__global__ void rope_table_kernel(float2* tab, int npos, int half, const float* inv_freq) {
+  const int64_t n = int64_t(npos) * half;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float pos = float(i / half);
+    float sn, cs;
+    sincosf(pos * inv_freq[i % half], &sn, &cs);
+    tab[i] = make_float2(sn, cs);
+  }
+}
+
 }  // namespace
+
+cudaError_t k_rope_table(float2* tab, int npos, int half, const float* inv_freq, cudaStream_t s) {
+  if (npos <= 0) return cudaSuccess;
+  ++g_kernel_launches;
+  rope_table_kernel<<<num_sms() * 4, 256, 0, s>>>(tab, npos, half, inv_freq);
+  return cudaGetLastError();
+}
 
 cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s) {
   int heads = 0;

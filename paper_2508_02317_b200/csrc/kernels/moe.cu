@@ -318,7 +318,11 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
                                 const int* __restrict__ counts_all, const int* __restrict__ excl,
                                 Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst,
                                 int W, int le_lo, int le_hi) {
-  extern __shared__ int st[];  // [ep][El+1] segment starts of every destination rank
+  // smem: [ep][El+1] segment starts of every destination rank, then per expert
+  // this rank's sorted offset (excl) and the rows earlier ranks put before ours
+  extern __shared__ int st[];
+  int* sx = st + L.ep * (L.El + 1);
+  int* sb = sx + L.E;
   if (threadIdx.x < L.ep) {
     const int d = threadIdx.x;
     int run = 0;
@@ -327,6 +331,12 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
       run += (seg_len(counts_all, L, d * L.El + le) + 127) / 128 * 128;
     }
     st[d * (L.El + 1) + L.El] = run;
+  }
+  for (int e = threadIdx.x; e < L.E; e += blockDim.x) {
+    sx[e] = excl[e];
+    int before = 0;
+    for (int s = 0; s < me; ++s) before += counts_all[s * L.E + e];
+    sb[e] = before;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -337,14 +347,12 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
     int lo = 0, hi = L.E - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (excl[mid] <= pos) lo = mid; else hi = mid - 1;
+      if (sx[mid] <= pos) lo = mid; else hi = mid - 1;
     }
     const int e = lo;
     const int d = e / L.El, le = e % L.El;
     if (le < le_lo || le >= le_hi) continue;  // another phase's experts (moe_overlap)
-    int before = 0;
-    for (int s = 0; s < me; ++s) before += counts_all[s * L.E + e];
-    const int row = st[d * (L.El + 1) + le] + before + (pos - excl[e]);
+    const int row = st[d * (L.El + 1) + le] + sb[e] + (pos - sx[e]);
     const bf16* s = src + int64_t(per_pair ? pos : p / k) * ld_src;
     bf16* o = dst[d] + int64_t(row) * ld_dst;
     copy_row(o, s, W, lane);
@@ -579,7 +587,7 @@ cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pai
                            int64_t ld_dst, int W, cudaStream_t s, int le_lo, int le_hi) {
   Layout L{ep, E, E / ep};
   if (le_hi < 0) le_hi = L.El;
-  const int smem = ep * (L.El + 1) * int(sizeof(int));
+  const int smem = (ep * (L.El + 1) + 2 * E) * int(sizeof(int));
   static const int max_blocks = getenv("OPX_A2A_BLOCKS") ? atoi(getenv("OPX_A2A_BLOCKS")) : num_sms() * 8;
   int blocks = (P * 32 + 255) / 256;
   if (blocks > max_blocks) blocks = max_blocks;

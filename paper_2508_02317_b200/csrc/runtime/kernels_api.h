@@ -95,7 +95,11 @@ struct A2AArgs {
   const int* pos;                  // [rows*S] position ids (global token index)
   const float* inv_freq;           // [hd/2]
   int hd = 0;                      // model head_dim (0 = 128); <= 128, multiple of 16
+  const float2* rope_tab = nullptr;  // optional [positions][hd/2] (sin, cos) table
 };
+// (sin, cos)(pos * inv_freq[i]) for pos < npos, i < half: the a2a kernels' RoPE
+// table (computed with the same sincosf, so results are unchanged)
+cudaError_t k_rope_table(float2* tab, int npos, int half, const float* inv_freq, cudaStream_t s);
 cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s);
 cudaError_t k_a2a_head2seq(const A2AArgs& a, cudaStream_t s);
 // Peer barrier: signal every peer then wait until every peer reached `epoch`.

@@ -461,6 +461,12 @@ int Step::alloc_acts() {
   for (int i = 0; i < 64; ++i)  // RoPE over head_dim d: theta^(-2i/d), i < d/2
     inv[size_t(i)] = i < d_ / 2 ? float(1.0 / std::pow(ex_.rope_theta, double(2 * i) / double(d_))) : 0.f;
   CU(cudaMemcpy(d_inv_freq_, inv.data(), 64 * sizeof(float), cudaMemcpyHostToDevice));
+  // RoPE (sin, cos) per position id (< S) and frequency, once: the exchange
+  // kernels read it instead of evaluating sincosf per element
+  d_rope_ = alloc<float2>(size_t(S_) * size_t(d_ / 2), false);
+  if (!d_rope_) return cuda_fail(cudaErrorMemoryAllocation, "rope table");
+  CU(k_rope_table(d_rope_, S_, d_ / 2, d_inv_freq_, cs_));
+  CU(cudaStreamSynchronize(cs_));
   if (moe_) TRY(moe_alloc());
   if (p_.sp == 1) {  // no peers: flags point at ourselves
     uint32_t* f = reinterpret_cast<uint32_t*>(arena_ + off_flags_);
@@ -561,6 +567,13 @@ int Step::load_batch(const int32_t* ids, const int32_t* labels, const int32_t* p
   n_valid_ = std::max<int64_t>(n_valid, 1);
   CU(cudaMemcpyAsync(d_ids_, ids, size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaMemcpyAsync(d_labels_, labels, size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
+  // the RoPE table covers position ids [0, S); other ids use per-element sincosf
+  rope_tab_ok_ = true;
+  for (int64_t i = 0; i < Ntok_; ++i)
+    if (pos[i] < 0 || pos[i] >= S_) {
+      rope_tab_ok_ = false;
+      break;
+    }
   CU(cudaMemcpyAsync(d_pos_, pos, size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaMemcpyAsync(d_sstart_, st.data(), size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaMemcpyAsync(d_send_, en.data(), size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
@@ -672,6 +685,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
     a.hd = d_;
+    a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
     TRY(barrier_sp(cs_));
   }
@@ -720,6 +734,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
     a.hd = d_;
+    a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
     TRY(barrier_sp(cs_));
     if (tr) {
@@ -894,6 +909,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
     a.hd = d_;
+    a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
     TRY(barrier_sp(cs_));
   }
@@ -952,6 +968,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.pos = d_pos_;
     a.inv_freq = d_inv_freq_;
     a.hd = d_;
+    a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
     TRY(barrier_sp(cs_));
   }

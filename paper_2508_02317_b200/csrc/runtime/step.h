@@ -210,6 +210,8 @@ class Step {
   }
   bool store_gu_ = false;
   std::vector<float*> x_saved_;  // layer inputs [L+1][T,H] fp32 (x_saved_[L] = final)
+  float2* d_rope_ = nullptr;  // [S][d/2] (sin, cos)
+  bool rope_tab_ok_ = true;   // every position id of the batch is < S
   bf16 *h_ = nullptr, *qkv_ = nullptr, *ofull_ = nullptr, *h2_ = nullptr, *gu_ = nullptr,
        *act_ = nullptr;
   float *x2_ = nullptr, *r1_ = nullptr, *r2_ = nullptr, *lse_ = nullptr;
