@@ -125,8 +125,9 @@ def nvlink_rates(trace, plan, arch, S):
         b = T * arch["moe"]["top_k"] * H * 2 * frac
         for key in ("fwd.a2a_dispatch", "fwd.a2a_combine", "bwd.a2a_combine_grad", "bwd.a2a_dispatch_grad"):
             if key in nodes:
-                # moe_overlap: the traced forward nodes carry the first expert half
-                bk = b / 2 if (plan.get("moe_overlap") and key.startswith("fwd")) else b
+                # moe_overlap: the traced nodes carry the first expert half (the
+                # second half's exchange runs concurrently on another stream)
+                bk = b / 2 if plan.get("moe_overlap") else b
                 out[key.replace(".", "_") + "_GBps"] = round(bk * len(nodes[key]) / sum(nodes[key]) / 1e9, 1)
     return out
 

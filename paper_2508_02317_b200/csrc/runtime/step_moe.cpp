@@ -505,36 +505,76 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
   CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
   // a2a_combine_grad: pair grads travel to the expert ranks (same layout as dispatch)
   mk("combine_bwd");
-  CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                    d_dyrecv_peers_, H, H, cs_));
-  mk("a2a_combine_grad");
-  TRY(barrier_ep(cs_));
-  mk("a2a_wait");
-  CU(k_moe_zero_pad(dyrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
-  // experts backward (grouped GEMMs; wgrad K = 128-padded segment rows)
-  CU(gemm_run(grouped(0, Fe, H, dyrecv, H, false, Wd, Fe, true, GEMM_EPI_BF16, dact_e_, Fe, El_, 0,
-                      g_start_, g_rows_, cap_rows_, 0),
-              cs_));
-  CU(gemm_run(grouped(H, Fe, 0, dyrecv, H, true, act_e_, Fe, true, eu.gbf ? GEMM_EPI_BF16 : GEMM_EPI_F32,
-                      eu.gat(Ge, eu.params[1].off), Fe, El_, 1, g_start_, g_rows_pad_, cap_rows_,
-                      int64_t(H) * Fe),
-              cs_));
-  CU(k_moe_swiglu_bwd(dact_e_, gu_e_, dgu_e_, g_start_, g_rows_, g_rows_pad_, El_, Fe,
-                      int(cap_rows_), cs_));
-  CU(gemm_run(grouped(0, H, 2 * Fe, dgu_e_, 2 * Fe, false, Wgu, H, true, GEMM_EPI_BF16, dx_e_, H,
-                      El_, 0, g_start_, g_rows_, cap_rows_, 0),
-              cs_));
-  CU(gemm_run(grouped(2 * Fe, H, 0, dgu_e_, 2 * Fe, true, xrecv, H, true,
-                      eu.gbf ? GEMM_EPI_BF16 : GEMM_EPI_F32, eu.gat(Ge, eu.params[0].off), H, El_, 1, g_start_, g_rows_pad_, cap_rows_,
-                      int64_t(2) * Fe * H),
-              cs_));
-  // a2a_dispatch_grad: input grads travel back to the token owners
-  mk("experts");
-  CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
-                   int(cap_rows_), cs_));
-  mk("a2a_dispatch_grad");
-  TRY(barrier_ep(cs_));
-  mk("a2a_wait");
+  // experts [lo, hi): zero-pad, dgrad/wgrad of down, SwiGLU backward,
+  // dgrad/wgrad of gate|up (wgrad K = 128-padded segment rows)
+  auto experts_bwd = [&](int lo, int hi, cudaStream_t st) -> int {
+    const int n = hi - lo;
+    const int64_t gs_d = int64_t(H) * Fe, gs_gu = int64_t(2) * Fe * H;  // slab sizes
+    const int epi_w = eu.gbf ? GEMM_EPI_BF16 : GEMM_EPI_F32;
+    CU(k_moe_zero_pad(dyrecv, H, H, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
+    CU(gemm_run(grouped(0, Fe, H, dyrecv, H, false, Wd + lo * gs_d, Fe, true, GEMM_EPI_BF16, dact_e_,
+                        Fe, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0),
+                st));
+    CU(gemm_run(grouped(H, Fe, 0, dyrecv, H, true, act_e_, Fe, true, epi_w,
+                        eu.gat(Ge, eu.params[1].off + lo * gs_d), Fe, n, 1, g_start_ + lo,
+                        g_rows_pad_ + lo, cap_rows_, gs_d),
+                st));
+    CU(k_moe_swiglu_bwd(dact_e_, gu_e_, dgu_e_, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, Fe,
+                        int(cap_rows_), st));
+    CU(gemm_run(grouped(0, H, 2 * Fe, dgu_e_, 2 * Fe, false, Wgu + lo * gs_gu, H, true, GEMM_EPI_BF16,
+                        dx_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0),
+                st));
+    CU(gemm_run(grouped(2 * Fe, H, 0, dgu_e_, 2 * Fe, true, xrecv, H, true, epi_w,
+                        eu.gat(Ge, eu.params[0].off + lo * gs_gu), H, n, 1, g_start_ + lo,
+                        g_rows_pad_ + lo, cap_rows_, gs_gu),
+                st));
+    return OPX_OK;
+  };
+  if (p_.moe_overlap && ep_ > 1 && El_ >= 2 && xs2_) {
+    // moe_overlap: the second expert half's dY dispatch overlaps the first
+    // half's expert backward, and the first half's dX combine the second's
+    const int h = El_ / 2;
+    cudaEvent_t ready = ev(), done_a = ev(), done_b = ev();
+    CU(cudaEventRecord(ready, cs_));
+    CU(cudaStreamWaitEvent(xs2_, ready, 0));
+    CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                      d_dyrecv_peers_, H, H, xs2_, h, El_));
+    TRY(barrier_ep3(xs2_));
+    CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                      d_dyrecv_peers_, H, H, cs_, 0, h));
+    mk("a2a_combine_grad");
+    TRY(barrier_ep(cs_));
+    mk("a2a_wait");
+    TRY(experts_bwd(0, h, cs_));
+    CU(cudaEventRecord(done_a, cs_));
+    mk("experts");
+    CU(cudaStreamWaitEvent(xs2_, done_a, 0));
+    TRY(experts_bwd(h, El_, xs2_));
+    CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
+                     int(cap_rows_), xs2_, h, El_ - h));
+    TRY(barrier_ep3(xs2_));
+    CU(cudaEventRecord(done_b, xs2_));
+    CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
+                     int(cap_rows_), cs_, 0, h));
+    mk("a2a_dispatch_grad");
+    TRY(barrier_ep(cs_));
+    CU(cudaStreamWaitEvent(cs_, done_b, 0));
+    mk("a2a_wait");
+  } else {
+    CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                      d_dyrecv_peers_, H, H, cs_));
+    mk("a2a_combine_grad");
+    TRY(barrier_ep(cs_));
+    mk("a2a_wait");
+    TRY(experts_bwd(0, El_, cs_));
+    // a2a_dispatch_grad: input grads travel back to the token owners
+    mk("experts");
+    CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
+                     int(cap_rows_), cs_));
+    mk("a2a_dispatch_grad");
+    TRY(barrier_ep(cs_));
+    mk("a2a_wait");
+  }
   CU(k_moe_unpermute(dxback, H, r_pos_, nullptr, T, k, H, nullptr, dh2, cs_));
   // router: renormalised-softmax backward, then dh2 += dlogits . Wr, dWr = dlogits^T h2
   CU(k_moe_router_bwd(r_dw_, r_wts_, r_idx_, T, k, E, dlogits_, cs_));
