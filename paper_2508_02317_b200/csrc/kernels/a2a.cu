@@ -16,6 +16,8 @@
 // consumer kernels on the other GPUs.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "../runtime/kernels_api.h"
 #include "ptx.cuh"
 
@@ -37,13 +39,14 @@ __global__ void seq2head_kernel(const A2AArgs a) {
   int heads = 0;
   for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total;
   const int T = a.rows * (a.seq / a.sp);
-  const int64_t total = int64_t(T) * heads * per_tok;
+  const int work = heads * per_tok;  // threads per token
   const bf16* src = reinterpret_cast<const bf16*>(a.local[0]);
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int c8 = int(idx % per_tok);
-    int hh = int((idx / per_tok) % heads);
-    const int r = int(idx / (int64_t(per_tok) * heads));
+  // blockDim.y tokens per block, threadIdx.x over (head, chunk) of one token:
+  // no 64-bit index arithmetic (it made the kernel instruction-bound)
+  for (int r = blockIdx.x * blockDim.y + threadIdx.y; r < T; r += gridDim.x * blockDim.y)
+  for (int w = threadIdx.x; w < work; w += blockDim.x) {
+    const int c8 = w % per_tok;
+    int hh = w / per_tok;
     int gi = 0;
     while (hh >= a.g[gi].heads_total) hh -= a.g[gi++].heads_total;
     const A2AGroup& G = a.g[gi];
@@ -87,19 +90,19 @@ __global__ void head2seq_kernel(const A2AArgs a) {
   const int per_tok = hd / 16;
   int heads_loc = 0;  // heads held by this rank across groups
   for (int i = 0; i < a.ngroups; ++i) heads_loc += a.g[i].heads_total / a.sp;
-  const int64_t Ntok = int64_t(a.rows) * a.seq;
-  const int64_t total = Ntok * heads_loc * per_tok;
+  const int Ntok = a.rows * a.seq;
+  const int work = heads_loc * per_tok;
   const int S_loc = a.seq / a.sp;
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int c8 = int(idx % per_tok);
-    int hh = int((idx / per_tok) % heads_loc);
-    const int64_t gtok = idx / (int64_t(per_tok) * heads_loc);
+  for (int gt = blockIdx.x * blockDim.y + threadIdx.y; gt < Ntok; gt += gridDim.x * blockDim.y)
+  for (int w = threadIdx.x; w < work; w += blockDim.x) {
+    const int c8 = w % per_tok;
+    int hh = w / per_tok;
+    const int64_t gtok = gt;
     int gi = 0;
     while (hh >= a.g[gi].heads_total / a.sp) hh -= a.g[gi++].heads_total / a.sp;
     const A2AGroup& G = a.g[gi];
     const int per_rank = G.heads_total / a.sp;
-    const int b = int(gtok / a.seq), sp_pos = int(gtok % a.seq);
+    const int b = gt / a.seq, sp_pos = gt % a.seq;
     const int dst_rank = sp_pos / S_loc;
     const int r = b * S_loc + sp_pos % S_loc;
     float x1[8], x2[8];
@@ -193,27 +196,36 @@ cudaError_t k_rope_table(float2* tab, int npos, int half, const float* inv_freq,
   return cudaGetLastError();
 }
 
+// block shape for `work` threads per token: x = work rounded to a warp
+// (<= 1024), y = tokens per block so a block has ~256 threads
+static dim3 a2a_block(int work) {
+  const int x = std::min(1024, (work + 31) / 32 * 32);
+  return dim3(x, std::max(1, 256 / x));
+}
+
 cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s) {
   int heads = 0;
   for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total;
-  const int64_t n = int64_t(a.rows) * (a.seq / a.sp) * heads * 8;
-  if (n <= 0) return cudaSuccess;
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  const int T = a.rows * (a.seq / a.sp);
+  const int hd = a.hd ? a.hd : D;
+  if (T <= 0 || heads <= 0) return cudaSuccess;
+  const dim3 blk = a2a_block(heads * (hd / 16));
+  const int blocks = std::min((T + int(blk.y) - 1) / int(blk.y), num_sms() * 32);
   ++g_kernel_launches;
-  seq2head_kernel<<<int(blocks), 256, 0, s>>>(a);
+  seq2head_kernel<<<blocks, blk, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t k_a2a_head2seq(const A2AArgs& a, cudaStream_t s) {
   int heads = 0;
   for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total / a.sp;
-  const int64_t n = int64_t(a.rows) * a.seq * heads * 8;
-  if (n <= 0) return cudaSuccess;
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  const int N = a.rows * a.seq;
+  const int hd = a.hd ? a.hd : D;
+  if (N <= 0 || heads <= 0) return cudaSuccess;
+  const dim3 blk = a2a_block(heads * (hd / 16));
+  const int blocks = std::min((N + int(blk.y) - 1) / int(blk.y), num_sms() * 32);
   ++g_kernel_launches;
-  head2seq_kernel<<<int(blocks), 256, 0, s>>>(a);
+  head2seq_kernel<<<blocks, blk, 0, s>>>(a);
   return cudaGetLastError();
 }
 
