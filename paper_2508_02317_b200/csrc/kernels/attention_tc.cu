@@ -60,10 +60,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   // 1024-B alignment by pointer arithmetic on the __shared__ array keeps the
   // shared address space (no generic LD/ST on the hot path).
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sQ[2] = {smem, smem + TILE_BYTES};
-  uint8_t* sK[2] = {smem + 2 * TILE_BYTES, smem + 3 * TILE_BYTES};
+  // tile addresses by arithmetic, not by runtime-indexed arrays (those went to
+  // the stack and turned the P stores into generic ST.E)
+  auto sQ = [&](int i) { return smem + i * TILE_BYTES; };
+  auto sK = [&](int i) { return smem + (2 + i) * TILE_BYTES; };
   uint8_t* sV = smem + 4 * TILE_BYTES;
-  uint8_t* sP[2] = {smem + 5 * TILE_BYTES, smem + 6 * TILE_BYTES};
+  auto sP = [&](int i) { return smem + (5 + i) * TILE_BYTES; };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 7 * TILE_BYTES);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;   // [2]
@@ -107,23 +109,23 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t TS[2] = {tmem, tmem + 128};
-  const uint32_t TO[2] = {tmem + 256, tmem + 384};
+  auto TS = [&](int i) { return tmem + uint32_t(i) * 128; };
+  auto TO = [&](int i) { return tmem + 256 + uint32_t(i) * 128; };
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       ptx::mbar_expect_tx(q_full, 2 * TILE_BYTES);
-      ptx::tma_load_3d(&tq, q_full, sQ[0], 0, h, q0);
-      ptx::tma_load_3d(&tq, q_full, sQ[0] + 16384, 64, h, q0);
-      ptx::tma_load_3d(&tq, q_full, sQ[1], 0, h, q0 + BM);
-      ptx::tma_load_3d(&tq, q_full, sQ[1] + 16384, 64, h, q0 + BM);
+      ptx::tma_load_3d(&tq, q_full, sQ(0), 0, h, q0);
+      ptx::tma_load_3d(&tq, q_full, sQ(0) + 16384, 64, h, q0);
+      ptx::tma_load_3d(&tq, q_full, sQ(1), 0, h, q0 + BM);
+      ptx::tma_load_3d(&tq, q_full, sQ(1) + 16384, 64, h, q0 + BM);
       auto load_k = [&](int j) {
         const int st = j & 1;
         if (j >= 2) ptx::mbar_wait(&k_empty[st], ((j >> 1) - 1) & 1);
         ptx::mbar_expect_tx(&k_full[st], TILE_BYTES);
-        ptx::tma_load_3d(&tk, &k_full[st], sK[st], 0, kh, kv0 + j * BN);
-        ptx::tma_load_3d(&tk, &k_full[st], sK[st] + 16384, 64, kh, kv0 + j * BN);
+        ptx::tma_load_3d(&tk, &k_full[st], sK(st), 0, kh, kv0 + j * BN);
+        ptx::tma_load_3d(&tk, &k_full[st], sK(st) + 16384, 64, kh, kv0 + j * BN);
       };
       load_k(0);
       for (int j = 0; j < nkv; ++j) {
@@ -138,14 +140,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false, false);
     constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(BM, D, false, true);
-    const uint32_t qa[2] = {ptx::smem_u32(sQ[0]), ptx::smem_u32(sQ[1])};
-    const uint32_t pa[2] = {ptx::smem_u32(sP[0]), ptx::smem_u32(sP[1])};
+    const uint32_t qa0 = ptx::smem_u32(sQ(0)), pa0 = ptx::smem_u32(sP(0));
     const uint32_t va = ptx::smem_u32(sV);
     ptx::mbar_wait(q_full, 0);
     auto issue_s = [&](int j) {
       const int st = j & 1;
       ptx::mbar_wait(&k_full[st], (j >> 1) & 1);
-      const uint32_t ka = ptx::smem_u32(sK[st]);
+      const uint32_t ka = ptx::smem_u32(sK(st));
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         if (j > 0) ptx::mbar_wait(&s_empty[t], (j - 1) & 1);
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         if (lane == 0) {
 #pragma unroll
           for (int k = 0; k < D / 16; ++k)
-            ptx::mma_bf16_ss(TS[t], kdesc(qa[t], k), kdesc(ka, k), idesc_s, k != 0);
+            ptx::mma_bf16_ss(TS(t), kdesc(qa0 + uint32_t(t) * TILE_BYTES, k), kdesc(ka, k), idesc_s, k != 0);
           ptx::mma_commit(&s_full[t]);
         }
         __syncwarp();
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         if (lane == 0) {
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            ptx::mma_bf16_ss(TO[t], kdesc(pa[t], k), mndesc(va, k), idesc_o, (j | k) != 0);
+            ptx::mma_bf16_ss(TO(t), kdesc(pa0 + uint32_t(t) * TILE_BYTES, k), mndesc(va, k), idesc_o, (j | k) != 0);
           ptx::mma_commit(&o_done[t]);
         }
         __syncwarp();
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const bool valid_row = row < p.N;
     const int sst = valid_row ? p.seq_start[row] : 0x7fffffff;
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
-    uint8_t* myP = sP[t];
+    uint8_t* myP = sP(t);
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(&s_full[t], j & 1);
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
-        ptx::tmem_ld32(TS[t] + lane_off + c * 32, v);
+        ptx::tmem_ld32(TS(t) + lane_off + c * 32, v);
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t v[32];
-          ptx::tmem_ld32(TO[t] + lane_off + c * 32, v);
+          ptx::tmem_ld32(TO(t) + lane_off + c * 32, v);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
@@ -259,8 +260,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
             lo[i] = v[i];
             hi[i] = v[16 + i];
           }
-          ptx::tmem_st16(TO[t] + lane_off + c * 32, lo);
-          ptx::tmem_st16(TO[t] + lane_off + c * 32 + 16, hi);
+          ptx::tmem_st16(TO(t) + lane_off + c * 32, lo);
+          ptx::tmem_st16(TO(t) + lane_off + c * 32 + 16, hi);
         }
         ptx::tmem_wait_st();
       }
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t v[32];
-      ptx::tmem_ld32(TO[t] + lane_off + c * 32, v);
+      ptx::tmem_ld32(TO(t) + lane_off + c * 32, v);
       ptx::tmem_wait_ld();
       if (valid_row) {
 #pragma unroll
