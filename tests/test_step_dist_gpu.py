@@ -96,6 +96,7 @@ MOE_PLANS = [
     (4, {"dp_replicate": 1, "dp_shard": 4, "sp": 1, "ep": 4, "micro_batch": 1, "recompute": "none",
          "moe_overlap": True}, 4),
     (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "moe_overlap": True}, 2),
+    (4, {"dp_replicate": 2, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1}, 4),  # HSDP x EP
 ]
 
 
