@@ -95,6 +95,15 @@ int opx_step_init_weights(opx_step* st, uint64_t seed);
 int opx_step_load_batch(opx_step* st, const int32_t* ids, const int32_t* labels,
                         const int32_t* positions, const int32_t* cu_seqlens, int n_cu,
                         int64_t n_valid_global);
+/* Frozen omni-modal encoder inputs (step_graph.cpp:141-166):
+ * the n_items image items placed in THIS rank's micro-batch rows, sorted by
+ * (row, position): rows[j] (0-based within the micro-batch), positions[j] =
+ * first of its tokens_per_item placeholder tokens in that row, and bf16
+ * patches [n_items, 4*tokens_per_item, patch_width].  Each SP rank encodes
+ * items j % sp == its SP index and stores the features to the ranks owning
+ * the placeholder positions.  Call after opx_step_load_batch, before run. */
+int opx_step_load_images(opx_step* st, const void* pixels_bf16, int n_items, const int32_t* rows,
+                         const int32_t* positions);
 int opx_step_run(opx_step* st, opx_step_report* rep);
 /* FSDP flat-shard checkpoint: every unit's fp32 master /
  * exp_avg / exp_avg_sq shards in the executor's chunked layout plus a
@@ -156,6 +165,12 @@ int opx_attn_fwd(const void* q, const void* k, const void* v, void* o, float* ls
 int opx_attn_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse,
                     int64_t ldq, int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
                     const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream);
+/* Bidirectional varlen attention (keys [seq_start[t], seq_end[t])), the frozen
+ * encoder's self-attention (step_graph.cpp:141-166). */
+int opx_attn_fwd_bidir_tc(const void* q, const void* k, const void* v, void* o, float* lse,
+                          int64_t ldq, int64_t ldk, int64_t ldv, int64_t ldo,
+                          const int32_t* seq_start, const int32_t* seq_end, int N, int hq, int hk,
+                          float scale, void* stream);
 int opx_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
                  const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
                  int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,

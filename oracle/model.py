@@ -295,9 +295,11 @@ class Step:
     def mm(self, x, w):  # x [N,K] . w[M,K]^T
         return (self.r(x).astype(np.float64) @ self.r(w).astype(np.float64).T).astype(F32)
 
-    def run(self, ids, labels, pos, cu, n_valid):
+    def run(self, ids, labels, pos, cu, n_valid, inject=None):
         """ids/labels/pos [N] (N = all tokens of the batch rows, concatenated);
-        cu: global cu_seqlens over those tokens.  Returns (loss_sum, grads)."""
+        cu: global cu_seqlens over those tokens.  inject = (mask [N], feats):
+        encoder features replacing the masked embeddings (oracle/encoder.py).
+        Returns (loss_sum, grads)."""
         a, P = self.a, self.P
         H, d, nh, nk = a.hidden, a.head_dim, a.heads, a.kv_heads
         N = ids.shape[0]
@@ -305,6 +307,8 @@ class Step:
         cos, sin = rope_tables(pos, d, a.rope_theta)
         G = {}
         x = self.r(P["model.embed_tokens.weight"])[ids].astype(F32)
+        if inject is not None and inject[0].any():
+            x[inject[0]] = inject[1]
         saved = []
         for l in range(a.layers):
             p = f"model.layers.{l}."
@@ -384,6 +388,8 @@ class Step:
                 dh.astype(F32), st["x"], self.r(P[p + "input_layernorm.weight"]), st["r1"])
             dx = (dx + ddx).astype(F32)
         dE = np.zeros((a.vocab, H), np.float64)
+        if inject is not None:
+            dx = np.where(inject[0][:, None], np.float32(0), dx)
         np.add.at(dE, ids, dx.astype(np.float64))
         G["model.embed_tokens.weight"] = dE.astype(F32)
         self.loss_rows = loss_rows.astype(F32)
@@ -484,7 +490,8 @@ def adamw(params, grads, state, step, lr=1e-4, betas=(0.9, 0.95), eps=1e-8, wd=0
 # ----------------------------------------------------------------------------
 # simulated ranks (FSDP x SP x DP) for one step
 # ----------------------------------------------------------------------------
-def simulate_ranks(a: Arch, params: dict, batch, plan: dict, forced_routes=None, flips=None):
+def simulate_ranks(a: Arch, params: dict, batch, plan: dict, forced_routes=None, flips=None,
+                   encoder=None):
     """Runs the step the way the mesh partitions the batch: dp index r
     (= dp_replicate_idx*dp_shard + dp_shard_idx) owns rows
     [r*micro_batch, (r+1)*micro_batch).  Inside an SP group the Ulysses
@@ -492,7 +499,8 @@ def simulate_ranks(a: Arch, params: dict, batch, plan: dict, forced_routes=None,
     so the SP ranks of one group are evaluated jointly on their gathered rows.
     Parameter gradients of the dp ranks are summed in rank order (the FSDP
     reduce-scatter / HSDP all-reduce) and the loss is normalised by the global
-    supervised-token count.  Returns (loss_mean, grads)."""
+    supervised-token count.  encoder = (EncArch, encoder params) runs the
+    frozen encoder over batch["img"] (oracle/encoder.py).  Returns (loss_mean, grads)."""
     rows_per_dp = plan["micro_batch"]
     dp = plan["dp_replicate"] * plan["dp_shard"]
     ids, labels, pos, cus = batch["ids"], batch["labels"], batch["pos"], batch["cu_rows"]
@@ -509,8 +517,14 @@ def simulate_ranks(a: Arch, params: dict, batch, plan: dict, forced_routes=None,
         fr = None
         if forced_routes:
             fr = {l: v[sl].reshape(-1, v.shape[-1]) for l, v in forced_routes.items()}
+        inj = None
+        if encoder is not None and "img" in batch:
+            from oracle.encoder import inject_for_rows
+
+            inj = inject_for_rows(encoder[0], encoder[1], batch["img"],
+                                  range(r * rows_per_dp, (r + 1) * rows_per_dp), S)
         st = Step(a, params, forced_routes=fr)
-        ls, g = st.run(rid, rlab, rpos, np.array(cu), n_valid)
+        ls, g = st.run(rid, rlab, rpos, np.array(cu), n_valid, inject=inj)
         if flips is not None:
             for l, f in st.flips.items():
                 flips.setdefault(l, []).append(f)

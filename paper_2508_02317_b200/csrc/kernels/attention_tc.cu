@@ -1,4 +1,5 @@
-// Causal packed-varlen GQA flash attention FORWARD on tcgen05 (sm_100a), d = 128.
+// Causal (or, for the frozen encoder, bidirectional) packed-varlen GQA flash
+// attention FORWARD on tcgen05 (sm_100a), d = 128.
 //
 // One CTA per (pair of consecutive 128-query tiles, q head), 320 threads:
 //   warp 0       TMA producer: Q0/Q1 once, K tiles (128 keys) into a 2-stage
@@ -48,7 +49,8 @@ struct FwdParams {
   float* lse;
   int64_t ldo;
   const int* seq_start;
-  int N, hq, hk, npairs;
+  const int* seq_end;  // bidirectional mode only
+  int N, hq, hk, npairs, causal;
   float scale_log2;
 };
 
@@ -85,7 +87,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const int q0 = pair * 2 * BM;
   const int qlast = min(q0 + 2 * BM, p.N) - 1;
   const int kv0 = p.seq_start[q0] & ~(BN - 1);
-  const int nkv = (qlast - kv0) / BN + 1;
+  // last key any row of the pair sees: the row itself (causal) or the end of
+  // its sample (bidirectional; seq_end is non-decreasing in the row)
+  const int klast = p.causal ? qlast : p.seq_end[qlast] - 1;
+  const int nkv = (klast - kv0) / BN + 1;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tq);
@@ -192,6 +197,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const int row = q0 + t * BM + r;
     const bool valid_row = row < p.N;
     const int sst = valid_row ? p.seq_start[row] : 0x7fffffff;
+    const int kend = p.causal ? row + 1 : (valid_row ? p.seq_end[row] : 0);  // keys [sst, kend)
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
     uint8_t* myP = sP(t);
     float m_used = -INFINITY, l = 0.f;
@@ -210,14 +216,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&s_empty[t]);
       const int kbase = kv0 + j * BN;
-      const bool full_vis = kbase >= sst && kbase + BN - 1 <= row;
+      const bool full_vis = kbase >= sst && kbase + BN <= kend;
       // row max of the raw scores (scale > 0), 3-input max
       float mr = -INFINITY;
       if (!full_vis) {
 #pragma unroll
         for (int i = 0; i < 128; ++i) {
           const int key = kbase + i;
-          s[i] = (key >= sst && key <= row) ? s[i] : -INFINITY;
+          s[i] = (key >= sst && key < kend) ? s[i] : -INFINITY;
         }
       }
 #pragma unroll
@@ -326,6 +332,9 @@ cudaError_t k_attn_fwd_tc(const AttnArgs& a, cudaStream_t s) {
   p.lse = a.lse;
   p.ldo = a.ldo;
   p.seq_start = a.seq_start;
+  p.seq_end = a.seq_end;
+  p.causal = a.causal;
+  if (!a.causal && !a.seq_end) return cudaErrorInvalidValue;
   p.N = a.N;
   p.hq = a.hq;
   p.hk = a.hk;

@@ -66,6 +66,9 @@ struct AttnArgs {
   float* dk_acc = nullptr;
   float* dv_acc = nullptr;
   int kv_splits = 0;
+  // tcgen05 forward only: 0 = bidirectional inside each sample (keys
+  // [seq_start[t], seq_end[t])), the frozen encoder's attention
+  int causal = 1;
 };
 cudaError_t k_attn_fwd(const AttnArgs& a, cudaStream_t s);
 cudaError_t k_attn_bwd(const AttnArgs& a, cudaStream_t s);
@@ -102,6 +105,18 @@ struct A2AArgs {
 cudaError_t k_rope_table(float2* tab, int npos, int half, const float* inv_freq, cudaStream_t s);
 cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s);
 cudaError_t k_a2a_head2seq(const A2AArgs& a, cudaStream_t s);
+// encoder.cu — frozen encoder glue: GELU in place on bf16,
+// feature rows -> the owning SP rank's feature buffer (peer stores), feature
+// rows -> the fp32 embedding output, and zeroing of the replaced rows' grads.
+struct FeatPeers {
+  __nv_bfloat16* p[kMaxSp];
+};
+cudaError_t k_gelu_bf16(__nv_bfloat16* x, int64_t n, cudaStream_t s);
+cudaError_t k_feat_scatter(const __nv_bfloat16* feat, int nf, int H, const int* dst_rank,
+                           const int* dst_tok, const FeatPeers& peers, cudaStream_t s);
+cudaError_t k_feat_inject(float* x, const __nv_bfloat16* feat, const int* fmask, int T, int H,
+                          cudaStream_t s);
+cudaError_t k_rows_zero(float* x, const int* fmask, int T, int H, cudaStream_t s);
 // Peer barrier: signal every peer then wait until every peer reached `epoch`.
 cudaError_t k_peer_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int n, int me,
                            uint32_t epoch, int* timeout_flag, cudaStream_t s);

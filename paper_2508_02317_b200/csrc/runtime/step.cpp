@@ -212,6 +212,7 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
   }
   TRY(build_units());
   if (shard_comm_head_) units_[0].comm = shard_comm_head_;
+  TRY(enc_setup());
   TRY(alloc_acts());
   return OPX_OK;
 }
@@ -386,6 +387,7 @@ int Step::alloc_acts() {
     off_dqkv_[b] = take(T * size_t(Wqkv_) * 2);
   }
   if (moe_) off = moe_arena(off);
+  if (enc_.on) off_feat_ = take(T * H * 2);
   arena_bytes_ = off;
   if (cudaMalloc(&arena_, arena_bytes_) != cudaSuccess) {
     set_error("out of device memory for the peer arena (" + std::to_string(arena_bytes_ >> 20) +
@@ -539,6 +541,7 @@ int Step::init_weights(uint64_t seed) {
     }
   }
   step_count_ = 0;
+  TRY(enc_init_weights(seed));
   CU(cudaStreamSynchronize(cs_));
   return OPX_OK;
 }
@@ -1055,6 +1058,7 @@ int Step::run(opx_step_report* rep) {
   // embedding grad region is scatter-added: zero it
   CU(cudaMemsetAsync(hu.gat(hu.gfull, hu.params[0].off), 0, size_t(hu.params[0].numel) * 4, cs_));
   CU(k_embed_fwd(d_ids_, hu.full + hu.params[0].off, x_saved_[0], T_, H_, cs_));
+  TRY(enc_forward());  // frozen encoder: features replace the placeholder embeddings
 
   auto issue_gather = [&](int l, bool bwd) -> int {
     Unit& u = units_[size_t(1 + l)];
@@ -1182,6 +1186,7 @@ int Step::run(opx_step_report* rep) {
       TRY(opt_unit(u, cs_, "opt.layer" + std::to_string(l)));
     }
   }
+  if (enc_.on && enc_.n_all) CU(k_rows_zero(dx_, d_fmask_, T_, H_, cs_));
   CU(k_embed_bwd(d_ids_, dx_, static_cast<float*>(hu.gfull) + hu.params[0].off, T_, H_, cs_));
   if (P > 1 || hu.rep_comm) {
     CU(cudaEventRecord(ev_head_rs_, cs_));
@@ -1292,6 +1297,20 @@ int Step::get(const std::string& full, void* dst, size_t bytes) {
       return OPX_ERR_ARG;
     }
     CU(cudaMemcpy(dst, route_idx_[size_t(l)], bytes, cudaMemcpyDeviceToHost));
+    return OPX_OK;
+  }
+  if (full == "features") {  // [T, H] feature rows received from the encoder (bf16 -> fp32)
+    if (!enc_.on || bytes != size_t(T_) * size_t(H_) * 4) {
+      set_error("features: no encoder or size mismatch");
+      return OPX_ERR_ARG;
+    }
+    std::vector<uint16_t> h(size_t(T_) * size_t(H_));
+    CU(cudaMemcpy(h.data(), arena_ + off_feat_, h.size() * 2, cudaMemcpyDeviceToHost));
+    float* o = static_cast<float*>(dst);
+    for (size_t i = 0; i < h.size(); ++i) {
+      const uint32_t w = uint32_t(h[i]) << 16;
+      std::memcpy(&o[i], &w, 4);
+    }
     return OPX_OK;
   }
   if (full == "loss_rows") {
@@ -1466,6 +1485,14 @@ int opx_step_init_weights(opx_step* st, uint64_t seed) { return st->impl.init_we
 int opx_step_load_batch(opx_step* st, const int32_t* ids, const int32_t* labels,
                         const int32_t* positions, const int32_t* cu, int n_cu, int64_t n_valid) {
   return st->impl.load_batch(ids, labels, positions, cu, n_cu, n_valid);
+}
+int opx_step_load_images(opx_step* st, const void* pixels_bf16, int n_items, const int32_t* rows,
+                         const int32_t* positions) {
+  if (n_items < 0 || (n_items > 0 && (!pixels_bf16 || !rows || !positions))) {
+    set_error("opx_step_load_images: bad arguments");
+    return OPX_ERR_ARG;
+  }
+  return st->impl.load_images(static_cast<const uint16_t*>(pixels_bf16), n_items, rows, positions);
 }
 int opx_step_run(opx_step* st, opx_step_report* rep) { return st->impl.run(rep); }
 int opx_step_save(opx_step* st, const char* dir) { return st->impl.save(dir ? dir : ""); }

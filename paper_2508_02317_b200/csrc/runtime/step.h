@@ -92,6 +92,9 @@ class Step {
   int init_weights(uint64_t seed);
   int load_batch(const int32_t* ids, const int32_t* labels, const int32_t* pos, const int32_t* cu,
                  int n_cu, int64_t n_valid);
+  // frozen encoder inputs (step_encoder.cpp): bf16 patches [n, 4*tpi, pd] of
+  // the n items placed in this rank's micro-batch rows, sorted by (row, pos)
+  int load_images(const uint16_t* pixels, int n, const int32_t* row, const int32_t* pos);
   int run(opx_step_report* rep);
   int save(const std::string& dir);  // checkpoint.cpp
   int load(const std::string& dir);
@@ -248,6 +251,27 @@ class Step {
   int layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int slot);
   int layer_bwd(int l, Unit& u, void* grads);
   int head_fwd_bwd(Unit& u, float* grads);
+  // ---- frozen omni-modal encoder (step_encoder.cpp)
+  struct Enc {
+    bool on = false;
+    std::string name;
+    int He = 0, L = 0, heads = 0, d = 0, F = 0, pd = 0, tpi = 0;
+    bf16* w = nullptr;  // every weight, 128-element aligned offsets
+    int64_t o_patch = 0, o_lnq = 0, o_m0 = 0, o_m2 = 0, numel = 0;
+    std::vector<int64_t> o_blk;  // per block: norm1 | qkv | proj | norm2 | gate_up | down
+    int cap = 0, n_loc = 0, n_all = 0;  // items: buffer capacity, encoded here, in the micro-batch
+    bf16 *pix = nullptr, *h = nullptr, *qkv = nullptr, *q = nullptr, *k = nullptr, *v = nullptr,
+         *o = nullptr, *o2 = nullptr, *act = nullptr, *y1 = nullptr, *feat = nullptr;
+    float *x = nullptr, *rstd = nullptr, *lse = nullptr;
+    int *st = nullptr, *en = nullptr, *dst_rank = nullptr, *dst_tok = nullptr;
+    std::vector<void*> bufs;  // item-sized buffers (re-allocated when cap grows)
+  } enc_;
+  int* d_fmask_ = nullptr;  // [T] local tokens replaced by encoder features
+  size_t off_feat_ = 0;     // arena: [T, H] bf16 feature rows written by the SP peers
+  int enc_setup();
+  int enc_alloc(int items);
+  int enc_init_weights(uint64_t seed);
+  int enc_forward();  // encoder fwd + scatter into the SP group + inject (cs_)
   // ---- MoE / expert parallelism (step_moe.cpp)
   bool moe_ = false;
   int E_ = 0, topk_ = 0, Fe_ = 0, El_ = 0, ep_ = 1, ep_i_ = 0, De_ = 1;

@@ -1,0 +1,346 @@
+// Frozen omni-modal encoder inside the step.
+//
+// Reference: step_graph.cpp:141-166 build_encoders — per micro-batch an
+// `encoder.<mod>` compute node over this rank's share of the modality tokens
+// (no backward node when the module is frozen) and a `scatter.<mod>`
+// all_to_all of the features into the SP group (comm.cpp:91-105); the module
+// fields come from specs.hpp:66-75 (name, kind, arch, trainable,
+// tokens_per_item).  The encoder math (a Qwen2.5-VL-shaped ViT without 2-D
+// RoPE / windows, then the 2x2 patch merger) is defined in oracle/encoder.py.
+//
+// B200 mapping: the items of a micro-batch are dealt round-robin to the SP
+// ranks (item j -> rank j % sp), each rank runs the ViT over its patches with
+// the backbone's kernels (tcgen05 GEMMs, SwiGLU epilogue, bidirectional
+// tcgen05 attention on 128-padded heads via the seq->head relayout kernel),
+// and the merger's output rows are stored straight into the feature buffer of
+// the SP rank that owns each placeholder position (NVLink peer stores into the
+// CUDA-IPC arena: the all-to-all and the masked scatter's addressing in one
+// pass).  After an SP barrier every rank overwrites its placeholder
+// embeddings with the received rows; the backward zeroes their gradient rows
+// before the embedding scatter-add (the features are frozen).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.h"
+#include "step.h"
+
+namespace opx {
+
+#define TRY(x)                     \
+  do {                             \
+    int rc_ = (x);                 \
+    if (rc_ != OPX_OK) return rc_; \
+  } while (0)
+#define CU(x) TRY(check((x), #x))
+
+namespace {
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+GemmDesc egd(int M, int N, int K, const bf16* A, int64_t lda, const bf16* B, int64_t ldb, int epi,
+             void* D, int64_t ldd) {
+  GemmDesc g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.A = A;
+  g.lda = lda;
+  g.a_mn = false;
+  g.B = B;
+  g.ldb = ldb;
+  g.b_mn = false;
+  g.epi = epi;
+  g.D = D;
+  g.ldd = ldd;
+  return g;
+}
+}  // namespace
+
+int Step::enc_setup() {
+  const Module* em = nullptr;
+  for (const Module& m : m_.modules)
+    if (m.kind == ModuleKind::encoder && m.arch) {
+      em = &m;
+      break;
+    }
+  if (!em) return OPX_OK;
+  if (em->trainable) {
+    set_error("encoder '" + em->name + "': only frozen (trainable=false) encoders are executed");
+    return OPX_ERR_CONFIG;
+  }
+  const Arch& ea = *em->arch;
+  Enc& e = enc_;
+  e.on = true;
+  e.name = em->name;
+  e.He = int(ea.hidden);
+  e.L = int(ea.layers);
+  e.heads = int(ea.heads);
+  e.d = int(ea.head_dim);
+  e.F = int(ea.ffn);
+  e.pd = int(ea.vocab);  // an encoder's "vocab" is its patch width
+  e.tpi = int(em->tokens_per_item);
+  if (ea.kv_heads != ea.heads || e.d > 128 || e.d % 16 || e.He % 128 || e.F % 128 || e.pd % 8 ||
+      e.tpi <= 0 || e.tpi > S_loc_) {
+    set_error("encoder requires kv_heads == heads, head_dim <= 128 (multiple of 16), hidden and ffn "
+              "multiples of 128, patch width (arch.vocab) a multiple of 8, 0 < tokens_per_item <= seq/sp");
+    return OPX_ERR_CONFIG;
+  }
+  const int64_t He = e.He, Wq = int64_t(e.heads) * e.d, F = e.F;
+  auto take = [&](int64_t n) {
+    const int64_t o = e.numel;
+    e.numel += round_up(n, 128);
+    return o;
+  };
+  e.o_patch = take(He * e.pd);
+  for (int i = 0; i < e.L; ++i) {
+    e.o_blk.push_back(take(He));          // norm1
+    e.o_blk.push_back(take(3 * Wq * He)); // qkv
+    e.o_blk.push_back(take(He * Wq));     // proj
+    e.o_blk.push_back(take(He));          // norm2
+    e.o_blk.push_back(take(2 * F * He));  // gate|up (128-row interleave)
+    e.o_blk.push_back(take(He * F));      // down
+  }
+  e.o_lnq = take(He);
+  e.o_m0 = take(16 * He * He);
+  e.o_m2 = take(int64_t(H_) * 4 * He);
+  e.w = alloc<bf16>(size_t(e.numel));
+  d_fmask_ = alloc<int>(size_t(T_));
+  if (!e.w || !d_fmask_) return cuda_fail(cudaErrorMemoryAllocation, "encoder weights");
+  return OPX_OK;
+}
+
+int Step::enc_init_weights(uint64_t seed) {
+  if (!enc_.on) return OPX_OK;
+  Enc& e = enc_;
+  const double c = 0.02 * std::sqrt(3.0) / 16777216.0;
+  const int64_t He = e.He, Wq = int64_t(e.heads) * e.d, F = e.F;
+  auto normal = [&](int64_t off, int64_t n, const std::string& name) -> int {
+    CU(k_init_param(nullptr, e.w + off, n, 0, param_key(name, seed), 0, c, 1.f, 0, 0, 0, cs_));
+    return OPX_OK;
+  };
+  auto ones = [&](int64_t off, int64_t n) -> int {
+    CU(k_init_param(nullptr, e.w + off, n, 0, 0, 0, 0.0, 1.f, 0, 0, 0, cs_));
+    return OPX_OK;
+  };
+  TRY(normal(e.o_patch, He * e.pd, "visual.patch_embed.proj.weight"));
+  for (int i = 0; i < e.L; ++i) {
+    const std::string p = "visual.blocks." + std::to_string(i) + ".";
+    const int64_t* o = &e.o_blk[size_t(i) * 6];
+    TRY(ones(o[0], He));
+    TRY(normal(o[1], 3 * Wq * He, p + "attn.qkv.weight"));
+    TRY(normal(o[2], He * Wq, p + "attn.proj.weight"));
+    TRY(ones(o[3], He));
+    CU(k_init_param(nullptr, e.w + o[4], 2 * F * He, 0, param_key(p + "mlp.gate_proj.weight", seed),
+                    param_key(p + "mlp.up_proj.weight", seed), c, 1.f, 1, 2 * F, He, cs_));
+    TRY(normal(o[5], He * F, p + "mlp.down_proj.weight"));
+  }
+  TRY(ones(e.o_lnq, He));
+  TRY(normal(e.o_m0, 16 * He * He, "visual.merger.mlp.0.weight"));
+  TRY(normal(e.o_m2, int64_t(H_) * 4 * He, "visual.merger.mlp.2.weight"));
+  return OPX_OK;
+}
+
+int Step::enc_alloc(int items) {
+  Enc& e = enc_;
+  if (items <= e.cap) return OPX_OK;
+  CU(cudaStreamSynchronize(cs_));
+  for (void* p : e.bufs) {
+    cudaFree(p);
+    allocs_.erase(std::remove(allocs_.begin(), allocs_.end(), p), allocs_.end());
+  }
+  e.bufs.clear();
+  const size_t Np = size_t(items) * 4 * size_t(e.tpi), He = size_t(e.He);
+  const size_t Wq = size_t(e.heads) * size_t(e.d);
+  auto a = [&](auto*& ptr, size_t n) {
+    using T = std::remove_reference_t<decltype(*ptr)>;
+    ptr = alloc<T>(n, false);
+    e.bufs.push_back(ptr);
+    return ptr != nullptr;
+  };
+  bool ok = a(e.pix, Np * size_t(e.pd)) && a(e.x, Np * He) && a(e.rstd, Np) &&
+            a(e.lse, Np * size_t(e.heads)) && a(e.h, Np * He) &&
+            a(e.qkv, Np * 3 * Wq) && a(e.q, Np * size_t(e.heads) * 128) &&
+            a(e.k, Np * size_t(e.heads) * 128) && a(e.v, Np * size_t(e.heads) * 128) &&
+            a(e.o, Np * size_t(e.heads) * 128) && a(e.o2, Np * Wq) && a(e.act, Np * size_t(e.F)) &&
+            a(e.y1, Np * He) && a(e.feat, Np / 4 * size_t(H_)) && a(e.st, Np) && a(e.en, Np) &&
+            a(e.dst_rank, Np / 4) && a(e.dst_tok, Np / 4);
+  if (!ok) return cuda_fail(cudaErrorMemoryAllocation, "encoder activations");
+  e.cap = items;
+  return OPX_OK;
+}
+
+int Step::load_images(const uint16_t* pixels, int n, const int32_t* row, const int32_t* pos) {
+  if (!enc_.on) {
+    set_error("the model has no encoder module with an arch");
+    return OPX_ERR_CONFIG;
+  }
+  Enc& e = enc_;
+  const int sp = int(p_.sp), tpi = e.tpi, P = 4 * tpi;
+  std::vector<int32_t> mask(size_t(T_), 0);
+  std::vector<int> mine;
+  for (int j = 0; j < n; ++j) {
+    if (row[j] < 0 || row[j] >= rows_ || pos[j] < 0 || pos[j] + tpi > S_ ||
+        (j > 0 && (row[j] < row[j - 1] || (row[j] == row[j - 1] && pos[j] < pos[j - 1] + tpi)))) {
+      set_error("image items must lie inside their row, sorted by (row, pos), without overlap");
+      return OPX_ERR_ARG;
+    }
+    for (int t = 0; t < tpi; ++t) {
+      const int s = pos[j] + t;
+      if (s / S_loc_ == sp_i_) mask[size_t(row[j]) * S_loc_ + s % S_loc_] = 1;
+    }
+    if (j % sp == sp_i_) mine.push_back(j);
+  }
+  e.n_all = n;
+  e.n_loc = int(mine.size());
+  CU(cudaMemcpyAsync(d_fmask_, mask.data(), size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
+  if (e.n_loc == 0) return OPX_OK;
+  TRY(enc_alloc(e.n_loc));
+  const size_t item_elems = size_t(P) * size_t(e.pd);
+  std::vector<uint16_t> px(size_t(e.n_loc) * item_elems);
+  std::vector<int32_t> st(size_t(e.n_loc) * P), en(size_t(e.n_loc) * P), dr(size_t(e.n_loc) * tpi),
+      dt(size_t(e.n_loc) * tpi);
+  for (int k = 0; k < e.n_loc; ++k) {
+    const int j = mine[size_t(k)];
+    std::memcpy(px.data() + size_t(k) * item_elems, pixels + size_t(j) * item_elems, item_elems * 2);
+    for (int i = 0; i < P; ++i) {
+      st[size_t(k) * P + i] = k * P;
+      en[size_t(k) * P + i] = (k + 1) * P;
+    }
+    for (int t = 0; t < tpi; ++t) {
+      const int s = pos[j] + t;
+      dr[size_t(k) * tpi + t] = s / S_loc_;
+      dt[size_t(k) * tpi + t] = row[j] * S_loc_ + s % S_loc_;
+    }
+  }
+  CU(cudaMemcpyAsync(e.pix, px.data(), px.size() * 2, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(e.st, st.data(), st.size() * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(e.en, en.data(), en.size() * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(e.dst_rank, dr.data(), dr.size() * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(e.dst_tok, dt.data(), dt.size() * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaStreamSynchronize(cs_));
+  return OPX_OK;
+}
+
+int Step::enc_forward() {
+  Enc& e = enc_;
+  if (!e.on || e.n_all == 0) return OPX_OK;
+  const bool tr = ex_.trace;
+  cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
+  if (tr) cudaEventRecord(e0, cs_);
+  const int Np = e.n_loc * 4 * e.tpi, He = e.He, Wq = e.heads * e.d, F = e.F, nf = e.n_loc * e.tpi;
+  const bool pad = e.d != 128;
+  if (Np > 0) {
+    CU(gemm_run(egd(Np, He, e.pd, e.pix, e.pd, e.w + e.o_patch, e.pd, GEMM_EPI_F32, e.x, He), cs_));
+    for (int i = 0; i < e.L; ++i) {
+      const int64_t* o = &e.o_blk[size_t(i) * 6];
+      CU(k_rmsnorm_fwd(e.x, e.w + o[0], e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
+      CU(gemm_run(egd(Np, 3 * Wq, He, e.h, He, e.w + o[1], He, GEMM_EPI_BF16, e.qkv, 3 * Wq), cs_));
+      const bf16 *q = e.qkv, *k = e.qkv + Wq, *v = e.qkv + 2 * Wq;
+      int64_t ld = 3 * Wq;
+      if (pad) {  // [Np, heads*d] -> zero-padded [Np, heads, 128] (sp = 1 relayout, no RoPE)
+        A2AArgs a{};
+        a.sp = 1;
+        a.rank = 0;
+        a.rows = 1;
+        a.seq = Np;
+        a.ngroups = 3;
+        bf16* dst[3] = {e.q, e.k, e.v};
+        for (int g = 0; g < 3; ++g) {
+          a.g[g].heads_total = e.heads;
+          a.g[g].col0 = g * Wq;
+          a.g[g].rope = 0;
+          a.g[g].full[0] = dst[g];
+        }
+        a.local[0] = e.qkv;
+        a.local_ld = 3 * Wq;
+        a.hd = e.d;
+        CU(k_a2a_seq2head(a, cs_));
+        q = e.q;
+        k = e.k;
+        v = e.v;
+        ld = int64_t(e.heads) * 128;
+      }
+      {
+        AttnArgs a{};
+        a.q = q;
+        a.k = k;
+        a.v = v;
+        a.o = e.o;
+        a.lse = e.lse;  // not kept: the encoder has no backward
+        a.ldq = a.ldk = a.ldv = ld;
+        a.ldo = int64_t(e.heads) * 128;
+        a.seq_start = e.st;
+        a.seq_end = e.en;
+        a.N = Np;
+        a.hq = a.hk = e.heads;
+        a.scale = 1.0f / std::sqrt(float(e.d));
+        a.causal = 0;
+        CU(k_attn_fwd_tc(a, cs_));
+      }
+      const bf16* o2 = e.o;
+      if (pad) {
+        A2AArgs a{};
+        a.sp = 1;
+        a.rank = 0;
+        a.rows = 1;
+        a.seq = Np;
+        a.ngroups = 1;
+        a.g[0].heads_total = e.heads;
+        a.g[0].full[0] = e.o;
+        a.local[0] = e.o2;
+        a.local_ld = Wq;
+        a.hd = e.d;
+        CU(k_a2a_head2seq(a, cs_));
+        o2 = e.o2;
+      }
+      {
+        GemmDesc g = egd(Np, He, Wq, o2, pad ? Wq : int64_t(e.heads) * 128, e.w + o[2], Wq,
+                         GEMM_EPI_F32_RESID, e.x, He);
+        g.R = e.x;
+        g.ldr = He;
+        CU(gemm_run(g, cs_));
+      }
+      CU(k_rmsnorm_fwd(e.x, e.w + o[3], e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
+      {
+        GemmDesc g = egd(Np, 2 * F, He, e.h, He, e.w + o[4], He, GEMM_EPI_SWIGLU, nullptr, 2 * F);
+        g.D2 = e.act;
+        g.ldd2 = F;
+        CU(gemm_run(g, cs_));
+      }
+      {
+        GemmDesc g = egd(Np, He, F, e.act, F, e.w + o[5], F, GEMM_EPI_F32_RESID, e.x, He);
+        g.R = e.x;
+        g.ldr = He;
+        CU(gemm_run(g, cs_));
+      }
+    }
+    // merger: rmsnorm_q, 2x2 merge (4 consecutive patches = one [4 He] row), MLP with GELU
+    CU(k_rmsnorm_fwd(e.x, e.w + e.o_lnq, e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
+    CU(gemm_run(egd(Np / 4, 4 * He, 4 * He, e.h, 4 * He, e.w + e.o_m0, 4 * He, GEMM_EPI_BF16, e.y1,
+                    4 * He),
+                cs_));
+    CU(k_gelu_bf16(e.y1, int64_t(Np / 4) * 4 * He, cs_));
+    CU(gemm_run(egd(nf, H_, 4 * He, e.y1, 4 * He, e.w + e.o_m2, 4 * He, GEMM_EPI_BF16, e.feat, H_),
+                cs_));
+  }
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark("encoder." + e.name + ".m0", "encoder", 0, e0, e1);
+    e0 = e1;
+  }
+  // scatter.<mod>: feature rows -> the owning SP rank's feature buffer
+  FeatPeers fp{};
+  for (int j = 0; j < int(p_.sp); ++j) fp.p[j] = reinterpret_cast<bf16*>(peer(j, off_feat_));
+  CU(k_feat_scatter(e.feat, nf, H_, e.dst_rank, e.dst_tok, fp, cs_));
+  TRY(barrier_sp(cs_));
+  CU(k_feat_inject(x_saved_[0], reinterpret_cast<const bf16*>(arena_ + off_feat_), d_fmask_, T_, H_,
+                   cs_));
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark("scatter." + e.name + ".m0", "encoder", 0, e0, e1);
+  }
+  return OPX_OK;
+}
+
+}  // namespace opx

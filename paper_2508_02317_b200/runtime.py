@@ -67,6 +67,42 @@ def synthetic_batch(vocab: int, seq_len: int, rows: int, seed: int = 2508, singl
     return {"ids": ids, "labels": labels, "pos": pos, "cu_rows": cu_rows}
 
 
+def synthetic_images(batch, tokens_per_item: int, patch_dim: int, items_per_row: int = 2,
+                     placeholder: int | None = None, seed: int = 2508):
+    """Places up to ``items_per_row`` image items in every row of ``batch`` (in
+    place) for a frozen encoder module: an item occupies
+    ``tokens_per_item`` placeholder tokens right after the first token of a
+    sample long enough to hold it; those positions, and the one predicting the
+    first of them, are unsupervised.  Adds batch["img"] = {"row", "pos",
+    "pixels" [n, 4*tokens_per_item, patch_dim] float32} sorted by (row, pos)."""
+    rng = np.random.default_rng(seed + 1)
+    ids, labels = batch["ids"], batch["labels"]
+    vocab_ph = int(ids.max()) if placeholder is None else placeholder
+    rows, pos = [], []
+    for r, cu in enumerate(batch["cu_rows"]):
+        placed = 0
+        for a, b in zip(cu[:-1], cu[1:]):
+            if placed == items_per_row:
+                break
+            if b - a < tokens_per_item + 2:
+                continue
+            p0 = a + 1
+            ids[r, p0:p0 + tokens_per_item] = vocab_ph
+            labels[r, p0 - 1:p0 + tokens_per_item] = -100
+            rows.append(r)
+            pos.append(p0)
+            placed += 1
+    n = len(rows)
+    pix = rng.standard_normal((n, 4 * tokens_per_item, patch_dim)).astype(np.float32)
+    batch["img"] = {"row": np.array(rows, np.int32), "pos": np.array(pos, np.int32), "pixels": pix}
+    return batch
+
+
+def _bf16_bits(x: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
 def rank_coords(rank: int, plan: dict):
     sp, sh = plan["sp"], plan["dp_shard"]
     return rank // (sp * sh), (rank // sp) % sh, rank % sp  # rep, shard, sp
@@ -147,6 +183,18 @@ class Session:
                                         labels.ctypes.data_as(ctypes.c_void_p),
                                         pos.ctypes.data_as(ctypes.c_void_p),
                                         cu.ctypes.data_as(ctypes.c_void_p), len(cu), n_valid))
+        if "img" in batch:  # frozen encoder inputs of this rank's dp rows
+            rep, sh, _ = rank_coords(self.rank, self.plan)
+            m = self.plan["micro_batch"]
+            dp = rep * self.plan["dp_shard"] + sh
+            img = batch["img"]
+            sel = np.nonzero((img["row"] >= dp * m) & (img["row"] < (dp + 1) * m))[0]
+            rows = np.ascontiguousarray(img["row"][sel] - dp * m, np.int32)
+            posi = np.ascontiguousarray(img["pos"][sel], np.int32)
+            pix = _bf16_bits(img["pixels"][sel]) if len(sel) else np.zeros(1, np.uint16)
+            check(lib().opx_step_load_images(self.h, pix.ctypes.data_as(ctypes.c_void_p), len(sel),
+                                             rows.ctypes.data_as(ctypes.c_void_p),
+                                             posi.ctypes.data_as(ctypes.c_void_p)))
         return n_valid
 
     def run(self) -> StepReport:
@@ -172,6 +220,13 @@ class Session:
         out = np.empty((T, k), np.int32)
         check(lib().opx_step_get(self.h, f"route:{layer}".encode(), out.ctypes.data_as(ctypes.c_void_p),
                                  out.nbytes))
+        return out
+
+    def features(self, T, H):
+        """[T, H] encoder feature rows this rank received (meaningful at its
+        placeholder positions only)."""
+        out = np.empty((T, H), np.float32)
+        check(lib().opx_step_get(self.h, b"features", out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
         return out
 
     def loss_rows(self, T):

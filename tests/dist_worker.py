@@ -3,7 +3,7 @@ the gloo host-logic tests).  Returns this rank's loss and tensor slices."""
 import os
 
 
-def step_worker(rank, world, port, model, plan, S, rows, q, names):
+def step_worker(rank, world, port, model, plan, S, rows, q, names, images=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     import torch.distributed as td
@@ -17,9 +17,16 @@ def step_worker(rank, world, port, model, plan, S, rows, q, names):
         s = Session(cluster(world), model, wl, plan, EXEC, rank=rank, device=rank, dist=td)
         s.init_weights(EXEC["seed"])
         batch = synthetic_batch(model["modules"][0]["arch"]["vocab"], S, rows, seed=2508)
+        if images:
+            from paper_2508_02317_b200.runtime import synthetic_images
+
+            synthetic_images(batch, **images)
         s.load(batch)
         r = s.run()
         out = {}
+        if images:
+            H = model["modules"][0]["arch"]["hidden"]
+            out[("features", 0)] = s.features(plan["micro_batch"] * S // plan["sp"], H)
         for kind in ("grad", "master"):
             for n in names:
                 v, numel, b, e = s.get(f"{kind}:{n}")

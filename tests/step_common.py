@@ -98,6 +98,13 @@ def global_routes(sessions, arch, plan, S):
 MAX_FLIP_RATE = 0.05  # fraction of tokens whose expert set differs from the oracle's own top-k (reported)
 
 
+def tiny_encoder(layers=2, hidden=640, heads=8, head_dim=80, ffn=512, patch_dim=96, tokens_per_item=16):
+    """Frozen ViT-shaped encoder module (oracle/encoder.py); arch.vocab = patch width."""
+    return {"name": "vision", "kind": "encoder", "trainable": False, "tokens_per_item": tokens_per_item,
+            "arch": {"layers": layers, "hidden": hidden, "heads": heads, "kv_heads": heads,
+                     "head_dim": head_dim, "ffn_dim": ffn, "vocab": patch_dim}}
+
+
 def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
     """Runs the oracle on the same batch/weights and compares loss, every
     gradient and the AdamW-updated master weights.  For MoE models the oracle
@@ -108,7 +115,13 @@ def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
     P0 = om.init_params(arch, EXEC["seed"])
     routes = global_routes(sessions, arch, plan, batch["ids"].shape[1]) if arch.experts else None
     flips = {}
-    loss_ref, G = om.simulate_ranks(arch, P0, batch, plan, forced_routes=routes, flips=flips)
+    enc = None
+    if "img" in batch:
+        from oracle import encoder as oe
+
+        ea = oe.EncArch.from_model_json(model)
+        enc = (ea, oe.init_encoder(ea, EXEC["seed"]))
+    loss_ref, G = om.simulate_ranks(arch, P0, batch, plan, forced_routes=routes, flips=flips, encoder=enc)
     rep = {"loss": step_loss, "loss_ref": loss_ref, "grads": {},
            "flip_rate": {l: float(np.mean(v)) for l, v in flips.items()}}
     for l, f in rep["flip_rate"].items():
