@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the fwd+bwd+AdamW training step (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c4|c0] [--impl opx|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4|c0] [--impl opx|reference]
 
 N > 1 is launched by the driver under torchrun (one rank per GPU).  Rank 0
 prints ONE JSON line.  `value` is whole-job tokens/s from device time (CUDA
@@ -35,6 +35,13 @@ QWEN2_72B_SLICE = {"layers": 8, "hidden": 8192, "heads": 64, "kv_heads": 8, "hea
 QWEN3_30B_A3B = {"layers": 48, "hidden": 2048, "heads": 16, "kv_heads": 4, "head_dim": 128,
                  "ffn_dim": 6144, "vocab": 151936,
                  "moe": {"num_experts": 128, "top_k": 8, "expert_ffn_dim": 768, "moe_layer_stride": 1}}
+# C3: Qwen2.5-VL-7B-shaped = the Qwen2-7B backbone + a frozen ViT (32 x 1280, 16
+# heads of 80; ffn 3420 rounded up to 3456 for the 128-wide tiles; 14x14x3x2
+# patches = 1176 wide; 2x2 merger -> 256 tokens per 448x448 image)
+QWEN25_VL_VIT = {"layers": 32, "hidden": 1280, "heads": 16, "kv_heads": 16, "head_dim": 80,
+                 "ffn_dim": 3456, "vocab": 1176}
+C3_TOKENS_PER_IMAGE = 256
+C3_IMAGES_PER_ROW = 64  # 16K of the 64K tokens are image tokens (25 % modality mix)
 # C0: 2 layers, H=256, 4 heads of 64, 2 kv heads, ffn 768, V=2048, S=1024
 TINY = {"layers": 2, "hidden": 256, "heads": 4, "kv_heads": 2, "head_dim": 64, "ffn_dim": 768,
         "vocab": 2048}
@@ -49,6 +56,10 @@ def plan_for(cfg: str, n: int) -> dict:
         # activations fit and recompute=none removes the extra forward.
         return {"dp_replicate": 1, "dp_shard": n // sp, "sp": sp, "ep": 1, "micro_batch": 1,
                 "recompute": "full" if n == 1 else "none", "fsdp_prefetch_depth": 1}
+    if cfg == "c3":  # FSDP + SP like C1 at 64K tokens per row: recompute below SP4
+        sp = min(n, 4)
+        return {"dp_replicate": 1, "dp_shard": n // sp, "sp": sp, "ep": 1, "micro_batch": 1,
+                "recompute": "full" if sp < 4 else "none", "fsdp_prefetch_depth": 1}
     if cfg == "c4":  # SP over all GPUs (SP8, shard 1); 128K tokens, one row
         # per-layer activations at 128K/sp tokens (~10 GB at SP4, ~5 GB at SP8):
         # keep them from 8 GPUs, recompute below
@@ -67,17 +78,21 @@ def plan_for(cfg: str, n: int) -> dict:
 
 
 def model_for(cfg: str, n: int = 8) -> dict:
-    arch = dict({"c1": QWEN2_7B, "c0": TINY, "c2": QWEN3_30B_A3B, "c4": QWEN2_72B_SLICE}[cfg])
+    arch = dict({"c1": QWEN2_7B, "c0": TINY, "c2": QWEN3_30B_A3B, "c3": QWEN2_7B,
+                 "c4": QWEN2_72B_SLICE}[cfg])
     if cfg == "c2" and n < 8:
         # 30B does not fit below 8 GPUs (reference memory model: 235/455 GiB at
         # EP2/EP1); scale the layer count with the GPU count (a layer slice)
         arch["layers"] = 48 * n // 8
-    return {"param_dtype_bytes": 2,
-            "modules": [{"name": "core", "kind": "foundation", "trainable": True, "arch": arch}]}
+    mods = [{"name": "core", "kind": "foundation", "trainable": True, "arch": arch}]
+    if cfg == "c3":
+        mods.append({"name": "vision", "kind": "encoder", "trainable": False,
+                     "tokens_per_item": C3_TOKENS_PER_IMAGE, "arch": dict(QWEN25_VL_VIT)})
+    return {"param_dtype_bytes": 2, "modules": mods}
 
 
 def seq_for(cfg: str) -> int:
-    return {"c1": 32768, "c0": 1024, "c2": 8192, "c4": 131072}[cfg]
+    return {"c1": 32768, "c0": 1024, "c2": 8192, "c3": 65536, "c4": 131072}[cfg]
 
 
 def cluster_for(n: int) -> dict:
@@ -334,8 +349,24 @@ def main():
     sess = Session(cluster_for(n), model, wl, plan, ex, rank=rank, device=local, dist=dist)
     sess.init_weights(2508)
     batch = synthetic_batch(arch["vocab"], S, rows, seed=2508)
+    enc = next((m for m in model["modules"] if m["kind"] == "encoder"), None)
+    if enc:
+        from paper_2508_02317_b200.runtime import rank_coords, synthetic_images
+
+        synthetic_images(batch, enc["tokens_per_item"], enc["arch"]["vocab"], C3_IMAGES_PER_ROW,
+                         placeholder=arch["vocab"] - 1)
     ids, labels, pos, cu, n_valid = local_slice(batch, rank, plan)
     h2d = ids.nbytes + labels.nbytes + pos.nbytes + cu.nbytes
+    n_img = n_patch_local = 0
+    if enc:  # this rank's dp rows' items; it uploads the patches of items j % sp == its SP index
+        rep_i, sh_i, sp_i = rank_coords(rank, plan)
+        dp_i = rep_i * plan["dp_shard"] + sh_i
+        img = batch["img"]
+        mine = np.nonzero((img["row"] >= dp_i * plan["micro_batch"]) &
+                          (img["row"] < (dp_i + 1) * plan["micro_batch"]))[0]
+        n_img = len(mine)
+        n_patch_local = len(mine[sp_i::plan["sp"]]) * 4 * enc["tokens_per_item"]
+        h2d += n_patch_local * enc["arch"]["vocab"] * 2 + n_img * 8 + n_img
     sess.load(batch)
     for _ in range(args.warmup):
         sess.run()
@@ -373,6 +404,26 @@ def main():
     fpt_ref = 6.0 * (arch["layers"] * active_layer_params(arch) + 2 * arch["vocab"] * arch["hidden"]
                      + arch["hidden"]) + 6.0 * arch["layers"] * arch["hidden"] * S
     exact = exact_flops_per_step(arch, batch, tokens_step)
+    enc_line = None
+    if enc:  # frozen encoder forward: 2 * params per patch + bidirectional attention
+        ea = enc["arch"]
+        He, Fe, nb = ea["hidden"], ea["ffn_dim"], ea["layers"]
+        Wq = ea["heads"] * ea["head_dim"]
+        P_item = 4 * enc["tokens_per_item"]
+        blk = He * 3 * Wq + Wq * He + 3 * He * Fe
+        per_patch = 2.0 * (nb * blk + ea["vocab"] * He + 4 * He * He + He * arch["hidden"])
+        n_items_all = len(batch["img"]["row"])
+        enc_flops = n_items_all * P_item * (per_patch + nb * 4.0 * Wq * P_item)
+        exact += enc_flops
+        fpt_ref += enc_flops / tokens_step
+        en = [e["dur"] for e in trace["traceEvents"] if e["name"] == f"encoder.{enc['name']}.m0"]
+        sc = [e["dur"] for e in trace["traceEvents"] if e["name"] == f"scatter.{enc['name']}.m0"]
+        enc_line = {"items_per_step": n_items_all, "patches_per_item": P_item,
+                    "image_token_fraction": n_items_all * enc["tokens_per_item"] / tokens_step,
+                    "encoder_ms": statistics.mean(en) / 1e3 if en else None,
+                    "scatter_ms": statistics.mean(sc) / 1e3 if sc else None,
+                    "encoder_tflops_per_gpu": (enc_flops / n) / (statistics.mean(en) * 1e-6) / 1e12 if en else None,
+                    "model": "qwen2.5-vl-7b-shaped ViT, frozen (fwd only, no 2-D RoPE / windows)"}
     per_gpu = value / n
     # roofline: dominant kernel = the forward MLP block (gate|up GEMM + SwiGLU
     # epilogue + down GEMM), 6*T*H*F algorithmic FLOPs per layer-call
@@ -404,6 +455,7 @@ def main():
         "mfu_exact": exact / t_mean / n / peak, "model_flops_per_token_ref": fpt_ref,
         "config": {"workload": cfg, "model": {"c1": "qwen2-7b-shaped (random init)",
                                               "c2": f"qwen3-30b-a3b-shaped, {arch['layers']} layers (random init)",
+                                              "c3": "qwen2.5-vl-7b-shaped: qwen2-7b backbone + frozen ViT (random init)",
                                               "c4": "qwen2-72b-shaped 8-layer slice (random init)"}.get(cfg, cfg),
                    "global_batch": rows, "seq_len": S, "tokens_per_step": tokens_step,
                    "parallelism": f"fsdp{plan['dp_shard']}xsp{plan['sp']}",
@@ -430,6 +482,8 @@ def main():
         "host_enqueue_ms": statistics.mean(enq) * 1e3, "host_cpus": os.cpu_count(),
         "hbm_free_gb": torch.cuda.mem_get_info(local)[0] / 1e9,
     }
+    if enc_line:
+        line["encoder"] = enc_line
     if not args.no_cpu_baseline and n == 1:
         ref = cpu_reference(cfg, budget_s=15.0)
         line["cpu_baseline"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -71,9 +71,9 @@ def synthetic_images(batch, tokens_per_item: int, patch_dim: int, items_per_row:
                      placeholder: int | None = None, seed: int = 2508):
     """Places up to ``items_per_row`` image items in every row of ``batch`` (in
     place) for a frozen encoder module: an item occupies
-    ``tokens_per_item`` placeholder tokens right after the first token of a
-    sample long enough to hold it; those positions, and the one predicting the
-    first of them, are unsupervised.  Adds batch["img"] = {"row", "pos",
+    ``tokens_per_item`` placeholder tokens inside one sample (from its second
+    token, 8 text tokens between consecutive images); those positions, and the
+    one predicting the first of them, are unsupervised.  Adds batch["img"] = {"row", "pos",
     "pixels" [n, 4*tokens_per_item, patch_dim] float32} sorted by (row, pos)."""
     rng = np.random.default_rng(seed + 1)
     ids, labels = batch["ids"], batch["labels"]
@@ -82,16 +82,14 @@ def synthetic_images(batch, tokens_per_item: int, patch_dim: int, items_per_row:
     for r, cu in enumerate(batch["cu_rows"]):
         placed = 0
         for a, b in zip(cu[:-1], cu[1:]):
-            if placed == items_per_row:
-                break
-            if b - a < tokens_per_item + 2:
-                continue
-            p0 = a + 1
-            ids[r, p0:p0 + tokens_per_item] = vocab_ph
-            labels[r, p0 - 1:p0 + tokens_per_item] = -100
-            rows.append(r)
-            pos.append(p0)
-            placed += 1
+            p0 = a + 1  # images back to back (8 text tokens apart) from the sample's 2nd token
+            while placed < items_per_row and p0 + tokens_per_item + 1 <= b:
+                ids[r, p0:p0 + tokens_per_item] = vocab_ph
+                labels[r, p0 - 1:p0 + tokens_per_item] = -100
+                rows.append(r)
+                pos.append(p0)
+                placed += 1
+                p0 += tokens_per_item + 8
     n = len(rows)
     pix = rng.standard_normal((n, 4 * tokens_per_item, patch_dim)).astype(np.float32)
     batch["img"] = {"row": np.array(rows, np.int32), "pos": np.array(pos, np.int32), "pixels": pix}
@@ -191,7 +189,10 @@ class Session:
             sel = np.nonzero((img["row"] >= dp * m) & (img["row"] < (dp + 1) * m))[0]
             rows = np.ascontiguousarray(img["row"][sel] - dp * m, np.int32)
             posi = np.ascontiguousarray(img["pos"][sel], np.int32)
-            pix = _bf16_bits(img["pixels"][sel]) if len(sel) else np.zeros(1, np.uint16)
+            if "_bf16" not in img:  # converted once per batch
+                img["_bf16"] = _bf16_bits(img["pixels"])
+            # items are sorted by row: this rank's rows are one contiguous (view) range
+            pix = img["_bf16"][sel[0]:sel[-1] + 1] if len(sel) else np.zeros(1, np.uint16)
             check(lib().opx_step_load_images(self.h, pix.ctypes.data_as(ctypes.c_void_p), len(sel),
                                              rows.ctypes.data_as(ctypes.c_void_p),
                                              posi.ctypes.data_as(ctypes.c_void_p)))
