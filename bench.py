@@ -439,7 +439,7 @@ def main():
     achieved = mlp_flops / node_s
     share = {}
     for e in trace["traceEvents"]:
-        if e["tid"] != 0:
+        if e["tid"] != 0 or e["name"].endswith(".m0.moe"):  # parent span of the MoE sub-nodes
             continue
         key = e["name"].split(".m0.")[-1] if ".m0." in e["name"] else e["name"]
         key = ("bwd." if e["name"].startswith("bwd") else "fwd." if e["name"].startswith("fwd.layer") else "") + key

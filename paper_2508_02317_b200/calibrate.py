@@ -89,10 +89,10 @@ def node_costs(plan: dict, model: dict, workload: dict, dtype_bytes: int = 2) ->
 # measured trace node (suffix after ".m0.") -> reference node (suffix) it realises
 _MEASURED_TO_REF = {
     "fwd": {"qkv_proj": "qkv_proj", "attn_core": "attn_core", "out_proj": "out_proj", "mlp": "mlp",
-            "router": "router", "experts": "experts", "unpermute": "experts",
+            "router": "router", "experts": "experts", "experts_b": "experts", "unpermute": "experts",
             "a2a_qkv": "a2a_q", "a2a_out": "a2a_out", "a2a_counts": "a2a_dispatch",
             "a2a_dispatch": "a2a_dispatch", "a2a_combine": "a2a_combine"},
-    "bwd": {"router": "router", "experts": "experts", "gate_up_recompute": "experts",
+    "bwd": {"router": "router", "experts": "experts", "experts_b": "experts", "gate_up_recompute": "experts",
             "a2a_combine_grad": "a2a_combine_grad", "a2a_dispatch_grad": "a2a_dispatch_grad",
             "a2a_redispatch_wait": "a2a_combine_grad", "combine_bwd": "experts"},
 }

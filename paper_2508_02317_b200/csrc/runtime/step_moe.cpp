@@ -454,7 +454,8 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
     mk("a2a_combine");
     TRY(barrier_ep(cs_));
     CU(cudaStreamWaitEvent(cs_, done_b, 0));
-    mk("a2a_wait");
+    // the compute stream now waits for half B: its expert GEMMs, combine and barrier
+    mk("experts_b");
   } else {
     TRY(phase(0, El_, cs_, 0, true));
   }
@@ -559,7 +560,7 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     mk("a2a_dispatch_grad");
     TRY(barrier_ep(cs_));
     CU(cudaStreamWaitEvent(cs_, done_b, 0));
-    mk("a2a_wait");
+    mk("experts_b");  // half B's expert backward, dX combine and barrier
   } else {
     CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
                       d_dyrecv_peers_, H, H, cs_));
