@@ -92,6 +92,11 @@ __device__ __forceinline__ uint64_t md(uint32_t base, int k, int lbo) {
   do {              \
   } while (0)
 #endif
+// 1/POLY_SHARE of the P exponentials on the FMA-pipe polynomial (8, 4 or 0 = none)
+#ifndef OPX_BWD_POLY_SHARE
+#define OPX_BWD_POLY_SHARE 0
+#endif
+constexpr int POLY_SHARE = OPX_BWD_POLY_SHARE;
 __device__ __forceinline__ void bar_sync_softmax() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -325,7 +330,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           f2unpack(ffma2(f2pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sc2,
                          f2pack(-lv[i], -lv[i + 1])),
                    x0, x1);
-          const float p0 = (i & 7) == 6 ? exp2_fma(x0) : ex2(x0);
+          const bool poly = POLY_SHARE == 8 ? (i & 7) == 6 : POLY_SHARE == 4 ? (i & 3) == 2 : false;
+          const float p0 = poly ? exp2_fma(x0) : ex2(x0);
           const float p1 = ex2(x1);
           const uint64_t pp = f2pack(p0, p1);
           const uint64_t dd = fadd2(f2pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
@@ -351,10 +357,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      pp[1] * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
         }
       }
-      // the gradient MMAs of tile it-1 read sP/sS: wait for them (dQ^T(it-1)
-      // drain), then publish P/dS(it)
+      // the gradient MMAs of tile it-1 read sP/sS: wait for them, publish
+      // P/dS(it) so the MMA warp can issue tile it's gradients at once, then
+      // drain dQ^T(it-1) from its TMEM buffer while they run
       if (pt) PROF(it, 6);
-      if (it > 0) drain_dq(it - 1);
+      if (it > 0) ptx::mbar_wait(&dq_full[(it - 1) & 1], ((it - 1) >> 1) & 1);
       if (pt) PROF(it, 9);
       uint8_t* sP = smem + OFF_P;
       uint8_t* sS = smem + OFF_S;
@@ -370,6 +377,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_ready);
       if (pt) PROF(it, 7);
+      if (it > 0) drain_dq(it - 1);
       if (it + 1 < niter) load_cols(it + 1);
       bar_sync_softmax();  // next tile's column data visible
       if (pt) PROF(it, 10);
