@@ -473,7 +473,11 @@ def main():
                      "frac": achieved / peak_sus, "peak_kind": f"{peak_kind} sustained",
                      "traffic": mlp_traffic(cfg, T_loc),
                      "traffic_unit": "bytes per node (ncu dram__bytes_read+write, profiles/ncu_traffic.json)",
-                     "flops_per_launch": mlp_flops, "launch_ms": node_s * 1e3},
+                     "flops_per_launch": mlp_flops, "launch_ms": node_s * 1e3,
+                     "frac_of_burst": achieved / peak,
+                     "note": "peak = the driver's sustained figure (cuBLAS bf16 8192^3 back to back under "
+                             "the power cap); the node's tcgen05 GEMMs can exceed it (frac > 1), "
+                             "frac_of_burst is against the burst figure"},
         "phase_share": {k: round(v / tot, 4) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:16]},
         "node_ms": {k: round(v * 1e3, 2) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:24]},
         "clocks": clk.summary(),
