@@ -24,10 +24,11 @@
 // The S^T/dP^T MMAs of tile i+1 are issued as soon as the softmax warps have
 // pulled S^T/dP^T(i) into registers (s_free), so they overlap the softmax of
 // tile i.  The softmax publishes tile i+1's P/dS before draining dQ^T(i), so
-// dV/dK(i+1) run during the drain and only dQ^T(i+1) waits for it.  With the
-// M=128, N=64 shapes the MMAs are bound by the 128 B/clk smem port (6 KB per
-// 32-cycle S/dP/dQ instruction); taking P^T/dS^T from TMEM halves the smem
-// reads of dV/dK (+3-4 %).
+// dV/dK(i+1) run during the drain and only dQ^T(i+1) waits for it.  The
+// M=128, N=64 S/dP/dQ MMAs read 6 KB of smem per 32-cycle instruction (above
+// the 128 B/clk port while they run); taking P^T/dS^T from TMEM halves the
+// smem reads of dV/dK (+3-4 %).  Over the kernel the tensor pipe is ~34 %
+// busy: one chain per SM is latency-bound.
 #include <cuda.h>
 
 #include <algorithm>
