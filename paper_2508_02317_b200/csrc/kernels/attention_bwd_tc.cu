@@ -55,7 +55,8 @@ constexpr float LOG2E = 1.4426950408889634f;
 // S/dP MMAs of the next tile)
 constexpr int QSTAGES = 3;
 constexpr int OFF_K = 0, OFF_V = 32768, OFF_Q = 65536 /*[3] x 16K*/, OFF_O = 114688 /*[3] x 16K*/,
-              OFF_P = 163840, OFF_S = 180224, OFF_STAGE = 196608 /*32K fp32*/, OFF_MISC = 229376;
+              /* [163840, 180224) unused since P^T moved to TMEM */
+              OFF_S = 180224, OFF_STAGE = 196608 /*32K fp32*/, OFF_MISC = 229376;
 constexpr int SMEM = 1024 + OFF_MISC + 3 * 2 * BQ * 4 + 256;
 static_assert(3 * 2 * BQ * 4 + 13 * 8 + 8 <= 3 * 2 * BQ * 4 + 256, "misc region");
 

@@ -320,7 +320,13 @@ class Step {
     return -1;
   }
   int** d_count_tables_ = nullptr;
-  bf16** d_xrecv_peers_ = nullptr;
+  bf16** d_xrecv_peers_ = nullptr;  // [1 + L][kMaxSp]: slot 0 shared, 1 + l kept by layer l
+  // recompute=none: layers whose dispatched tokens stay in their own arena
+  // slot until the backward (no re-send on xs_), chosen by free HBM at setup
+  std::vector<size_t> off_xrecv_l_;  // [L], 0 = uses the shared buffer
+  bool keeps_x(int l) const { return l >= 0 && size_t(l) < off_xrecv_l_.size() && off_xrecv_l_[size_t(l)]; }
+  bf16* xrecv_of(int l) { return reinterpret_cast<bf16*>(arena_ + (keeps_x(l) ? off_xrecv_l_[size_t(l)] : off_xrecv_)); }
+  bf16** xrecv_peers_of(int l) { return d_xrecv_peers_ + (keeps_x(l) ? size_t(1 + l) * kMaxSp : 0); }
   bf16** d_yback_peers_ = nullptr;
   bf16** d_dyrecv_peers_ = nullptr;
   bf16** d_dxback_peers_ = nullptr;

@@ -13,6 +13,7 @@
 // (step_graph.cpp:253-293); the backward mirrors it (a2a_combine_grad,
 // experts, a2a_dispatch_grad) and adds the router gradient.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.h"
@@ -148,6 +149,40 @@ size_t Step::moe_arena(size_t off) {
   off_xrecv_ = take(size_t(cap_rows_) * H * 2);
   off_dyrecv_ = take(size_t(cap_rows_) * H * 2);
   off_dxback_ = take(P * H * 2);
+  // recompute=none with EP: give the top MoE layers their own dispatch buffer
+  // (worst-case rows) while HBM allows, so their backward needs no token
+  // re-send (OPX_MOE_KEEP_X_MARGIN_GB of headroom kept for the rest)
+  off_xrecv_l_.assign(size_t(L), 0);
+  if (save_acts_ && ep_ > 1) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      const char* e = getenv("OPX_MOE_KEEP_X_MARGIN_GB");
+      const size_t margin = size_t(e ? atof(e) : 48.0) << 30;
+      const size_t per = size_t(rup(int64_t(size_t(cap_rows_) * H * 2), 256));
+      const size_t budget = free_b > off + margin ? free_b - off - margin : 0;
+      int K = int(std::min<size_t>(size_t(L), budget / per));
+      // every rank must agree (peers store into each other's kept slots)
+      if (world_comm_) {
+        int* d = nullptr;
+        if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
+          cudaMemcpy(d, &K, sizeof(int), cudaMemcpyHostToDevice);
+          if (ncclAllReduce(d, d, 1, ncclInt32, ncclMin, world_comm_, cs_) == ncclSuccess &&
+              cudaStreamSynchronize(cs_) == cudaSuccess)
+            cudaMemcpy(&K, d, sizeof(int), cudaMemcpyDeviceToHost);
+          else
+            K = 0;
+          cudaFree(d);
+        } else {
+          K = 0;
+        }
+      }
+      for (int l = L - 1; l >= 0 && K > 0; --l) {
+        if (!a_.is_moe_layer(l)) continue;
+        off_xrecv_l_[size_t(l)] = take(size_t(cap_rows_) * H * 2);
+        --K;
+      }
+    }
+  }
   return off;
 }
 
@@ -200,7 +235,7 @@ int Step::moe_alloc() {
     for (auto& e : ev_redisp_) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   d_count_tables_ = alloc<int*>(kMaxSp * routes_.size());
-  d_xrecv_peers_ = alloc<bf16*>(kMaxSp);
+  d_xrecv_peers_ = alloc<bf16*>(kMaxSp * (1 + size_t(a_.layers)));
   d_yback_peers_ = alloc<bf16*>(kMaxSp * routes_.size());
   d_dyrecv_peers_ = alloc<bf16*>(kMaxSp);
   d_dxback_peers_ = alloc<bf16*>(kMaxSp);
@@ -251,7 +286,7 @@ int Step::moe_import() {
   const size_t ns = routes_.size();
   std::vector<void*> fl(kMaxSp, nullptr), fl2(kMaxSp, nullptr), fl3(kMaxSp, nullptr),
       ct(kMaxSp * ns, nullptr),
-      xr(kMaxSp, nullptr),
+      xr(kMaxSp * (1 + size_t(a_.layers)), nullptr),
       yb(kMaxSp * ns, nullptr), dy(kMaxSp, nullptr), dx(kMaxSp, nullptr);
   for (int j = 0; j < ep_; ++j) {
     fl[size_t(j)] = ep_peer(j, off_flags_ep_);
@@ -262,6 +297,8 @@ int Step::moe_import() {
       yb[sl * kMaxSp + size_t(j)] = ep_peer(j, off_yback_s_[sl]);
     }
     xr[size_t(j)] = ep_peer(j, off_xrecv_);
+    for (int l = 0; l < a_.layers; ++l)
+      if (keeps_x(l)) xr[size_t(1 + l) * kMaxSp + size_t(j)] = ep_peer(j, off_xrecv_l_[size_t(l)]);
     dy[size_t(j)] = ep_peer(j, off_dyrecv_);
     dx[size_t(j)] = ep_peer(j, off_dxback_);
   }
@@ -270,7 +307,7 @@ int Step::moe_import() {
   CU(cudaMemcpy(d_ep_flags2_, fl2.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_ep_flags3_, fl3.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_count_tables_, ct.data(), b * ns, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(d_xrecv_peers_, xr.data(), b, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_xrecv_peers_, xr.data(), b * (1 + size_t(a_.layers)), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_yback_peers_, yb.data(), b * ns, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_dyrecv_peers_, dy.data(), b, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_dxback_peers_, dx.data(), b, cudaMemcpyHostToDevice));
@@ -278,7 +315,7 @@ int Step::moe_import() {
 }
 
 int Step::moe_redispatch(int l) {
-  if (l < 0 || !xs_ || !keeps_acts(l) || !a_.is_moe_layer(l)) return OPX_OK;
+  if (l < 0 || !xs_ || !keeps_acts(l) || !a_.is_moe_layer(l) || keeps_x(l)) return OPX_OK;
   const MoeRoute& r = routes_[size_t(1 + l)];
   const int* counts = reinterpret_cast<const int*>(arena_ + off_counts_s_[size_t(1 + l)]);
   const int P = T_ * topk_;
@@ -362,7 +399,9 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   const bf16* Wgu = eu.full + eu.params[0].off;
   const bf16* Wd = eu.full + eu.params[1].off;
   int* counts_all = counts_cur();
-  bf16* xrecv = reinterpret_cast<bf16*>(arena_ + off_xrecv_);
+  const int xl = in_recompute_ ? -1 : l;  // a kept layer's own dispatch buffer
+  bf16* xrecv = xrecv_of(xl);
+  bf16** xpeers = xrecv_peers_of(xl);
   bf16* yback = yback_cur();
   CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_));
   CU(k_moe_topk(r_logits_, T, E, k, r_idx_, r_wts_, cs_));
@@ -379,7 +418,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   // down -> combine -> barrier, on stream st with barrier flag set `fs`
   auto phase = [&](int lo, int hi, cudaStream_t st, int fs, bool marks) -> int {
     CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                      d_xrecv_peers_, H, H, st, lo, hi));
+                      xpeers, H, H, st, lo, hi));
     if (marks) mk("a2a_dispatch");
     TRY(fs ? barrier_ep3(st) : barrier_ep(st));
     if (marks) mk("a2a_wait");
@@ -417,11 +456,11 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
     CU(cudaStreamWaitEvent(xs2_, ready, 0));
     // half B: dispatch, then its GEMMs after half A's
     CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                      d_xrecv_peers_, H, H, xs2_, h, El_));
+                      xpeers, H, H, xs2_, h, El_));
     TRY(barrier_ep3(xs2_));
     // half A on the compute stream
     CU(k_moe_dispatch(h2_, H, 0, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                      d_xrecv_peers_, H, H, cs_, 0, h));
+                      xpeers, H, H, cs_, 0, h));
     mk("a2a_dispatch");
     TRY(barrier_ep(cs_));
     mk("a2a_wait");
@@ -483,7 +522,7 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
   const bf16* Wgu = eu.full + eu.params[0].off;
   const bf16* Wd = eu.full + eu.params[1].off;
   int* counts_all = counts_cur();
-  bf16* xrecv = reinterpret_cast<bf16*>(arena_ + off_xrecv_);
+  bf16* xrecv = xrecv_of(kept ? l : -1);
   bf16* yback = yback_cur();
   bf16* dyrecv = reinterpret_cast<bf16*>(arena_ + off_dyrecv_);
   bf16* dxback = reinterpret_cast<bf16*>(arena_ + off_dxback_);
@@ -491,8 +530,10 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     // selective recompute: routing and combined outputs are resident; the
     // tokens were re-sent on xs_ (moe_redispatch, overlapping the layer above);
     // redo gate|up, storing the pre-activations for the SwiGLU backward
-    CU(cudaStreamWaitEvent(cs_, ev_redisp_[size_t(l)], 0));
-    mk("a2a_redispatch_wait");
+    if (!keeps_x(l)) {
+      CU(cudaStreamWaitEvent(cs_, ev_redisp_[size_t(l)], 0));
+      mk("a2a_redispatch_wait");
+    }
     CU(k_moe_zero_pad(xrecv, H, H, g_start_, g_rows_, g_rows_pad_, El_, cs_));
     GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu, H, false, GEMM_EPI_SWIGLU, gu_e_,
                          2 * Fe, El_, 0, g_start_, g_rows_, cap_rows_, 0);

@@ -118,6 +118,24 @@ def test_dist_moe_step_matches_oracle(world, plan, rows):
 
 
 @gpu
+def test_dist_moe_redispatch_path(monkeypatch):
+    """recompute=none with no HBM headroom for per-layer dispatch buffers:
+    the backward re-sends the tokens on the side stream (moe_redispatch)."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    from tests.step_common import tiny_moe
+
+    monkeypatch.setenv("OPX_MOE_KEEP_X_MARGIN_GB", "100000")
+    model = tiny_moe(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048, experts=64, top_k=4,
+                     expert_ffn=256)
+    plan = {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "recompute": "none"}
+    loss, sessions = _run(2, model, plan, 512, 2)
+    from paper_2508_02317_b200.runtime import synthetic_batch
+
+    compare_step(sessions, model, synthetic_batch(2048, 512, 2, seed=2508), plan, loss)
+
+
+@gpu
 def test_dist_c0_fsdp2_sp2_head_dim_64():
     """BASELINE C0 as specified: 2 layers, H=256, 4 heads of 64 (2 kv),
     ffn 768, V=2048, S=1024, FSDP2 x SP2 on 4 GPUs, global batch 2."""
