@@ -327,6 +327,10 @@ class Step {
   bool keeps_x(int l) const { return l >= 0 && size_t(l) < off_xrecv_l_.size() && off_xrecv_l_[size_t(l)]; }
   bf16* xrecv_of(int l) { return reinterpret_cast<bf16*>(arena_ + (keeps_x(l) ? off_xrecv_l_[size_t(l)] : off_xrecv_)); }
   bf16** xrecv_peers_of(int l) { return d_xrecv_peers_ + (keeps_x(l) ? size_t(1 + l) * kMaxSp : 0); }
+  // ... and, while HBM allows, their gate|up pre-activations and SwiGLU output
+  // (the backward then skips the gate|up recompute)
+  std::vector<bf16*> gu_l_, act_l_;  // [L]
+  bool keeps_gu(int l) const { return l >= 0 && size_t(l) < gu_l_.size() && gu_l_[size_t(l)]; }
   bf16** d_yback_peers_ = nullptr;
   bf16** d_dyrecv_peers_ = nullptr;
   bf16** d_dxback_peers_ = nullptr;

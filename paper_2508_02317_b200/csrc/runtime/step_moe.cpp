@@ -263,6 +263,26 @@ int Step::moe_alloc() {
   route_idx_.assign(size_t(a_.layers), nullptr);
   for (int l = 0; l < a_.layers; ++l)
     if (a_.is_moe_layer(l)) route_idx_[size_t(l)] = alloc<int>(P, false);
+  // kept-token layers (top first) also keep gate|up + SwiGLU while HBM leaves
+  // OPX_MOE_KEEP_GU_MARGIN_GB of headroom (a local choice: no peer sees them)
+  gu_l_.assign(size_t(a_.layers), nullptr);
+  act_l_.assign(size_t(a_.layers), nullptr);
+  {
+    size_t free_b = 0, total_b = 0;
+    const char* e = getenv("OPX_MOE_KEEP_GU_MARGIN_GB");
+    const size_t margin = size_t(e ? atof(e) : 16.0) << 30;
+    const size_t per = cap * 3 * Fe * 2 + 1024;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      size_t budget = free_b > margin ? free_b - margin : 0;
+      for (int l = a_.layers - 1; l >= 0 && budget >= per; --l) {
+        if (!keeps_x(l)) continue;
+        gu_l_[size_t(l)] = alloc<bf16>(cap * 2 * Fe, false);
+        act_l_[size_t(l)] = alloc<bf16>(cap * Fe);
+        if (!gu_l_[size_t(l)] || !act_l_[size_t(l)]) return cuda_fail(cudaErrorMemoryAllocation, "MoE kept gate|up");
+        budget -= per;
+      }
+    }
+  }
   if (ep_ == 1) TRY(moe_import());
   return OPX_OK;
 }
@@ -401,6 +421,12 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   int* counts_all = counts_cur();
   const int xl = in_recompute_ ? -1 : l;  // a kept layer's own dispatch buffer
   bf16* xrecv = xrecv_of(xl);
+  bf16 *gu_sv = gu_e_, *act_sv = act_e_;
+  const bool kg = !in_recompute_ && keeps_gu(l);  // store this layer's gate|up + SwiGLU
+  if (kg) {
+    gu_e_ = gu_l_[size_t(l)];
+    act_e_ = act_l_[size_t(l)];
+  }
   bf16** xpeers = xrecv_peers_of(xl);
   bf16* yback = yback_cur();
   CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_));
@@ -427,7 +453,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
     {
       // gate|up pre-activations are only needed by the backward (recompute pass)
       GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu + int64_t(lo) * 2 * Fe * H, H, false,
-                           GEMM_EPI_SWIGLU, in_recompute_ ? gu_e_ : nullptr, 2 * Fe, n, 0,
+                           GEMM_EPI_SWIGLU, (in_recompute_ || kg) ? gu_e_ : nullptr, 2 * Fe, n, 0,
                            g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
       g.D2 = act_e_;
       g.ldd2 = Fe;
@@ -468,7 +494,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
       const int n = hi - lo;
       CU(k_moe_zero_pad(xrecv, H, H, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
       GemmDesc g = grouped(0, 2 * Fe, H, xrecv, H, false, Wgu + int64_t(lo) * 2 * Fe * H, H, false,
-                           GEMM_EPI_SWIGLU, in_recompute_ ? gu_e_ : nullptr, 2 * Fe, n, 0,
+                           GEMM_EPI_SWIGLU, (in_recompute_ || kg) ? gu_e_ : nullptr, 2 * Fe, n, 0,
                            g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
       g.D2 = act_e_;
       g.ldd2 = Fe;
@@ -500,6 +526,8 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   }
   CU(k_moe_unpermute(yback, H, r_pos_, r_wts_, T, k, H, x2, x_out, cs_));
   mk("unpermute");
+  gu_e_ = gu_sv;
+  act_e_ = act_sv;
   return OPX_OK;
 }
 
@@ -526,7 +554,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
   bf16* yback = yback_cur();
   bf16* dyrecv = reinterpret_cast<bf16*>(arena_ + off_dyrecv_);
   bf16* dxback = reinterpret_cast<bf16*>(arena_ + off_dxback_);
-  if (kept) {
+  bf16 *gu_sv = gu_e_, *act_sv = act_e_;
+  if (kept && keeps_gu(l)) {  // gate|up and SwiGLU kept from the forward
+    gu_e_ = gu_l_[size_t(l)];
+    act_e_ = act_l_[size_t(l)];
+  } else if (kept) {
     // selective recompute: routing and combined outputs are resident; the
     // tokens were re-sent on xs_ (moe_redispatch, overlapping the layer above);
     // redo gate|up, storing the pre-activations for the SwiGLU backward
@@ -653,6 +685,8 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
       TRY(moe_redispatch(ln));
     }
   }
+  gu_e_ = gu_sv;
+  act_e_ = act_sv;
   return OPX_OK;
 }
 
