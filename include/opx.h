@@ -207,8 +207,8 @@ int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void*
                   int hq, int hk, int rows, int S, const int32_t* pos, const float* inv_freq,
                   void* stream);
 
-/* MoE routing (moe.cu): fp32 router logits with a fixed sequential K order and
- * separately rounded multiply/add, top-k with lower-index tie break, weights =
+/* MoE routing (moe.cu): fp32 router logits with a fixed sequential K order, each
+ * step one rounding of acc + h*w (the bf16 x bf16 product is exact), top-k with lower-index tie break, weights =
  * softmax renormalised over the selected experts (Qwen3 norm_topk_prob). */
 int opx_moe_route(const void* h, const void* w_router, int T, int H, int E, int k,
                   float* logits, int32_t* topk_idx, float* topk_w, void* stream);

@@ -243,8 +243,10 @@ def silu(x):
 
 
 def router_logits(h_bf16, w_bf16):
-    """fp32 logits with the GPU's fixed sequential K order and separate
-    rounding of every multiply and add (kernels/moe.cu router kernel)."""
+    """fp32 logits with the GPU's fixed sequential K order: every step rounds
+    acc + h*w once (the bf16 x bf16 product is exact in fp32, so the kernel's
+    fused multiply-add and this multiply-then-add agree bit for bit;
+    kernels/moe.cu router kernel)."""
     T, H = h_bf16.shape
     acc = np.zeros((T, w_bf16.shape[0]), F32)
     for kk in range(H):

@@ -29,7 +29,7 @@ using bf16 = __nv_bfloat16;
 // 32 staged through smem with 16-B loads; the next chunk is fetched into
 // registers while the current one is consumed.
 constexpr int RT = 32, RE = 128, RK = 32;
-// 256 threads; thread (ty, tx): tokens ty*2 .. +1, experts tx + 16*j (j < 8).
+// 256 threads; thread (ty, tx): tokens ty*2 .. +1, experts tx*4 + {0..3}, 64 + tx*4 + {0..3}.
 __global__ void __launch_bounds__(256, 2) router_kernel(const bf16* __restrict__ h,
                                                         const bf16* __restrict__ w,
                                                         float* __restrict__ logits, int T, int H,
@@ -88,18 +88,22 @@ __global__ void __launch_bounds__(256, 2) router_kernel(const bf16* __restrict__
     stash();
     __syncthreads();
     if (k0 + RK < H) fetch(k0 + RK);  // in flight during the FMAs below
-#pragma unroll 4
+#pragma unroll 8
     for (int kk = 0; kk < RK; ++kk) {
-      float hv[2], wv[8];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) hv[i] = sh[kk][ty * 2 + i];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) wv[j] = sw[kk][tx + 16 * j];
-      // k ascending, separately rounded multiply and add: the CPU oracle's order
+      // this thread's experts: tx*4 + {0..3} and 64 + tx*4 + {0..3} (two
+      // conflict-free 16-B loads); its tokens ty*2, ty*2 + 1 (one 8-B load)
+      const float2 hv = *reinterpret_cast<const float2*>(&sh[kk][ty * 2]);
+      const float4 wa = *reinterpret_cast<const float4*>(&sw[kk][tx * 4]);
+      const float4 wb = *reinterpret_cast<const float4*>(&sw[kk][64 + tx * 4]);
+      const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+      const float hh[2] = {hv.x, hv.y};
+      // k ascending; the product of two bf16 values is exact in fp32, so the
+      // fused multiply-add rounds exactly like the oracle's separate
+      // multiply (exact) and add (rounded)
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(hv[i], wv[j]));
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fmaf_rn(hh[i], wv[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(256, 2) router_kernel(const bf16* __restrict__
     if (t >= T) continue;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int e = e0 + tx + 16 * j;
+      const int e = e0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
       if (e < E) logits[int64_t(t) * E + e] = acc[i][j];
     }
   }
