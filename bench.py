@@ -132,9 +132,12 @@ def nvlink_rates(trace, plan, arch, S):
     if sp > 1:
         frac = (sp - 1) / sp
         qkv = T * (H + 2 * kvw) * 2 * frac
-        for key, b in (("fwd.a2a_qkv", qkv), ("fwd.a2a_out", T * H * 2 * frac)):
+        # kernel-only spans: the flag barrier after each exchange is its own
+        # node (a2a_wait, rank skew), not counted here
+        for key, b in (("fwd.a2a_qkv", qkv), ("fwd.a2a_out", T * H * 2 * frac),
+                       ("bwd.a2a_dqkv", qkv)):
             if key in nodes:
-                out[key.split(".")[1] + "_GBps"] = round(b * len(nodes[key]) / sum(nodes[key]) / 1e9, 1)
+                out[key.replace(".", "_") + "_GBps"] = round(b * len(nodes[key]) / sum(nodes[key]) / 1e9, 1)
     if ep > 1 and "moe" in arch:
         frac = (ep - 1) / ep
         b = T * arch["moe"]["top_k"] * H * 2 * frac

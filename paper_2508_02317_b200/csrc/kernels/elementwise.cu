@@ -2,6 +2,8 @@
 // fwd/bwd, embedding gather/scatter, fused softmax-cross-entropy fwd+bwd,
 // SwiGLU backward, fused AdamW, and small casts/reductions.  All are
 // vectorised (16 B per thread per access) and grid-strided.
+#include <algorithm>
+#include <cstdint>
 #include <cuda_bf16.h>
 
 #include "../runtime/kernels_api.h"
@@ -341,18 +343,24 @@ __global__ void __launch_bounds__(NT) ce_kernel(bf16* __restrict__ logits, int64
 // SwiGLU backward on 128-column interleaved gate|up:
 //   act = silu(g) * u ;  dg = da * u * silu'(g) ;  du = da * silu(g)
 // ---------------------------------------------------------------------------
-__global__ void swiglu_bwd_kernel(const bf16* __restrict__ dact, const bf16* __restrict__ gu,
-                                  bf16* __restrict__ dgu, int64_t T, int F) {
-  const int64_t n8 = T * (F / 8);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t row = i / (F / 8);
-    const int f = int(i % (F / 8)) * 8;
-    const int blk = f / 128, off = f % 128;
-    const int64_t gcol = int64_t(blk) * 256 + off;
-    const uint4 da = *reinterpret_cast<const uint4*>(dact + row * F + f);
-    const uint4 gq = *reinterpret_cast<const uint4*>(gu + row * 2 * F + gcol);
-    const uint4 uq = *reinterpret_cast<const uint4*>(gu + row * 2 * F + gcol + 128);
+// 2-D launch: x over 16-B column chunks of one row, y over rows, so no 64-bit
+// index division per element (it made the kernel instruction-bound);
+// sigmoid by the MUFU reciprocal (no IEEE-division slow path).
+__global__ void __launch_bounds__(NT) swiglu_bwd_kernel(const bf16* __restrict__ dact,
+                                                        const bf16* __restrict__ gu,
+                                                        bf16* __restrict__ dgu, int T, int F) {
+  const int n8 = F / 8;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n8) return;
+  const int f = c * 8;
+  const int gcol = (f / 128) * 256 + f % 128;
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < T; row += gridDim.y * blockDim.y) {
+    const bf16* dr = dact + int64_t(row) * F;
+    const bf16* gr = gu + int64_t(row) * 2 * F;
+    bf16* orow = dgu + int64_t(row) * 2 * F;
+    const uint4 da = *reinterpret_cast<const uint4*>(dr + f);
+    const uint4 gq = *reinterpret_cast<const uint4*>(gr + gcol);
+    const uint4 uq = *reinterpret_cast<const uint4*>(gr + gcol + 128);
     const uint32_t a[4] = {da.x, da.y, da.z, da.w}, g[4] = {gq.x, gq.y, gq.z, gq.w},
                    u[4] = {uq.x, uq.y, uq.z, uq.w};
     uint32_t og[4], ou[4];
@@ -364,7 +372,7 @@ __global__ void swiglu_bwd_kernel(const bf16* __restrict__ dact, const bf16* __r
       const float gg[2] = {gv.x, gv.y}, uu[2] = {uv.x, uv.y}, aa[2] = {av.x, av.y};
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const float sg = 1.f / (1.f + __expf(-gg[k]));
+        const float sg = __fdividef(1.f, 1.f + __expf(-gg[k]));
         const float si = gg[k] * sg;
         du[k] = aa[k] * si;
         dg[k] = aa[k] * uu[k] * sg * (1.f + gg[k] * (1.f - sg));
@@ -372,9 +380,8 @@ __global__ void swiglu_bwd_kernel(const bf16* __restrict__ dact, const bf16* __r
       og[e] = ptx::pack_bf16(dg[0], dg[1]);
       ou[e] = ptx::pack_bf16(du[0], du[1]);
     }
-    *reinterpret_cast<uint4*>(dgu + row * 2 * F + gcol) = make_uint4(og[0], og[1], og[2], og[3]);
-    *reinterpret_cast<uint4*>(dgu + row * 2 * F + gcol + 128) =
-        make_uint4(ou[0], ou[1], ou[2], ou[3]);
+    *reinterpret_cast<uint4*>(orow + gcol) = make_uint4(og[0], og[1], og[2], og[3]);
+    *reinterpret_cast<uint4*>(orow + gcol + 128) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
   }
 }
 
@@ -526,7 +533,20 @@ cudaError_t k_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __n
   if (F % 128) return cudaErrorInvalidValue;
   if (T <= 0) return cudaSuccess;
   ++g_kernel_launches;
-  swiglu_bwd_kernel<<<grid_for(T * F / 8), NT, 0, s>>>(dact, gu, dgu, T, F);
+  if (T > INT32_MAX) return cudaErrorInvalidValue;
+  // block = bx column chunks x (NT / bx) rows, bx the widest that wastes <= 1/16 of the lanes
+  const int n8 = F / 8;
+  int bx = 32;
+  for (int cand = NT; cand >= 32; cand /= 2)
+    if ((n8 + cand - 1) / cand * cand - n8 <= n8 / 16) {
+      bx = cand;
+      break;
+    }
+  const dim3 blk(bx, NT / bx);
+  const int gx = (n8 + bx - 1) / bx;
+  const int64_t gy_need = (T + blk.y - 1) / blk.y;
+  const int gy = int(std::min<int64_t>(gy_need, std::max(1, num_sms() * 16 / gx)));
+  swiglu_bwd_kernel<<<dim3(gx, gy), blk, 0, s>>>(dact, gu, dgu, int(T), F);
   return cudaGetLastError();
 }
 

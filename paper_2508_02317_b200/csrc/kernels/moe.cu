@@ -524,7 +524,7 @@ __global__ void swiglu_bwd_grouped_kernel(const bf16* __restrict__ dact, const b
       float dg[2], du[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const float sg = 1.f / (1.f + __expf(-gg[k]));
+        const float sg = __fdividef(1.f, 1.f + __expf(-gg[k]));
         du[k] = aa[k] * gg[k] * sg;
         dg[k] = aa[k] * uu[k] * sg * (1.f + gg[k] * (1.f - sg));
       }

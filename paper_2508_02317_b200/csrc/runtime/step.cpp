@@ -690,13 +690,21 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.hd = d_;
     a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
+    // the exchange kernel and the flag barrier are traced apart, so the
+    // node's NVLink rate is the kernel's own (the wait absorbs rank skew)
+    if (tr) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_qkv", ph, 0, e0, e1);
+      e0 = e1;
+    }
     TRY(barrier_sp(cs_));
-  }
-  if (tr) {
-    e1 = ev();
-    cudaEventRecord(e1, cs_);
-    mark(pre + ".a2a_qkv", ph, 0, e0, e1);
-    e0 = e1;
+    if (tr && p_.sp > 1) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_wait", ph, 0, e0, e1);
+      e0 = e1;
+    }
   }
   bf16* attn_out = relay_ ? ofull_ : o_loc(ob);
   {
@@ -739,11 +747,17 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.hd = d_;
     a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
-    TRY(barrier_sp(cs_));
     if (tr) {
       e1 = ev();
       cudaEventRecord(e1, cs_);
       mark(pre + ".a2a_out", ph, 0, e0, e1);
+      e0 = e1;
+    }
+    TRY(barrier_sp(cs_));
+    if (tr && p_.sp > 1) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_wait", ph, 0, e0, e1);
       e0 = e1;
     }
   }
@@ -973,13 +987,19 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.hd = d_;
     a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_head2seq(a, cs_));
+    if (tr) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_dqkv", ph, 0, e0, e1);
+      e0 = e1;
+    }
     TRY(barrier_sp(cs_));
-  }
-  if (tr) {
-    e1 = ev();
-    cudaEventRecord(e1, cs_);
-    mark(pre + ".a2a_dqkv", ph, 0, e0, e1);
-    e0 = e1;
+    if (tr && p_.sp > 1) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_wait", ph, 0, e0, e1);
+      e0 = e1;
+    }
   }
   bf16* dqkv = dqkv_loc(xb);
   CU(gemm_run(gd(T, H, Wqkv_, dqkv, Wqkv_, false, W.qkv, H, true, GEMM_EPI_F32, dtmp_, H), cs_));

@@ -168,9 +168,11 @@ def test_cross_entropy():
 
 # ---------------------------------------------------------------- SwiGLU bwd
 @gpu
-def test_swiglu_bwd():
+@pytest.mark.parametrize("T,F", [(64, 384), (3001, 1152), (517, 18944)])
+def test_swiglu_bwd(T, F):
+    """Ragged row counts and column-chunk counts that do not fill a block
+    (2-D launch: grid-strided rows, masked chunk lanes)."""
     torch.manual_seed(1)
-    T, F = 64, 384
     gu = bf(torch.randn(T, 2 * F, device=DEV))
     da = bf(torch.randn(T, F, device=DEV))
     dgu = torch.empty_like(gu)
