@@ -389,6 +389,15 @@ def main():
             kept = int(r.kept_layers)
             losses.append(r.loss)
     trace = sess.trace()
+    if os.environ.get("OPX_TRACE_DIR"):  # diagnostics: every rank's compute-stream node totals
+        tot_r = {}
+        for e in trace["traceEvents"]:
+            if e.get("tid", 0) == 0:
+                k = e["name"].split(".m0.")[-1] if ".m0." in e["name"] else e["name"]
+                k = e["name"].split(".", 1)[0] + "." + k
+                tot_r[k] = round(tot_r.get(k, 0.0) + e["dur"] * 1e-3, 3)
+        with open(os.path.join(os.environ["OPX_TRACE_DIR"], f"nodes_rank{rank}.json"), "w") as f:
+            json.dump(tot_r, f, indent=0, sort_keys=True)
     if dist:
         import torch.distributed as td
 
