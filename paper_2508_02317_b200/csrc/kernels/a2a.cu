@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../runtime/kernels_api.h"
 #include "ptx.cuh"
@@ -83,6 +84,89 @@ __global__ void seq2head_kernel(const A2AArgs a) {
     *reinterpret_cast<uint4*>(d) = lo;
     *reinterpret_cast<uint4*>(d + HALF) = hi;
   }
+}
+
+// seq->head with TMA bulk stores (hd == 128): a CTA rotates TB consecutive
+// tokens of one row into shared memory already in the destination layout
+// ([group][dst rank][TB tokens][per_rank heads][128]), then one thread per
+// (group, dst rank) issues a single cp.async.bulk of TB * per_rank * 256 B
+// straight into that rank's buffer (the TB tokens' rows are contiguous there).
+// Two staging buffers: the next chunk is rotated while the previous chunk's
+// copies drain over NVLink; an issuing thread waits for its own bulk group to
+// have READ the buffer before it is overwritten.
+__global__ void __launch_bounds__(512) seq2head_tma_kernel(const A2AArgs a, int TB) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  int heads = 0;
+  for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total;
+  const int S_loc = a.seq / a.sp;
+  const int nchunks = a.rows * S_loc / TB;
+  const int buf_elems = TB * heads * D;
+  const int work = TB * heads * 8;  // 8 threads per head vector (16 + 16 elements each)
+  const int ncopy = a.ngroups * a.sp;
+  const bf16* src = reinterpret_cast<const bf16*>(a.local[0]);
+  int it = 0;
+  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
+    bf16* sb = reinterpret_cast<bf16*>(smem_raw) + (it & 1) * buf_elems;
+    if (it >= 2) {
+      // the copies that read this buffer two chunks ago must be done reading it
+      if (threadIdx.x < ncopy) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncthreads();
+    }
+    const int r0 = chunk * TB;
+    for (int w = threadIdx.x; w < work; w += blockDim.x) {
+      const int t = w / (heads * 8);
+      const int rem = w - t * heads * 8;
+      int hh = rem >> 3;
+      const int c8 = rem & 7;
+      int gi = 0, hbase = 0;
+      while (hh >= a.g[gi].heads_total) hh -= a.g[gi].heads_total, hbase += a.g[gi++].heads_total;
+      const A2AGroup& G = a.g[gi];
+      const int per_rank = G.heads_total / a.sp;
+      const int dst_rank = hh / per_rank, hl = hh - dst_rank * per_rank;
+      const int r = r0 + t;
+      const int b = r / S_loc, p = r - b * S_loc;
+      const int gtok = b * a.seq + a.rank * S_loc + p;
+      const bf16* sp_ = src + int64_t(r) * a.local_ld + G.col0 + hh * D + c8 * 8;
+      uint4 lo = *reinterpret_cast<const uint4*>(sp_);
+      uint4 hi = *reinterpret_cast<const uint4*>(sp_ + D / 2);
+      if (G.rope) {
+        const float2* tb = a.rope_tab + int64_t(a.pos[gtok]) * (D / 2) + c8 * 8;
+        uint32_t* l = reinterpret_cast<uint32_t*>(&lo);
+        uint32_t* h = reinterpret_cast<uint32_t*>(&hi);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 x1 = ptx::unpack_bf16(l[e]), x2 = ptx::unpack_bf16(h[e]);
+          const float4 v = *reinterpret_cast<const float4*>(tb + 2 * e);
+          l[e] = ptx::pack_bf16(x1.x * v.y - x2.x * v.x, x1.y * v.w - x2.y * v.z);
+          h[e] = ptx::pack_bf16(x2.x * v.y + x1.x * v.x, x2.y * v.w + x1.y * v.z);
+        }
+      }
+      // staging: group gi's region, dst rank's slab, token t, local head hl
+      bf16* d = sb + int64_t(TB) * D * (hbase + dst_rank * per_rank) + (t * per_rank + hl) * D + c8 * 8;
+      *reinterpret_cast<uint4*>(d) = lo;
+      *reinterpret_cast<uint4*>(d + D / 2) = hi;
+    }
+    ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk copies
+    __syncthreads();
+    if (threadIdx.x < ncopy) {
+      const int gi = threadIdx.x / a.sp, j = threadIdx.x - gi * a.sp;
+      int hbase = 0;
+      for (int i = 0; i < gi; ++i) hbase += a.g[i].heads_total;
+      const A2AGroup& G = a.g[gi];
+      const int per_rank = G.heads_total / a.sp;
+      const int b = r0 / S_loc, p0 = r0 - b * S_loc;
+      const int64_t gtok0 = int64_t(b) * a.seq + int64_t(a.rank) * S_loc + p0;
+      const bf16* s = sb + int64_t(TB) * D * (hbase + j * per_rank);
+      bf16* dst = reinterpret_cast<bf16*>(G.full[j]) + gtok0 * per_rank * D;
+      const uint32_t bytes = uint32_t(TB) * per_rank * D * 2;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"(ptx::smem_u32(s)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  // every copy complete (written, not only read) before the kernel ends
+  if (threadIdx.x < ncopy) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __global__ void head2seq_kernel(const A2AArgs a) {
@@ -203,12 +287,42 @@ static dim3 a2a_block(int work) {
   return dim3(x, std::max(1, 256 / x));
 }
 
+// staging tokens per chunk for the bulk-store seq->head (0 = use the
+// per-thread peer-store kernel): hd 128 with a RoPE table, the chunk must not
+// cross a row, two buffers of TB token rows within ~100 KB
+static int seq2head_tb(const A2AArgs& a, int heads) {
+  // opt-in: measured slower than the per-thread peer stores (C1 SP2 q/k/v
+  // exchange 421 vs 524 GB/s)
+  static const int mode = getenv("OPX_A2A_TMA") ? atoi(getenv("OPX_A2A_TMA")) : 0;
+  const int hd = a.hd ? a.hd : D;
+  if (!mode || hd != D || !a.rope_tab || a.ngroups * a.sp > 512) return 0;
+  for (int i = 0; i < a.ngroups; ++i)
+    if (a.g[i].rope && !a.rope_tab) return 0;
+  const int S_loc = a.seq / a.sp;
+  for (int tb = 8; tb >= 1; tb /= 2)
+    if (S_loc % tb == 0 && 2 * tb * heads * D * 2 <= 100 * 1024) return tb;
+  return 0;
+}
+
 cudaError_t k_a2a_seq2head(const A2AArgs& a, cudaStream_t s) {
   int heads = 0;
   for (int i = 0; i < a.ngroups; ++i) heads += a.g[i].heads_total;
   const int T = a.rows * (a.seq / a.sp);
   const int hd = a.hd ? a.hd : D;
   if (T <= 0 || heads <= 0) return cudaSuccess;
+  if (const int tb = seq2head_tb(a, heads)) {
+    const int smem = 2 * tb * heads * D * 2;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(seq2head_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    const int per_sm = std::max(1, std::min(4, (220 * 1024) / (smem + 1024)));
+    const int blocks = std::min(T / tb, num_sms() * per_sm);
+    ++g_kernel_launches;
+    seq2head_tma_kernel<<<blocks, 512, smem, s>>>(a, tb);
+    return cudaGetLastError();
+  }
   const dim3 blk = a2a_block(heads * (hd / 16));
   const int blocks = std::min((T + int(blk.y) - 1) / int(blk.y), num_sms() * 32);
   ++g_kernel_launches;
