@@ -218,12 +218,34 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
   }
 }
 
-__global__ void colsum_kernel(const float* __restrict__ part, int rows, int cols,
-                              void* __restrict__ out, int accumulate, int out_bf16) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+// out[c] (+)= sum_r part[r, c].  Block = 32 columns x 16 row groups: each
+// thread sums every 16th row in order (4 interleaved accumulators), then the
+// 16 group sums are added in order, so the result is deterministic.  (One
+// thread per column walking all rows was latency-bound: 28 CTAs, ~0.2 TB/s.)
+constexpr int CS_COLS = 32, CS_GROUPS = 16;
+__global__ void __launch_bounds__(CS_COLS * CS_GROUPS) colsum_kernel(
+    const float* __restrict__ part, int rows, int cols, void* __restrict__ out, int accumulate,
+    int out_bf16) {
+  __shared__ float red[CS_GROUPS][CS_COLS + 1];
+  const int cx = threadIdx.x % CS_COLS, ry = threadIdx.x / CS_COLS;
+  const int c = blockIdx.x * CS_COLS + cx;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (c < cols) {
+    int r = ry;
+    for (; r + 3 * CS_GROUPS < rows; r += 4 * CS_GROUPS) {
+      a0 += part[int64_t(r) * cols + c];
+      a1 += part[int64_t(r + CS_GROUPS) * cols + c];
+      a2 += part[int64_t(r + 2 * CS_GROUPS) * cols + c];
+      a3 += part[int64_t(r + 3 * CS_GROUPS) * cols + c];
+    }
+    for (; r < rows; r += CS_GROUPS) a0 += part[int64_t(r) * cols + c];
+  }
+  red[ry][cx] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (ry != 0 || c >= cols) return;
   float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += part[int64_t(r) * cols + c];
+#pragma unroll
+  for (int g = 0; g < CS_GROUPS; ++g) s += red[g][cx];
   if (out_bf16) {
     bf16* o = static_cast<bf16*>(out);
     o[c] = __float2bfloat16(accumulate ? __bfloat162float(o[c]) + s : s);
@@ -493,7 +515,8 @@ cudaError_t k_rmsnorm_bwd(const float* dy, const float* x, const __nv_bfloat16* 
   else
     rmsnorm_bwd_kernel<8><<<nb, NT, 0, s>>>(dy, x, w, rstd, dres, dx, dw_part, T, H);
   ++g_kernel_launches;
-  colsum_kernel<<<(H + 127) / 128, 128, 0, s>>>(dw_part, nb, H, dw, accumulate_dw, dw_bf16);
+  colsum_kernel<<<(H + CS_COLS - 1) / CS_COLS, CS_COLS * CS_GROUPS, 0, s>>>(dw_part, nb, H, dw,
+                                                                           accumulate_dw, dw_bf16);
   return cudaGetLastError();
 }
 

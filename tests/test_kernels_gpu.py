@@ -120,7 +120,7 @@ def test_gemm_grouped(mode):
 
 # ---------------------------------------------------------------- RMSNorm
 @gpu
-@pytest.mark.parametrize("T,H", [(64, 256), (300, 3584), (17, 8192)])
+@pytest.mark.parametrize("T,H", [(64, 256), (300, 3584), (17, 8192), (2100, 3584), (1500, 1000)])
 def test_rmsnorm(T, H):
     torch.manual_seed(T)
     x = torch.randn(T, H, device=DEV)
@@ -144,6 +144,11 @@ def test_rmsnorm(T, H):
     torch.cuda.synchronize()
     assert rel_err(dx, xr.grad + dres) < 1e-4
     assert rel_err(dw, wr.grad) < 1e-4
+    # the dW column reduction has a fixed order: a second call is bit-identical
+    dw2 = torch.empty(H, device=DEV)
+    call("opx_rmsnorm_bwd", P(dy), P(x), P(w), P(rstd), P(dres), P(dx), P(part), P(dw2), T, H, S())
+    torch.cuda.synchronize()
+    assert torch.equal(dw, dw2)
 
 
 # ---------------------------------------------------------------- CE
