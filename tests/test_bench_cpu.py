@@ -1,0 +1,49 @@
+"""bench.py's trace accounting on synthetic traces (no GPU): the NVLink rates
+of the exchange kernels use the kernels' own spans, not the flag-barrier
+waits traced after them (Ulysses row)."""
+import importlib.util
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def bench():
+    spec = importlib.util.spec_from_file_location("bench_under_test", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _ev(name, dur_us):
+    return {"name": name, "ph": "X", "tid": 0, "ts": 0, "dur": dur_us, "args": {}}
+
+
+def test_ulysses_rates_exclude_barrier_wait(bench):
+    arch = {"hidden": 3584, "kv_heads": 4, "head_dim": 128}
+    plan = {"sp": 4, "micro_batch": 1}
+    S = 32768
+    T = S // 4
+    qkv = T * (3584 + 2 * 512) * 2 * 3 / 4          # bytes that leave the rank
+    out = T * 3584 * 2 * 3 / 4
+    ev = []
+    for l in range(3):
+        ev += [_ev(f"fwd.layer{l}.m0.a2a_qkv", qkv / 500e9 * 1e6),
+               _ev(f"fwd.layer{l}.m0.a2a_wait", 5000.0),   # rank skew: must not count
+               _ev(f"fwd.layer{l}.m0.a2a_out", out / 400e9 * 1e6),
+               _ev(f"bwd.layer{l}.m0.a2a_dqkv", qkv / 450e9 * 1e6),
+               _ev(f"bwd.layer{l}.m0.a2a_wait", 7000.0)]
+    r = bench.nvlink_rates({"traceEvents": ev}, plan, arch, S)
+    assert r["fwd_a2a_qkv_GBps"] == pytest.approx(500.0, abs=0.1)
+    assert r["fwd_a2a_out_GBps"] == pytest.approx(400.0, abs=0.1)
+    assert r["bwd_a2a_dqkv_GBps"] == pytest.approx(450.0, abs=0.1)
+    assert not any("wait" in k for k in r)
+
+
+def test_no_exchange_rates_without_sp(bench):
+    arch = {"hidden": 256, "kv_heads": 2, "head_dim": 64}
+    r = bench.nvlink_rates({"traceEvents": [_ev("fwd.layer0.m0.a2a_qkv", 10.0)]},
+                           {"sp": 1, "micro_batch": 1}, arch, 1024)
+    assert r == {"peak_GBps_per_direction": 900.0}
