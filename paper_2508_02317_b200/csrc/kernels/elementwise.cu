@@ -130,10 +130,8 @@ __global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const float* __restrict
 // dx_out = dres + rstd * (g - xhat * mean(g * xhat)),  g = dy * w,  xhat = x * rstd
 // dw partial over the block's rows -> dw_part[blockIdx.x, H]
 // V = float4s per thread (H <= NT*4*V), so registers scale with H; the next
-// row's x/dy/dres loads are issued before the current row's block reduction,
-// which keeps HBM busy across the __syncthreads (the kernel was latency bound;
-// the residual-gradient read used to be a dependent load after the reduction).
-// w is re-read per row from L1 (7 KB) to leave registers for the prefetch.
+// row's x/dy loads are issued before the current row's block reduction, which
+// keeps HBM busy across the __syncthreads (the kernel was latency bound).
 constexpr int BWD_ROWS = 16;
 template <int V>
 __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
@@ -142,47 +140,50 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
     float* __restrict__ dw_part, int T, int H) {
   __shared__ float red[2][NT / 32];
   const int nv = H / 4;
-  float4 dwacc[V], xn[V], dn[V], rn[V];
+  float4 dwacc[V], wv[V], xn[V], dn[V];
   const uint2* wr = reinterpret_cast<const uint2*>(w);
   const int r0 = blockIdx.x * BWD_ROWS;
   const int rows = min(BWD_ROWS, T - r0);
   auto load = [&](int64_t row) {
     const float4* xr = reinterpret_cast<const float4*>(x + row * H);
     const float4* gr = reinterpret_cast<const float4*>(dy + row * H);
-    const float4* rr = dres ? reinterpret_cast<const float4*>(dres + row * H) : nullptr;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const int idx = threadIdx.x + i * NT;
       if (idx < nv) {
         xn[i] = xr[idx];
         dn[i] = gr[idx];
-        rn[i] = rr ? rr[idx] : make_float4(0, 0, 0, 0);
       }
     }
   };
 #pragma unroll
-  for (int i = 0; i < V; ++i) dwacc[i] = make_float4(0, 0, 0, 0);
+  for (int i = 0; i < V; ++i) {
+    dwacc[i] = make_float4(0, 0, 0, 0);
+    const int idx = threadIdx.x + i * NT;
+    if (idx < nv) {
+      const uint2 q = wr[idx];
+      const float2 a = ptx::unpack_bf16(q.x), b = ptx::unpack_bf16(q.y);
+      wv[i] = make_float4(a.x, a.y, b.x, b.y);
+    }
+  }
   if (rows > 0) load(r0);
   for (int rr = 0; rr < rows; ++rr) {
     const int64_t row = r0 + rr;
     const float rs = rstd[row];
-    float4 xh[V], g[V], res[V];
+    float4 xh[V], g[V];
     float dot = 0.f;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       const int idx = threadIdx.x + i * NT;
       if (idx < nv) {
-        const uint2 q = wr[idx];
-        const float2 wa = ptx::unpack_bf16(q.x), wb = ptx::unpack_bf16(q.y);
         const float4 xv = xn[i], dv = dn[i];
         xh[i] = make_float4(xv.x * rs, xv.y * rs, xv.z * rs, xv.w * rs);
-        g[i] = make_float4(dv.x * wa.x, dv.y * wa.y, dv.z * wb.x, dv.w * wb.y);
+        g[i] = make_float4(dv.x * wv[i].x, dv.y * wv[i].y, dv.z * wv[i].z, dv.w * wv[i].w);
         dot += g[i].x * xh[i].x + g[i].y * xh[i].y + g[i].z * xh[i].z + g[i].w * xh[i].w;
         dwacc[i].x += dv.x * xh[i].x;
         dwacc[i].y += dv.y * xh[i].y;
         dwacc[i].z += dv.z * xh[i].z;
         dwacc[i].w += dv.w * xh[i].w;
-        res[i] = rn[i];
       }
     }
     if (rr + 1 < rows) load(row + 1);  // in flight during the reduction
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
 #pragma unroll
     for (int i = 0; i < NT / 32; ++i) tot += red[rr & 1][i];
     const float mean = tot / float(H);
+    const float4* rr4 = dres ? reinterpret_cast<const float4*>(dres + row * H) : nullptr;
     float4* o4 = reinterpret_cast<float4*>(dx_out + row * H);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
@@ -202,10 +204,13 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(
       if (idx < nv) {
         float4 o = make_float4(rs * (g[i].x - xh[i].x * mean), rs * (g[i].y - xh[i].y * mean),
                                rs * (g[i].z - xh[i].z * mean), rs * (g[i].w - xh[i].w * mean));
-        o.x += res[i].x;
-        o.y += res[i].y;
-        o.z += res[i].z;
-        o.w += res[i].w;
+        if (rr4) {
+          const float4 r = rr4[idx];
+          o.x += r.x;
+          o.y += r.y;
+          o.z += r.z;
+          o.w += r.w;
+        }
         o4[idx] = o;
       }
     }
