@@ -143,9 +143,13 @@ def nvlink_rates(trace, plan, arch, S):
         b = T * arch["moe"]["top_k"] * H * 2 * frac
         for key in ("fwd.a2a_dispatch", "fwd.a2a_combine", "bwd.a2a_combine_grad", "bwd.a2a_dispatch_grad"):
             if key in nodes:
-                # moe_overlap: the traced nodes carry the first expert half (the
-                # second half's exchange runs concurrently on another stream)
-                bk = b / 2 if plan.get("moe_overlap") else b
+                # moe_overlap: the dispatch-direction nodes (fwd dispatch, bwd dY
+                # dispatch = a2a_combine_grad) span BOTH halves' kernels (half B's
+                # is launched first on the side stream and fills the GPU, half A's
+                # ends the node); the combine-direction nodes carry half A only
+                # (half B's combine runs after its GEMMs)
+                dispatch_dir = key in ("fwd.a2a_dispatch", "bwd.a2a_combine_grad")
+                bk = b / 2 if plan.get("moe_overlap") and not dispatch_dir else b
                 out[key.replace(".", "_") + "_GBps"] = round(bk * len(nodes[key]) / sum(nodes[key]) / 1e9, 1)
     return out
 

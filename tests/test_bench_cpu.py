@@ -47,3 +47,21 @@ def test_no_exchange_rates_without_sp(bench):
     r = bench.nvlink_rates({"traceEvents": [_ev("fwd.layer0.m0.a2a_qkv", 10.0)]},
                            {"sp": 1, "micro_batch": 1}, arch, 1024)
     assert r == {"peak_GBps_per_direction": 900.0}
+
+
+def test_moe_overlap_rates_count_both_halves_in_dispatch_nodes(bench):
+    """With moe_overlap the dispatch-direction nodes span both expert halves'
+    kernels (full payload), the combine-direction nodes half A's only."""
+    arch = {"hidden": 2048, "kv_heads": 4, "head_dim": 128, "moe": {"top_k": 8}}
+    plan = {"sp": 1, "ep": 4, "micro_batch": 1, "moe_overlap": True}
+    S = 8192
+    b = S * 8 * 2048 * 2 * 3 / 4
+    ev = [_ev("fwd.layer0.m0.a2a_dispatch", b / 600e9 * 1e6),
+          _ev("fwd.layer0.m0.a2a_combine", b / 2 / 600e9 * 1e6),
+          _ev("bwd.layer0.m0.a2a_combine_grad", b / 400e9 * 1e6),
+          _ev("bwd.layer0.m0.a2a_dispatch_grad", b / 2 / 650e9 * 1e6)]
+    r = bench.nvlink_rates({"traceEvents": ev}, plan, arch, S)
+    assert r["fwd_a2a_dispatch_GBps"] == pytest.approx(600.0, abs=0.1)
+    assert r["fwd_a2a_combine_GBps"] == pytest.approx(600.0, abs=0.1)
+    assert r["bwd_a2a_combine_grad_GBps"] == pytest.approx(400.0, abs=0.1)
+    assert r["bwd_a2a_dispatch_grad_GBps"] == pytest.approx(650.0, abs=0.1)
