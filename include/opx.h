@@ -158,10 +158,7 @@ int opx_init_param(float* f32, void* b16, int64_t n, int64_t phys0, uint64_t key
                    uint64_t key_b, double c, float constant, int interleave,
                    int64_t rows_per_slab, int64_t cols, void* stream);
 uint64_t opx_param_key(const char* name, uint64_t seed);
-/* Causal varlen GQA attention, head_dim 128, layouts in kernels_api.h. */
-int opx_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t ldq,
-                 int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
-                 const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream);
+/* Causal varlen GQA attention (tcgen05/TMEM), head_dim 128, layouts in kernels_api.h. */
 int opx_attn_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse,
                     int64_t ldq, int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
                     const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream);
@@ -171,10 +168,6 @@ int opx_attn_fwd_bidir_tc(const void* q, const void* k, const void* v, void* o, 
                           int64_t ldq, int64_t ldk, int64_t ldv, int64_t ldo,
                           const int32_t* seq_start, const int32_t* seq_end, int N, int hq, int hk,
                           float scale, void* stream);
-int opx_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
-                 const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
-                 int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,
-                 int N, int hq, int hk, float scale, void* stream);
 int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, const float* lse,
                     const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
                     int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,

@@ -38,6 +38,28 @@ import numpy as np
 F32 = np.float32
 MASK64 = (1 << 64) - 1
 
+# C helpers (oracle/c/oracle_init.c, built by oracle/Makefile): bit-identical
+# restatements of init_values / bf16_round that only make large-width parity
+# tests fast; the numpy code below is the definition and the fallback.
+_CLIB = None
+
+
+def _clib():
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+        import os
+
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "liboracle_init.so")
+        _CLIB = False
+        if os.path.exists(path) and not os.environ.get("ORACLE_NO_C"):
+            L = ctypes.CDLL(path)
+            L.oracle_init_values.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_double, ctypes.c_void_p]
+            L.oracle_bf16_round.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+            _CLIB = L
+    return _CLIB
+
 
 # ----------------------------------------------------------------------------
 # configuration
@@ -97,6 +119,16 @@ def _splitmix(x: np.ndarray) -> np.ndarray:
 
 
 def init_values(key: int, n: int, std: float = 0.02, start: int = 0) -> np.ndarray:
+    L = _clib()
+    if L and n > 4096:
+        out = np.empty(n, F32)
+        L.oracle_init_values(key & MASK64, n, start, std * math.sqrt(3.0) / 16777216.0,
+                             out.ctypes.data)
+        return out
+    return init_values_np(key, n, std, start)
+
+
+def init_values_np(key: int, n: int, std: float = 0.02, start: int = 0) -> np.ndarray:
     i = np.arange(start, start + n, dtype=np.uint64)
     k = np.uint64(key)
     c = np.uint64(0xD1B54A32D192ED03)
@@ -150,6 +182,16 @@ def init_params(a: Arch, seed: int) -> dict:
 
 def bf16_round(x: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even to bfloat16, returned as float32."""
+    x = np.ascontiguousarray(x, dtype=F32)
+    L = _clib()
+    if L and x.size > 4096:
+        out = np.empty_like(x)
+        L.oracle_bf16_round(x.ctypes.data, out.ctypes.data, x.size)
+        return out
+    return bf16_round_np(x)
+
+
+def bf16_round_np(x: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=F32)
     u = x.view(np.uint32).astype(np.uint64)
     r = ((u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)

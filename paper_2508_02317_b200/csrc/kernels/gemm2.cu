@@ -424,20 +424,38 @@ cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const P2& p, int
 }  // namespace
 
 // Pool of zeroed ticket counters (per device).  Each launch takes the next
-// slot; kernels leave their slot at 0, so a slot is reusable once its launch
-// has finished (1024 launches later).
-static int* ticket_counter() {
+// slot; kernels leave their slot at 0, so a slot is reusable once its previous
+// launch has finished.  An event recorded after every launch orders the reuse:
+// the launch that takes a slot again first waits for that event on its own
+// stream, so more than kSlots launches in flight (no host sync, several
+// streams) can never share a live counter.
+static cudaError_t ticket_acquire(cudaStream_t s, int** ctr, cudaEvent_t* done) {
   constexpr int kSlots = 1024;
   static int* pool[64] = {};
+  static cudaEvent_t* evs[64] = {};
+  static bool used[64][kSlots] = {};
   static int next[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   if (!pool[dev]) {
-    if (cudaMalloc(&pool[dev], kSlots * sizeof(int)) != cudaSuccess) return nullptr;
-    if (cudaMemset(pool[dev], 0, kSlots * sizeof(int)) != cudaSuccess) return nullptr;
+    cudaError_t e = cudaMalloc(&pool[dev], kSlots * sizeof(int));
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemset(pool[dev], 0, kSlots * sizeof(int))) != cudaSuccess) return e;
+    evs[dev] = new cudaEvent_t[kSlots];
+    for (int i = 0; i < kSlots; ++i)
+      if ((e = cudaEventCreateWithFlags(&evs[dev][i], cudaEventDisableTiming)) != cudaSuccess)
+        return e;
   }
-  return pool[dev] + (next[dev]++ % kSlots);
+  const int i = next[dev]++ % kSlots;
+  if (used[dev][i]) {
+    cudaError_t e = cudaStreamWaitEvent(s, evs[dev][i], 0);
+    if (e != cudaSuccess) return e;
+  }
+  used[dev][i] = true;
+  *ctr = pool[dev] + i;
+  *done = evs[dev][i];
+  return cudaSuccess;
 }
 
 cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
@@ -466,8 +484,11 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   p.G2 = g.G2;
   p.ldg2 = g.ldg2;
   p.scale = g.scale == 0.f ? 1.f : g.scale;
-  p.ctr = ticket_counter();
-  if (!p.ctr) return cudaErrorMemoryAllocation;
+  cudaEvent_t slot_done = nullptr;
+  {
+    cudaError_t e = ticket_acquire(s, &p.ctr, &slot_done);
+    if (e != cudaSuccess) return e;
+  }
   p.groups = g.groups;
   p.g_start = g.g_start;
   p.g_rows = g.g_rows;
@@ -476,10 +497,13 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   int clusters = num_sms() / 2;
   if (tiles < clusters) clusters = tiles;
   const int grid = 2 * (clusters < 1 ? 1 : clusters);
-  if (!g.a_mn && !g.b_mn) return launch2<false, false>(ma, mb, p, grid, s);
-  if (!g.a_mn && g.b_mn) return launch2<false, true>(ma, mb, p, grid, s);
-  if (g.a_mn && !g.b_mn) return launch2<true, false>(ma, mb, p, grid, s);
-  return launch2<true, true>(ma, mb, p, grid, s);
+  cudaError_t e;
+  if (!g.a_mn && !g.b_mn) e = launch2<false, false>(ma, mb, p, grid, s);
+  else if (!g.a_mn && g.b_mn) e = launch2<false, true>(ma, mb, p, grid, s);
+  else if (g.a_mn && !g.b_mn) e = launch2<true, false>(ma, mb, p, grid, s);
+  else e = launch2<true, true>(ma, mb, p, grid, s);
+  if (e != cudaSuccess) return e;
+  return cudaEventRecord(slot_done, s);
 }
 
 }  // namespace opx

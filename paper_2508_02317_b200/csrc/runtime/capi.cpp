@@ -304,28 +304,6 @@ int opx_init_param(float* f32, void* b16, int64_t n, int64_t phys0, uint64_t key
 }
 uint64_t opx_param_key(const char* name, uint64_t seed) { return param_key(name, seed); }
 
-int opx_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t ldq,
-                 int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
-                 const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream) {
-  AttnArgs a{};
-  a.q = static_cast<const __nv_bfloat16*>(q);
-  a.k = static_cast<const __nv_bfloat16*>(k);
-  a.v = static_cast<const __nv_bfloat16*>(v);
-  a.o = static_cast<__nv_bfloat16*>(o);
-  a.lse = lse;
-  a.ldq = ldq;
-  a.ldk = ldk;
-  a.ldv = ldv;
-  a.ldo = ldo;
-  a.seq_start = seq_start;
-  a.seq_end = seq_end;
-  a.N = N;
-  a.hq = hq;
-  a.hk = hk;
-  a.scale = scale;
-  OPX_CALL(k_attn_fwd(a, static_cast<cudaStream_t>(stream)), "opx_attn_fwd");
-}
-
 int opx_attn_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse,
                     int64_t ldq, int64_t ldk, int64_t ldv, int64_t ldo, const int32_t* seq_start,
                     const int32_t* seq_end, int N, int hq, int hk, float scale, void* stream) {
@@ -370,37 +348,6 @@ int opx_attn_fwd_bidir_tc(const void* q, const void* k, const void* v, void* o, 
   a.scale = scale;
   a.causal = 0;
   OPX_CALL(k_attn_fwd_tc(a, static_cast<cudaStream_t>(stream)), "opx_attn_fwd_bidir_tc");
-}
-
-int opx_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
-                 const void* dout, float* dq_acc, void* dk, void* dv, float* delta,
-                 int64_t ld_q, int64_t ld_kv, const int32_t* seq_start, const int32_t* seq_end,
-                 int N, int hq, int hk, float scale, void* stream) {
-  AttnArgs a{};
-  a.q = static_cast<const __nv_bfloat16*>(q);
-  a.k = static_cast<const __nv_bfloat16*>(k);
-  a.v = static_cast<const __nv_bfloat16*>(v);
-  a.o = static_cast<__nv_bfloat16*>(const_cast<void*>(o));
-  a.lse = const_cast<float*>(lse);
-  a.ldq = ld_q;
-  a.ldk = ld_kv;
-  a.ldv = ld_kv;
-  a.ldo = ld_q;
-  a.seq_start = seq_start;
-  a.seq_end = seq_end;
-  a.N = N;
-  a.hq = hq;
-  a.hk = hk;
-  a.scale = scale;
-  a.dout = static_cast<const __nv_bfloat16*>(dout);
-  a.lddo = ld_q;
-  a.dq_acc = dq_acc;
-  a.dk = static_cast<__nv_bfloat16*>(dk);
-  a.dv = static_cast<__nv_bfloat16*>(dv);
-  a.lddk = ld_kv;
-  a.lddv = ld_kv;
-  a.delta = delta;
-  OPX_CALL(k_attn_bwd(a, static_cast<cudaStream_t>(stream)), "opx_attn_bwd");
 }
 
 int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, const float* lse,

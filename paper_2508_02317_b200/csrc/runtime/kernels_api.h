@@ -70,8 +70,6 @@ struct AttnArgs {
   // [seq_start[t], seq_end[t])), the frozen encoder's attention
   int causal = 1;
 };
-cudaError_t k_attn_fwd(const AttnArgs& a, cudaStream_t s);
-cudaError_t k_attn_bwd(const AttnArgs& a, cudaStream_t s);
 // attention_tc.cu — the same forward on tcgen05/TMEM/TMA.
 cudaError_t k_attn_fwd_tc(const AttnArgs& a, cudaStream_t s);
 cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s);

@@ -160,6 +160,8 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
   for (int j = 0; j < int(p.dp_replicate); ++j)
     rep_members_.push_back(int64_t(j) * sh * sp + shard_i_ * sp + sp_i_);
 
+  d_agree_ = alloc<int>(4);
+  if (!d_agree_) return cuda_fail(cudaErrorMemoryAllocation, "setup scratch");
   if (world_ > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
@@ -386,7 +388,7 @@ int Step::alloc_acts() {
     off_do_[b] = take(N * size_t(hql_) * 128 * 2);
     off_dqkv_[b] = take(T * size_t(Wqkv_) * 2);
   }
-  if (moe_) off = moe_arena(off);
+  if (moe_) TRY(moe_arena(&off));
   if (enc_.on) off_feat_ = take(T * H * 2);
   arena_bytes_ = off;
   if (cudaMalloc(&arena_, arena_bytes_) != cudaSuccess) {
@@ -477,20 +479,26 @@ int Step::alloc_acts() {
   return OPX_OK;
 }
 
+// Export = the arena's CUDA-IPC handle + its byte size.  Peers store into
+// each other's arenas at locally computed offsets, so import refuses a peer
+// whose arena layout (size) differs from ours.
 int Step::ipc_export(void* out, size_t cap, size_t* len) {
-  if (cap < sizeof(cudaIpcMemHandle_t)) {
+  const size_t need = sizeof(cudaIpcMemHandle_t) + sizeof(uint64_t);
+  if (cap < need) {
     set_error("ipc export buffer too small");
     return OPX_ERR_ARG;
   }
   cudaIpcMemHandle_t h;
   CU(cudaIpcGetMemHandle(&h, arena_));
+  const uint64_t bytes = arena_bytes_;
   std::memcpy(out, &h, sizeof(h));
-  *len = sizeof(h);
+  std::memcpy(static_cast<char*>(out) + sizeof(h), &bytes, sizeof(bytes));
+  *len = need;
   return OPX_OK;
 }
 
 int Step::ipc_import(const void* all, size_t len) {
-  if (len != sizeof(cudaIpcMemHandle_t)) {
+  if (len != sizeof(cudaIpcMemHandle_t) + sizeof(uint64_t)) {
     set_error("ipc import: unexpected handle size");
     return OPX_ERR_ARG;
   }
@@ -503,7 +511,15 @@ int Step::ipc_import(const void* all, size_t len) {
   for (int64_t r : peers) {
     if (r == rank_ || peer_arena_[size_t(r)]) continue;
     cudaIpcMemHandle_t h;
-    std::memcpy(&h, base + size_t(r) * len, len);
+    uint64_t bytes = 0;
+    std::memcpy(&h, base + size_t(r) * len, sizeof(h));
+    std::memcpy(&bytes, base + size_t(r) * len + sizeof(h), sizeof(bytes));
+    if (bytes != arena_bytes_) {
+      set_error("ipc import: rank " + std::to_string(r) + " has a " + std::to_string(bytes) +
+                "-byte peer arena, this rank " + std::to_string(arena_bytes_) +
+                " (layouts differ; peer stores would land at wrong offsets)");
+      return OPX_ERR_CONFIG;
+    }
     void* p = nullptr;
     CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     peer_arena_[size_t(r)] = static_cast<char*>(p);

@@ -153,6 +153,7 @@ class Step {
   std::vector<size_t> off_q_, off_k_, off_v_, off_o_;
   uint32_t** d_peer_flags_ = nullptr;  // device array [sp] of peer flag pointers
   int* d_timeout_ = nullptr;
+  int* d_agree_ = nullptr;  // scratch of the setup-time agreement reductions (allocated before any collective)
   uint32_t epoch_ = 0;
   int xq_ = 0, xo_ = 0, xdo_ = 0, xd_ = 0;  // double-buffer selectors
 
@@ -352,7 +353,7 @@ class Step {
   }
   int moe_setup_groups();      // in create(), before build_units
   int moe_build_units();       // expert units
-  size_t moe_arena(size_t off);  // reserve arena regions, returns new offset
+  int moe_arena(size_t* off);   // reserve arena regions (advances *off); ranks agree on the layout
   int moe_alloc();             // local scratch
   int moe_import();            // peer tables after ipc import
   int barrier_ep(cudaStream_t s);

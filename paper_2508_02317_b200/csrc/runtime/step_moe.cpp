@@ -126,7 +126,8 @@ int Step::moe_build_units() {
   return OPX_OK;
 }
 
-size_t Step::moe_arena(size_t off) {
+int Step::moe_arena(size_t* off_io) {
+  size_t off = *off_io;
   auto take = [&](size_t bytes) {
     const size_t o = off;
     off += size_t(rup(int64_t(bytes), 256));
@@ -154,36 +155,34 @@ size_t Step::moe_arena(size_t off) {
   // re-send (OPX_MOE_KEEP_X_MARGIN_GB of headroom kept for the rest)
   off_xrecv_l_.assign(size_t(L), 0);
   if (save_acts_ && ep_ > 1) {
+    int K = 0;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
       const char* e = getenv("OPX_MOE_KEEP_X_MARGIN_GB");
       const size_t margin = size_t(e ? atof(e) : 48.0) << 30;
       const size_t per = size_t(rup(int64_t(size_t(cap_rows_) * H * 2), 256));
       const size_t budget = free_b > off + margin ? free_b - off - margin : 0;
-      int K = int(std::min<size_t>(size_t(L), budget / per));
-      // every rank must agree (peers store into each other's kept slots)
-      if (world_comm_) {
-        int* d = nullptr;
-        if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
-          cudaMemcpy(d, &K, sizeof(int), cudaMemcpyHostToDevice);
-          if (ncclAllReduce(d, d, 1, ncclInt32, ncclMin, world_comm_, cs_) == ncclSuccess &&
-              cudaStreamSynchronize(cs_) == cudaSuccess)
-            cudaMemcpy(&K, d, sizeof(int), cudaMemcpyDeviceToHost);
-          else
-            K = 0;
-          cudaFree(d);
-        } else {
-          K = 0;
-        }
-      }
-      for (int l = L - 1; l >= 0 && K > 0; --l) {
-        if (!a_.is_moe_layer(l)) continue;
-        off_xrecv_l_[size_t(l)] = take(size_t(cap_rows_) * H * 2);
-        --K;
-      }
+      K = int(std::min<size_t>(size_t(L), budget / per));
+    }
+    if (const char* e = getenv("OPX_MOE_KEEP_X_MAX")) K = std::min(K, std::max(0, atoi(e)));
+    // Every rank must agree on K: peers store into each other's kept slots at
+    // locally computed offsets.  Every rank always joins the min-reduction
+    // (a local failure above contributes 0), and a failed collective is an
+    // error, never a silent K = 0 that would diverge from the peers' layout.
+    if (world_comm_) {
+      CU(cudaMemcpy(d_agree_, &K, sizeof(int), cudaMemcpyHostToDevice));
+      NC(ncclAllReduce(d_agree_, d_agree_, 1, ncclInt32, ncclMin, world_comm_, cs_));
+      CU(cudaStreamSynchronize(cs_));
+      CU(cudaMemcpy(&K, d_agree_, sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    for (int l = L - 1; l >= 0 && K > 0; --l) {
+      if (!a_.is_moe_layer(l)) continue;
+      off_xrecv_l_[size_t(l)] = take(size_t(cap_rows_) * H * 2);
+      --K;
     }
   }
-  return off;
+  *off_io = off;
+  return OPX_OK;
 }
 
 int Step::moe_alloc() {

@@ -157,14 +157,39 @@ def compare_step(sessions, model, batch, plan, step_loss, check_params=True):
     if check_params:
         P1 = om.adamw(P0, G, {}, 1, lr=EXEC["lr"], betas=tuple(EXEC["betas"]), eps=EXEC["eps"],
                       wd=EXEC["weight_decay"])
+        masters = _gpu_masters(sessions, arch, P1)
         for name, ref in P1.items():
-            if name.endswith(("gate_proj.weight", "up_proj.weight", "experts.gate_proj", "experts.up_proj")):
-                continue
-            x = gather_full(sessions, "master", name).reshape(ref.shape)
+            x = masters[name].reshape(ref.shape)
             d = np.abs(x - ref)
+            # step 1 AdamW moves each element by ~lr*sign(g): a near-zero
+            # gradient whose sign differs between bf16 and fp64 costs 2*lr
             assert d.max() <= 2.05 * EXEC["lr"], (name, d.max())
             assert d.mean() <= 0.02 * EXEC["lr"], (name, d.mean())
+        rep["masters_checked"] = len(P1)
     return rep
+
+
+def _gpu_masters(sessions, arch, names):
+    """Every master weight in HF naming; the interleaved gate|up matrices
+    (dense and expert) are split back into gate_proj / up_proj."""
+    out = {}
+    H = arch.hidden
+    for name in names:
+        if name in out:
+            continue
+        if name.endswith(("mlp.gate_proj.weight", "mlp.up_proj.weight")):
+            p = name.rsplit("mlp.", 1)[0] + "mlp."
+            g, u = om_deint(gather_full(sessions, "master", p + "gate_up_proj.weight"), arch.ffn, H)
+            out[p + "gate_proj.weight"], out[p + "up_proj.weight"] = g, u
+        elif name.endswith(("experts.gate_proj", "experts.up_proj")):
+            p = name.rsplit("experts.", 1)[0] + "experts."
+            E, Fe = arch.experts, arch.expert_ffn
+            gu = gather_full(sessions, "master", p + "gate_up_proj").reshape(E, Fe // 128, 2, 128, H)
+            out[p + "gate_proj"] = gu[:, :, 0].reshape(E, Fe, H)
+            out[p + "up_proj"] = gu[:, :, 1].reshape(E, Fe, H)
+        else:
+            out[name] = gather_full(sessions, "master", name)
+    return out
 
 
 def om_deint(flat, F, H):

@@ -279,39 +279,6 @@ def _attn_ref(q, k, v, st, hq, hk):
     return o.permute(1, 0, 2), lse
 
 
-@gpu
-@pytest.mark.parametrize("N,lens,hq,hk", [(256, [256], 2, 1), (640, [100, 300, 64, 176], 4, 2),
-                                          (1024, [1000, 24], 7, 1)])
-def test_attention_fwd_bwd(N, lens, hq, hk):
-    torch.manual_seed(N)
-    q = bf(torch.randn(N, hq, 128, device=DEV))
-    k = bf(torch.randn(N, hk, 128, device=DEV))
-    v = bf(torch.randn(N, hk, 128, device=DEV))
-    st, en = _varlen(N, lens)
-    o = torch.empty(N, hq, 128, device=DEV, dtype=torch.bfloat16)
-    lse = torch.empty(hq, N, device=DEV)
-    scale = 1 / math.sqrt(128)
-    call("opx_attn_fwd", P(q), P(k), P(v), P(o), P(lse), hq * 128, hk * 128, hk * 128, hq * 128,
-         P(st), P(en), N, hq, hk, scale, S())
-    qr, kr, vr = (t.float().clone().requires_grad_(True) for t in (q, k, v))
-    o_ref, lse_ref = _attn_ref(qr, kr, vr, st, hq, hk)
-    torch.cuda.synchronize()
-    assert rel_err(o, o_ref.detach()) < 2e-2
-    assert (lse - lse_ref.detach()).abs().max().item() < 1e-2
-    do = bf(torch.randn(N, hq, 128, device=DEV))
-    o_ref.backward(do.float())
-    dq = torch.empty(N, hq, 128, device=DEV)
-    dk = torch.empty(N, hk, 128, device=DEV, dtype=torch.bfloat16)
-    dv = torch.empty_like(dk)
-    delta = torch.empty(hq, N, device=DEV)
-    call("opx_attn_bwd", P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv), P(delta),
-         hq * 128, hk * 128, P(st), P(en), N, hq, hk, scale, S())
-    torch.cuda.synchronize()
-    for got, ref in ((dq, qr.grad), (dk, kr.grad), (dv, vr.grad)):
-        assert rel_err(got, ref) < 3e-2, (rel_err(got, ref))
-        assert cosine(got, ref) > 0.999
-
-
 # ---------------------------------------------------------------- RoPE pack (sp=1 Ulysses)
 @gpu
 def test_rope_pack():

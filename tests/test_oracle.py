@@ -42,6 +42,23 @@ def test_bf16_round_matches_torch():
     assert np.array_equal(om.bf16_round(x), ref)
 
 
+def test_c_helpers_bit_identical_to_numpy():
+    """oracle/c/oracle_init.c (fast path for large widths) against the numpy
+    definitions: init at odd offsets and bf16 rounding incl. ties, NaN, inf,
+    subnormals and overflow to inf."""
+    if not om._clib():
+        pytest.skip("oracle/_build/liboracle_init.so not built")
+    for name, start, n in (("a", 0, 5000), ("model.layers.3.mlp.down_proj.weight", 123457, 70001)):
+        key = om.param_key(name, 2508)
+        assert np.array_equal(om.init_values(key, n, start=start), om.init_values_np(key, n, start=start))
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(50000).astype(np.float32) * np.float32(10.0) ** rng.integers(-40, 39, 50000)
+    x[:8] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e-45, 3.3961514e38, 1.00390625]
+    x[8:16] = (np.arange(8, dtype=np.uint32) << 16 | 0x8000).view(np.float32)  # exact ties
+    got, ref = om.bf16_round(x), om.bf16_round_np(x)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
 # ---------------------------------------------------------------- torch autograd restatement
 def _torch_step(a: om.Arch, P: dict, ids, labels, pos, cu, n_valid):
     T = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in P.items()}

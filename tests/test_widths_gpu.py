@@ -1,0 +1,267 @@
+"""Parity at the BASELINE configs' true widths on one B200 (SURVEY §8(d)
+C1 / C2 / C4 shapes; proj/configs/dense-7b.json:8-16, moe-30b.json:8-22).
+
+The step tests elsewhere run toy widths (H <= 640, E <= 64), where the GEMM
+band-raster planner always picks one full band and the >1000-tile ticket
+path never runs.  Here:
+  * full training steps (fwd + bwd + AdamW) of 1-2 layers at the real hidden,
+    head, ffn and expert widths against the CPU oracle, at the north_star
+    tolerances (loss 1e-3 relative; every gradient max-err/max-ref 2e-2 and
+    cosine 0.999; every AdamW master incl. gate/up within 2.05 lr);
+  * the step's GEMMs at the real C1 shapes (gate|up 4096 x 37888 x 3584: a
+    ragged last band and 2368 tiles; down K = 18944; weight gradients with
+    K = T = 8192) against torch fp32;
+  * the grouped expert GEMMs at the C2 expert shapes (128 experts, top-8,
+    ffn_e 768) against torch fp32;
+  * a 1-GPU checkpoint round trip: save -> new session -> load gives
+    bit-identical masters / moments and the same next-step loss.
+Sequence lengths and vocab are reduced so the fp64 oracle finishes in
+seconds to a couple of minutes; widths are not.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from tests.step_common import EXEC, cluster, compare_step, tiny_dense, tiny_moe
+
+gpu = pytest.mark.gpu
+if torch.cuda.is_available():
+    from tests.gpu_util import P, S, call, cosine, rel_err
+
+DEV = "cuda"
+
+
+def _session(model, Sq, rows, recompute="full", selective=True):
+    from paper_2508_02317_b200.runtime import Session, synthetic_batch
+
+    arch = model["modules"][0]["arch"]
+    wl = {"seq_len": Sq, "micro_batch": rows, "global_batch": rows}
+    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": rows,
+            "recompute": recompute}
+    ex = dict(EXEC)
+    ex["selective_recompute"] = selective
+    s = Session(cluster(1), model, wl, plan, ex, rank=0, device=0)
+    s.init_weights(EXEC["seed"])
+    batch = synthetic_batch(arch["vocab"], Sq, rows, seed=2508)
+    s.load(batch)
+    return s, batch, plan
+
+
+def _report(tag, rep):
+    worst = max(rep["grads"].items(), key=lambda kv: kv[1][0])
+    print(f"{tag}: loss {rep['loss']:.6f} oracle {rep['loss_ref']:.6f} "
+          f"worst grad {worst[0]} err {worst[1][0]:.2e} cos {worst[1][1]:.6f}; "
+          f"{rep.get('masters_checked', 0)} masters checked")
+
+
+# ---------------------------------------------------------------- full steps
+@gpu
+@pytest.mark.parametrize("recompute,selective", [("full", True), ("full", False), ("none", True)])
+def test_step_c1_width(recompute, selective):
+    """Qwen2-7B block widths: H 3584, 28 q / 4 kv heads of 128, ffn 18944
+    (gate|up N = 37888), two layers, one 1024-token packed row, V 4096."""
+    model = tiny_dense(layers=2, hidden=3584, heads=28, kv=4, ffn=18944, vocab=4096)
+    s, batch, plan = _session(model, 1024, 1, recompute, selective)
+    r = s.run()
+    rep = compare_step([s], model, batch, plan, r.loss)
+    _report(f"C1 width ({recompute}, selective={selective})", rep)
+    s.close()
+
+
+@gpu
+def test_step_c2_width_moe():
+    """Qwen3-30B-A3B block widths: H 2048, 16 q / 4 kv heads of 128, 128
+    experts, top-8, expert ffn 768 (the grouped GEMMs see 128 segments of
+    ~32 rows), one MoE layer, 512 tokens.  Routing is forced to the GPU's
+    choices in the oracle; the flip rate against the oracle's own top-k is
+    bounded by compare_step."""
+    model = tiny_moe(layers=1, hidden=2048, heads=16, kv=4, ffn=6144, vocab=4096, experts=128,
+                     top_k=8, expert_ffn=768, stride=1)
+    s, batch, plan = _session(model, 512, 1)
+    r = s.run()
+    rep = compare_step([s], model, batch, plan, r.loss)
+    _report("C2 width", rep)
+    s.close()
+
+
+@gpu
+def test_step_c4_width():
+    """Qwen2-72B block widths: H 8192, 64 q / 8 kv heads of 128, ffn 29568
+    (gate|up N = 59136), one layer, 256 tokens."""
+    model = tiny_dense(layers=1, hidden=8192, heads=64, kv=8, ffn=29568, vocab=4096)
+    s, batch, plan = _session(model, 256, 1)
+    r = s.run()
+    rep = compare_step([s], model, batch, plan, r.loss)
+    _report("C4 width", rep)
+    s.close()
+
+
+# ---------------------------------------------------------------- GEMMs at the C1 shapes
+def _gemm(M, N, K, A, lda, a_mn, B, ldb, b_mn, epi, D, ldd, R=None, D2=None, ldd2=0):
+    call("opx_gemm", M, N, K, P(A), lda, a_mn, P(B), ldb, b_mn, epi, P(D), ldd, P(R), ldd if R is not None else 0,
+         P(D2), ldd2, 1.0, S())
+
+
+@gpu
+def test_gemm_c1_gate_up_swiglu():
+    """gate|up + SwiGLU at T=4096: N = 2*18944 = 37888 -> 148 column blocks
+    (ragged last L2 band), 2368 output tiles (dynamic tickets)."""
+    T, H, F = 4096, 3584, 18944
+    torch.manual_seed(11)
+    A = (torch.randn(T, H, device=DEV) * 0.5).bfloat16()
+    W = (torch.randn(2 * F, H, device=DEV) * 0.02).bfloat16()
+    gu = torch.empty(T, 2 * F, device=DEV, dtype=torch.bfloat16)
+    act = torch.empty(T, F, device=DEV, dtype=torch.bfloat16)
+    _gemm(T, 2 * F, H, A, H, 0, W, H, 0, 4, gu, 2 * F, D2=act, ldd2=F)
+    ref = A.float() @ W.float().t()
+    torch.cuda.synchronize()
+    assert rel_err(gu, ref) < 1e-2
+    v = ref.view(T, F // 128, 2, 128)
+    g = v[:, :, 0].reshape(T, F).bfloat16().float()
+    u = v[:, :, 1].reshape(T, F).bfloat16().float()
+    a_ref = torch.nn.functional.silu(g) * u
+    assert rel_err(act, a_ref) < 2e-2 and cosine(act, a_ref) > 0.9999
+
+
+@gpu
+def test_gemm_c1_down_residual():
+    """down projection + fp32 residual: M 4096, N 3584, K 18944."""
+    T, H, F = 4096, 3584, 18944
+    torch.manual_seed(12)
+    A = (torch.randn(T, F, device=DEV) * 0.5).bfloat16()
+    W = (torch.randn(H, F, device=DEV) * 0.02).bfloat16()
+    R = torch.randn(T, H, device=DEV)
+    D = torch.empty(T, H, device=DEV)
+    _gemm(T, H, F, A, F, 0, W, F, 0, 2, D, H, R=R)
+    ref = A.float() @ W.float().t() + R
+    torch.cuda.synchronize()
+    assert (D - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
+
+
+@gpu
+@pytest.mark.parametrize("M,N", [(3584, 18944), (37888, 3584), (4608, 3584)])
+def test_gemm_c1_wgrad_k8192(M, N):
+    """Weight gradients dW[M,N] = dY^T X with K = T = 8192 tokens, both
+    operands stored K-major (a_mn = b_mn = 1): down (H x F), gate|up (2F x H),
+    qkv (4608 x H), bf16 and fp32 epilogues."""
+    K = 8192
+    torch.manual_seed(M + N)
+    dY = (torch.randn(K, M, device=DEV) * 0.1).bfloat16()
+    X = torch.randn(K, N, device=DEV).bfloat16()
+    ref = dY.float().t() @ X.float()
+    Db = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    _gemm(M, N, K, dY, M, 1, X, N, 1, 0, Db, N)
+    Df = torch.empty(M, N, device=DEV)
+    _gemm(M, N, K, dY, M, 1, X, N, 1, 1, Df, N)
+    torch.cuda.synchronize()
+    assert rel_err(Db, ref) < 1e-2
+    assert (Df - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
+
+
+@gpu
+def test_gemm_c1_dgrad_transposed_b():
+    """dgrad of gate|up: dX[T,H] = dGU[T,2F] . Wgu[2F,H] (b_mn = 1), K = 37888."""
+    T, H, F = 4096, 3584, 18944
+    torch.manual_seed(13)
+    dgu = (torch.randn(T, 2 * F, device=DEV) * 0.1).bfloat16()
+    W = (torch.randn(2 * F, H, device=DEV) * 0.02).bfloat16()
+    D = torch.empty(T, H, device=DEV)
+    _gemm(T, H, 2 * F, dgu, 2 * F, 0, W, H, 1, 1, D, H)
+    ref = dgu.float() @ W.float()
+    torch.cuda.synchronize()
+    assert (D - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
+
+
+# ---------------------------------------------------------------- grouped GEMMs at the C2 expert shapes
+def _segments(E, total, rng):
+    """Random per-expert row counts summing to `total` (some experts empty),
+    each segment starting at a 128-aligned row like the dispatch layout."""
+    w = rng.dirichlet(np.full(E, 0.7))
+    rows = np.floor(w * total).astype(np.int64)
+    rows[0] += total - rows.sum()
+    rows[rng.choice(E, 5, replace=False)] = 0
+    starts, at = [], 0
+    for r in rows:
+        starts.append(at)
+        at += int(-(-r // 128) * 128) if r else 0
+    return rows.astype(np.int32), np.array(starts, np.int32), at
+
+
+@gpu
+def test_grouped_gemm_c2_experts():
+    """Expert gate|up (+SwiGLU), down and the K-grouped weight gradient with
+    128 experts, H 2048, ffn_e 768, 8192 tokens x top-8 = 65536 rows."""
+    E, H, Fe, rows_total = 128, 2048, 768, 65536
+    rng = np.random.default_rng(7)
+    g_rows, g_start, cap = _segments(E, rows_total, rng)
+    cap = max(cap, 128)
+    torch.manual_seed(7)
+    X = torch.zeros(cap, H, device=DEV, dtype=torch.bfloat16)
+    for e in range(E):
+        X[g_start[e]:g_start[e] + g_rows[e]] = torch.randn(int(g_rows[e]), H, device=DEV).bfloat16()
+    Wgu = (torch.randn(E, 2 * Fe, H, device=DEV) * 0.02).bfloat16()
+    Wd = (torch.randn(E, H, Fe, device=DEV) * 0.02).bfloat16()
+    gs = torch.from_numpy(g_start).to(DEV)
+    gr = torch.from_numpy(g_rows).to(DEV)
+    gu = torch.zeros(cap, 2 * Fe, device=DEV, dtype=torch.bfloat16)
+    act = torch.zeros(cap, Fe, device=DEV, dtype=torch.bfloat16)
+    call("opx_gemm_grouped", 0, 2 * Fe, H, P(X), H, 0, P(Wgu), H, 0, 4, P(gu), 2 * Fe, P(act), Fe, E, 0,
+         P(gs), P(gr), cap, 0, S())
+    Y = torch.zeros(cap, H, device=DEV, dtype=torch.bfloat16)
+    call("opx_gemm_grouped", 0, H, Fe, P(act), Fe, 0, P(Wd), Fe, 0, 0, P(Y), H, None, 0, E, 0,
+         P(gs), P(gr), cap, 0, S())
+    # K-grouped weight gradient dWd[e] = dY_e^T act_e over each expert's rows
+    # (segments zero padded to a multiple of 64 rows, as the step pads them)
+    gr_pad = torch.from_numpy(((g_rows + 63) // 64 * 64).astype(np.int32)).to(DEV)
+    dY = torch.zeros(cap, H, device=DEV, dtype=torch.bfloat16)
+    for e in range(E):
+        dY[g_start[e]:g_start[e] + g_rows[e]] = (torch.randn(int(g_rows[e]), H, device=DEV) * 0.1).bfloat16()
+    dWd = torch.zeros(E, H, Fe, device=DEV)
+    call("opx_gemm_grouped", H, Fe, 0, P(dY), H, 1, P(act), Fe, 1, 1, P(dWd), Fe, None, 0, E, 1,
+         P(gs), P(gr_pad), cap, H * Fe, S())
+    torch.cuda.synchronize()
+    worst = 0.0
+    for e in range(E):
+        a, n = int(g_start[e]), int(g_rows[e])
+        if n == 0:
+            assert dWd[e].abs().max().item() == 0
+            continue
+        ref = X[a:a + n].float() @ Wgu[e].float().t()
+        worst = max(worst, rel_err(gu[a:a + n], ref))
+        v = ref.view(n, Fe // 128, 2, 128)
+        g = v[:, :, 0].reshape(n, Fe).bfloat16().float()
+        u = v[:, :, 1].reshape(n, Fe).bfloat16().float()
+        a_ref = torch.nn.functional.silu(g) * u
+        assert rel_err(act[a:a + n], a_ref) < 2e-2, e
+        y_ref = act[a:a + n].float() @ Wd[e].float().t()
+        assert rel_err(Y[a:a + n], y_ref) < 1e-2, e
+        w_ref = dY[a:a + n].float().t() @ act[a:a + n].float()
+        assert (dWd[e] - w_ref).abs().max().item() <= 1e-3 * w_ref.abs().max().item(), e
+    assert worst < 1e-2
+
+
+# ---------------------------------------------------------------- checkpoint round trip on one GPU
+@gpu
+def test_checkpoint_roundtrip_1gpu(tmp_path):
+    """f3 on one GPU: step, save, new session, load -> masters, moments and
+    bf16 params bit-identical; the next step's loss equals the saving
+    session's next-step loss."""
+    model = tiny_dense(layers=2, hidden=512, heads=4, kv=2, ffn=1024, vocab=2048)
+    s, batch, plan = _session(model, 1024, 2)
+    s.run()
+    s.save(tmp_path)
+    names = ["model.layers.1.self_attn.q_proj.weight", "model.layers.0.mlp.gate_up_proj.weight",
+             "lm_head.weight", "model.embed_tokens.weight"]
+    snap = {(k, n): s.get(f"{k}:{n}")[0].copy() for k in ("master", "exp_avg", "exp_avg_sq", "param")
+            for n in names}
+    loss_next = s.run().loss
+    s.close()
+    s2, _, _ = _session(model, 1024, 2)
+    s2.load_checkpoint(tmp_path)
+    for (k, n), v in snap.items():
+        got = s2.get(f"{k}:{n}")[0]
+        assert np.array_equal(got.view(np.uint8), v.view(np.uint8)), (k, n)
+    assert s2.run().loss == loss_next
+    s2.close()

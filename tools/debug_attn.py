@@ -15,7 +15,7 @@ for (N, lens, hq, hk) in [(128, [128], 1, 1), (256, [256], 1, 1), (256, [256], 2
     o = o_ref.detach().bfloat16(); lse = lse_ref.detach().contiguous()
     do = torch.randn(N, hq, 128, device="cuda").bfloat16()
     o_ref.backward(do.float())
-    for name in ("opx_attn_bwd", "opx_attn_bwd_tc"):
+    for name in ("opx_attn_bwd_tc",):
         dq = torch.empty(N, hq, 128, device="cuda"); dk = torch.empty(N, hk, 128, device="cuda").bfloat16(); dv = torch.empty_like(dk)
         delta = torch.empty(hq, N, device="cuda")
         check(getattr(lib(), name)(P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv), P(delta), hq*128, hk*128, P(st), P(en), N, hq, hk, 1/math.sqrt(128), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
