@@ -63,16 +63,28 @@ int opx_plan_resolve(const char* cluster_json, const char* model_json,
  * ------------------------------------------------------------------------ */
 typedef struct opx_step opx_step;
 
-/* Measured StepReport (simulator.hpp:43-50), device-timed on this rank. */
+/* Measured StepReport (simulator.hpp:43-50), device-timed on this rank.  The
+ * reference's fields keep their meaning, computed as report() does
+ * (simulator.cpp:106-131) but on measured CUDA-event intervals of this rank's
+ * streams instead of simulated ones.  The interval-based fields (comm_s,
+ * comm_wait_s, exposed_comm, phase breakdown) need exec "trace" (default on). */
 typedef struct {
   double step_time_s;   /* first kernel -> optimizer end, CUDA events */
-  double fwd_s, bwd_s, opt_s, comm_wait_s;
+  double fwd_s, bwd_s, opt_s;  /* summed over micro-batches; opt_s = tail after the backward */
+  double comm_wait_s;   /* seconds of comm intervals not covered by compute (simulator.cpp:71-104) */
   double loss;          /* global mean token loss (all-reduced) */
-  double tokens;        /* tokens processed by this rank this step */
+  double tokens;        /* tokens processed by this rank this step (all micro-batches) */
   double n_valid;       /* global count of supervised tokens */
   int64_t launches;     /* opx kernels launched during the step */
   double enqueue_s;     /* host wall time spent enqueueing the step (launch-bound if ~step_time_s) */
   int64_t kept_layers;  /* layers whose activations stay resident (no full recompute) */
+  /* ---- StepReport (simulator.hpp:43-50) */
+  double throughput;    /* global_batch*seq_len / (step_time_s*world), tokens/s/GPU (simulator.cpp:113-115) */
+  double mfu;           /* throughput * model_flops_per_token / cluster.gpu.peak_flops (:116-117) */
+  double exposed_comm;  /* comm_wait_s / step_time_s (:118) */
+  double model_flops_per_token;  /* flops_per_token(model, seq_len) (specs.cpp:93-107) */
+  double comm_s;        /* summed duration of the comm nodes */
+  int64_t accum_steps;  /* micro-batches in the step: global_batch/(dp_width*micro_batch) */
 } opx_step_report;
 
 /* 128-byte NCCL unique id for the world communicator (rank 0 creates it). */
@@ -91,7 +103,10 @@ int opx_step_init_weights(opx_step* st, uint64_t seed);
 /* Host arrays for THIS rank: ids/labels of its local tokens (rows x S/sp,
  * row-major), positions of ALL rows*S tokens of its sequences (position
  * within sample), cu_seqlens over those rows*S tokens (packing.hpp:28
- * convention), and the global supervised-token count. */
+ * convention), and the global supervised-token count.  With gradient
+ * accumulation (global_batch = k*dp_width*micro_batch, step_graph.cpp:57)
+ * "rows" is k*micro_batch: micro-batch j is rows [j*m, (j+1)*m) of the
+ * arrays, and n_valid counts all k micro-batches of all ranks. */
 int opx_step_load_batch(opx_step* st, const int32_t* ids, const int32_t* labels,
                         const int32_t* positions, const int32_t* cu_seqlens, int n_cu,
                         int64_t n_valid_global);
@@ -123,6 +138,12 @@ int opx_step_get(opx_step* st, const char* name, void* host_dst, size_t bytes);
  * flattened logical tensor held by this rank. */
 int opx_step_tensor_info(opx_step* st, const char* name, int64_t* numel, int64_t* begin,
                          int64_t* end);
+/* The last step's report as to_json(StepReport) (report.cpp:117-128):
+ * {"step_time_s","throughput_tokens_per_s_per_gpu","mfu","exposed_comm_fraction",
+ *  "model_flops_per_token","phase_breakdown":{phase:{"compute_s","comm_s"}}}
+ * with phase names from step_graph.cpp (fwd.layer<i>, bwd.layer<i>, fwd.head,
+ * bwd.head, encoder, optimizer).  len receives strlen; cap must exceed it. */
+int opx_step_report_json(opx_step* st, char* out_json, size_t cap, size_t* len);
 /* Chrome trace of the last step in simulator.cpp:133-151's schema. */
 int opx_step_trace(opx_step* st, char* out_json, size_t cap, size_t* len);
 int opx_step_destroy(opx_step* st);

@@ -38,6 +38,19 @@ import numpy as np
 F32 = np.float32
 MASK64 = (1 << 64) - 1
 
+# Accumulation dtype of the GEMMs, attention and reductions: fp64 (the
+# checker).  bench.py's CPU baseline legs switch it to fp32 (set_accumulate)
+# so the timed CPU path is an all-core fp32 BLAS implementation of the step.
+_ACC = [np.float64]
+
+
+def ACC():
+    return _ACC[0]
+
+
+def set_accumulate(dtype) -> None:
+    _ACC[0] = np.dtype(dtype).type
+
 # C helpers (oracle/c/oracle_init.c, built by oracle/Makefile): bit-identical
 # restatements of init_values / bf16_round that only make large-width parity
 # tests fast; the numpy code below is the definition and the fallback.
@@ -203,7 +216,7 @@ def bf16_round_np(x: np.ndarray) -> np.ndarray:
 # building blocks
 # ----------------------------------------------------------------------------
 def rmsnorm_fwd(x, w, eps):
-    ms = (x.astype(np.float64) ** 2).mean(-1, keepdims=True)
+    ms = (x.astype(ACC(), copy=False) ** 2).mean(-1, keepdims=True)
     rstd = (1.0 / np.sqrt(ms + eps)).astype(F32)
     return (x * rstd * w).astype(F32), rstd
 
@@ -211,9 +224,9 @@ def rmsnorm_fwd(x, w, eps):
 def rmsnorm_bwd(dy, x, w, rstd):
     xh = x * rstd
     g = dy * w
-    mean = (g.astype(np.float64) * xh).mean(-1, keepdims=True).astype(F32)
+    mean = (g.astype(ACC(), copy=False) * xh).mean(-1, keepdims=True).astype(F32)
     dx = rstd * (g - xh * mean)
-    dw = (dy.astype(np.float64) * xh).sum(0).astype(F32)
+    dw = (dy.astype(ACC(), copy=False) * xh).sum(0).astype(F32)
     return dx.astype(F32), dw
 
 
@@ -245,7 +258,7 @@ def attention_fwd(q, k, v, cu, scale):
         L = b - a
         mask = np.tril(np.ones((L, L), bool))
         for h in range(hq):
-            s = (q[a:b, h].astype(np.float64) @ k[a:b, h // G].astype(np.float64).T) * scale
+            s = (q[a:b, h].astype(ACC(), copy=False) @ k[a:b, h // G].astype(ACC(), copy=False).T) * scale
             s = np.where(mask, s, -np.inf)
             m = s.max(-1, keepdims=True)
             e = np.exp(s - m)
@@ -260,20 +273,20 @@ def attention_bwd(q, k, v, o, lse, do, cu, scale):
     hk = k.shape[1]
     G = hq // hk
     dq = np.zeros_like(q)
-    dk = np.zeros(k.shape, np.float64)
-    dv = np.zeros(v.shape, np.float64)
+    dk = np.zeros(k.shape, ACC())
+    dv = np.zeros(v.shape, ACC())
     for a, b in zip(cu[:-1], cu[1:]):
         L = b - a
         mask = np.tril(np.ones((L, L), bool))
         for h in range(hq):
             kh = h // G
-            qq, kk, vv = (t.astype(np.float64) for t in (q[a:b, h], k[a:b, kh], v[a:b, kh]))
+            qq, kk, vv = (t.astype(ACC(), copy=False) for t in (q[a:b, h], k[a:b, kh], v[a:b, kh]))
             s = np.where(mask, (qq @ kk.T) * scale, -np.inf)
-            p = np.exp(s - lse[h, a:b, None].astype(np.float64))
-            dO = do[a:b, h].astype(np.float64)
+            p = np.exp(s - lse[h, a:b, None].astype(ACC(), copy=False))
+            dO = do[a:b, h].astype(ACC(), copy=False)
             dv[a:b, kh] += p.T @ dO
             dp = dO @ vv.T
-            delta = (dO * o[a:b, h].astype(np.float64)).sum(-1, keepdims=True)
+            delta = (dO * o[a:b, h].astype(ACC(), copy=False)).sum(-1, keepdims=True)
             ds = p * (dp - delta)
             dq[a:b, h] = (ds @ kk * scale).astype(F32)
             dk[a:b, kh] += ds.T @ qq * scale
@@ -329,7 +342,7 @@ class Step:
     def __init__(self, a: Arch, params: dict, round_operands: bool = True, forced_routes=None):
         self.a = a
         self.P = params
-        self.r = bf16_round if round_operands else (lambda x: x.astype(F32))
+        self.r = bf16_round if round_operands else (lambda x: x.astype(F32, copy=False))
         # {layer: [N, k] expert indices}: route with these instead of the
         # oracle's own top-k (the weights still come from the oracle's logits);
         # used to separate discrete routing flips from arithmetic differences.
@@ -337,7 +350,7 @@ class Step:
         self.flips = {}  # {layer: fraction of tokens whose expert set differs}
 
     def mm(self, x, w):  # x [N,K] . w[M,K]^T
-        return (self.r(x).astype(np.float64) @ self.r(w).astype(np.float64).T).astype(F32)
+        return (self.r(x).astype(ACC(), copy=False) @ self.r(w).astype(ACC(), copy=False).T).astype(F32)
 
     def run(self, ids, labels, pos, cu, n_valid, inject=None):
         """ids/labels/pos [N] (N = all tokens of the batch rows, concatenated);
@@ -382,7 +395,7 @@ class Step:
             x = (x2 + y).astype(F32)
             saved.append(st)
         hf, rf = rmsnorm_fwd(x, self.r(P["model.norm.weight"]), a.rms_eps)
-        logits = self.mm(hf, P["lm_head.weight"]).astype(np.float64)
+        logits = self.mm(hf, P["lm_head.weight"]).astype(ACC(), copy=False)
         valid = labels >= 0
         m = logits.max(-1, keepdims=True)
         lse_v = (m + np.log(np.exp(logits - m).sum(-1, keepdims=True)))[:, 0]
@@ -392,8 +405,8 @@ class Step:
         dlog[np.arange(N), lab] -= 1.0
         dlog = (dlog * valid[:, None] / n_valid).astype(F32)
         # head backward
-        G["lm_head.weight"] = (self.r(dlog).astype(np.float64).T @ self.r(hf).astype(np.float64)).astype(F32)
-        dhf = (self.r(dlog).astype(np.float64) @ self.r(P["lm_head.weight"]).astype(np.float64)).astype(F32)
+        G["lm_head.weight"] = (self.r(dlog).astype(ACC(), copy=False).T @ self.r(hf).astype(ACC(), copy=False)).astype(F32)
+        dhf = (self.r(dlog).astype(ACC(), copy=False) @ self.r(P["lm_head.weight"]).astype(ACC(), copy=False)).astype(F32)
         dx, G["model.norm.weight"] = rmsnorm_bwd(dhf, x, self.r(P["model.norm.weight"]), rf)
         for l in reversed(range(a.layers)):
             p = f"model.layers.{l}."
@@ -431,19 +444,19 @@ class Step:
             ddx, G[p + "input_layernorm.weight"] = rmsnorm_bwd(
                 dh.astype(F32), st["x"], self.r(P[p + "input_layernorm.weight"]), st["r1"])
             dx = (dx + ddx).astype(F32)
-        dE = np.zeros((a.vocab, H), np.float64)
+        dE = np.zeros((a.vocab, H), ACC())
         if inject is not None:
             dx = np.where(inject[0][:, None], np.float32(0), dx)
-        np.add.at(dE, ids, dx.astype(np.float64))
+        np.add.at(dE, ids, dx.astype(ACC(), copy=False))
         G["model.embed_tokens.weight"] = dE.astype(F32)
         self.loss_rows = loss_rows.astype(F32)
         return float(loss_rows.sum()), G
 
     def wgrad(self, dy, x):  # dW[M,K] = dy[N,M]^T x[N,K]
-        return (self.r(dy).astype(np.float64).T @ self.r(x).astype(np.float64)).astype(F32)
+        return (self.r(dy).astype(ACC(), copy=False).T @ self.r(x).astype(ACC(), copy=False)).astype(F32)
 
     def dgrad(self, dy, w):  # dx[N,K] = dy[N,M] w[M,K]
-        return (self.r(dy).astype(np.float64) @ self.r(w).astype(np.float64)).astype(F32)
+        return (self.r(dy).astype(ACC(), copy=False) @ self.r(w).astype(ACC(), copy=False)).astype(F32)
 
     # -------------------------------------------------------------- MoE
     def moe_fwd(self, l, h2):
@@ -460,7 +473,7 @@ class Step:
             e = np.exp(sel - sel.max(-1, keepdims=True))
             w = (e / e.sum(-1, keepdims=True)).astype(F32)
         N = h2.shape[0]
-        y = np.zeros((N, a.hidden), np.float64)
+        y = np.zeros((N, a.hidden), ACC())
         cache = {"idx": idx, "w": w, "logits": logits, "eo": {}}
         Wg, Wu, Wd = P[p + "experts.gate_proj"], P[p + "experts.up_proj"], P[p + "experts.down_proj"]
         for e in range(a.experts):
@@ -473,7 +486,7 @@ class Step:
             act = silu(g) * u
             out = self.mm(act, Wd[e])
             cache["eo"][e] = (rows, slots, g, u, act, out)
-            np.add.at(y, rows, out.astype(np.float64) * w[rows, slots][:, None])
+            np.add.at(y, rows, out.astype(ACC(), copy=False) * w[rows, slots][:, None])
         return y.astype(F32), cache
 
     def moe_bwd(self, l, h2, cache, dy, G):
@@ -484,12 +497,12 @@ class Step:
         dWg = np.zeros(Wg.shape, F32)
         dWu = np.zeros(Wu.shape, F32)
         dWd = np.zeros(Wd.shape, F32)
-        dh = np.zeros((N, a.hidden), np.float64)
-        dw = np.zeros((N, a.top_k), np.float64)
+        dh = np.zeros((N, a.hidden), ACC())
+        dw = np.zeros((N, a.top_k), ACC())
         w = cache["w"]
         for e, (rows, slots, g, u, act, out) in cache["eo"].items():
             dout = (dy[rows] * w[rows, slots][:, None]).astype(F32)
-            dw[rows, slots] = (dy[rows].astype(np.float64) * out.astype(np.float64)).sum(-1)
+            dw[rows, slots] = (dy[rows].astype(ACC(), copy=False) * out.astype(ACC(), copy=False)).sum(-1)
             dWd[e] = self.wgrad(dout, act)
             dact = self.r(self.dgrad(dout, Wd[e]))
             g, u = self.r(g), self.r(u)
@@ -499,7 +512,7 @@ class Step:
             dWg[e] = self.wgrad(dg, h2[rows])
             dWu[e] = self.wgrad(du, h2[rows])
             dxe = self.dgrad(dg, Wg[e]) + self.dgrad(du, Wu[e])
-            np.add.at(dh, rows, dxe.astype(np.float64))
+            np.add.at(dh, rows, dxe.astype(ACC(), copy=False))
         # renormalised softmax over the selected logits
         dsel = w * (dw - (w * dw).sum(-1, keepdims=True))
         dlog = np.zeros((N, a.experts), F32)
@@ -535,23 +548,29 @@ def adamw(params, grads, state, step, lr=1e-4, betas=(0.9, 0.95), eps=1e-8, wd=0
 # simulated ranks (FSDP x SP x DP) for one step
 # ----------------------------------------------------------------------------
 def simulate_ranks(a: Arch, params: dict, batch, plan: dict, forced_routes=None, flips=None,
-                   encoder=None):
+                   encoder=None, round_operands=True):
     """Runs the step the way the mesh partitions the batch: dp index r
     (= dp_replicate_idx*dp_shard + dp_shard_idx) owns rows
-    [r*micro_batch, (r+1)*micro_batch).  Inside an SP group the Ulysses
+    [r*k*micro_batch, (r+1)*k*micro_batch), k = rows/(dp*micro_batch) the
+    gradient-accumulation steps (step_graph.cpp:57), and runs them as k
+    micro-batches of micro_batch consecutive rows.  Inside an SP group the Ulysses
     exchange is a pure relayout and every token-local op is row-independent,
     so the SP ranks of one group are evaluated jointly on their gathered rows.
     Parameter gradients of the dp ranks are summed in rank order (the FSDP
     reduce-scatter / HSDP all-reduce) and the loss is normalised by the global
     supervised-token count.  encoder = (EncArch, encoder params) runs the
-    frozen encoder over batch["img"] (oracle/encoder.py).  Returns (loss_mean, grads)."""
+    frozen encoder over batch["img"] (oracle/encoder.py).  round_operands=False
+    skips the bf16 rounding of matmul operands (pure fp32/fp64 arithmetic: the
+    reference point for the bf16 sensitivity floor the width-parity tests
+    report).  Returns (loss_mean, grads)."""
     rows_per_dp = plan["micro_batch"]
     dp = plan["dp_replicate"] * plan["dp_shard"]
     ids, labels, pos, cus = batch["ids"], batch["labels"], batch["pos"], batch["cu_rows"]
     n_valid = int((labels >= 0).sum())
     total = None
     loss = 0.0
-    for r in range(dp):
+    assert ids.shape[0] % (dp * rows_per_dp) == 0, "rows must be a multiple of dp*micro_batch"
+    for r in range(ids.shape[0] // rows_per_dp):  # micro-batches in (dp rank, micro) order
         sl = slice(r * rows_per_dp, (r + 1) * rows_per_dp)
         rid, rlab, rpos = ids[sl].reshape(-1), labels[sl].reshape(-1), pos[sl].reshape(-1)
         S = ids.shape[1]
@@ -567,7 +586,7 @@ def simulate_ranks(a: Arch, params: dict, batch, plan: dict, forced_routes=None,
 
             inj = inject_for_rows(encoder[0], encoder[1], batch["img"],
                                   range(r * rows_per_dp, (r + 1) * rows_per_dp), S)
-        st = Step(a, params, forced_routes=fr)
+        st = Step(a, params, round_operands=round_operands, forced_routes=fr)
         ls, g = st.run(rid, rlab, rpos, np.array(cu), n_valid, inject=inj)
         if flips is not None:
             for l, f in st.flips.items():

@@ -465,6 +465,33 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, bf16* __restri
   }
 }
 
+// gradient accumulation over micro-batches (step_graph.cpp:57,75-87): acc =
+// (first ? 0 : acc) + g in fp32, g the micro-batch's fp32 or bf16 shard gradient
+template <typename G>
+__global__ void grad_accum_kernel(float* __restrict__ acc, const G* __restrict__ g, int64_t n,
+                                  int first) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float4 gv;
+    if constexpr (sizeof(G) == 4) {
+      gv = reinterpret_cast<const float4*>(g)[i];
+    } else {
+      const uint2 q = reinterpret_cast<const uint2*>(g)[i];
+      const float2 a = ptx::unpack_bf16(q.x), b = ptx::unpack_bf16(q.y);
+      gv = make_float4(a.x, a.y, b.x, b.y);
+    }
+    if (!first) {
+      const float4 av = reinterpret_cast<const float4*>(acc)[i];
+      gv.x += av.x;
+      gv.y += av.y;
+      gv.z += av.z;
+      gv.w += av.w;
+    }
+    reinterpret_cast<float4*>(acc)[i] = gv;
+  }
+}
+
 // sum of a float vector (fixed order, one block) -> out[0]
 __global__ void sum_kernel(const float* __restrict__ x, int64_t n, float* out) {
   __shared__ float red[NT / 32];
@@ -596,6 +623,18 @@ cudaError_t k_cast_f32_bf16(const float* x, __nv_bfloat16* y, int64_t n, cudaStr
   if (n <= 0) return cudaSuccess;
   ++g_kernel_launches;
   cast_f32_bf16_kernel<<<grid_for(n / 4), NT, 0, s>>>(x, y, n);
+  return cudaGetLastError();
+}
+
+cudaError_t k_grad_accum(float* acc, const void* g, int g_bf16, int64_t n, int first,
+                         cudaStream_t s) {
+  if (n % 4) return cudaErrorInvalidValue;
+  if (n <= 0) return cudaSuccess;
+  ++g_kernel_launches;
+  if (g_bf16)
+    grad_accum_kernel<<<grid_for(n / 4), NT, 0, s>>>(acc, static_cast<const bf16*>(g), n, first);
+  else
+    grad_accum_kernel<<<grid_for(n / 4), NT, 0, s>>>(acc, static_cast<const float*>(g), n, first);
   return cudaGetLastError();
 }
 

@@ -37,6 +37,9 @@ cudaError_t k_adamw(float* p, float* m, float* v, const void* g, int g_bf16, __n
                     int64_t n, float lr, float b1, float b2, float eps, float wd, int step,
                     cudaStream_t s);
 cudaError_t k_cast_f32_bf16(const float* x, __nv_bfloat16* y, int64_t n, cudaStream_t s);
+// acc = (first ? 0 : acc) + g (g fp32, or bf16 when g_bf16), n % 4 == 0
+cudaError_t k_grad_accum(float* acc, const void* g, int g_bf16, int64_t n, int first,
+                         cudaStream_t s);
 cudaError_t k_sum(const float* x, int64_t n, float* out, cudaStream_t s);
 
 // attention.cu — causal varlen GQA flash attention, head dim 128.

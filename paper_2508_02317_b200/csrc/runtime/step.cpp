@@ -61,8 +61,16 @@ cudaEvent_t Step::ev() {
 }
 
 void Step::mark(const std::string& name, const std::string& phase, int tid, cudaEvent_t a,
-                cudaEvent_t b) {
-  trace_.push_back({name, phase, tid, a, b});
+                cudaEvent_t b, const char* fused) {
+  TraceEv t{name, phase, tid, a, b};
+  // the reference's collective nodes: FSDP/HSDP NCCL ops on the comm stream,
+  // the Ulysses / EP exchanges (and their flag barriers) on the compute
+  // stream, the encoder feature scatter (step_graph.cpp:150-160, 215-247, 265-283)
+  auto starts = [&](const char* p) { return name.rfind(p, 0) == 0; };
+  t.comm = tid == 1 || name.find(".a2a_") != std::string::npos || starts("scatter.") ||
+           starts("fwd.ag.") || starts("bwd.ag.") || starts("bwd.rs.") || starts("bwd.ar.");
+  if (fused) t.fused = fused;
+  trace_.push_back(std::move(t));
 }
 
 Step::~Step() {
@@ -78,6 +86,8 @@ Step::~Step() {
   for (auto* v : {&ev_ag_, &ev_use_done_, &ev_grad_done_, &ev_rs_done_})
     for (auto e : *v) cudaEventDestroy(e);
   for (auto e : {ev_start_, ev_fwd_, ev_bwd_, ev_end_, ev_head_ag_, ev_head_rs_})
+    if (e) cudaEventDestroy(e);
+  for (auto e : ev_mb_)
     if (e) cudaEventDestroy(e);
   if (expert_comm_) ncclCommDestroy(expert_comm_);
   if (rep_comm_) ncclCommDestroy(rep_comm_);
@@ -98,8 +108,9 @@ int Step::opt_unit(Unit& u, cudaStream_t after, const std::string& name) {
   cudaEvent_t ready = ev();
   CU(cudaEventRecord(ready, after));
   CU(cudaStreamWaitEvent(os_, ready, 0));
-  CU(k_adamw(u.master, u.m, u.v, u.gshard, u.gbf, u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2,
-             ex_.eps, ex_.wd, step_count_, os_));
+  const bool acc = accum_ > 1;  // AdamW reads the fp32 micro-batch sum
+  CU(k_adamw(u.master, u.m, u.v, acc ? static_cast<void*>(u.gacc) : u.gshard, acc ? 0 : u.gbf,
+             u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps, ex_.wd, step_count_, os_));
   if (ex_.trace) {
     cudaEvent_t done = ev();
     CU(cudaEventRecord(done, os_));
@@ -190,6 +201,15 @@ int Step::create(const Cluster& c, const Model& m, const Workload& w, const Plan
       NC(ncclCommSplit(world_comm_, NCCL_SPLIT_NOCOLOR, rank_, &rep_comm_, &cfg));
   }
 
+  // gradient accumulation: global_batch = accum * dp_width * micro_batch
+  // (step_graph.cpp:57; validate's batch_divisibility guarantees the division)
+  accum_ = int(w.global_batch / (p.dp_width() * p.micro_batch));
+  if (accum_ < 1) {
+    set_error("global_batch must be a positive multiple of dp_replicate*dp_shard*micro_batch");
+    return OPX_ERR_CONFIG;
+  }
+  ev_mb_.resize(size_t(2 * accum_));
+  for (auto& e : ev_mb_) CU(cudaEventCreate(&e));
   rows_ = int(p.micro_batch);
   S_ = int(w.seq_len);
   S_loc_ = S_ / sp;
@@ -235,6 +255,13 @@ int Step::build_units() {
     u.gshard = u.gbf ? static_cast<void*>(alloc<bf16>(size_t(u.shard)))
                      : static_cast<void*>(alloc<float>(size_t(u.shard)));
     u.pshard = alloc<bf16>(size_t(u.shard));
+    if (accum_ > 1) {
+      u.gacc = alloc<float>(size_t(u.shard), false);
+      if (!u.gacc) {
+        set_error("out of device memory for gradient accumulation shards");
+        return OPX_ERR_CUDA;
+      }
+    }
     if (!u.master || !u.m || !u.v || !u.gshard || !u.pshard) {
       set_error("out of device memory for parameter shards");
       return OPX_ERR_CUDA;
@@ -451,13 +478,15 @@ int Step::alloc_acts() {
   dhf_ = alloc<float>(T * H, false);
   const int64_t chunk = std::min<int64_t>(ex_.ce_chunk, T_);
   logits_ = alloc<bf16>(size_t(chunk) * size_t(V_), false);
-  loss_rows_ = alloc<float>(T);
+  const size_t A = size_t(accum_);
+  loss_rows_ = alloc<float>(T * A);
   loss_sum_ = alloc<float>(4);
-  d_ids_ = alloc<int32_t>(T);
-  d_labels_ = alloc<int32_t>(T);
-  d_pos_ = alloc<int32_t>(N);
-  d_sstart_ = alloc<int32_t>(N);
-  d_send_ = alloc<int32_t>(N);
+  d_ids_all_ = alloc<int32_t>(T * A);
+  d_labels_all_ = alloc<int32_t>(T * A);
+  d_pos_all_ = alloc<int32_t>(N * A);
+  d_sstart_all_ = alloc<int32_t>(N * A);
+  d_send_all_ = alloc<int32_t>(N * A);
+  bind_micro(0);
   d_inv_freq_ = alloc<float>(64);
   for (void* q : {(void*)h_, (void*)logits_, (void*)dq_acc_, (void*)d_inv_freq_, (void*)x2_})
     if (!q) return cuda_fail(cudaErrorMemoryAllocation, "activations");
@@ -564,11 +593,18 @@ int Step::init_weights(uint64_t seed) {
 
 int Step::load_batch(const int32_t* ids, const int32_t* labels, const int32_t* pos,
                      const int32_t* cu, int n_cu, int64_t n_valid) {
-  if (n_cu < 2 || cu[0] != 0 || cu[n_cu - 1] != Ntok_) {
+  // accum_ micro-batches of rows_ rows each, back to back
+  const int64_t Nall = int64_t(Ntok_) * accum_;
+  if (n_cu < 2 || cu[0] != 0 || cu[n_cu - 1] != Nall) {
     set_error("cu_seqlens must start at 0 and end at rows*seq_len (packing.hpp:28)");
     return OPX_ERR_ARG;
   }
-  std::vector<int32_t> st(static_cast<size_t>(Ntok_)), en(static_cast<size_t>(Ntok_));
+  if (enc_.on && accum_ > 1) {
+    set_error("a frozen encoder module with gradient accumulation is not supported");
+    return OPX_ERR_CONFIG;
+  }
+  // per token: start / end of its sample, relative to its micro-batch
+  std::vector<int32_t> st(static_cast<size_t>(Nall)), en(static_cast<size_t>(Nall));
   for (int i = 0; i + 1 < n_cu; ++i) {
     if (cu[i + 1] <= cu[i]) {
       set_error("cu_seqlens must be strictly increasing");
@@ -578,24 +614,26 @@ int Step::load_batch(const int32_t* ids, const int32_t* labels, const int32_t* p
       set_error("a packed sample crosses a row boundary");
       return OPX_ERR_ARG;
     }
+    const int32_t base = cu[i] / Ntok_ * Ntok_;
     for (int t = cu[i]; t < cu[i + 1]; ++t) {
-      st[size_t(t)] = cu[i];
-      en[size_t(t)] = cu[i + 1];
+      st[size_t(t)] = cu[i] - base;
+      en[size_t(t)] = cu[i + 1] - base;
     }
   }
   n_valid_ = std::max<int64_t>(n_valid, 1);
-  CU(cudaMemcpyAsync(d_ids_, ids, size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
-  CU(cudaMemcpyAsync(d_labels_, labels, size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
+  const size_t TA = size_t(T_) * size_t(accum_);
+  CU(cudaMemcpyAsync(d_ids_all_, ids, TA * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_labels_all_, labels, TA * 4, cudaMemcpyHostToDevice, cs_));
   // the RoPE table covers position ids [0, S); other ids use per-element sincosf
   rope_tab_ok_ = true;
-  for (int64_t i = 0; i < Ntok_; ++i)
+  for (int64_t i = 0; i < Nall; ++i)
     if (pos[i] < 0 || pos[i] >= S_) {
       rope_tab_ok_ = false;
       break;
     }
-  CU(cudaMemcpyAsync(d_pos_, pos, size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
-  CU(cudaMemcpyAsync(d_sstart_, st.data(), size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
-  CU(cudaMemcpyAsync(d_send_, en.data(), size_t(Ntok_) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_pos_all_, pos, size_t(Nall) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_sstart_all_, st.data(), size_t(Nall) * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(d_send_all_, en.data(), size_t(Nall) * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaStreamSynchronize(cs_));
   return OPX_OK;
 }
@@ -664,7 +702,7 @@ GemmDesc gd(int M, int N, int K, const bf16* A, int64_t lda, bool amn, const bf1
 int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int slot) {
   const LayerW W = layer_w(u, u.full);
   const int T = T_, H = H_, F = F_;
-  const std::string pre = "fwd.layer" + std::to_string(l) + ".m0";
+  const std::string pre = "fwd.layer" + std::to_string(l) + mtag();
   const std::string ph = "fwd.layer" + std::to_string(l);
   const bool tr = ex_.trace;
   cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
@@ -711,7 +749,7 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     if (tr) {
       e1 = ev();
       cudaEventRecord(e1, cs_);
-      mark(pre + ".a2a_qkv", ph, 0, e0, e1);
+      mark(pre + ".a2a_qkv", ph, 0, e0, e1, "a2a_q,a2a_k,a2a_v");
       e0 = e1;
     }
     TRY(barrier_sp(cs_));
@@ -826,7 +864,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
   const int T = T_, H = H_, F = F_, Q = hq_ * d_;
   const LayerW W = layer_w(u, u.full);
   const bool tr = ex_.trace;
-  const std::string pre = "bwd.layer" + std::to_string(l) + ".m0";
+  const std::string pre = "bwd.layer" + std::to_string(l) + mtag();
   const std::string ph = "bwd.layer" + std::to_string(l);
   cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
   if (tr) cudaEventRecord(e0, cs_);
@@ -928,6 +966,12 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
   }
   CU(gemm_run(gd(T, Q, H, dxb_, H, false, W.o, Q, true, GEMM_EPI_BF16, do_loc, Q), cs_));
   CU(gemm_run(gd(H, Q, T, dxb_, H, true, o_loc(ob), Q, true, EPI_G, g_o, Q), cs_));
+  if (tr) {
+    e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(pre + ".out_proj", ph, 0, e0, e1);
+    e0 = e1;
+  }
   if (relay_) {
     A2AArgs a{};
     a.sp = int(p_.sp);
@@ -944,13 +988,19 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     a.hd = d_;
     a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
     if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
+    if (tr) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_do", ph, 0, e0, e1);
+      e0 = e1;
+    }
     TRY(barrier_sp(cs_));
-  }
-  if (tr) {
-    e1 = ev();
-    cudaEventRecord(e1, cs_);
-    mark(pre + ".out_proj", ph, 0, e0, e1);
-    e0 = e1;
+    if (tr && p_.sp > 1) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".a2a_wait", ph, 0, e0, e1);
+      e0 = e1;
+    }
   }
   // ---- attention core
   {
@@ -1006,7 +1056,7 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     if (tr) {
       e1 = ev();
       cudaEventRecord(e1, cs_);
-      mark(pre + ".a2a_dqkv", ph, 0, e0, e1);
+      mark(pre + ".a2a_dqkv", ph, 0, e0, e1, "a2a_dq,a2a_dk,a2a_dv");
       e0 = e1;
     }
     TRY(barrier_sp(cs_));
@@ -1038,8 +1088,18 @@ int Step::head_fwd_bwd(Unit& u, float* G) {
   float* g_head = G + u.params[2].off;
   const float* xf = x_saved_.back();
   const bool tr = ex_.trace;
+  // the loss is computed chunk by chunk with the backward of each chunk right
+  // behind its forward: the logits GEMM + CE of a chunk are fwd.head nodes,
+  // its dgrad / wgrad GEMMs (and the final norm's backward) bwd.head nodes
   cudaEvent_t e0 = tr ? ev() : nullptr;
   if (tr) cudaEventRecord(e0, cs_);
+  auto node = [&](const char* name) {
+    if (!tr) return;
+    cudaEvent_t e1 = ev();
+    cudaEventRecord(e1, cs_);
+    mark(std::string(name) + mtag(), name, 0, e0, e1);
+    e0 = e1;
+  };
   CU(k_rmsnorm_fwd(xf, W_norm, hf_, rf_, T, H, ex_.rms_eps, cs_));
   const int C = int(std::min<int64_t>(ex_.ce_chunk, T));
   for (int c0 = 0; c0 < T; c0 += C) {
@@ -1047,27 +1107,51 @@ int Step::head_fwd_bwd(Unit& u, float* G) {
     CU(gemm_run(gd(n, V, H, hf_ + int64_t(c0) * H, H, false, W_head, H, false, GEMM_EPI_BF16,
                    logits_, V),
                 cs_));
-    CU(k_ce_fwd_bwd(logits_, V, d_labels_ + c0, loss_rows_ + c0, n, V, 1.0f / float(n_valid_),
-                    cs_));
+    CU(k_ce_fwd_bwd(logits_, V, d_labels_ + c0, loss_rows_ + int64_t(mb_) * T + c0, n, V,
+                    1.0f / float(n_valid_), cs_));
+    node("fwd.head");
     CU(gemm_run(gd(n, H, V, logits_, V, false, W_head, H, true, GEMM_EPI_F32,
                    dhf_ + int64_t(c0) * H, H),
                 cs_));
     CU(gemm_run(gd(V, H, n, logits_, V, true, hf_ + int64_t(c0) * H, H, true,
                    c0 == 0 ? GEMM_EPI_F32 : GEMM_EPI_F32_ACCUM, g_head, H),
                 cs_));
+    node("bwd.head");
   }
   CU(k_rmsnorm_bwd(dhf_, xf, W_norm, rf_, nullptr, dx_, dw_part_, g_norm, 0, T, H, cs_));
-  if (tr) {
-    cudaEvent_t e1 = ev();
-    cudaEventRecord(e1, cs_);
-    mark("fwd_bwd.head.m0", "head", 0, e0, e1);
-  }
+  node("bwd.head");
   return OPX_OK;
 }
 
 // ---------------------------------------------------------------------------
 // the step
 // ---------------------------------------------------------------------------
+int Step::unit_grad_ready(Unit& u, cudaStream_t s, const std::string& name, int layer) {
+  if (u.params.empty()) return OPX_OK;
+  const ncclDataType_t gdt = u.gbf ? ncclBfloat16 : ncclFloat;
+  void* g = u.gshard;
+  if (accum_ > 1) {
+    CU(k_grad_accum(u.gacc, u.gshard, u.gbf, u.shard, mb_ == 0, s));
+    if (!last_mb()) return OPX_OK;
+    g = u.gacc;
+  }
+  if (u.rep_comm) {
+    // HSDP: replicas all-reduce the (accumulated) shard gradient on the last
+    // micro-batch only (step_graph.cpp:356-364)
+    const bool tr = ex_.trace;
+    cudaEvent_t a = tr ? ev() : nullptr;
+    if (tr) cudaEventRecord(a, s);
+    NC(ncclAllReduce(g, g, size_t(u.shard), accum_ > 1 ? ncclFloat : gdt, ncclSum, u.rep_comm, s));
+    if (tr) {
+      cudaEvent_t b = ev();
+      cudaEventRecord(b, s);
+      mark("bwd.ar." + name + mtag(), layer < 0 ? "bwd.head" : "bwd.layer" + std::to_string(layer),
+           s == ms_ ? 1 : 0, a, b);
+    }
+  }
+  return opt_unit(u, s, "opt." + name);
+}
+
 int Step::run(opx_step_report* rep) {
   const int L = int(a_.layers);
   const bool tr = ex_.trace;
@@ -1082,25 +1166,25 @@ int Step::run(opx_step_report* rep) {
   Unit& hu = units_[0];
   const int P = hu.P;
 
-  // ---------------- forward ----------------
+  // the head's parameters are gathered once and stay resident for every
+  // micro-batch (its gradient is reduce-scattered per micro-batch)
+  bind_micro(0);
   if (P > 1) {
     cudaEvent_t a = tr ? ev() : nullptr;
     if (tr) cudaEventRecord(a, ms_);
     TRY(gather(hu, -1, nullptr));
     CU(cudaEventRecord(ev_head_ag_, ms_));
-    if (tr) mark("fwd.ag.head.m0", "fwd.head", 1, a, ev_head_ag_);
+    if (tr) mark("fwd.ag.head" + mtag(), "fwd.head", 1, a, ev_head_ag_);
     CU(cudaStreamWaitEvent(cs_, ev_head_ag_, 0));
   }
-  // embedding grad region is scatter-added: zero it
-  CU(cudaMemsetAsync(hu.gat(hu.gfull, hu.params[0].off), 0, size_t(hu.params[0].numel) * 4, cs_));
-  CU(k_embed_fwd(d_ids_, hu.full + hu.params[0].off, x_saved_[0], T_, H_, cs_));
-  TRY(enc_forward());  // frozen encoder: features replace the placeholder embeddings
 
   auto issue_gather = [&](int l, bool bwd) -> int {
     Unit& u = units_[size_t(1 + l)];
     if (u.P == 1) return OPX_OK;
     const int slot = l % nslots_;
-    // the slot was last used by layer l + nslots (bwd) or l - nslots (fwd)
+    // the slot was last used by layer l + nslots (bwd) or l - nslots (fwd);
+    // across micro-batches the gather queues behind the previous micro-batch's
+    // reduce-scatters on ms_, which each waited for their layer's backward
     const int prev = bwd ? l + nslots_ : l - nslots_;
     cudaEvent_t wait = (prev >= 0 && prev < L) ? ev_use_done_[size_t(prev)] : nullptr;
     cudaEvent_t a = tr ? ev() : nullptr;
@@ -1109,141 +1193,156 @@ int Step::run(opx_step_report* rep) {
     TRY(gather(u, slot, nullptr));
     CU(cudaEventRecord(ev_ag_[size_t(l)], ms_));
     if (tr)
-      mark(std::string(bwd ? "bwd" : "fwd") + ".ag.layer" + std::to_string(l) + ".m0",
+      mark(std::string(bwd ? "bwd" : "fwd") + ".ag.layer" + std::to_string(l) + mtag(),
            std::string(bwd ? "bwd" : "fwd") + ".layer" + std::to_string(l), 1, a,
            ev_ag_[size_t(l)]);
     return OPX_OK;
   };
 
-  for (int l = 0; l < std::min(L, nslots_ - 1); ++l) TRY(issue_gather(l, false));
-  for (int l = 0; l < L; ++l) {
-    Unit& u = units_[size_t(1 + l)];
-    if (u.P > 1) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
-    if (l + nslots_ - 1 < L) TRY(issue_gather(l + nslots_ - 1, false));
-    int slot;
-    if (keeps_acts(l)) {
-      bind_layer(l);
-      slot = 2 + l;
-      store_gu_ = keeps_mlp(l);
-    } else {
-      bind(scratch_);
-      slot = next_rslot();
+  for (int mb = 0; mb < accum_; ++mb) {
+    bind_micro(mb);
+    // ---------------- forward ----------------
+    // embedding grad region is scatter-added: zero it
+    CU(cudaMemsetAsync(hu.gat(hu.gfull, hu.params[0].off), 0, size_t(hu.params[0].numel) * 4, cs_));
+    CU(k_embed_fwd(d_ids_, hu.full + hu.params[0].off, x_saved_[0], T_, H_, cs_));
+    TRY(enc_forward());  // frozen encoder: features replace the placeholder embeddings
+
+    for (int l = 0; l < std::min(L, nslots_ - 1); ++l) TRY(issue_gather(l, false));
+    for (int l = 0; l < L; ++l) {
+      Unit& u = units_[size_t(1 + l)];
+      if (u.P > 1) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
+      if (l + nslots_ - 1 < L) TRY(issue_gather(l + nslots_ - 1, false));
+      int slot;
+      if (keeps_acts(l)) {
+        bind_layer(l);
+        slot = 2 + l;
+        store_gu_ = keeps_mlp(l);
+      } else {
+        bind(scratch_);
+        slot = next_rslot();
+        store_gu_ = false;
+      }
+      if (moe_ && a_.is_moe_layer(l) && De_ > 1) {
+        Unit& eu = expert_units_[size_t(l)];
+        eu.full = eslot_;
+        NC(ncclAllGather(eu.pshard, eslot_, size_t(eu.shard), ncclBfloat16, eu.comm, cs_));
+      }
+      TRY(layer_fwd(l, u, x_saved_[size_t(l)], x_saved_[size_t(l + 1)], slot));
       store_gu_ = false;
+      CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
     }
-    if (moe_ && a_.is_moe_layer(l) && De_ > 1) {
-      Unit& eu = expert_units_[size_t(l)];
-      eu.full = eslot_;
-      NC(ncclAllGather(eu.pshard, eslot_, size_t(eu.shard), ncclBfloat16, eu.comm, cs_));
-    }
-    TRY(layer_fwd(l, u, x_saved_[size_t(l)], x_saved_[size_t(l + 1)], slot));
-    store_gu_ = false;
-    CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
-  }
-  CU(cudaEventRecord(ev_fwd_, cs_));
+    CU(cudaEventRecord(ev_mb_[size_t(2 * mb)], cs_));
 
-  if (moe_ && save_acts_) {
-    // the top MoE layer's token re-send can start now, overlapping the head:
-    // every peer passed that layer's forward combine barrier, so its expert
-    // GEMMs no longer read the receive buffer
-    const int lt = next_moe_below(L);
-    if (lt >= 0) {
-      cudaEvent_t e = ev();
-      CU(cudaEventRecord(e, cs_));
-      CU(cudaStreamWaitEvent(xs_, e, 0));
-      TRY(moe_redispatch(lt));
+    if (moe_ && save_acts_) {
+      // the top MoE layer's token re-send can start now, overlapping the head:
+      // every peer passed that layer's forward combine barrier, so its expert
+      // GEMMs no longer read the receive buffer
+      const int lt = next_moe_below(L);
+      if (lt >= 0) {
+        cudaEvent_t e = ev();
+        CU(cudaEventRecord(e, cs_));
+        CU(cudaStreamWaitEvent(xs_, e, 0));
+        TRY(moe_redispatch(lt));
+      }
     }
-  }
-  // ---------------- head (fwd + CE + bwd) ----------------
-  TRY(head_fwd_bwd(hu, static_cast<float*>(hu.gfull)));  // the head keeps fp32 grads
+    // ---------------- head (fwd + CE + bwd) ----------------
+    TRY(head_fwd_bwd(hu, static_cast<float*>(hu.gfull)));  // the head keeps fp32 grads
 
-  // ---------------- backward ----------------
-  // layers L-nslots .. L-1 are still resident in their slots from the forward
-  const int resident_from = std::max(0, L - nslots_);
-  for (int l = L - 1; l >= 0; --l) {
-    Unit& u = units_[size_t(1 + l)];
-    if (u.P > 1) {
-      if (l < resident_from) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
-      // prefetch the next (lower) layer that is not resident
-      const int nxt = l - 1;
-      if (nxt >= 0 && nxt < resident_from) {
-        // only issue once per layer: when l is the first layer above nxt
-        TRY(issue_gather(nxt, true));
-      }
-      u.full = gslot_[size_t(l % nslots_)];
-      u.gfull = gradslot_[size_t(l % 2)];
-      if (l + 2 < L) CU(cudaStreamWaitEvent(cs_, ev_rs_done_[size_t(l + 2)], 0));
-    }
-    if (moe_ && a_.is_moe_layer(l) && De_ > 1) {
-      Unit& eu = expert_units_[size_t(l)];
-      eu.full = eslot_;
-      eu.gfull = egrad_slot_;
-      NC(ncclAllGather(eu.pshard, eslot_, size_t(eu.shard), ncclBfloat16, eu.comm, cs_));
-    }
-    TRY(layer_bwd(l, u, u.gfull));
-    if (moe_ && a_.is_moe_layer(l)) {
-      // expert grads: sum over the ranks holding the same experts, then replicas
-      Unit& eu = expert_units_[size_t(l)];
-      if (eu.P > 1) {
-        if (eu.padded > eu.numel)
-          CU(cudaMemsetAsync(eu.gat(eu.gfull, eu.numel), 0, size_t(eu.padded - eu.numel) * eu.gbytes(),
-                             cs_));
-        NC(ncclReduceScatter(eu.gfull, eu.gshard, size_t(eu.shard), eu.gbf ? ncclBfloat16 : ncclFloat,
-                             ncclSum, eu.comm,
-                             cs_));
-      }
-      if (eu.rep_comm)
-        NC(ncclAllReduce(eu.gshard, eu.gshard, size_t(eu.shard), eu.gbf ? ncclBfloat16 : ncclFloat,
-                         ncclSum,
-                         eu.rep_comm, cs_));
-      TRY(opt_unit(eu, cs_, "opt.experts.layer" + std::to_string(l)));
-    }
-    CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
-    if (u.P > 1 || u.rep_comm) {
-      CU(cudaEventRecord(ev_grad_done_[size_t(l)], cs_));
-      CU(cudaStreamWaitEvent(ms_, ev_grad_done_[size_t(l)], 0));
-      cudaEvent_t a = tr ? ev() : nullptr;
-      if (tr) cudaEventRecord(a, ms_);
+    // ---------------- backward ----------------
+    // layers L-nslots .. L-1 are still resident in their slots from the forward
+    const int resident_from = std::max(0, L - nslots_);
+    for (int l = L - 1; l >= 0; --l) {
+      Unit& u = units_[size_t(1 + l)];
       if (u.P > 1) {
-        if (u.padded > u.numel)
-          CU(cudaMemsetAsync(u.gat(u.gfull, u.numel), 0, size_t(u.padded - u.numel) * u.gbytes(),
-                             ms_));
-        NC(ncclReduceScatter(u.gfull, u.gshard, size_t(u.shard), u.gbf ? ncclBfloat16 : ncclFloat,
-                             ncclSum, u.comm, ms_));
+        if (l < resident_from) CU(cudaStreamWaitEvent(cs_, ev_ag_[size_t(l)], 0));
+        // prefetch the next (lower) layer that is not resident
+        const int nxt = l - 1;
+        if (nxt >= 0 && nxt < resident_from) {
+          // only issue once per layer: when l is the first layer above nxt
+          TRY(issue_gather(nxt, true));
+        }
+        u.full = gslot_[size_t(l % nslots_)];
+        u.gfull = gradslot_[size_t(l % 2)];
+        if (l + 2 < L) CU(cudaStreamWaitEvent(cs_, ev_rs_done_[size_t(l + 2)], 0));
       }
-      if (u.rep_comm)
-        NC(ncclAllReduce(u.gshard, u.gshard, size_t(u.shard), u.gbf ? ncclBfloat16 : ncclFloat,
-                         ncclSum, u.rep_comm, ms_));
-      CU(cudaEventRecord(ev_rs_done_[size_t(l)], ms_));
-      if (tr)
-        mark("bwd.rs.layer" + std::to_string(l) + ".m0", "bwd.layer" + std::to_string(l), 1, a,
-             ev_rs_done_[size_t(l)]);
-      TRY(opt_unit(u, ms_, "opt.layer" + std::to_string(l)));
+      if (moe_ && a_.is_moe_layer(l) && De_ > 1) {
+        Unit& eu = expert_units_[size_t(l)];
+        eu.full = eslot_;
+        eu.gfull = egrad_slot_;
+        NC(ncclAllGather(eu.pshard, eslot_, size_t(eu.shard), ncclBfloat16, eu.comm, cs_));
+      }
+      TRY(layer_bwd(l, u, u.gfull));
+      if (moe_ && a_.is_moe_layer(l)) {
+        // expert grads: sum over the ranks holding the same experts, then replicas
+        Unit& eu = expert_units_[size_t(l)];
+        if (eu.P > 1) {
+          if (eu.padded > eu.numel)
+            CU(cudaMemsetAsync(eu.gat(eu.gfull, eu.numel), 0,
+                               size_t(eu.padded - eu.numel) * eu.gbytes(), cs_));
+          NC(ncclReduceScatter(eu.gfull, eu.gshard, size_t(eu.shard),
+                               eu.gbf ? ncclBfloat16 : ncclFloat, ncclSum, eu.comm, cs_));
+        }
+        TRY(unit_grad_ready(eu, cs_, "experts.layer" + std::to_string(l), l));
+      }
+      CU(cudaEventRecord(ev_use_done_[size_t(l)], cs_));
+      if (u.P > 1 || u.rep_comm) {
+        CU(cudaEventRecord(ev_grad_done_[size_t(l)], cs_));
+        CU(cudaStreamWaitEvent(ms_, ev_grad_done_[size_t(l)], 0));
+        if (u.P > 1) {
+          cudaEvent_t a = tr ? ev() : nullptr;
+          if (tr) cudaEventRecord(a, ms_);
+          if (u.padded > u.numel)
+            CU(cudaMemsetAsync(u.gat(u.gfull, u.numel), 0, size_t(u.padded - u.numel) * u.gbytes(),
+                               ms_));
+          NC(ncclReduceScatter(u.gfull, u.gshard, size_t(u.shard), u.gbf ? ncclBfloat16 : ncclFloat,
+                               ncclSum, u.comm, ms_));
+          if (tr) {
+            cudaEvent_t b = ev();
+            cudaEventRecord(b, ms_);
+            mark("bwd.rs.layer" + std::to_string(l) + mtag(), "bwd.layer" + std::to_string(l), 1,
+                 a, b);
+          }
+        }
+        TRY(unit_grad_ready(u, ms_, "layer" + std::to_string(l), l));
+        CU(cudaEventRecord(ev_rs_done_[size_t(l)], ms_));
+      } else {
+        TRY(unit_grad_ready(u, cs_, "layer" + std::to_string(l), l));
+      }
+    }
+    if (enc_.on && enc_.n_all) CU(k_rows_zero(dx_, d_fmask_, T_, H_, cs_));
+    CU(k_embed_bwd(d_ids_, dx_, static_cast<float*>(hu.gfull) + hu.params[0].off, T_, H_, cs_));
+    if (P > 1 || hu.rep_comm) {
+      CU(cudaEventRecord(ev_head_rs_, cs_));
+      CU(cudaStreamWaitEvent(ms_, ev_head_rs_, 0));
+      if (P > 1) {
+        cudaEvent_t a = tr ? ev() : nullptr;
+        if (tr) cudaEventRecord(a, ms_);
+        if (hu.padded > hu.numel)
+          CU(cudaMemsetAsync(hu.gat(hu.gfull, hu.numel), 0, size_t(hu.padded - hu.numel) * 4, ms_));
+        NC(ncclReduceScatter(hu.gfull, hu.gshard, size_t(hu.shard), ncclFloat, ncclSum, hu.comm,
+                             ms_));
+        if (tr) {
+          cudaEvent_t b = ev();
+          cudaEventRecord(b, ms_);
+          mark("bwd.rs.head" + mtag(), "bwd.head", 1, a, b);
+        }
+      }
+      TRY(unit_grad_ready(hu, ms_, "head", -1));
     } else {
-      TRY(opt_unit(u, cs_, "opt.layer" + std::to_string(l)));
+      TRY(unit_grad_ready(hu, cs_, "head", -1));
     }
-  }
-  if (enc_.on && enc_.n_all) CU(k_rows_zero(dx_, d_fmask_, T_, H_, cs_));
-  CU(k_embed_bwd(d_ids_, dx_, static_cast<float*>(hu.gfull) + hu.params[0].off, T_, H_, cs_));
-  if (P > 1 || hu.rep_comm) {
-    CU(cudaEventRecord(ev_head_rs_, cs_));
-    CU(cudaStreamWaitEvent(ms_, ev_head_rs_, 0));
-    if (P > 1) {
-      if (hu.padded > hu.numel)
-        CU(cudaMemsetAsync(hu.gat(hu.gfull, hu.numel), 0, size_t(hu.padded - hu.numel) * 4, ms_));
-      NC(ncclReduceScatter(hu.gfull, hu.gshard, size_t(hu.shard), ncclFloat, ncclSum, hu.comm,
-                           ms_));
+    // join the comm stream (and the MoE side stream): the next micro-batch
+    // reuses the gradient slots, exchange buffers and routing state
+    cudaEvent_t join = ev();
+    CU(cudaEventRecord(join, ms_));
+    CU(cudaStreamWaitEvent(cs_, join, 0));
+    if (xs_) {
+      cudaEvent_t xj = ev();
+      CU(cudaEventRecord(xj, xs_));
+      CU(cudaStreamWaitEvent(cs_, xj, 0));
     }
-    if (hu.rep_comm)
-      NC(ncclAllReduce(hu.gshard, hu.gshard, size_t(hu.shard), ncclFloat, ncclSum, hu.rep_comm,
-                       ms_));
-    TRY(opt_unit(hu, ms_, "opt.head"));
-  } else {
-    TRY(opt_unit(hu, cs_, "opt.head"));
+    CU(cudaEventRecord(ev_mb_[size_t(2 * mb + 1)], cs_));
   }
-  // join the comm stream
-  cudaEvent_t join = ev();
-  CU(cudaEventRecord(join, ms_));
-  CU(cudaStreamWaitEvent(cs_, join, 0));
   CU(cudaEventRecord(ev_bwd_, cs_));
 
   // ---------------- optimizer ----------------
@@ -1253,16 +1352,14 @@ int Step::run(opx_step_report* rep) {
   cudaEvent_t opt_join = ev();
   CU(cudaEventRecord(opt_join, os_));
   CU(cudaStreamWaitEvent(cs_, opt_join, 0));
-  if (xs_) {
-    cudaEvent_t xj = ev();
-    CU(cudaEventRecord(xj, xs_));
-    CU(cudaStreamWaitEvent(cs_, xj, 0));
-  }
   CU(cudaEventRecord(ev_end_, cs_));
-  if (tr) mark("optimizer", "optimizer", 0, ev_bwd_, ev_end_);
+  if (tr) {
+    mark("optimizer", "optimizer", 0, ev_bwd_, ev_end_);
+    trace_.back().span = true;  // the exposed tail; the opt.* nodes are the busy intervals
+  }
 
   // loss: local sum -> world all-reduce (reporting only, off the timed path)
-  CU(k_sum(loss_rows_, T_, loss_sum_, cs_));
+  CU(k_sum(loss_rows_, int64_t(T_) * accum_, loss_sum_, cs_));
   if (world_comm_) NC(ncclAllReduce(loss_sum_, loss_sum_, 1, ncclFloat, ncclSum, world_comm_, cs_));
   const double enqueue_s =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - host_t0).count();
@@ -1276,26 +1373,89 @@ int Step::run(opx_step_report* rep) {
     set_error("peer barrier timed out (a peer rank stalled)");
     return OPX_ERR_TIMEOUT;
   }
-  float t_all = 0, t_fwd = 0, t_bwd = 0, t_opt = 0;
+  float t_all = 0, t_opt = 0;
   CU(cudaEventElapsedTime(&t_all, ev_start_, ev_end_));
-  CU(cudaEventElapsedTime(&t_fwd, ev_start_, ev_fwd_));
-  CU(cudaEventElapsedTime(&t_bwd, ev_fwd_, ev_bwd_));
   CU(cudaEventElapsedTime(&t_opt, ev_bwd_, ev_end_));
-  if (rep) {
-    std::memset(rep, 0, sizeof(*rep));
-    rep->step_time_s = t_all * 1e-3;
-    rep->fwd_s = t_fwd * 1e-3;
-    rep->bwd_s = t_bwd * 1e-3;
-    rep->opt_s = t_opt * 1e-3;
-    rep->loss = double(loss) / double(n_valid_);
-    rep->tokens = double(T_);
-    rep->n_valid = double(n_valid_);
-    rep->launches = g_kernel_launches - launches0 - 1;  // minus the loss reduction
-    rep->enqueue_s = enqueue_s;
-    rep->kept_layers = 0;
-    for (int m : keep_mode_) rep->kept_layers += m >= 1;
+  double t_fwd = 0, t_bwd = 0;
+  for (int mb = 0; mb < accum_; ++mb) {
+    float f = 0, b = 0;
+    CU(cudaEventElapsedTime(&f, mb ? ev_mb_[size_t(2 * mb - 1)] : ev_start_, ev_mb_[size_t(2 * mb)]));
+    CU(cudaEventElapsedTime(&b, ev_mb_[size_t(2 * mb)], ev_mb_[size_t(2 * mb + 1)]));
+    t_fwd += f;
+    t_bwd += b;
   }
+  opx_step_report& r = last_;
+  std::memset(&r, 0, sizeof(r));
+  r.step_time_s = t_all * 1e-3;
+  r.fwd_s = t_fwd * 1e-3;
+  r.bwd_s = t_bwd * 1e-3;
+  r.opt_s = t_opt * 1e-3;
+  r.loss = double(loss) / double(n_valid_);
+  r.tokens = double(T_) * accum_;
+  r.n_valid = double(n_valid_);
+  r.launches = g_kernel_launches - launches0 - 1;  // minus the loss reduction
+  r.enqueue_s = enqueue_s;
+  for (int m : keep_mode_) r.kept_layers += m >= 1;
+  r.accum_steps = accum_;
+  // simulator.cpp:111-118 on the measured step time
+  r.throughput = double(w_.global_batch) * double(w_.seq_len) / (r.step_time_s * double(world_));
+  r.model_flops_per_token = flops_per_token_ref(m_, w_.seq_len);
+  r.mfu = c_.peak_flops > 0 ? r.throughput * r.model_flops_per_token / c_.peak_flops : 0.0;
+  measure_nodes(&r);
+  if (rep) *rep = r;
   return OPX_OK;
+}
+
+void Step::measure_nodes(opx_step_report* r) {
+  // exposed_comm_seconds (simulator.cpp:71-104) and the phase breakdown
+  // (:120-129) over this rank's measured node intervals
+  phases_.clear();
+  std::vector<std::pair<double, double>> compute, comm;
+  for (auto& t : trace_) {
+    if (t.span) continue;
+    float s = 0, e = 0;
+    if (cudaEventElapsedTime(&s, ev_start_, t.a) != cudaSuccess) continue;
+    if (cudaEventElapsedTime(&e, ev_start_, t.b) != cudaSuccess) continue;
+    const double a = s * 1e-3, b = e * 1e-3;
+    (t.comm ? comm : compute).push_back({a, b});
+    auto& ph = phases_[t.phase];
+    (t.comm ? ph.second : ph.first) += b - a;
+    if (t.comm) r->comm_s += b - a;
+  }
+  cudaGetLastError();
+  std::sort(compute.begin(), compute.end());
+  std::sort(comm.begin(), comm.end());
+  double exposed = 0;
+  size_t ci = 0;
+  for (const auto& [start, end] : comm) {
+    double cur = start;
+    while (ci < compute.size() && compute[ci].second <= cur) ++ci;
+    // intervals on several streams can nest: scan every compute interval
+    // starting before `end` (sorted by start), advancing the covered cursor
+    for (size_t j = ci; cur < end; ++j) {
+      if (j >= compute.size() || compute[j].first >= end) {
+        exposed += end - cur;
+        break;
+      }
+      if (compute[j].second <= cur) continue;
+      if (compute[j].first > cur) exposed += compute[j].first - cur;
+      cur = std::max(cur, compute[j].second);
+    }
+  }
+  r->comm_wait_s = exposed;
+  r->exposed_comm = r->step_time_s > 0 ? exposed / r->step_time_s : 0.0;
+}
+
+std::string Step::report_json() {
+  nlohmann::json ph = nlohmann::json::object();
+  for (const auto& [name, c] : phases_) ph[name] = {{"compute_s", c.first}, {"comm_s", c.second}};
+  nlohmann::json j{{"step_time_s", last_.step_time_s},
+                   {"throughput_tokens_per_s_per_gpu", last_.throughput},
+                   {"mfu", last_.mfu},
+                   {"exposed_comm_fraction", last_.exposed_comm},
+                   {"model_flops_per_token", last_.model_flops_per_token},
+                   {"phase_breakdown", std::move(ph)}};
+  return j.dump();
 }
 
 // ---------------------------------------------------------------------------
@@ -1325,10 +1485,10 @@ int Step::info(const std::string& full, int64_t* numel, int64_t* b, int64_t* e) 
 }
 
 int Step::get(const std::string& full, void* dst, size_t bytes) {
-  if (full.rfind("route:", 0) == 0) {  // forward top-k indices of MoE layer l (this rank's T*k)
+  if (full.rfind("route:", 0) == 0) {  // forward top-k indices of MoE layer l (this rank's accum*T*k)
     const int l = std::atoi(full.c_str() + 6);
     if (l < 0 || l >= int(route_idx_.size()) || !route_idx_[size_t(l)] ||
-        bytes != size_t(T_) * size_t(topk_) * 4) {
+        bytes != size_t(T_) * size_t(topk_) * size_t(accum_) * 4) {
       set_error("route: bad layer or size");
       return OPX_ERR_ARG;
     }
@@ -1350,7 +1510,7 @@ int Step::get(const std::string& full, void* dst, size_t bytes) {
     return OPX_OK;
   }
   if (full == "loss_rows") {
-    if (bytes != size_t(T_) * 4) {
+    if (bytes != size_t(T_) * size_t(accum_) * 4) {
       set_error("loss_rows: size mismatch");
       return OPX_ERR_ARG;
     }
@@ -1386,6 +1546,10 @@ int Step::get(const std::string& full, void* dst, size_t bytes) {
       set_error("size mismatch for " + full);
       return OPX_ERR_ARG;
     }
+    if (kind == "grad" && accum_ > 1) {  // the step's gradient: the micro-batch sum
+      if (cnt) CU(cudaMemcpy(dst, u.gacc + src0, bytes, cudaMemcpyDeviceToHost));
+      return OPX_OK;
+    }
     if (kind == "grad" && u.gbf) {  // bf16 gradients are returned widened to fp32
       std::vector<uint16_t> h(static_cast<size_t>(cnt));
       if (cnt) CU(cudaMemcpy(h.data(), static_cast<const bf16*>(u.gshard) + src0, size_t(cnt) * 2,
@@ -1419,14 +1583,17 @@ std::string Step::trace_json() {
     float s = 0, e = 0;
     if (cudaEventElapsedTime(&s, ev_start_, t.a) != cudaSuccess) continue;
     if (cudaEventElapsedTime(&e, ev_start_, t.b) != cudaSuccess) continue;
+    nlohmann::json args{{"phase", t.phase}};
+    if (!t.fused.empty()) args["fused"] = t.fused;
+    if (t.span) args["span"] = true;
     evs.push_back({{"name", t.name},
-                   {"cat", t.tid == 0 ? "compute" : "comm"},
+                   {"cat", t.comm ? "comm" : "compute"},
                    {"ph", "X"},
                    {"ts", double(s) * 1e3},
                    {"dur", double(e - s) * 1e3},
                    {"pid", rank_},
                    {"tid", t.tid},
-                   {"args", {{"phase", t.phase}}}});
+                   {"args", args}});
   }
   nlohmann::json j{{"traceEvents", evs}, {"displayTimeUnit", "ms"}};
   return j.dump();
@@ -1482,7 +1649,7 @@ int opx_step_create(const char* cj, const char* mj, const char* wj, const char* 
     ex.rope_theta = e.value("rope_theta", ex.rope_theta);
     ex.rms_eps = e.value("rms_eps", ex.rms_eps);
     ex.ce_chunk = e.value("ce_chunk", ex.ce_chunk);
-    ex.trace = e.value("trace", false);
+    ex.trace = e.value("trace", true);
     ex.selective_recompute = e.value("selective_recompute", true);
     ex.bf16_grads = e.value("bf16_grads", true);
   } catch (const std::exception& e) {
@@ -1495,11 +1662,6 @@ int opx_step_create(const char* cj, const char* mj, const char* wj, const char* 
     for (auto& x : v) s += x.code + " ";
     set_error("plan invalid: " + s);
     return OPX_ERR_PLAN;
-  }
-  if (w.global_batch != p.dp_width() * p.micro_batch) {
-    set_error("executor runs one micro-batch per dp rank: global_batch must equal "
-              "dp_replicate*dp_shard*micro_batch");
-    return OPX_ERR_CONFIG;
   }
   auto* st = new opx_step;
   int rc = st->impl.create(c, m, w, p, ex, rank, device, nccl_id);
@@ -1538,6 +1700,17 @@ int opx_step_get(opx_step* st, const char* name, void* dst, size_t bytes) {
 }
 int opx_step_tensor_info(opx_step* st, const char* name, int64_t* numel, int64_t* b, int64_t* e) {
   return st->impl.info(name, numel, b, e);
+}
+int opx_step_report_json(opx_step* st, char* out, size_t cap, size_t* len) {
+  const std::string s = st->impl.report_json();
+  *len = s.size();
+  if (!out || cap <= s.size()) {
+    set_error("report buffer too small");
+    return OPX_ERR_ARG;
+  }
+  std::memcpy(out, s.data(), s.size());
+  out[s.size()] = 0;
+  return OPX_OK;
 }
 int opx_step_trace(opx_step* st, char* out, size_t cap, size_t* len) {
   const std::string s = st->impl.trace_json();

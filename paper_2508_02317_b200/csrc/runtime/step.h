@@ -24,7 +24,7 @@ struct ExecCfg {
   double rope_theta = 1e6;
   float rms_eps = 1e-6f;
   int64_t ce_chunk = 8192;
-  bool trace = false;
+  bool trace = true;  // node events for the report (exposed comm, phases) and the chrome trace
   // recompute=full: keep the attention activations of as many dense layers as
   // free HBM allows (their backward recomputes only gate|up)
   bool selective_recompute = true;
@@ -66,6 +66,9 @@ struct Unit {
   bool gbf = false;
   size_t gbytes() const { return gbf ? 2 : 4; }
   void* gat(void* base, int64_t off) const { return static_cast<char*>(base) + off * int64_t(gbytes()); }
+  // gradient accumulation (accum_steps > 1): fp32 sum of the micro-batches'
+  // shard gradients; AdamW and the HSDP all-reduce read it after the last one
+  float* gacc = nullptr;
   bf16* pshard = nullptr;
   bf16* full = nullptr;        // gathered params (alias of pshard when P == 1)
   void* gfull = nullptr;       // full-layout grads (alias of gshard when P == 1)
@@ -76,10 +79,17 @@ struct Unit {
   }
 };
 
+// One measured node: name / phase follow step_graph.cpp (a16); tid is the
+// stream it ran on (0 compute, 1 FSDP comm, 2 optimizer, 3/4 MoE side
+// streams); comm marks the reference's collective nodes (NCCL gathers and
+// reduce-scatters, Ulysses and EP exchanges incl. their flag barriers);
+// span marks an enclosing interval that is not a busy node of its own.
 struct TraceEv {
   std::string name, phase;
   int tid;
   cudaEvent_t a, b;
+  bool comm = false, span = false;
+  std::string fused;  // names of the reference nodes a fused exchange stands for
 };
 
 class Step {
@@ -101,6 +111,8 @@ class Step {
   int get(const std::string& name, void* dst, size_t bytes);
   int info(const std::string& name, int64_t* numel, int64_t* b, int64_t* e);
   std::string trace_json();
+  // to_json(StepReport) keys (report.cpp:117-128) of the last step
+  std::string report_json();
 
  private:
   // ---- configuration
@@ -118,6 +130,14 @@ class Step {
   int H_ = 0, d_ = 128, hq_ = 0, hk_ = 0, hql_ = 0, hkl_ = 0, Wqkv_ = 0, F_ = 0, V_ = 0;
   int step_count_ = 0;
   int64_t n_valid_ = 1;
+  // gradient accumulation (step_graph.cpp:57): micro-batches per step, the
+  // one being executed, and its trace suffix (".m<k>", step_graph.cpp:133-135)
+  int accum_ = 1, mb_ = 0;
+  bool last_mb() const { return mb_ == accum_ - 1; }
+  std::string mtag() const { return ".m" + std::to_string(mb_); }
+  // final gradient of a unit's shard for this micro-batch is ready on stream s:
+  // accumulate, and on the last micro-batch HSDP all-reduce + AdamW
+  int unit_grad_ready(Unit& u, cudaStream_t s, const std::string& name, int layer);
   int64_t bytes_alloc_ = 0;
 
   // ---- streams, comms, events
@@ -129,6 +149,7 @@ class Step {
   ncclComm_t world_comm_ = nullptr, shard_comm_ = nullptr, rep_comm_ = nullptr,
              shard_comm_head_ = nullptr;
   cudaEvent_t ev_start_ = nullptr, ev_fwd_ = nullptr, ev_bwd_ = nullptr, ev_end_ = nullptr;
+  std::vector<cudaEvent_t> ev_mb_;  // [2*accum]: forward end / backward end of each micro-batch
   std::vector<cudaEvent_t> ev_ag_, ev_use_done_, ev_grad_done_, ev_rs_done_;
   cudaEvent_t ev_head_ag_ = nullptr, ev_head_rs_ = nullptr;
   std::vector<TraceEv> trace_;
@@ -158,8 +179,19 @@ class Step {
   int xq_ = 0, xo_ = 0, xdo_ = 0, xd_ = 0;  // double-buffer selectors
 
   // ---- batch
+  // d_* point at the current micro-batch inside the *_all_ arrays (accum_ of each)
   int32_t *d_ids_ = nullptr, *d_labels_ = nullptr, *d_pos_ = nullptr, *d_sstart_ = nullptr,
           *d_send_ = nullptr;
+  int32_t *d_ids_all_ = nullptr, *d_labels_all_ = nullptr, *d_pos_all_ = nullptr,
+          *d_sstart_all_ = nullptr, *d_send_all_ = nullptr;
+  void bind_micro(int mb) {
+    mb_ = mb;
+    d_ids_ = d_ids_all_ + int64_t(mb) * T_;
+    d_labels_ = d_labels_all_ + int64_t(mb) * T_;
+    d_pos_ = d_pos_all_ + int64_t(mb) * Ntok_;
+    d_sstart_ = d_sstart_all_ + int64_t(mb) * Ntok_;
+    d_send_ = d_send_all_ + int64_t(mb) * Ntok_;
+  }
   float* d_inv_freq_ = nullptr;
 
   // ---- activations
@@ -234,7 +266,11 @@ class Step {
   std::vector<void*> allocs_;
   cudaEvent_t ev();
   void mark(const std::string& name, const std::string& phase, int tid, cudaEvent_t a,
-            cudaEvent_t b);
+            cudaEvent_t b, const char* fused = nullptr);
+  // measured StepReport of the last step (simulator.cpp:106-131 on real intervals)
+  opx_step_report last_{};
+  std::map<std::string, std::pair<double, double>> phases_;  // phase -> (compute_s, comm_s)
+  void measure_nodes(opx_step_report* r);
   int build_units();
   int alloc_acts();
   int gather(Unit& u, int slot, cudaEvent_t wait_ev);

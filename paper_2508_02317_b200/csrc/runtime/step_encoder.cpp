@@ -325,7 +325,7 @@ int Step::enc_forward() {
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
-    mark("encoder." + e.name + ".m0", "encoder", 0, e0, e1);
+    mark("encoder." + e.name + mtag(), "encoder", 0, e0, e1);
     e0 = e1;
   }
   // scatter.<mod>: feature rows -> the owning SP rank's feature buffer
@@ -338,7 +338,7 @@ int Step::enc_forward() {
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
-    mark("scatter." + e.name + ".m0", "encoder", 0, e0, e1);
+    mark("scatter." + e.name + mtag(), "encoder", 0, e0, e1);
   }
   return OPX_OK;
 }

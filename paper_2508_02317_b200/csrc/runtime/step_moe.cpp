@@ -107,6 +107,10 @@ int Step::moe_build_units() {
     u.gshard = u.gbf ? static_cast<void*>(alloc<bf16>(size_t(u.shard)))
                      : static_cast<void*>(alloc<float>(size_t(u.shard)));
     u.pshard = alloc<bf16>(size_t(u.shard));
+    if (accum_ > 1 && !(u.gacc = alloc<float>(size_t(u.shard), false))) {
+      set_error("out of device memory for expert gradient accumulation shards");
+      return OPX_ERR_CUDA;
+    }
     if (!u.master || !u.m || !u.v || !u.gshard || !u.pshard) {
       set_error("out of device memory for expert shards");
       return OPX_ERR_CUDA;
@@ -261,7 +265,7 @@ int Step::moe_alloc() {
   }
   route_idx_.assign(size_t(a_.layers), nullptr);
   for (int l = 0; l < a_.layers; ++l)
-    if (a_.is_moe_layer(l)) route_idx_[size_t(l)] = alloc<int>(P, false);
+    if (a_.is_moe_layer(l)) route_idx_[size_t(l)] = alloc<int>(P * size_t(accum_), false);
   // kept-token layers (top first) also keep gate|up + SwiGLU while HBM leaves
   // OPX_MOE_KEEP_GU_MARGIN_GB of headroom (a local choice: no peer sees them)
   gu_l_.assign(size_t(a_.layers), nullptr);
@@ -351,7 +355,7 @@ int Step::moe_redispatch(int l) {
   if (a) {
     cudaEvent_t b = ev();
     cudaEventRecord(b, xs_);
-    mark("bwd.layer" + std::to_string(l) + ".m0.a2a_redispatch", "bwd.layer" + std::to_string(l), 3,
+    mark("bwd.layer" + std::to_string(l) + mtag() + ".a2a_redispatch", "bwd.layer" + std::to_string(l), 3,
          a, b);
   }
   return OPX_OK;
@@ -401,7 +405,7 @@ GemmDesc grouped(int M, int N, int K, const bf16* A, int64_t lda, bool amn, cons
 }  // namespace
 
 int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out) {
-  const std::string pre = std::string(in_recompute_ ? "bwd" : "fwd") + ".layer" + std::to_string(l) + ".m0.";
+  const std::string pre = std::string(in_recompute_ ? "bwd" : "fwd") + ".layer" + std::to_string(l) + mtag() + ".";
   const std::string ph = std::string(in_recompute_ ? "bwd" : "fwd") + ".layer" + std::to_string(l);
   cudaEvent_t e0 = nullptr;
   auto mk = [&](const char* name) {
@@ -431,7 +435,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_));
   CU(k_moe_topk(r_logits_, T, E, k, r_idx_, r_wts_, cs_));
   if (!in_recompute_ && route_idx_[size_t(l)])
-    CU(cudaMemcpyAsync(route_idx_[size_t(l)], r_idx_, size_t(P) * sizeof(int),
+    CU(cudaMemcpyAsync(route_idx_[size_t(l)] + int64_t(mb_) * P, r_idx_, size_t(P) * sizeof(int),
                        cudaMemcpyDeviceToDevice, cs_));
   CU(k_moe_sort(r_idx_, P, E, r_hist_, r_cnt_, r_excl_, r_pos_, r_pairat_, cs_));
   mk("router");
@@ -531,7 +535,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
 }
 
 int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2) {
-  const std::string pre = "bwd.layer" + std::to_string(l) + ".m0.";
+  const std::string pre = "bwd.layer" + std::to_string(l) + mtag() + ".";
   const std::string ph = "bwd.layer" + std::to_string(l);
   cudaEvent_t e0 = nullptr;
   auto mk = [&](const char* name) {

@@ -24,7 +24,11 @@ class StepReport(ctypes.Structure):
                 ("comm_wait_s", ctypes.c_double), ("loss", ctypes.c_double),
                 ("tokens", ctypes.c_double), ("n_valid", ctypes.c_double),
                 ("launches", ctypes.c_int64), ("enqueue_s", ctypes.c_double),
-                ("kept_layers", ctypes.c_int64)]
+                ("kept_layers", ctypes.c_int64),
+                # StepReport (simulator.hpp:43-50) on the measured step
+                ("throughput", ctypes.c_double), ("mfu", ctypes.c_double),
+                ("exposed_comm", ctypes.c_double), ("model_flops_per_token", ctypes.c_double),
+                ("comm_s", ctypes.c_double), ("accum_steps", ctypes.c_int64)]
 
 
 def _s(x) -> bytes:
@@ -106,10 +110,21 @@ def rank_coords(rank: int, plan: dict):
     return rank // (sp * sh), (rank // sp) % sh, rank % sp  # rep, shard, sp
 
 
+def accum_steps(batch, plan: dict) -> int:
+    """Gradient-accumulation steps of a global batch: rows/(dp_width*micro_batch)
+    (step_graph.cpp:57)."""
+    unit = plan["dp_replicate"] * plan["dp_shard"] * plan["micro_batch"]
+    rows = batch["ids"].shape[0]
+    if rows % unit:
+        raise ValueError(f"batch rows {rows} not divisible by dp_width*micro_batch = {unit}")
+    return rows // unit
+
+
 def local_slice(batch, rank: int, plan: dict):
-    """What rank `rank` feeds its executor: its dp rows, its SP token slice."""
+    """What rank `rank` feeds its executor: its dp rows (k micro-batches of
+    micro_batch consecutive rows, k = accum_steps), its SP token slice."""
     rep, sh, spi = rank_coords(rank, plan)
-    m, sp = plan["micro_batch"], plan["sp"]
+    m, sp = plan["micro_batch"] * accum_steps(batch, plan), plan["sp"]
     dp = rep * plan["dp_shard"] + sh
     rows = slice(dp * m, (dp + 1) * m)
     S = batch["ids"].shape[1]
@@ -142,6 +157,8 @@ class Session:
         for k, v in (("dp_replicate", 1), ("sp", 1), ("ep", 1), ("micro_batch", 1)):
             self.plan.setdefault(k, v)
         self.rank, self.world, self.dist = rank, world, dist
+        dpw = self.plan["dp_replicate"] * self.plan["dp_shard"]
+        self.accum = max(1, workload["global_batch"] // (dpw * self.plan["micro_batch"]))
         nid = ctypes.create_string_buffer(128)
         if world > 1:
             if rank == 0:
@@ -217,7 +234,8 @@ class Session:
         return out, n, b, e
 
     def routes(self, layer: int, T: int, k: int):
-        """Forward top-k expert indices of MoE layer `layer` for this rank's T tokens."""
+        """Forward top-k expert indices of MoE layer `layer` for this rank's T
+        tokens (T = every micro-batch's local tokens under accumulation)."""
         out = np.empty((T, k), np.int32)
         check(lib().opx_step_get(self.h, f"route:{layer}".encode(), out.ctypes.data_as(ctypes.c_void_p),
                                  out.nbytes))
@@ -248,6 +266,14 @@ class Session:
         if self.dist is not None and self.world > 1:
             self.dist.barrier()
         check(lib().opx_step_load(self.h, os.fspath(path).encode()))
+
+    def report_json(self) -> dict:
+        """The last step as to_json(StepReport) (report.cpp:117-128)."""
+        cap = 1 << 20
+        buf = ctypes.create_string_buffer(cap)
+        n = ctypes.c_size_t()
+        check(lib().opx_step_report_json(self.h, buf, cap, ctypes.byref(n)))
+        return json.loads(buf.value.decode())
 
     def trace(self) -> dict:
         cap = 1 << 24

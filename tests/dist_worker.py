@@ -31,9 +31,12 @@ def step_worker(rank, world, port, model, plan, S, rows, q, names, images=None):
             for n in names:
                 v, numel, b, e = s.get(f"{kind}:{n}")
                 out[(kind, n)] = (v, numel, b, e)
+        out[("trace", 0)] = s.trace()
+        out[("report", 0)] = s.report_json()
+        out[("report_struct", 0)] = {f[0]: getattr(r, f[0]) for f in r._fields_}
         arch = model["modules"][0]["arch"]
         if "moe" in arch:
-            T = plan["micro_batch"] * S // plan["sp"]
+            T = s.accum * plan["micro_batch"] * S // plan["sp"]
             k = arch["moe"]["top_k"]
             stride = arch["moe"].get("moe_layer_stride", 1)
             for l in range(arch["layers"]):

@@ -25,3 +25,25 @@ def test_no_torch_types_in_header():
     text = open(_abi.HEADER).read()
     for bad in ("torch", "at::", "Tensor", "std::"):
         assert bad not in text
+
+
+def test_step_report_struct_matches_header():
+    """runtime.StepReport (ctypes) has exactly the fields, order and types of
+    the opx_step_report typedef in include/opx.h."""
+    import re
+
+    from paper_2508_02317_b200.runtime import StepReport
+
+    text = open(_abi.HEADER).read()
+    body = text[text.index("typedef struct {"):text.index("} opx_step_report;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = []
+    for decl in body.split(";"):
+        decl = decl.replace("typedef struct {", "").strip()
+        if not decl:
+            continue
+        typ, names = decl.split(None, 1)
+        for n in names.split(","):
+            fields.append((n.strip(), typ))
+    want = {"double": ctypes.c_double, "int64_t": ctypes.c_int64}
+    assert [(n, want[t]) for n, t in fields] == [(n, t) for n, t in StepReport._fields_]

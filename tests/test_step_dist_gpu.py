@@ -19,6 +19,7 @@ class _Remote:
 
     def __init__(self, out):
         self.out = out
+        self.accum = int(out[("report_struct", 0)]["accum_steps"])
 
     def get(self, name):
         kind, n = name.split(":", 1)
@@ -83,6 +84,10 @@ PLANS = [
     (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 1, "micro_batch": 1}, 2),
     (4, {"dp_replicate": 2, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1}, 2),
     (4, {"dp_replicate": 1, "dp_shard": 1, "sp": 4, "ep": 1, "micro_batch": 1}, 1),
+    # gradient accumulation (step_graph.cpp:57,75-87,351-364): 2 micro-batches
+    # per dp rank, per-micro reduce-scatter, HSDP all-reduce on the last one
+    (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 1, "micro_batch": 1}, 4),
+    (4, {"dp_replicate": 2, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1}, 4),
 ]
 
 
@@ -97,6 +102,7 @@ MOE_PLANS = [
          "moe_overlap": True}, 4),
     (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "moe_overlap": True}, 2),
     (4, {"dp_replicate": 2, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1}, 4),  # HSDP x EP
+    (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1}, 4),  # 2 micro-batches
 ]
 
 
@@ -208,3 +214,88 @@ def test_checkpoint_reshard_fsdp2_to_1(tmp_path):
     r2 = s.run()
     assert abs(r2.loss - res[0][0]) <= 1e-3 * abs(res[0][0]), (r2.loss, res[0][0])
     s.close()
+
+
+# ---------------------------------------------------------------------------
+# the reference's step-graph structure pins (test_simulator.cpp:183-263)
+# replayed on MEASURED traces.  A fused exchange node carries the reference
+# node names it stands for in args.fused ("a2a_q,a2a_k,a2a_v").
+# ---------------------------------------------------------------------------
+def _comm_nodes(trace):
+    out = []
+    for e in trace["traceEvents"]:
+        if e["cat"] != "comm" or e["name"].endswith(".a2a_wait"):
+            continue
+        fused = e["args"].get("fused")
+        if fused:
+            base = e["name"].rsplit(".", 1)[0]
+            out += [base + "." + f for f in fused.split(",")]
+        else:
+            out.append(e["name"])
+    return out
+
+
+@gpu
+def test_measured_trace_sp2_dense_layer_structure():
+    """test_simulator.cpp:183-208 (sp=2, one dense layer): four forward
+    attention exchanges (q, k, v, out); the executor adds the four backward
+    ones the model omits (dO, dq, dk, dv).  No FSDP
+    gathers / reduce-scatters: dp_shard*sp = 2 shards, so one per unit."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    model = tiny_dense(layers=1, hidden=512, heads=4, kv=2, ffn=768, vocab=2048)
+    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1}
+    loss, sessions = _run(2, model, plan, 1024, 1)
+    for s in sessions:
+        names = _comm_nodes(s.out[("trace", 0)])
+        fwd = sorted(n.rsplit(".", 1)[1] for n in names if n.startswith("fwd.layer0.m0.a2a_"))
+        bwd = sorted(n.rsplit(".", 1)[1] for n in names if n.startswith("bwd.layer0.m0.a2a_"))
+        assert fwd == ["a2a_k", "a2a_out", "a2a_q", "a2a_v"], fwd
+        assert bwd == ["a2a_dk", "a2a_do", "a2a_dq", "a2a_dv"], bwd
+        assert sum(n.startswith("bwd.rs.layer0.m0") for n in names) == 1
+        rep = s.out[("report", 0)]
+        assert set(rep) == {"step_time_s", "throughput_tokens_per_s_per_gpu", "mfu",
+                            "exposed_comm_fraction", "model_flops_per_token", "phase_breakdown"}
+        assert rep["phase_breakdown"]["fwd.layer0"]["comm_s"] > 0
+        assert 0 <= rep["exposed_comm_fraction"] <= 1
+
+
+@gpu
+def test_measured_trace_ep2_moe_routing_nodes():
+    """test_simulator.cpp:210-229: an ep=2 MoE layer has one dispatch, one
+    combine, one dispatch_grad and one combine_grad node."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    from tests.step_common import tiny_moe
+
+    model = tiny_moe(layers=1, hidden=512, heads=4, kv=2, ffn=768, vocab=2048, experts=64, top_k=4,
+                     expert_ffn=256)
+    plan = {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1}
+    loss, sessions = _run(2, model, plan, 512, 2)
+    for s in sessions:
+        names = _comm_nodes(s.out[("trace", 0)])
+        for suf in (".a2a_dispatch", ".a2a_combine", ".a2a_dispatch_grad", ".a2a_combine_grad"):
+            n = sum(x.endswith(suf) and ".recompute" not in x for x in names)
+            assert n >= 1, (suf, names)
+
+
+@gpu
+def test_measured_trace_hsdp_accum_all_reduce_on_last_micro():
+    """test_simulator.cpp:231-251: with two micro-batches the replicate
+    all-reduce happens once per unit, on the last micro-batch (.m1), while
+    reduce-scatters run per micro-batch."""
+    if NGPU < 4:
+        pytest.skip("needs 4 GPUs")
+    model = tiny_dense(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048)
+    plan = {"dp_replicate": 2, "dp_shard": 2, "sp": 1, "ep": 1, "micro_batch": 1}
+    loss, sessions = _run(4, model, plan, 512, 8)
+    from paper_2508_02317_b200.runtime import synthetic_batch
+
+    compare_step(sessions, model, synthetic_batch(2048, 512, 8, seed=2508), plan, loss)
+    for s in sessions:
+        names = _comm_nodes(s.out[("trace", 0)])
+        ar = [n for n in names if n.startswith("bwd.ar.")]
+        assert len(ar) == 3 and all(n.endswith(".m1") for n in ar), ar  # 2 layers + head
+        for l in range(2):
+            assert sum(n.startswith(f"bwd.rs.layer{l}.") for n in names) == 2
+        assert s.accum == 2

