@@ -46,8 +46,11 @@ namespace {
 using bf16 = __nv_bfloat16;
 using namespace attn;
 constexpr int BQ = 64, BK = 128, D = 128;
-constexpr int THREADS = 320;  // TMA, MMA, 8 softmax/dQ warps (2 per TMEM lane quadrant)
+// TMA, MMA, 8 softmax warps (2 per TMEM lane quadrant), 4 dQ warps (1 per quadrant)
+constexpr int THREADS = 448;
 constexpr int NSM = 256;       // softmax threads
+constexpr int NDQ = 128;       // dQ drain threads (warps 10..13)
+constexpr int DQ_T0 = 320;     // first dQ drain thread
 constexpr float LOG2E = 1.4426950408889634f;
 // smem map (bytes, 1024-aligned base)
 // Q/dO: 3-stage ring (a stage is released only when the gradient MMAs of its
@@ -105,6 +108,7 @@ __device__ __forceinline__ uint64_t md(uint32_t base, int k, int lbo) {
 #endif
 constexpr int POLY_SHARE = OPX_BWD_POLY_SHARE;
 __device__ __forceinline__ void bar_sync_softmax() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bar_sync_dq() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
 
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       if (i == 0) {
         ptx::mbar_init(dq_full, 1);
-        ptx::mbar_init(dqt_free, NSM);
+        ptx::mbar_init(dqt_free, NDQ);
       }
     }
     ptx::mbar_init(s_free, NSM);
@@ -258,8 +262,47 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
     }
+  } else if (warp >= 10) {
+    // ---------------- dQ drain warps ----------------
+    // dQ^T(j) (thread: d row r = quad*32 + lane, all 64 q columns) -> fp32
+    // staging [q][d] -> one TMA bulk reduce-add into the fp32 dQ accumulator.
+    // Off the softmax warps' critical path: they only publish P/dS.
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = uint32_t(quad * 32) << 16;
+    const bool dq_issuer = threadIdx.x == DQ_T0;
+    for (int j = 0; j < niter; ++j) {
+      const int h = hbase + j / nq;
+      const int q0 = k0 + (j % nq) * BQ;
+      ptx::mbar_wait(dq_full, j & 1);
+      if (dq_issuer) PROF(j + 1, 8);
+      ptx::tc_fence_after();
+      uint32_t qa[32], qb[32];
+      ptx::tmem_ld32(TDQ + lane_off, qa);
+      ptx::tmem_ld32(TDQ + lane_off + 32, qb);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dqt_free);  // the MMA warp may issue dQ^T(j+1)
+      if (dq_issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      bar_sync_dq();  // staging buffer free
+#pragma unroll
+      for (int q = 0; q < 32; ++q) stage[q * D + r] = __uint_as_float(qa[q]) * p.scale;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) stage[(32 + q) * D + r] = __uint_as_float(qb[q]) * p.scale;
+      ptx::fence_proxy_async();
+      bar_sync_dq();
+      if (dq_issuer && !p.skip_dq) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&tdq)),
+            "r"(ptx::smem_u32(stage)), "r"(0), "r"(h), "r"(q0)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (dq_issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else {
-    // ---------------- softmax / dQ warps ----------------
+    // ---------------- softmax warps ----------------
     // warps 2..9: lane quadrant = warp & 3 (TMEM access rule), column half =
     // (warp - 2) / 4, so every quadrant is served by two warps.
     const int quad = warp & 3;
@@ -281,48 +324,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         s_sst[buf * BQ + r] = ok ? p.seq_start[q] : 0x7fffffff;
       }
     };
-    // dQ^T(j) (thread: d row r, q columns c0..c0+31) -> fp32 staging [q][d] -> bulk reduce-add
-    auto drain_dq = [&](int j) {
-      const int h = hbase + j / nq;
-      const int q0 = k0 + (j % nq) * BQ;
-      ptx::mbar_wait(dq_full, j & 1);
-      if (pt) PROF(j + 1, 8);
-      ptx::tc_fence_after();
-      uint32_t qv[32];
-      ptx::tmem_ld32(TDQ + lane_off + c0, qv);
-      ptx::tmem_wait_ld();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(dqt_free);
-      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      bar_sync_softmax();  // staging buffer free
-#pragma unroll
-      for (int q = 0; q < 32; ++q) stage[(c0 + q) * D + r] = __uint_as_float(qv[q]) * p.scale;
-      ptx::fence_proxy_async();
-      bar_sync_softmax();
-      if (issuer && !p.skip_dq) {
-        asm volatile(
-            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                reinterpret_cast<uint64_t>(&tdq)),
-            "r"(ptx::smem_u32(stage)), "r"(0), "r"(h), "r"(q0)
-            : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    };
     if (niter > 0) load_cols(0);
     bar_sync_softmax();
     for (int it = 0; it < niter; ++it) {
       if (pt) PROF(it, 4);
       const int q0 = k0 + (it % nq) * BQ;
       const int buf = it & 1;
-      // broadcast vector loads of this thread's 32 columns
-      float lv[32], dl[32];
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 a = *reinterpret_cast<const float4*>(s_lse + buf * BQ + c0 + i);
-        const float4 b = *reinterpret_cast<const float4*>(s_dlt + buf * BQ + c0 + i);
-        lv[i] = a.x; lv[i + 1] = a.y; lv[i + 2] = a.z; lv[i + 3] = a.w;
-        dl[i] = b.x; dl[i + 1] = b.y; dl[i + 2] = b.z; dl[i + 3] = b.w;
-      }
+      // this thread's 32 columns of lse / delta: broadcast smem loads inside
+      // the math loops (not held in registers: the kernel runs at 128 regs)
+      const float* lvp = s_lse + buf * BQ + c0;
+      const float* dlp = s_dlt + buf * BQ + c0;
       const int* sst = s_sst + buf * BQ;
       const bool full_vis = key <= q0 + c0 && q0 + c0 + 31 < p.N && sst[c0 + 31] <= key;
       ptx::mbar_wait(s_full, it & 1);
@@ -341,16 +352,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint64_t sc2 = f2pack(p.scale_log2, p.scale_log2);
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
+          const float2 lv = *reinterpret_cast<const float2*>(lvp + i);
+          const float2 dl = *reinterpret_cast<const float2*>(dlp + i);
           float x0, x1;
           f2unpack(ffma2(f2pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), sc2,
-                         f2pack(-lv[i], -lv[i + 1])),
+                         f2pack(-lv.x, -lv.y)),
                    x0, x1);
           const bool poly = POLY_SHARE == 8 ? (i & 7) == 6 : POLY_SHARE == 4 ? (i & 3) == 2 : false;
           const float p0 = poly ? exp2_fma(x0) : ex2(x0);
           const float p1 = ex2(x1);
           const uint64_t pp = f2pack(p0, p1);
           const uint64_t dd = fadd2(f2pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
-                                    f2pack(-dl[i], -dl[i + 1]));
+                                    f2pack(-dl.x, -dl.y));
           float d0, d1;
           f2unpack(fmul2(pp, dd), d0, d1);
           pw[i / 2] = ptx::pack_bf16(p0, p1);
@@ -364,12 +377,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int e = 0; e < 2; ++e) {
             const int q = q0 + c0 + i + e;
             const bool ok = (key <= q) & (key >= sst[c0 + i + e]) & (key < p.N);
-            const float x = ex2(fmaf(__uint_as_float(sv[i + e]), p.scale_log2, -lv[i + e]));
+            const float x = ex2(fmaf(__uint_as_float(sv[i + e]), p.scale_log2, -lvp[i + e]));
             pp[e] = ok ? x : 0.f;
           }
           pw[i / 2] = ptx::pack_bf16(pp[0], pp[1]);
-          dw[i / 2] = ptx::pack_bf16(pp[0] * (__uint_as_float(dv[i]) - dl[i]),
-                                     pp[1] * (__uint_as_float(dv[i + 1]) - dl[i + 1]));
+          dw[i / 2] = ptx::pack_bf16(pp[0] * (__uint_as_float(dv[i]) - dlp[i]),
+                                     pp[1] * (__uint_as_float(dv[i + 1]) - dlp[i + 1]));
         }
       }
       // the gradient MMAs of tile it-1 read P^T/dS^T (TMEM) and dS (smem):
@@ -395,18 +408,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_ready);
       if (pt) PROF(it, 7);
-      if (it > 0) drain_dq(it - 1);
       if (it + 1 < niter) load_cols(it + 1);
       bar_sync_softmax();  // next tile's column data visible
       if (pt) PROF(it, 10);
     }
-    if (niter > 0) drain_dq(niter - 1);
-    if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // every MMA of the CTA is complete (dK/dV final in TMEM)
+    if (niter > 0) ptx::mbar_wait(dq_full, (niter - 1) & 1);
+    ptx::tc_fence_after();
     if (p.f32kv) {
       // ---- dK (scaled), dV -> fp32 SW128 staging [4 col chunks][128 rows][32]
       // over the free Q/dO/P/S/stage buffers, then TMA store / reduce-add.
-      bar_sync_softmax();  // dQ staging reads done
-      uint8_t* stk = smem + OFF_Q;
+      uint8_t* stk = smem + OFF_Q;  // [OFF_Q, OFF_STAGE): Q/dO ring + dS (the dQ warps own OFF_STAGE)
       uint8_t* stv = smem + OFF_Q + 65536;
 #pragma unroll 1
       for (int c = half * 2; c < half * 2 + 2; ++c) {
