@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libopx.so")
+# OPX_LIB_PATH: diagnostics only (tools/ profiling builds of the same sources)
+LIB_PATH = os.environ.get("OPX_LIB_PATH") or os.path.join(_HERE, "libopx.so")
 _lib = None
 
 

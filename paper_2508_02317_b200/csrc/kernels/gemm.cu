@@ -515,6 +515,8 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   if (g.N <= 0) return cudaSuccess;
   if (g.N % 8 != 0 || (g.epi == GEMM_EPI_SWIGLU && g.N % 256 != 0)) return cudaErrorInvalidValue;
   if (g.epi == GEMM_EPI_SWIGLU_BWD && (g.N % 128 != 0 || !g.G2 || g.groups)) return cudaErrorInvalidValue;
+  if (g.epi == GEMM_EPI_SEQ2HEAD && (g.N % 128 != 0 || !g.s2h || g.groups || getenv("OPX_GEMM_1CTA")))
+    return cudaErrorNotSupported;  // the fused exchange epilogue exists on the 2-CTA kernel only
   CUtensorMap ma, mb;
   const bool grouped = g.groups > 0;
   const bool gm = grouped && !g.grouped_k;  // rows of A vary per group

@@ -21,6 +21,7 @@
 
 #include "../runtime/gemm_api.h"
 #include "../runtime/kernels_api.h"
+#include "../runtime/kernels_api.h"
 #include "epilogue.cuh"
 #include "ptx.cuh"
 
@@ -57,6 +58,7 @@ struct P2 {
   int groups;
   const int* g_start;
   const int* g_rows;
+  A2AArgs s2h;  // GEMM_EPI_SEQ2HEAD
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -313,6 +315,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             epi::swiglu_bwd32(v, p.G2 + int64_t(row) * p.ldg2,
                               reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd, f0);
         }
+      } else if (p.epi == GEMM_EPI_SEQ2HEAD) {
+        // this thread's row = local token `row` of SP rank s2h.rank; each head
+        // vector of the tile goes to its owner's [rows*S, heads/sp, 128] slot
+        const A2AArgs& a = p.s2h;
+        const int S_loc = a.seq / a.sp;
+        const int rb = row / S_loc;
+        const int64_t gtok = int64_t(rb) * a.seq + int64_t(a.rank) * S_loc + (row - rb * S_loc);
+        const int pos = row_ok ? a.pos[gtok] : 0;
+#pragma unroll 1
+        for (int hv = 0; hv < BNP / 128; ++hv) {
+          const int c0 = nb * BNP + hv * 128;
+          if (c0 >= p.N) break;
+          int gi = 0;
+          while (gi + 1 < a.ngroups && c0 >= a.g[gi + 1].col0) ++gi;
+          const A2AGroup& G = a.g[gi];
+          const int hh = (c0 - G.col0) >> 7;
+          const int per_rank = G.heads_total / a.sp;
+          const int dst = hh / per_rank, hl = hh - dst * per_rank;
+          __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(G.full[dst]) +
+                             (gtok * per_rank + hl) * 128;
+#pragma unroll 1
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t x1[32], x2[32];
+            ptx::tmem_ld32(tbase + hv * 128 + ch * 32, x1);
+            ptx::tmem_ld32(tbase + hv * 128 + 64 + ch * 32, x2);
+            ptx::tmem_wait_ld();
+            if (!row_ok) continue;
+            uint32_t lo[16], hi[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              // bf16 rounding where the unfused path stores qkv, then RoPE in fp32
+              lo[e] = ptx::pack_bf16(__uint_as_float(x1[2 * e]) * p.scale,
+                                     __uint_as_float(x1[2 * e + 1]) * p.scale);
+              hi[e] = ptx::pack_bf16(__uint_as_float(x2[2 * e]) * p.scale,
+                                     __uint_as_float(x2[2 * e + 1]) * p.scale);
+              if (G.rope) {
+                const int j = ch * 32 + 2 * e;
+                const float2 a1 = ptx::unpack_bf16(lo[e]), a2 = ptx::unpack_bf16(hi[e]);
+                float sn0, cs0, sn1, cs1;
+                if (a.rope_tab) {
+                  const float4 t = *reinterpret_cast<const float4*>(a.rope_tab + int64_t(pos) * 64 + j);
+                  sn0 = t.x; cs0 = t.y; sn1 = t.z; cs1 = t.w;
+                } else {
+                  sincosf(float(pos) * a.inv_freq[j], &sn0, &cs0);
+                  sincosf(float(pos) * a.inv_freq[j + 1], &sn1, &cs1);
+                }
+                lo[e] = ptx::pack_bf16(a1.x * cs0 - a2.x * sn0, a1.y * cs1 - a2.y * sn1);
+                hi[e] = ptx::pack_bf16(a2.x * cs0 + a1.x * sn0, a2.y * cs1 + a1.y * sn1);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              *reinterpret_cast<uint4*>(d + ch * 32 + q * 8) =
+                  make_uint4(lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
+              *reinterpret_cast<uint4*>(d + 64 + ch * 32 + q * 8) =
+                  make_uint4(hi[4 * q], hi[4 * q + 1], hi[4 * q + 2], hi[4 * q + 3]);
+            }
+          }
+        }
       } else if (p.epi == GEMM_EPI_SWIGLU) {
 #pragma unroll 1
         for (int ch = 0; ch < 4; ++ch) {
@@ -492,6 +553,10 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   p.groups = g.groups;
   p.g_start = g.g_start;
   p.g_rows = g.g_rows;
+  if (g.epi == GEMM_EPI_SEQ2HEAD) {
+    if (!g.s2h || gm) return cudaErrorInvalidValue;
+    p.s2h = *g.s2h;
+  }
   // grouped: the tile count lives in device memory; idle clusters exit at once
   const int tiles = gm ? num_sms() / 2 : ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BNP - 1) / BNP);
   int clusters = num_sms() / 2;

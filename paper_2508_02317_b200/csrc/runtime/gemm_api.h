@@ -6,6 +6,8 @@
 
 namespace opx {
 
+struct A2AArgs;  // kernels_api.h
+
 enum GemmEpi : int {
   GEMM_EPI_BF16 = 0,       // D(bf16) = acc*scale
   GEMM_EPI_F32 = 1,        // D(f32)  = acc*scale
@@ -15,6 +17,12 @@ enum GemmEpi : int {
   // acc = dact[., N] (N = F); G2 = the forward's bf16 gate|up [., 2N] (128-col
   // interleave); D(bf16)[., 2N] = d(gate)|d(up) of silu(gate)*up, same layout
   GEMM_EPI_SWIGLU_BWD = 5,
+  // Ulysses seq->head fused into the epilogue (async_ulysses, step_graph.cpp:
+  // 217-241): every 128-column head vector of a row goes, rounded to bf16 and
+  // RoPE'd per its group, straight to the owning SP rank's head-layout buffer
+  // over NVLink (the k_a2a_seq2head addressing); D is unused.  head_dim 128,
+  // plain (non-grouped) GEMMs on the 2-CTA kernel only.
+  GEMM_EPI_SEQ2HEAD = 6,
 };
 
 // D[M,N] = A . B^T with
@@ -51,6 +59,7 @@ struct GemmDesc {
   const int* g_rows = nullptr;
   int64_t rows_total = 0;
   int64_t d_group_stride = 0;
+  const A2AArgs* s2h = nullptr;  // GEMM_EPI_SEQ2HEAD routing (copied at launch)
 };
 
 cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s);

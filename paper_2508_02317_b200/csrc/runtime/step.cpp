@@ -66,9 +66,16 @@ void Step::mark(const std::string& name, const std::string& phase, int tid, cuda
   // the reference's collective nodes: FSDP/HSDP NCCL ops on the comm stream,
   // the Ulysses / EP exchanges (and their flag barriers) on the compute
   // stream, the encoder feature scatter (step_graph.cpp:150-160, 215-247, 265-283)
+  // (an exchange over a group of one rank is a local relayout, not a
+  // collective: the reference emits no node for it, step_graph.cpp add_collective)
   auto starts = [&](const char* p) { return name.rfind(p, 0) == 0; };
-  t.comm = tid == 1 || name.find(".a2a_") != std::string::npos || starts("scatter.") ||
-           starts("fwd.ag.") || starts("bwd.ag.") || starts("bwd.rs.") || starts("bwd.ar.");
+  auto has = [&](const char* p) { return name.find(p) != std::string::npos; };
+  const bool ep_x = has(".a2a_dispatch") || has(".a2a_combine") || has(".a2a_counts") ||
+                    has(".a2a_redispatch");
+  const bool a2a = has(".a2a_") && (ep_x ? ep_ > 1 : has(".a2a_wait") ? (p_.sp > 1 || ep_ > 1)
+                                                                       : p_.sp > 1);
+  t.comm = tid == 1 || a2a || (starts("scatter.") && p_.sp > 1) || starts("fwd.ag.") || starts("bwd.ag.") ||
+           starts("bwd.rs.") || starts("bwd.ar.");
   if (fused) t.fused = fused;
   trace_.push_back(std::move(t));
 }
@@ -708,14 +715,20 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
   cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
   if (tr) cudaEventRecord(e0, cs_);
   CU(k_rmsnorm_fwd(x_in, W.ln1, h_, r1_, T, H, ex_.rms_eps, cs_));
-  CU(gemm_run(gd(T, Wqkv_, H, h_, H, false, W.qkv, H, false, GEMM_EPI_BF16, qkv_, Wqkv_), cs_));
-  if (tr) {
-    e1 = ev();
-    cudaEventRecord(e1, cs_);
-    mark(pre + ".qkv_proj", ph, 0, e0, e1);
-    e0 = e1;
-  }
   const int qb = slot, ob = slot;
+  // async_ulysses (step_graph.cpp:217-241): the seq->head exchange runs inside
+  // the QKV GEMM's epilogue (peer stores tile by tile, overlapping the
+  // mainloop of the other tiles) instead of as a kernel after it
+  const bool fused = async_s2h();
+  if (!fused) {
+    CU(gemm_run(gd(T, Wqkv_, H, h_, H, false, W.qkv, H, false, GEMM_EPI_BF16, qkv_, Wqkv_), cs_));
+    if (tr) {
+      e1 = ev();
+      cudaEventRecord(e1, cs_);
+      mark(pre + ".qkv_proj", ph, 0, e0, e1);
+      e0 = e1;
+    }
+  }
   {
     A2AArgs a{};
     a.sp = int(p_.sp);
@@ -743,14 +756,26 @@ int Step::layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int s
     a.inv_freq = d_inv_freq_;
     a.hd = d_;
     a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
-    if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
-    // the exchange kernel and the flag barrier are traced apart, so the
-    // node's NVLink rate is the kernel's own (the wait absorbs rank skew)
-    if (tr) {
-      e1 = ev();
-      cudaEventRecord(e1, cs_);
-      mark(pre + ".a2a_qkv", ph, 0, e0, e1, "a2a_q,a2a_k,a2a_v");
-      e0 = e1;
+    if (fused) {
+      GemmDesc g = gd(T, Wqkv_, H, h_, H, false, W.qkv, H, false, GEMM_EPI_SEQ2HEAD, nullptr, 0);
+      g.s2h = &a;
+      CU(gemm_run(g, cs_));
+      if (tr) {  // one node: projection + the exchange it carries
+        e1 = ev();
+        cudaEventRecord(e1, cs_);
+        mark(pre + ".qkv_proj", ph, 0, e0, e1, "qkv_proj,a2a_q,a2a_k,a2a_v");
+        e0 = e1;
+      }
+    } else {
+      if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
+      // the exchange kernel and the flag barrier are traced apart, so the
+      // node's NVLink rate is the kernel's own (the wait absorbs rank skew)
+      if (tr) {
+        e1 = ev();
+        cudaEventRecord(e1, cs_);
+        mark(pre + ".a2a_qkv", ph, 0, e0, e1, "a2a_q,a2a_k,a2a_v");
+        e0 = e1;
+      }
     }
     TRY(barrier_sp(cs_));
     if (tr && p_.sp > 1) {
@@ -964,34 +989,43 @@ int Step::layer_bwd(int l, Unit& u, void* G) {
     do_scratch = dact_;
     do_loc = do_scratch;
   }
-  CU(gemm_run(gd(T, Q, H, dxb_, H, false, W.o, Q, true, GEMM_EPI_BF16, do_loc, Q), cs_));
+  A2AArgs a_do{};
+  if (relay_) {
+    a_do.sp = int(p_.sp);
+    a_do.rank = sp_i_;
+    a_do.rows = rows_;
+    a_do.seq = S_;
+    a_do.ngroups = 1;
+    a_do.g[0].heads_total = hq_;
+    for (int j = 0; j < int(p_.sp); ++j) a_do.g[0].full[j] = peer(j, off_do_[db]);
+    a_do.local[0] = do_loc;
+    a_do.local_ld = Q;
+    a_do.pos = d_pos_;
+    a_do.inv_freq = d_inv_freq_;
+    a_do.hd = d_;
+    a_do.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
+  }
+  const bool fused_do = relay_ && async_s2h();
+  if (fused_do) {  // async_ulysses: dO goes to its head owners from the dgrad epilogue
+    GemmDesc g = gd(T, Q, H, dxb_, H, false, W.o, Q, true, GEMM_EPI_SEQ2HEAD, nullptr, 0);
+    g.s2h = &a_do;
+    CU(gemm_run(g, cs_));
+  } else {
+    CU(gemm_run(gd(T, Q, H, dxb_, H, false, W.o, Q, true, GEMM_EPI_BF16, do_loc, Q), cs_));
+  }
   CU(gemm_run(gd(H, Q, T, dxb_, H, true, o_loc(ob), Q, true, EPI_G, g_o, Q), cs_));
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);
-    mark(pre + ".out_proj", ph, 0, e0, e1);
+    mark(pre + ".out_proj", ph, 0, e0, e1, fused_do ? "out_proj,a2a_do" : nullptr);
     e0 = e1;
   }
   if (relay_) {
-    A2AArgs a{};
-    a.sp = int(p_.sp);
-    a.rank = sp_i_;
-    a.rows = rows_;
-    a.seq = S_;
-    a.ngroups = 1;
-    a.g[0].heads_total = hq_;
-    for (int j = 0; j < int(p_.sp); ++j) a.g[0].full[j] = peer(j, off_do_[db]);
-    a.local[0] = do_loc;
-    a.local_ld = Q;
-    a.pos = d_pos_;
-    a.inv_freq = d_inv_freq_;
-    a.hd = d_;
-    a.rope_tab = rope_tab_ok_ ? d_rope_ : nullptr;
-    if (!dbg_no_a2a()) CU(k_a2a_seq2head(a, cs_));
+    if (!fused_do && !dbg_no_a2a()) CU(k_a2a_seq2head(a_do, cs_));
     if (tr) {
       e1 = ev();
       cudaEventRecord(e1, cs_);
-      mark(pre + ".a2a_do", ph, 0, e0, e1);
+      if (!fused_do) mark(pre + ".a2a_do", ph, 0, e0, e1);
       e0 = e1;
     }
     TRY(barrier_sp(cs_));

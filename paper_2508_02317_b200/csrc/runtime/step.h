@@ -284,6 +284,9 @@ class Step {
     return (sp_j == sp_i_ ? arena_ : peer_arena_[size_t(sp_members_[size_t(sp_j)])]) + off;
   }
   int barrier_sp(cudaStream_t s);
+  // async_ulysses: the seq->head exchanges ride in the producing GEMM's
+  // epilogue (GEMM_EPI_SEQ2HEAD; head_dim 128 only, else the exchange kernel)
+  bool async_s2h() const { return p_.async_ulysses && d_ == 128; }
   // layer pieces
   int layer_fwd(int l, const Unit& u, const float* x_in, float* x_out, int slot);
   int layer_bwd(int l, Unit& u, void* grads);

@@ -88,6 +88,11 @@ PLANS = [
     # per dp rank, per-micro reduce-scatter, HSDP all-reduce on the last one
     (2, {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 1, "micro_batch": 1}, 4),
     (4, {"dp_replicate": 2, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1}, 4),
+    # async_ulysses: the seq->head exchanges (q/k/v forward, dO backward) are
+    # peer stores from the producing GEMM's epilogue
+    (2, {"dp_replicate": 1, "dp_shard": 1, "sp": 2, "ep": 1, "micro_batch": 1, "async_ulysses": True}, 1),
+    (4, {"dp_replicate": 1, "dp_shard": 2, "sp": 2, "ep": 1, "micro_batch": 1, "async_ulysses": True,
+         "recompute": "none"}, 2),
 ]
 
 

@@ -121,3 +121,39 @@ def test_step_head_dim_below_128(hidden, heads, kv):
     s, batch, plan, r = _run(model, 1024, 2)
     compare_step([s], model, batch, plan, r.loss)
     s.close()
+
+
+@gpu
+def test_step_async_ulysses_fused_epilogue_matches_kernel_path():
+    """async_ulysses (step_graph.cpp:217-241): the seq->head exchange rides in
+    the QKV GEMM epilogue (GEMM_EPI_SEQ2HEAD) instead of a separate kernel.
+    Same bf16 rounding point and RoPE arithmetic, so the step must agree with
+    the kernel path (and with the oracle)."""
+    from paper_2508_02317_b200.runtime import Session, synthetic_batch
+    from tests.step_common import gather_full, gpu_param_names
+    from oracle import model as om
+
+    model = tiny_dense(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048)
+    arch = model["modules"][0]["arch"]
+    wl = {"seq_len": 1024, "micro_batch": 2, "global_batch": 2}
+    batch = synthetic_batch(arch["vocab"], 1024, 2, seed=2508)
+    out = {}
+    for asy in (False, True):
+        plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": 2,
+                "async_ulysses": asy}
+        s = Session(cluster(1), model, wl, plan, EXEC, rank=0, device=0)
+        s.init_weights(EXEC["seed"])
+        s.load(batch)
+        r = s.run()
+        names = gpu_param_names(om.Arch.from_model_json(model))
+        out[asy] = (r.loss, {n: gather_full([s], "grad", n) for n in names})
+        if asy:
+            tr = s.trace()["traceEvents"]
+            assert not any(e["name"].endswith(".a2a_qkv") for e in tr)
+            assert any(e["args"].get("fused", "").startswith("qkv_proj,a2a_q") for e in tr)
+            compare_step([s], model, batch, plan, r.loss)
+        s.close()
+    assert abs(out[True][0] - out[False][0]) <= 1e-6 * abs(out[False][0])
+    for n, g in out[False][1].items():
+        d = np.abs(out[True][1][n] - g).max() / max(np.abs(g).max(), 1e-30)
+        assert d < 1e-3, (n, d)
