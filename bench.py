@@ -421,6 +421,8 @@ def main():
         S = int(os.environ["OPX_BENCH_SEQ"])
     if os.environ.get("OPX_BENCH_RECOMPUTE"):
         plan["recompute"] = os.environ["OPX_BENCH_RECOMPUTE"]
+    if os.environ.get("OPX_BENCH_ASYNC"):  # async_ulysses: exchanges fused into the GEMM epilogues
+        plan["async_ulysses"] = os.environ["OPX_BENCH_ASYNC"] == "1"
     rows = plan["dp_replicate"] * plan["dp_shard"] * plan["micro_batch"]
     wl = {"seq_len": S, "micro_batch": plan["micro_batch"], "global_batch": rows}
     ex = {"seed": 2508, "lr": 1e-4, "betas": [0.9, 0.95], "eps": 1e-8, "weight_decay": 0.1,
@@ -550,6 +552,7 @@ def main():
                    "global_batch": rows, "seq_len": S, "tokens_per_step": tokens_step,
                    "parallelism": f"fsdp{plan['dp_shard']}xsp{plan['sp']}",
                    "recompute": plan["recompute"], "kept_layers": kept,
+                   "async_ulysses": bool(plan.get("async_ulysses", False)),
                    "packing": "lognormal varlen, 0 padding",
                    "l2": "inputs+weights >> 126 MB L2 (no flush needed)",
                    "peak_kind": peak_kind},

@@ -19,16 +19,25 @@
 //     dV  += P^T  dO_i   (M=128 keys, N=128 d, K=64 q; A from TMEM)
 //     dK  += dS^T Q_i    (A from TMEM)
 //     dQ^T = K^T  dS^T   (M=128 d, N=64 q, K=128 keys)            -> dq_full
-//     -- softmax warps: dQ^T rows (one d per thread) -> fp32 smem [q][d]
-//        -> one TMA bulk reduce-add into the fp32 dQ accumulator
+//     -- dQ warps (4, one per TMEM lane quadrant): dQ^T rows (one d per
+//        thread, 64 q) -> fp32 smem [q][d] -> one TMA bulk reduce-add into the
+//        fp32 dQ accumulator, off the softmax warps' path
 // The S^T/dP^T MMAs of tile i+1 are issued as soon as the softmax warps have
 // pulled S^T/dP^T(i) into registers (s_free), so they overlap the softmax of
-// tile i.  The softmax publishes tile i+1's P/dS before draining dQ^T(i), so
-// dV/dK(i+1) run during the drain and only dQ^T(i+1) waits for it.  The
-// M=128, N=64 S/dP/dQ MMAs read 6 KB of smem per 32-cycle instruction (above
-// the 128 B/clk port while they run); taking P^T/dS^T from TMEM halves the
-// smem reads of dV/dK (+3-4 %).  Over the kernel the tensor pipe is ~34 %
-// busy: one chain per SM is latency-bound.
+// tile i.  dS is double-buffered in smem, so the softmax publishes tile i's
+// P/dS once dV/dK(i-1) are done (kv_done) without waiting for dQ^T(i-1).
+//
+// What bounds it (phase stamps, tools/prof_attn_phases.py, C1 SP4 shape):
+// ~3100 cycles per 64-query step; the dQ warps idle ~78 % of it and the
+// softmax warps wait ~1100 cycles for S, while the MMA warp's issues block
+// for ~2100 cycles (the tensor pipe queue is full): 32 MMAs of K=16 take
+// ~95 cycles each instead of 48-64.  Per step the MMAs read 176 KB of smem
+// (S/dP/dQ^T with N=64 read 6 KB per instruction), TMA writes 32 KB of Q/dO,
+// the softmax 16 KB of dS, the dQ stage 32 KB + its bulk read 32 KB: ~290 KB
+// against 128 B/clk -> a ~2270-cycle shared-memory floor.  dQ by
+// red.global.add.f32 from registers (no staging) measured 1.6x slower
+// (533 vs 821 TF/s); K^T / K / V as TMEM A operands would cut the MMA reads
+// but the 512 TMEM columns are all in use (S^T, dP^T, dQ^T, P^T|dS^T, dV, dK).
 #include <cuda.h>
 
 #include <algorithm>
@@ -58,8 +67,8 @@ constexpr float LOG2E = 1.4426950408889634f;
 // S/dP MMAs of the next tile)
 constexpr int QSTAGES = 3;
 constexpr int OFF_K = 0, OFF_V = 32768, OFF_Q = 65536 /*[3] x 16K*/, OFF_O = 114688 /*[3] x 16K*/,
-              /* [163840, 180224) unused since P^T moved to TMEM */
-              OFF_S = 180224, OFF_STAGE = 196608 /*32K fp32*/, OFF_MISC = 229376;
+              /* dS (bf16 [keys][q], SW128), double-buffered: tile it uses buffer it & 1 */
+              OFF_S2 = 163840, OFF_S = 180224, OFF_STAGE = 196608 /*32K fp32*/, OFF_MISC = 229376;
 constexpr int SMEM = 1024 + OFF_MISC + 3 * 2 * BQ * 4 + 256;
 static_assert(3 * 2 * BQ * 4 + 13 * 8 + 8 <= 3 * 2 * BQ * 4 + 256, "misc region");
 
@@ -128,8 +137,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* qdo_empty = bars + 4;  // [3]
   uint64_t* s_full = bars + 7;
   uint64_t* p_ready = bars + 8;
-  uint64_t* dq_full = bars + 9;    // dQ^T(it) complete (also: the P^T/dS^T/dS reads of tile it)
+  uint64_t* dq_full = bars + 9;    // [2] dQ^T(it) complete -> [it & 1] (every MMA of tile it done)
   uint64_t* dqt_free = bars + 11;  // dQ^T(it) read out of TMEM
+  uint64_t* kv_done = bars + 12;   // dV/dK(it) complete: P^T/dS^T (TMEM) of tile it read
   uint64_t* s_free = bars + 13;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   float* stage = reinterpret_cast<float*>(smem + OFF_STAGE);
@@ -158,12 +168,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(p_ready, NSM);
-    for (int i = 0; i < 2; ++i) {
-      if (i == 0) {
-        ptx::mbar_init(dq_full, 1);
-        ptx::mbar_init(dqt_free, NDQ);
-      }
-    }
+    ptx::mbar_init(&dq_full[0], 1);
+    ptx::mbar_init(&dq_full[1], 1);
+    ptx::mbar_init(dqt_free, NDQ);
+    ptx::mbar_init(kv_done, 1);
     ptx::mbar_init(s_free, NSM);
     ptx::fence_mbar_init();
   }
@@ -205,8 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, BQ, false, false);   // S^T, dP^T
     constexpr uint32_t id_kv = ptx::idesc_bf16_f32(128, D, false, true);    // dV, dK
     constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, BQ, true, true);     // dQ^T
-    const uint32_t ak = ptx::smem_u32(smem + OFF_K), av = ptx::smem_u32(smem + OFF_V),
-                   as = ptx::smem_u32(smem + OFF_S);
+    const uint32_t ak = ptx::smem_u32(smem + OFF_K), av = ptx::smem_u32(smem + OFF_V);
     ptx::mbar_wait(kv_full, 0);
     // issue order: S/dP(i+1) right after P(i) is ready, then dV/dK/dQ(i), so
     // the softmax of tile i+1 overlaps the gradient MMAs of tile i.
@@ -249,16 +256,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < BQ / 16; ++k)
           ptx::mma_bf16_ts(TDK, TDST + uint32_t(k) * 8, md(aq, k, 8192), id_kv, (it | k) != 0);
         ptx::mma_commit(&qdo_empty[qs]);  // release the Q/dO stage early: dQ^T does not read it
+        ptx::mma_commit(kv_done);         // P^T/dS^T(it) in TMEM may be overwritten
       }
       __syncwarp();
       if (it >= 1) ptx::mbar_wait(dqt_free, (it - 1) & 1);  // dQ^T(it-1) read out of TMEM
       if (lane == 0) PROF(it, 2);
       ptx::tc_fence_after();
       if (lane == 0) {
+        const uint32_t as = ptx::smem_u32(smem + ((it & 1) ? OFF_S2 : OFF_S));
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
           ptx::mma_bf16_ss(TDQ, md(ak, k, 16384), md(as, k, 8192), id_q, k != 0);
-        ptx::mma_commit(dq_full);
+        ptx::mma_commit(&dq_full[it & 1]);
       }
       __syncwarp();
     }
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int j = 0; j < niter; ++j) {
       const int h = hbase + j / nq;
       const int q0 = k0 + (j % nq) * BQ;
-      ptx::mbar_wait(dq_full, j & 1);
+      ptx::mbar_wait(&dq_full[j & 1], (j >> 1) & 1);
       if (dq_issuer) PROF(j + 1, 8);
       ptx::tc_fence_after();
       uint32_t qa[32], qb[32];
@@ -283,14 +292,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
       ptx::mbar_arrive(dqt_free);  // the MMA warp may issue dQ^T(j+1)
+      if (dq_issuer) PROF(j + 1, 11);
       if (dq_issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       bar_sync_dq();  // staging buffer free
+      if (dq_issuer) PROF(j + 1, 12);
 #pragma unroll
       for (int q = 0; q < 32; ++q) stage[q * D + r] = __uint_as_float(qa[q]) * p.scale;
 #pragma unroll
       for (int q = 0; q < 32; ++q) stage[(32 + q) * D + r] = __uint_as_float(qb[q]) * p.scale;
       ptx::fence_proxy_async();
       bar_sync_dq();
+      if (dq_issuer) PROF(j + 1, 13);
       if (dq_issuer && !p.skip_dq) {
         asm volatile(
             "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
@@ -391,12 +403,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       // MMA warp can issue its gradients at once, then drain dQ^T(it-1) while
       // dV/dK run
       if (pt) PROF(it, 6);
-      if (it > 0) ptx::mbar_wait(dq_full, (it - 1) & 1);
+      // P^T/dS^T (TMEM) are free once dV/dK(it-1) are done; the dS smem
+      // buffer it & 1 once dQ^T(it-2) is (the other buffer feeds dQ^T(it-1))
+      if (it > 0) ptx::mbar_wait(kv_done, (it - 1) & 1);
+      if (it > 1) ptx::mbar_wait(&dq_full[it & 1], ((it - 2) >> 1) & 1);
       if (pt) PROF(it, 9);
       ptx::tc_fence_after();
       ptx::tmem_st16(TPT + lane_off + uint32_t(half) * 16, pw);
       ptx::tmem_st16(TDST + lane_off + uint32_t(half) * 16, dw);
-      uint8_t* sS = smem + OFF_S;
+      uint8_t* sS = smem + ((it & 1) ? OFF_S2 : OFF_S);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         const int chunk = half * 4 + cc;
@@ -413,7 +428,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (pt) PROF(it, 10);
     }
     // every MMA of the CTA is complete (dK/dV final in TMEM)
-    if (niter > 0) ptx::mbar_wait(dq_full, (niter - 1) & 1);
+    if (niter > 0) ptx::mbar_wait(&dq_full[(niter - 1) & 1], ((niter - 1) >> 1) & 1);
     ptx::tc_fence_after();
     if (p.f32kv) {
       // ---- dK (scaled), dV -> fp32 SW128 staging [4 col chunks][128 rows][32]
@@ -620,14 +635,22 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
       acc[9] += double(a[3] - a[0]);   // MMA: S/dP issue incl. qdo_full wait
       acc[10] += double(a[0] - a[5]);  // s_free seen by MMA - s_full seen by softmax (same it)
       acc[11] += double(b[5] - a[3]);  // S(it+1) issued -> softmax sees s_full(it+1)
+      // dQ drain warps (stamps of tile it at row it+1): dq_full seen -> ld+arrive ->
+      // previous reduce read done + bar -> stage written + bar; next dq_full seen
+      acc[12] += double(b[11] - b[8]);
+      acc[13] += double(b[12] - b[11]);
+      acc[14] += double(b[13] - b[12]);
+      acc[15] += double(h[(it + 2) * 16 + 8] - b[13] > 0 ? h[(it + 2) * 16 + 8] - b[13] : 0);
     }
     if (n)
       fprintf(stderr,
               "[attn_bwd prof cta %d, %d iters] iter %.0f | wait_S %.0f ld+math %.0f publish %.0f "
               "drain(wait dq %.0f, total %.0f) cols+bar %.0f | mma: s_free->p_ready %.0f wait_dqt %.0f "
-              "issue_S %.0f sfull->sfree %.0f S_issue->S_seen %.0f\n",
+              "issue_S %.0f sfull->sfree %.0f S_issue->S_seen %.0f | dq warps: ld %.0f "
+              "reduce_read+bar %.0f stage %.0f idle %.0f\n",
               p.prof_cta, n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n,
-              acc[6] / n, acc[7] / n, acc[8] / n, acc[9] / n, acc[10] / n, acc[11] / n);
+              acc[6] / n, acc[7] / n, acc[8] / n, acc[9] / n, acc[10] / n, acc[11] / n,
+              acc[12] / n, acc[13] / n, acc[14] / n, acc[15] / n);
   }
   return cudaGetLastError();
 }

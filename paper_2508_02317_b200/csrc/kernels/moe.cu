@@ -372,14 +372,23 @@ __global__ void combine_kernel(const bf16* __restrict__ src, int64_t ld_src,
   const int lane = threadIdx.x & 31;
   const int le = le_lo + blockIdx.y;
   const int e = me * L.El + le;
+  // per source rank s: its count of expert e and its sorted offset of expert
+  // e (sum of its counts of the experts before e), computed once per block
+  __shared__ int s_cnt[kMaxSp], s_excl[kMaxSp];
+  if (threadIdx.x < L.ep) {
+    const int* c = counts_all + threadIdx.x * L.E;
+    int x = 0;
+    for (int e2 = 0; e2 < e; ++e2) x += c[e2];
+    s_excl[threadIdx.x] = x;
+    s_cnt[threadIdx.x] = c[e];
+  }
+  __syncthreads();
   const int n = seg_len(counts_all, L, e);
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
     int s = 0, off = r;
-    while (off >= counts_all[s * L.E + e]) off -= counts_all[s * L.E + e], ++s;
-    int excl_src = 0;  // source s's sorted offset of expert e
-    for (int e2 = 0; e2 < e; ++e2) excl_src += counts_all[s * L.E + e2];
+    while (off >= s_cnt[s]) off -= s_cnt[s], ++s;
     const bf16* a = src + int64_t(g_start[le] + r) * ld_src;
-    bf16* o = dst[s] + int64_t(excl_src + off) * ld_dst;
+    bf16* o = dst[s] + int64_t(s_excl[s] + off) * ld_dst;
     copy_row(o, a, W, lane);
   }
 }
