@@ -57,6 +57,11 @@ struct KParams {
   int64_t g_b_rows;    // rows of B per group slab (B row coordinate offset = g * g_b_rows)
   int64_t g_d_stride;  // element offset of D between groups (grouped_k only)
   int band;            // plain GEMMs: n-blocks per raster band (L2 reuse, chosen on host)
+  // GEMM_EPI_ROWMAP (grouped-M): destination of row r of group g
+  __nv_bfloat16* const* rm_dst;
+  const int* rm_cnt;
+  const int* rm_off;
+  int rm_ep;
 };
 
 struct TileCoord {
@@ -325,6 +330,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       } else {
+        // the output row: D's own, or (ROWMAP) its token owner's combine slot
+        __nv_bfloat16* brow = reinterpret_cast<__nv_bfloat16*>(p.D) + dgoff + int64_t(row) * p.ldd;
+        if (p.epi == GEMM_EPI_ROWMAP && row_ok) {
+          int r = c.mb * BM + r_local;  // row within group c.g
+          const int* cnt = p.rm_cnt + c.g * p.rm_ep;
+          int s = 0;
+          while (s + 1 < p.rm_ep && r >= cnt[s]) r -= cnt[s++];
+          brow = p.rm_dst[s] + int64_t(p.rm_off[c.g * p.rm_ep + s] + r) * p.ldd;
+        }
 #pragma unroll 1
         for (int ch = 0; ch < BN / 32; ++ch) {
           uint32_t v[32];
@@ -336,9 +350,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = empty_k ? 0.f : __uint_as_float(v[i]) * p.scale;
           const bool full_chunk = col0 + 32 <= p.N;
-          if (p.epi == GEMM_EPI_BF16) {
-            __nv_bfloat16* d =
-                reinterpret_cast<__nv_bfloat16*>(p.D) + dgoff + int64_t(row) * p.ldd + col0;
+          if (p.epi == GEMM_EPI_BF16 || p.epi == GEMM_EPI_ROWMAP) {
+            __nv_bfloat16* d = brow + col0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               if (!full_chunk && col0 + q * 8 >= p.N) break;
@@ -566,7 +579,14 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   // lists) is opt-in: on the C2 expert shapes it measured equal (dgrad, down)
   // or slower (gate|up + SwiGLU: 0.54 vs 0.36 ms) than the 1-CTA kernel
   static const bool grouped_2cta = getenv("OPX_GEMM_GROUPED_2CTA") != nullptr;
-  if (gm && grouped_2cta && !force_1cta && g.K % BK == 0) return gemm2_run(g, 1, s);
+  if (g.epi == GEMM_EPI_ROWMAP && (!gm || !g.rm_dst || !g.rm_cnt || !g.rm_off))
+    return cudaErrorInvalidValue;
+  kp.rm_dst = g.rm_dst;
+  kp.rm_cnt = g.rm_cnt;
+  kp.rm_off = g.rm_off;
+  kp.rm_ep = g.rm_ep;
+  if (gm && grouped_2cta && !force_1cta && g.K % BK == 0 && g.epi != GEMM_EPI_ROWMAP)
+    return gemm2_run(g, 1, s);
   if (!grouped && !force_1cta) {
     // 2-CTA path: same traffic model with 256-row pair tiles and 74 pairs per wave
     const double a_bytes = double(g.M) * g.K * 2, b_blk = 256.0 * g.K * 2;

@@ -363,34 +363,21 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
   }
 }
 
-// Combine: every valid row of this rank's receive buffer goes back to its
-// source rank, at the source's sorted position of that pair.
-__global__ void combine_kernel(const bf16* __restrict__ src, int64_t ld_src,
-                               const int* __restrict__ counts_all, Layout L, int me,
-                               const int* __restrict__ g_start, bf16* const* __restrict__ dst,
-                               int64_t ld_dst, int W, int le_lo) {
-  const int lane = threadIdx.x & 31;
-  const int le = le_lo + blockIdx.y;
+// Combine map for GEMM_EPI_ROWMAP: for local expert le and source rank s, the
+// rows of segment le that came from s (cnt) and where they go back (off: s's
+// sorted offset of expert e = me*El + le): the combine's addressing as a
+// table the expert GEMM epilogue reads
+__global__ void combine_map_kernel(const int* __restrict__ counts_all, Layout L, int me,
+                                   int* __restrict__ cnt, int* __restrict__ off) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.El * L.ep) return;
+  const int le = i / L.ep, s = i % L.ep;
   const int e = me * L.El + le;
-  // per source rank s: its count of expert e and its sorted offset of expert
-  // e (sum of its counts of the experts before e), computed once per block
-  __shared__ int s_cnt[kMaxSp], s_excl[kMaxSp];
-  if (threadIdx.x < L.ep) {
-    const int* c = counts_all + threadIdx.x * L.E;
-    int x = 0;
-    for (int e2 = 0; e2 < e; ++e2) x += c[e2];
-    s_excl[threadIdx.x] = x;
-    s_cnt[threadIdx.x] = c[e];
-  }
-  __syncthreads();
-  const int n = seg_len(counts_all, L, e);
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
-    int s = 0, off = r;
-    while (off >= s_cnt[s]) off -= s_cnt[s], ++s;
-    const bf16* a = src + int64_t(g_start[le] + r) * ld_src;
-    bf16* o = dst[s] + int64_t(s_excl[s] + off) * ld_dst;
-    copy_row(o, a, W, lane);
-  }
+  const int* c = counts_all + s * L.E;
+  int x = 0;
+  for (int e2 = 0; e2 < e; ++e2) x += c[e2];
+  cnt[i] = c[e];
+  off[i] = x;
 }
 
 // out[t] = resid[t] + sum_j w[t,j] * Y[pos(t,j)]  (fp32; one warp per token)
@@ -611,20 +598,12 @@ cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pai
   return cudaGetLastError();
 }
 
-cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* counts_all, int ep,
-                          int E, int me, const int* g_start, __nv_bfloat16* const* dst,
-                          int64_t ld_dst, int W, int max_rows, cudaStream_t s, int le_lo,
-                          int le_n) {
+cudaError_t k_moe_combine_map(const int* counts_all, int ep, int E, int me, int* cnt, int* off,
+                              cudaStream_t s) {
   Layout L{ep, E, E / ep};
-  static const int max_bx = getenv("OPX_COMBINE_BX") ? atoi(getenv("OPX_COMBINE_BX")) : 64;
-  int bx = (max_rows * 32 + 255) / 256 / L.El + 1;
-  if (bx > max_bx) bx = max_bx;
-  if (le_n < 0) le_n = L.El - le_lo;
-  if (le_n <= 0) return cudaSuccess;
-  dim3 grid(bx, le_n);
+  const int n = L.El * ep;
   ++g_kernel_launches;
-  combine_kernel<<<grid, 256, 0, s>>>(src, ld_src, counts_all, L, me, g_start, dst, ld_dst, W,
-                                      le_lo);
+  combine_map_kernel<<<(n + 255) / 256, 256, 0, s>>>(counts_all, L, me, cnt, off);
   return cudaGetLastError();
 }
 

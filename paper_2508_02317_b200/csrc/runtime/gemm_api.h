@@ -23,6 +23,11 @@ enum GemmEpi : int {
   // over NVLink (the k_a2a_seq2head addressing); D is unused.  head_dim 128,
   // plain (non-grouped) GEMMs on the 2-CTA kernel only.
   GEMM_EPI_SEQ2HEAD = 6,
+  // grouped-M (expert) GEMMs: bf16 row r of group g goes to peer rank s's
+  // buffer rm_dst[s] at row rm_off[g*ep+s] + (r - sum of rm_cnt[g*ep+0..s-1])
+  // -- the MoE combine (rows back to their token owners' sorted positions,
+  // step_graph.cpp:253-293) fused into the expert GEMM as NVLink peer stores
+  GEMM_EPI_ROWMAP = 7,
 };
 
 // D[M,N] = A . B^T with
@@ -60,6 +65,12 @@ struct GemmDesc {
   int64_t rows_total = 0;
   int64_t d_group_stride = 0;
   const A2AArgs* s2h = nullptr;  // GEMM_EPI_SEQ2HEAD routing (copied at launch)
+  // GEMM_EPI_ROWMAP: device array [rm_ep] of destination bases; per-group
+  // tables [groups][rm_ep] of row counts and destination row offsets
+  __nv_bfloat16* const* rm_dst = nullptr;
+  const int* rm_cnt = nullptr;
+  const int* rm_off = nullptr;
+  int rm_ep = 1;
 };
 
 cudaError_t gemm_run(const GemmDesc& g, cudaStream_t s);

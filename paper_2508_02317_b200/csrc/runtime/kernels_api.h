@@ -141,10 +141,9 @@ cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pai
                            const int* pair_at, int P, int k, const int* counts_all,
                            const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
                            int64_t ld_dst, int W, cudaStream_t s, int le_lo = 0, int le_hi = -1);
-cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* counts_all, int ep,
-                          int E, int me, const int* g_start, __nv_bfloat16* const* dst,
-                          int64_t ld_dst, int W, int max_rows, cudaStream_t s, int le_lo = 0,
-                          int le_n = -1);
+// [El][ep] row counts / destination offsets of the combine (GEMM_EPI_ROWMAP)
+cudaError_t k_moe_combine_map(const int* counts_all, int ep, int E, int me, int* cnt, int* off,
+                              cudaStream_t s);
 cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_of_pair,
                             const float* wts, int T, int k, int H, const float* resid, float* out,
                             cudaStream_t s);

@@ -382,6 +382,7 @@ class Step {
       *r_excl_ = nullptr, *r_hist_ = nullptr, *g_start_ = nullptr, *g_rows_ = nullptr,
       *g_rows_pad_ = nullptr, *g_total_ = nullptr;
   float* wr_part_ = nullptr;          // split-K partials of the router wgrad
+  int *rm_cnt_ = nullptr, *rm_off_ = nullptr;  // [El][ep] combine map (GEMM_EPI_ROWMAP)
   int* wr_gs_ = nullptr;              // chunk starts / rows for the split
   int* wr_gr_ = nullptr;
   int wr_split_ = 1;

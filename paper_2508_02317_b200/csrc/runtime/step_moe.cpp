@@ -217,6 +217,9 @@ int Step::moe_alloc() {
   gu_e_ = alloc<bf16>(cap * 2 * Fe, false);
   act_e_ = alloc<bf16>(cap * Fe);
   y_e_ = alloc<bf16>(cap * H, false);
+  rm_cnt_ = alloc<int>(size_t(El_) * size_t(ep_));
+  rm_off_ = alloc<int>(size_t(El_) * size_t(ep_));
+  if (!rm_cnt_ || !rm_off_) return cuda_fail(cudaErrorMemoryAllocation, "MoE combine map");
   dact_e_ = alloc<bf16>(cap * Fe, false);
   dgu_e_ = alloc<bf16>(cap * 2 * Fe);
   dx_e_ = alloc<bf16>(cap * H, false);
@@ -408,11 +411,11 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   const std::string pre = std::string(in_recompute_ ? "bwd" : "fwd") + ".layer" + std::to_string(l) + mtag() + ".";
   const std::string ph = std::string(in_recompute_ ? "bwd" : "fwd") + ".layer" + std::to_string(l);
   cudaEvent_t e0 = nullptr;
-  auto mk = [&](const char* name) {
+  auto mk = [&](const char* name, const char* fused = nullptr) {
     if (!ex_.trace) return;
     cudaEvent_t e1 = ev();
     cudaEventRecord(e1, cs_);
-    if (e0) mark(pre + name, ph, 0, e0, e1);
+    if (e0) mark(pre + name, ph, 0, e0, e1, fused);
     e0 = e1;
   };
   mk("");
@@ -442,7 +445,20 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   CU(k_moe_publish_counts(r_cnt_, count_tab_cur(), ep_, ep_i_, E, cs_));
   TRY(barrier_ep(cs_));
   CU(k_moe_groups(counts_all, ep_, E, ep_i_, g_start_, g_rows_, g_rows_pad_, g_total_, cs_));
+  CU(k_moe_combine_map(counts_all, ep_, E, ep_i_, rm_cnt_, rm_off_, cs_));
   mk("a2a_counts");
+  // down projection of experts [lo, hi) whose epilogue stores every row
+  // straight into its token owner's combine buffer (the a2a_combine)
+  auto down_combine = [&](int lo, int n, cudaStream_t st) -> int {
+    GemmDesc g = grouped(0, H, Fe, act_e_, Fe, false, Wd + int64_t(lo) * H * Fe, Fe, false,
+                         GEMM_EPI_ROWMAP, y_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
+    g.rm_dst = yback_tab_cur();
+    g.rm_cnt = rm_cnt_ + int64_t(lo) * ep_;
+    g.rm_off = rm_off_ + int64_t(lo) * ep_;
+    g.rm_ep = ep_;
+    CU(gemm_run(g, st));
+    return OPX_OK;
+  };
   // experts [lo, hi) of every rank: dispatch -> barrier -> gate|up + SwiGLU ->
   // down -> combine -> barrier, on stream st with barrier flag set `fs`
   auto phase = [&](int lo, int hi, cudaStream_t st, int fs, bool marks) -> int {
@@ -463,13 +479,8 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
       CU(gemm_run(g, st));
     }
     CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
-    CU(gemm_run(grouped(0, H, Fe, act_e_, Fe, false, Wd + int64_t(lo) * H * Fe, Fe, false,
-                        GEMM_EPI_BF16, y_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0),
-                st));
-    if (marks) mk("experts");
-    CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
-                     int(cap_rows_), st, lo, n));
-    if (marks) mk("a2a_combine");
+    TRY(down_combine(lo, n, st));
+    if (marks) mk("experts", "experts,a2a_combine");
     TRY(fs ? barrier_ep3(st) : barrier_ep(st));
     if (marks) mk("a2a_wait");
     return OPX_OK;
@@ -503,23 +514,15 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
       g.ldd2 = Fe;
       CU(gemm_run(g, st));
       CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
-      CU(gemm_run(grouped(0, H, Fe, act_e_, Fe, false, Wd + int64_t(lo) * H * Fe, Fe, false,
-                          GEMM_EPI_BF16, y_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0),
-                  st));
-      return OPX_OK;
+      return down_combine(lo, n, st);
     };
     TRY(experts(0, h, cs_));
     CU(cudaEventRecord(gemm_a, cs_));
-    mk("experts");
+    mk("experts", "experts,a2a_combine");
     CU(cudaStreamWaitEvent(xs2_, gemm_a, 0));
     TRY(experts(h, El_, xs2_));
-    CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
-                     int(cap_rows_), xs2_, h, El_ - h));
     TRY(barrier_ep3(xs2_));
     CU(cudaEventRecord(done_b, xs2_));
-    CU(k_moe_combine(y_e_, H, counts_all, ep_, E, ep_i_, g_start_, yback_tab_cur(), H, H,
-                     int(cap_rows_), cs_, 0, h));
-    mk("a2a_combine");
     TRY(barrier_ep(cs_));
     CU(cudaStreamWaitEvent(cs_, done_b, 0));
     // the compute stream now waits for half B: its expert GEMMs, combine and barrier
@@ -538,11 +541,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
   const std::string pre = "bwd.layer" + std::to_string(l) + mtag() + ".";
   const std::string ph = "bwd.layer" + std::to_string(l);
   cudaEvent_t e0 = nullptr;
-  auto mk = [&](const char* name) {
+  auto mk = [&](const char* name, const char* fused = nullptr) {
     if (!ex_.trace) return;
     cudaEvent_t e1 = ev();
     cudaEventRecord(e1, cs_);
-    if (e0) mark(pre + name, ph, 0, e0, e1);
+    if (e0) mark(pre + name, ph, 0, e0, e1, fused);
     e0 = e1;
   };
   mk("");
@@ -578,6 +581,7 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_, g_rows_, g_rows_pad_, El_, cs_));
     mk("gate_up_recompute");
   }
+  CU(k_moe_combine_map(counts_all, ep_, E, ep_i_, rm_cnt_, rm_off_, cs_));
   // weighted combine backward: per-pair output grads and router-weight grads
   CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
   // a2a_combine_grad: pair grads travel to the expert ranks (same layout as dispatch)
@@ -598,9 +602,16 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
                 st));
     CU(k_moe_swiglu_bwd(dact_e_, gu_e_, dgu_e_, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, Fe,
                         int(cap_rows_), st));
-    CU(gemm_run(grouped(0, H, 2 * Fe, dgu_e_, 2 * Fe, false, Wgu + lo * gs_gu, H, true, GEMM_EPI_BF16,
-                        dx_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0),
-                st));
+    {
+      // dX rows go straight back to their token owners (the a2a_dispatch_grad)
+      GemmDesc g = grouped(0, H, 2 * Fe, dgu_e_, 2 * Fe, false, Wgu + lo * gs_gu, H, true,
+                           GEMM_EPI_ROWMAP, dx_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
+      g.rm_dst = d_dxback_peers_;
+      g.rm_cnt = rm_cnt_ + int64_t(lo) * ep_;
+      g.rm_off = rm_off_ + int64_t(lo) * ep_;
+      g.rm_ep = ep_;
+      CU(gemm_run(g, st));
+    }
     CU(gemm_run(grouped(2 * Fe, H, 0, dgu_e_, 2 * Fe, true, xrecv, H, true, epi_w,
                         eu.gat(Ge, eu.params[0].off + lo * gs_gu), H, n, 1, g_start_ + lo,
                         g_rows_pad_ + lo, cap_rows_, gs_gu),
@@ -624,16 +635,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     mk("a2a_wait");
     TRY(experts_bwd(0, h, cs_));
     CU(cudaEventRecord(done_a, cs_));
-    mk("experts");
+    mk("experts", "experts,a2a_dispatch_grad");
     CU(cudaStreamWaitEvent(xs2_, done_a, 0));
     TRY(experts_bwd(h, El_, xs2_));
-    CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
-                     int(cap_rows_), xs2_, h, El_ - h));
     TRY(barrier_ep3(xs2_));
     CU(cudaEventRecord(done_b, xs2_));
-    CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
-                     int(cap_rows_), cs_, 0, h));
-    mk("a2a_dispatch_grad");
     TRY(barrier_ep(cs_));
     CU(cudaStreamWaitEvent(cs_, done_b, 0));
     mk("experts_b");  // half B's expert backward, dX combine and barrier
@@ -643,12 +649,10 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     mk("a2a_combine_grad");
     TRY(barrier_ep(cs_));
     mk("a2a_wait");
+    // a2a_dispatch_grad: input grads travel back to the token owners from
+    // the dgrad epilogue
     TRY(experts_bwd(0, El_, cs_));
-    // a2a_dispatch_grad: input grads travel back to the token owners
-    mk("experts");
-    CU(k_moe_combine(dx_e_, H, counts_all, ep_, E, ep_i_, g_start_, d_dxback_peers_, H, H,
-                     int(cap_rows_), cs_));
-    mk("a2a_dispatch_grad");
+    mk("experts", "experts,a2a_dispatch_grad");
     TRY(barrier_ep(cs_));
     mk("a2a_wait");
   }

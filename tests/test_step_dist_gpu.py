@@ -227,15 +227,17 @@ def test_checkpoint_reshard_fsdp2_to_1(tmp_path):
 # node names it stands for in args.fused ("a2a_q,a2a_k,a2a_v").
 # ---------------------------------------------------------------------------
 def _comm_nodes(trace):
+    """Collective node names of a measured trace; a fused node (an exchange
+    carried by a kernel's epilogue) contributes every name it stands for."""
     out = []
     for e in trace["traceEvents"]:
-        if e["cat"] != "comm" or e["name"].endswith(".a2a_wait"):
+        if e["name"].endswith(".a2a_wait"):
             continue
         fused = e["args"].get("fused")
+        base = e["name"].rsplit(".", 1)[0]
         if fused:
-            base = e["name"].rsplit(".", 1)[0]
-            out += [base + "." + f for f in fused.split(",")]
-        else:
+            out += [base + "." + f for f in fused.split(",") if ".a2a_" in "." + f]
+        elif e["cat"] == "comm":
             out.append(e["name"])
     return out
 
