@@ -41,7 +41,7 @@ QWEN3_30B_A3B = {"layers": 48, "hidden": 2048, "heads": 16, "kv_heads": 4, "head
 QWEN25_VL_VIT = {"layers": 32, "hidden": 1280, "heads": 16, "kv_heads": 16, "head_dim": 80,
                  "ffn_dim": 3456, "vocab": 1176}
 C3_TOKENS_PER_IMAGE = 256
-C3_IMAGES_PER_ROW = 64  # 16K of the 64K tokens are image tokens (25 % modality mix)
+C3_IMAGE_MIX = 0.25  # workload modality_mix: 16K of the 64K tokens are image tokens
 # C0: 2 layers, H=256, 4 heads of 64, 2 kv heads, ffn 768, V=2048, S=1024
 TINY = {"layers": 2, "hidden": 256, "heads": 4, "kv_heads": 2, "head_dim": 64, "ffn_dim": 768,
         "vocab": 2048}
@@ -425,6 +425,8 @@ def main():
         plan["async_ulysses"] = os.environ["OPX_BENCH_ASYNC"] == "1"
     rows = plan["dp_replicate"] * plan["dp_shard"] * plan["micro_batch"]
     wl = {"seq_len": S, "micro_batch": plan["micro_batch"], "global_batch": rows}
+    if cfg == "c3":  # WorkloadSpec.modality_mix (config_io.cpp:144-147)
+        wl["modality_mix"] = {"vision": C3_IMAGE_MIX, "text": 1.0 - C3_IMAGE_MIX}
     ex = {"seed": 2508, "lr": 1e-4, "betas": [0.9, 0.95], "eps": 1e-8, "weight_decay": 0.1,
           "trace": True}
     sess = Session(cluster_for(n), model, wl, plan, ex, rank=rank, device=local, dist=dist)
@@ -434,7 +436,9 @@ def main():
     if enc:
         from paper_2508_02317_b200.runtime import rank_coords, synthetic_images
 
-        synthetic_images(batch, enc["tokens_per_item"], enc["arch"]["vocab"], C3_IMAGES_PER_ROW,
+        # images per row from the mix: mix_fraction * tokens (step_graph.cpp:147)
+        per_row = int(round(wl["modality_mix"][enc["name"]] * S / enc["tokens_per_item"]))
+        synthetic_images(batch, enc["tokens_per_item"], enc["arch"]["vocab"], per_row,
                          placeholder=arch["vocab"] - 1)
     ids, labels, pos, cu, n_valid = local_slice(batch, rank, plan)
     # opx_step_load_batch uploads ids, labels, positions and, per token, the
@@ -515,7 +519,8 @@ def main():
                     "encoder_ms": statistics.mean(en) / 1e3 if en else None,
                     "scatter_ms": statistics.mean(sc) / 1e3 if sc else None,
                     "encoder_tflops_per_gpu": (enc_flops / n) / (statistics.mean(en) * 1e-6) / 1e12 if en else None,
-                    "model": "qwen2.5-vl-7b-shaped ViT, frozen (fwd only, no 2-D RoPE / windows)"}
+                    "model": "qwen2.5-vl-7b-shaped ViT, frozen (fwd only; 2-D RoPE, 112 px windows, "
+                             "full attention in blocks 7/15/23/31)"}
     per_gpu = value / n
     # roofline: dominant kernel = the forward MLP block (gate|up GEMM + SwiGLU
     # epilogue + down GEMM), 6*T*H*F algorithmic FLOPs per layer-call

@@ -430,6 +430,9 @@ Arch arch_from(const json& j, const std::string& ctx) {
   a.head_dim = get<i64>(j, "head_dim", ctx);
   a.ffn = get<i64>(j, "ffn_dim", ctx);
   a.vocab = get<i64>(j, "vocab", ctx);
+  a.window_merge = j.value("window_merge", i64{4});
+  if (j.contains("fullatt_blocks")) a.fullatt_blocks = get<std::vector<i64>>(j, "fullatt_blocks", ctx);
+  a.rope_theta = j.value("rope_theta", 10000.0);
   if (j.contains("moe")) {
     const json& mj = j.at("moe");
     need(mj, {"num_experts", "top_k", "expert_ffn_dim"}, ctx + ".moe");

@@ -46,6 +46,12 @@ struct Moe {
 struct Arch {
   i64 layers = 0, hidden = 0, heads = 1, kv_heads = 1, head_dim = 1, ffn = 1, vocab = 0;
   std::optional<Moe> moe;
+  // Vision encoders (Qwen2.5-VL; optional arch keys the reference ignores):
+  // window side in 2x2 merge units, full-attention blocks (default: every 8th
+  // and the last), 2-D RoPE base
+  i64 window_merge = 4;
+  std::optional<std::vector<i64>> fullatt_blocks;
+  double rope_theta = 10000.0;
   bool is_moe_layer(i64 l) const { return moe && (l + 1) % moe->stride == 0; }
   i64 q_width() const { return heads * head_dim; }
   i64 kv_width() const { return kv_heads * head_dim; }

@@ -5,6 +5,22 @@
 namespace opx {
 namespace epi {
 
+// f[0..31] += bias[0..31] (bf16 column bias, 16-B aligned)
+__device__ __forceinline__ void add_bias32(float* f, const __nv_bfloat16* b) {
+  const uint4* bp = reinterpret_cast<const uint4*>(b);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = bp[q];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = ptx::unpack_bf16(w[e]);
+      f[q * 8 + 2 * e] += x.x;
+      f[q * 8 + 2 * e + 1] += x.y;
+    }
+  }
+}
+
 // SwiGLU backward fused into the dact GEMM: 32 accumulator columns (dact for
 // features f0 .. f0+31 of one row, rounded to bf16 exactly as the unfused path
 // stored it) with the forward's gate/up (128-column interleave: gate of

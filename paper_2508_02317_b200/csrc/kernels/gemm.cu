@@ -62,6 +62,7 @@ struct KParams {
   const int* rm_cnt;
   const int* rm_off;
   int rm_ep;
+  const __nv_bfloat16* bias;  // optional column bias
 };
 
 struct TileCoord {
@@ -298,6 +299,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::tmem_ld32(tbase + ch * 32, g);
           ptx::tmem_ld32(tbase + 128 + ch * 32, u);
           ptx::tmem_wait_ld();
+          if (p.bias) {
+            float bg[32], bu[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bg[i] = __uint_as_float(g[i]), bu[i] = __uint_as_float(u[i]);
+            epi::add_bias32(bg, p.bias + c.nb * BN + ch * 32);
+            epi::add_bias32(bu, p.bias + c.nb * BN + 128 + ch * 32);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) g[i] = __float_as_uint(bg[i]), u[i] = __float_as_uint(bu[i]);
+          }
           const int f0 = c.nb * 128 + ch * 32;
           if (row_ok && f0 < p.N / 2) {
             __nv_bfloat16* act = p.D2 + int64_t(row) * p.ldd2 + f0;
@@ -349,6 +359,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           float f[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = empty_k ? 0.f : __uint_as_float(v[i]) * p.scale;
+          if (p.bias) epi::add_bias32(f, p.bias + col0);
           const bool full_chunk = col0 + 32 <= p.N;
           if (p.epi == GEMM_EPI_BF16 || p.epi == GEMM_EPI_ROWMAP) {
             __nv_bfloat16* d = brow + col0;
@@ -579,12 +590,16 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   // lists) is opt-in: on the C2 expert shapes it measured equal (dgrad, down)
   // or slower (gate|up + SwiGLU: 0.54 vs 0.36 ms) than the 1-CTA kernel
   static const bool grouped_2cta = getenv("OPX_GEMM_GROUPED_2CTA") != nullptr;
+  if (g.bias && (g.N % 32 || (g.epi != GEMM_EPI_BF16 && g.epi != GEMM_EPI_F32 &&
+                              g.epi != GEMM_EPI_F32_RESID && g.epi != GEMM_EPI_SWIGLU)))
+    return cudaErrorInvalidValue;
   if (g.epi == GEMM_EPI_ROWMAP && (!gm || !g.rm_dst || !g.rm_cnt || !g.rm_off))
     return cudaErrorInvalidValue;
   kp.rm_dst = g.rm_dst;
   kp.rm_cnt = g.rm_cnt;
   kp.rm_off = g.rm_off;
   kp.rm_ep = g.rm_ep;
+  kp.bias = g.bias;
   if (gm && grouped_2cta && !force_1cta && g.K % BK == 0 && g.epi != GEMM_EPI_ROWMAP)
     return gemm2_run(g, 1, s);
   if (!grouped && !force_1cta) {

@@ -59,6 +59,7 @@ struct P2 {
   const int* g_start;
   const int* g_rows;
   A2AArgs s2h;  // GEMM_EPI_SEQ2HEAD
+  const __nv_bfloat16* bias;  // optional column bias
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -381,6 +382,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           ptx::tmem_ld32(tbase + ch * 32, g);
           ptx::tmem_ld32(tbase + 128 + ch * 32, u);
           ptx::tmem_wait_ld();
+          if (p.bias) {
+            float bg[32], bu[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bg[i] = __uint_as_float(g[i]), bu[i] = __uint_as_float(u[i]);
+            epi::add_bias32(bg, p.bias + nb * BNP + ch * 32);
+            epi::add_bias32(bu, p.bias + nb * BNP + 128 + ch * 32);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) g[i] = __float_as_uint(bg[i]), u[i] = __float_as_uint(bu[i]);
+          }
           const int f0 = nb * 128 + ch * 32;
           if (row_ok && f0 < p.N / 2) {
             __nv_bfloat16* act = p.D2 + int64_t(row) * p.ldd2 + f0;
@@ -422,6 +432,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           float f[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.scale;
+          if (p.bias) epi::add_bias32(f, p.bias + col0);
           const bool full_chunk = col0 + 32 <= p.N;
           if (p.epi == GEMM_EPI_BF16) {
             __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd + col0;
@@ -545,6 +556,7 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   p.G2 = g.G2;
   p.ldg2 = g.ldg2;
   p.scale = g.scale == 0.f ? 1.f : g.scale;
+  p.bias = g.bias;
   cudaEvent_t slot_done = nullptr;
   {
     cudaError_t e = ticket_acquire(s, &p.ctr, &slot_done);

@@ -65,6 +65,10 @@ struct GemmDesc {
   int64_t rows_total = 0;
   int64_t d_group_stride = 0;
   const A2AArgs* s2h = nullptr;  // GEMM_EPI_SEQ2HEAD routing (copied at launch)
+  // optional bf16 column bias [N] (BF16 / F32 / F32_RESID / SWIGLU epilogues;
+  // SWIGLU: in the 128-column gate|up interleave of B's rows), added to the
+  // accumulator before rounding / activation
+  const __nv_bfloat16* bias = nullptr;
   // GEMM_EPI_ROWMAP: device array [rm_ep] of destination bases; per-group
   // tables [groups][rm_ep] of row counts and destination row offsets
   __nv_bfloat16* const* rm_dst = nullptr;

@@ -296,14 +296,28 @@ class Step {
     bool on = false;
     std::string name;
     int He = 0, L = 0, heads = 0, d = 0, F = 0, pd = 0, tpi = 0;
-    bf16* w = nullptr;  // every weight, 128-element aligned offsets
-    int64_t o_patch = 0, o_lnq = 0, o_m0 = 0, o_m2 = 0, numel = 0;
-    std::vector<int64_t> o_blk;  // per block: norm1 | qkv | proj | norm2 | gate_up | down
+    bf16* w = nullptr;  // every weight and bias, 128-element aligned offsets
+    int64_t o_patch = 0, o_lnq = 0, o_m0 = 0, o_m0b = 0, o_m2 = 0, o_m2b = 0, numel = 0;
+    // per block (kBlk entries): norm1 | qkv | qkv bias | proj | proj bias | norm2 |
+    // gate_up | gate_up bias (128-interleaved like the weight) | down | down bias
+    static constexpr int kBlk = 10;
+    std::vector<int64_t> o_blk;
+    // Qwen2.5-VL geometry: g x g patches per item, windows of window_merge^2
+    // merge units, full-attention blocks, 2-D RoPE (sin, cos) per patch of an
+    // item in window order [P][d/2]
+    int g = 0, window_merge = 4;
+    std::vector<char> fullatt;
+    std::vector<int> worder;  // merge units in window order (get_window_index)
+    std::vector<int> wlens;   // window lengths in patches
+    double rope_theta = 1e4;
+    float2* rope = nullptr;
     int cap = 0, n_loc = 0, n_all = 0;  // items: buffer capacity, encoded here, in the micro-batch
     bf16 *pix = nullptr, *h = nullptr, *qkv = nullptr, *q = nullptr, *k = nullptr, *v = nullptr,
          *o = nullptr, *o2 = nullptr, *act = nullptr, *y1 = nullptr, *feat = nullptr;
     float *x = nullptr, *rstd = nullptr, *lse = nullptr;
-    int *st = nullptr, *en = nullptr, *dst_rank = nullptr, *dst_tok = nullptr;
+    // per patch row: item span (full attention), window span, RoPE row (i % P)
+    int *st = nullptr, *en = nullptr, *wst = nullptr, *wen = nullptr, *rpos = nullptr,
+        *dst_rank = nullptr, *dst_tok = nullptr;
     std::vector<void*> bufs;  // item-sized buffers (re-allocated when cap grows)
   } enc_;
   int* d_fmask_ = nullptr;  // [T] local tokens replaced by encoder features

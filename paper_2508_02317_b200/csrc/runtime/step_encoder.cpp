@@ -5,19 +5,29 @@
 // (no backward node when the module is frozen) and a `scatter.<mod>`
 // all_to_all of the features into the SP group (comm.cpp:91-105); the module
 // fields come from specs.hpp:66-75 (name, kind, arch, trainable,
-// tokens_per_item).  The encoder math (a Qwen2.5-VL-shaped ViT without 2-D
-// RoPE / windows, then the 2x2 patch merger) is defined in oracle/encoder.py.
+// tokens_per_item).  The encoder math is HF transformers' Qwen2.5-VL vision
+// tower (modeling_qwen2_5_vl.py:345-518: biases, 2-D RoPE, windowed and
+// full-attention blocks, 2x2 patch merger), restated in oracle/encoder.py and
+// pinned against the HF module there.
 //
 // B200 mapping: the items of a micro-batch are dealt round-robin to the SP
-// ranks (item j -> rank j % sp), each rank runs the ViT over its patches with
-// the backbone's kernels (tcgen05 GEMMs, SwiGLU epilogue, bidirectional
-// tcgen05 attention on 128-padded heads via the seq->head relayout kernel),
-// and the merger's output rows are stored straight into the feature buffer of
-// the SP rank that owns each placeholder position (NVLink peer stores into the
-// CUDA-IPC arena: the all-to-all and the masked scatter's addressing in one
+// ranks (item j -> rank j % sp; every rank then encodes mix_fraction x its
+// share of the tokens, step_graph.cpp:147), each rank runs the ViT over its
+// patches with the backbone's kernels (tcgen05 GEMMs with bias / SwiGLU
+// epilogues, bidirectional tcgen05 attention on 128-padded heads through the
+// seq->head relayout kernel, which also applies the 2-D RoPE from a per-patch
+// (sin, cos) table).  Windows cost nothing extra: the host uploads each
+// item's patches already in window order (get_window_index's permutation),
+// windowed blocks see per-window [seq_start, seq_end) spans, full-attention
+// blocks per-item spans, and the merger's rows are stored straight into the
+// feature buffer of the SP rank that owns each placeholder position in the
+// inverse order (NVLink peer stores into the CUDA-IPC arena: the
+// all-to-all, the un-permutation and the masked scatter's addressing in one
 // pass).  After an SP barrier every rank overwrites its placeholder
 // embeddings with the received rows; the backward zeroes their gradient rows
-// before the embedding scatter-add (the features are frozen).
+// before the embedding scatter-add (the features are frozen).  The frozen
+// weights are replicated, not FSDP-sharded (no gradient or optimizer state;
+// sharding would trade ~1.3 GB at the 7B ViT for a per-step all-gather).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -78,11 +88,43 @@ int Step::enc_setup() {
   e.F = int(ea.ffn);
   e.pd = int(ea.vocab);  // an encoder's "vocab" is its patch width
   e.tpi = int(em->tokens_per_item);
+  e.g = int(std::lround(std::sqrt(4.0 * e.tpi)));
+  e.window_merge = int(ea.window_merge);
+  e.rope_theta = ea.rope_theta;
   if (ea.kv_heads != ea.heads || e.d > 128 || e.d % 16 || e.He % 128 || e.F % 128 || e.pd % 8 ||
-      e.tpi <= 0 || e.tpi > S_loc_) {
+      e.tpi <= 0 || e.tpi > S_loc_ || e.g * e.g != 4 * e.tpi || e.g % 2 || e.window_merge < 1) {
     set_error("encoder requires kv_heads == heads, head_dim <= 128 (multiple of 16), hidden and ffn "
-              "multiples of 128, patch width (arch.vocab) a multiple of 8, 0 < tokens_per_item <= seq/sp");
+              "multiples of 128, patch width (arch.vocab) a multiple of 8, 0 < tokens_per_item <= "
+              "seq/sp with 4*tokens_per_item a square of even side, window_merge >= 1");
     return OPX_ERR_CONFIG;
+  }
+  // full-attention blocks: the arch's list, else Qwen2.5-VL's every 8th + the last
+  e.fullatt.assign(size_t(e.L), 0);
+  if (ea.fullatt_blocks) {
+    for (i64 b : *ea.fullatt_blocks)
+      if (b >= 0 && b < e.L) e.fullatt[size_t(b)] = 1;
+  } else {
+    for (int i = 0; i < e.L; ++i) e.fullatt[size_t(i)] = (i + 1) % 8 == 0 || i == e.L - 1;
+  }
+  // window order of the merge units (get_window_index, padding windows dropped)
+  {
+    const int lg = e.g / 2, wm = e.window_merge;
+    const int nw = (lg + wm - lg % wm) / wm;
+    e.worder.clear();
+    e.wlens.clear();
+    for (int wh = 0; wh < nw; ++wh)
+      for (int ww = 0; ww < nw; ++ww) {
+        int n = 0;
+        for (int i = 0; i < wm; ++i)
+          for (int j = 0; j < wm; ++j) {
+            const int uh = wh * wm + i, uw = ww * wm + j;
+            if (uh < lg && uw < lg) {
+              e.worder.push_back(uh * lg + uw);
+              ++n;
+            }
+          }
+        if (n) e.wlens.push_back(4 * n);
+      }
   }
   const int64_t He = e.He, Wq = int64_t(e.heads) * e.d, F = e.F;
   auto take = [&](int64_t n) {
@@ -94,17 +136,42 @@ int Step::enc_setup() {
   for (int i = 0; i < e.L; ++i) {
     e.o_blk.push_back(take(He));          // norm1
     e.o_blk.push_back(take(3 * Wq * He)); // qkv
+    e.o_blk.push_back(take(3 * Wq));      // qkv bias
     e.o_blk.push_back(take(He * Wq));     // proj
+    e.o_blk.push_back(take(He));          // proj bias
     e.o_blk.push_back(take(He));          // norm2
     e.o_blk.push_back(take(2 * F * He));  // gate|up (128-row interleave)
+    e.o_blk.push_back(take(2 * F));       // gate|up bias (same interleave)
     e.o_blk.push_back(take(He * F));      // down
+    e.o_blk.push_back(take(He));          // down bias
   }
   e.o_lnq = take(He);
   e.o_m0 = take(16 * He * He);
+  e.o_m0b = take(4 * He);
   e.o_m2 = take(int64_t(H_) * 4 * He);
+  e.o_m2b = take(H_);
   e.w = alloc<bf16>(size_t(e.numel));
   d_fmask_ = alloc<int>(size_t(T_));
-  if (!e.w || !d_fmask_) return cuda_fail(cudaErrorMemoryAllocation, "encoder weights");
+  // 2-D RoPE table of one item's patches in window order: pair (j, j + d/2)
+  // turns by hpos * inv[j] (j < d/4) or wpos * inv[j - d/4] (rot_pos_emb,
+  // apply_rotary_pos_emb_vision); sin/cos of the fp32 angle in double
+  const int P = 4 * e.tpi, hd2 = e.d / 2, hd4 = e.d / 4;
+  e.rope = alloc<float2>(size_t(P) * hd2, false);
+  if (!e.w || !d_fmask_ || !e.rope) return cuda_fail(cudaErrorMemoryAllocation, "encoder weights");
+  std::vector<float> inv(static_cast<size_t>(hd4));
+  for (int i = 0; i < hd4; ++i)
+    inv[size_t(i)] = float(1.0 / std::pow(e.rope_theta, double(2 * i) / double(hd2)));
+  std::vector<float2> tab(size_t(P) * hd2);
+  for (int r = 0; r < P; ++r) {
+    const int patch = e.worder[size_t(r / 4)] * 4 + r % 4;  // processor-order patch of row r
+    const int unit = patch / 4, sub = patch % 4;
+    const int hp = (unit / (e.g / 2)) * 2 + sub / 2, wp = (unit % (e.g / 2)) * 2 + sub % 2;
+    for (int j = 0; j < hd2; ++j) {
+      const float ang = j < hd4 ? float(hp) * inv[size_t(j)] : float(wp) * inv[size_t(j - hd4)];
+      tab[size_t(r) * hd2 + j] = make_float2(float(std::sin(double(ang))), float(std::cos(double(ang))));
+    }
+  }
+  CU(cudaMemcpy(e.rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   return OPX_OK;
 }
 
@@ -124,18 +191,25 @@ int Step::enc_init_weights(uint64_t seed) {
   TRY(normal(e.o_patch, He * e.pd, "visual.patch_embed.proj.weight"));
   for (int i = 0; i < e.L; ++i) {
     const std::string p = "visual.blocks." + std::to_string(i) + ".";
-    const int64_t* o = &e.o_blk[size_t(i) * 6];
+    const int64_t* o = &e.o_blk[size_t(i) * Enc::kBlk];
     TRY(ones(o[0], He));
     TRY(normal(o[1], 3 * Wq * He, p + "attn.qkv.weight"));
-    TRY(normal(o[2], He * Wq, p + "attn.proj.weight"));
-    TRY(ones(o[3], He));
-    CU(k_init_param(nullptr, e.w + o[4], 2 * F * He, 0, param_key(p + "mlp.gate_proj.weight", seed),
+    TRY(normal(o[2], 3 * Wq, p + "attn.qkv.bias"));
+    TRY(normal(o[3], He * Wq, p + "attn.proj.weight"));
+    TRY(normal(o[4], He, p + "attn.proj.bias"));
+    TRY(ones(o[5], He));
+    CU(k_init_param(nullptr, e.w + o[6], 2 * F * He, 0, param_key(p + "mlp.gate_proj.weight", seed),
                     param_key(p + "mlp.up_proj.weight", seed), c, 1.f, 1, 2 * F, He, cs_));
-    TRY(normal(o[5], He * F, p + "mlp.down_proj.weight"));
+    CU(k_init_param(nullptr, e.w + o[7], 2 * F, 0, param_key(p + "mlp.gate_proj.bias", seed),
+                    param_key(p + "mlp.up_proj.bias", seed), c, 1.f, 1, 2 * F, 1, cs_));
+    TRY(normal(o[8], He * F, p + "mlp.down_proj.weight"));
+    TRY(normal(o[9], He, p + "mlp.down_proj.bias"));
   }
   TRY(ones(e.o_lnq, He));
   TRY(normal(e.o_m0, 16 * He * He, "visual.merger.mlp.0.weight"));
+  TRY(normal(e.o_m0b, 4 * He, "visual.merger.mlp.0.bias"));
   TRY(normal(e.o_m2, int64_t(H_) * 4 * He, "visual.merger.mlp.2.weight"));
+  TRY(normal(e.o_m2b, H_, "visual.merger.mlp.2.bias"));
   return OPX_OK;
 }
 
@@ -152,7 +226,7 @@ int Step::enc_alloc(int items) {
   const size_t Wq = size_t(e.heads) * size_t(e.d);
   auto a = [&](auto*& ptr, size_t n) {
     using T = std::remove_reference_t<decltype(*ptr)>;
-    ptr = alloc<T>(n, false);
+    ptr = alloc<T>(n);  // zeroed: the 128-padded head lanes (d < 128) must read 0
     e.bufs.push_back(ptr);
     return ptr != nullptr;
   };
@@ -162,7 +236,8 @@ int Step::enc_alloc(int items) {
             a(e.k, Np * size_t(e.heads) * 128) && a(e.v, Np * size_t(e.heads) * 128) &&
             a(e.o, Np * size_t(e.heads) * 128) && a(e.o2, Np * Wq) && a(e.act, Np * size_t(e.F)) &&
             a(e.y1, Np * He) && a(e.feat, Np / 4 * size_t(H_)) && a(e.st, Np) && a(e.en, Np) &&
-            a(e.dst_rank, Np / 4) && a(e.dst_tok, Np / 4);
+            a(e.wst, Np) && a(e.wen, Np) && a(e.rpos, Np) && a(e.dst_rank, Np / 4) &&
+            a(e.dst_tok, Np / 4);
   if (!ok) return cuda_fail(cudaErrorMemoryAllocation, "encoder activations");
   e.cap = items;
   return OPX_OK;
@@ -194,26 +269,44 @@ int Step::load_images(const uint16_t* pixels, int n, const int32_t* row, const i
   CU(cudaMemcpyAsync(d_fmask_, mask.data(), size_t(T_) * 4, cudaMemcpyHostToDevice, cs_));
   if (e.n_loc == 0) return OPX_OK;
   TRY(enc_alloc(e.n_loc));
-  const size_t item_elems = size_t(P) * size_t(e.pd);
+  // patches are staged in window order (merge unit worder[m] becomes unit m);
+  // merger row m of an item is the feature of its placeholder token worder[m]
+  const size_t patch_elems = size_t(e.pd), item_elems = size_t(P) * patch_elems;
   std::vector<uint16_t> px(size_t(e.n_loc) * item_elems);
-  std::vector<int32_t> st(size_t(e.n_loc) * P), en(size_t(e.n_loc) * P), dr(size_t(e.n_loc) * tpi),
+  const size_t NpL = size_t(e.n_loc) * P;
+  std::vector<int32_t> st(NpL), en(NpL), wst(NpL), wen(NpL), rp(NpL), dr(size_t(e.n_loc) * tpi),
       dt(size_t(e.n_loc) * tpi);
   for (int k = 0; k < e.n_loc; ++k) {
     const int j = mine[size_t(k)];
-    std::memcpy(px.data() + size_t(k) * item_elems, pixels + size_t(j) * item_elems, item_elems * 2);
+    for (int m = 0; m < P / 4; ++m)
+      std::memcpy(px.data() + size_t(k) * item_elems + size_t(m) * 4 * patch_elems,
+                  pixels + size_t(j) * item_elems + size_t(e.worder[size_t(m)]) * 4 * patch_elems,
+                  4 * patch_elems * 2);
+    int w0 = 0;
+    for (int len : e.wlens) {
+      for (int i = 0; i < len; ++i) {
+        wst[size_t(k) * P + w0 + i] = k * P + w0;
+        wen[size_t(k) * P + w0 + i] = k * P + w0 + len;
+      }
+      w0 += len;
+    }
     for (int i = 0; i < P; ++i) {
       st[size_t(k) * P + i] = k * P;
       en[size_t(k) * P + i] = (k + 1) * P;
+      rp[size_t(k) * P + i] = i;
     }
-    for (int t = 0; t < tpi; ++t) {
-      const int s = pos[j] + t;
-      dr[size_t(k) * tpi + t] = s / S_loc_;
-      dt[size_t(k) * tpi + t] = row[j] * S_loc_ + s % S_loc_;
+    for (int m = 0; m < tpi; ++m) {
+      const int s = pos[j] + e.worder[size_t(m)];
+      dr[size_t(k) * tpi + m] = s / S_loc_;
+      dt[size_t(k) * tpi + m] = row[j] * S_loc_ + s % S_loc_;
     }
   }
   CU(cudaMemcpyAsync(e.pix, px.data(), px.size() * 2, cudaMemcpyHostToDevice, cs_));
   CU(cudaMemcpyAsync(e.st, st.data(), st.size() * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaMemcpyAsync(e.en, en.data(), en.size() * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(e.wst, wst.data(), wst.size() * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(e.wen, wen.data(), wen.size() * 4, cudaMemcpyHostToDevice, cs_));
+  CU(cudaMemcpyAsync(e.rpos, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaMemcpyAsync(e.dst_rank, dr.data(), dr.size() * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaMemcpyAsync(e.dst_tok, dt.data(), dt.size() * 4, cudaMemcpyHostToDevice, cs_));
   CU(cudaStreamSynchronize(cs_));
@@ -227,16 +320,20 @@ int Step::enc_forward() {
   cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
   if (tr) cudaEventRecord(e0, cs_);
   const int Np = e.n_loc * 4 * e.tpi, He = e.He, Wq = e.heads * e.d, F = e.F, nf = e.n_loc * e.tpi;
-  const bool pad = e.d != 128;
+  const int64_t ldh = int64_t(e.heads) * 128;  // 128-padded head layout
   if (Np > 0) {
     CU(gemm_run(egd(Np, He, e.pd, e.pix, e.pd, e.w + e.o_patch, e.pd, GEMM_EPI_F32, e.x, He), cs_));
     for (int i = 0; i < e.L; ++i) {
-      const int64_t* o = &e.o_blk[size_t(i) * 6];
+      const int64_t* o = &e.o_blk[size_t(i) * Enc::kBlk];
       CU(k_rmsnorm_fwd(e.x, e.w + o[0], e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
-      CU(gemm_run(egd(Np, 3 * Wq, He, e.h, He, e.w + o[1], He, GEMM_EPI_BF16, e.qkv, 3 * Wq), cs_));
-      const bf16 *q = e.qkv, *k = e.qkv + Wq, *v = e.qkv + 2 * Wq;
-      int64_t ld = 3 * Wq;
-      if (pad) {  // [Np, heads*d] -> zero-padded [Np, heads, 128] (sp = 1 relayout, no RoPE)
+      {
+        GemmDesc g = egd(Np, 3 * Wq, He, e.h, He, e.w + o[1], He, GEMM_EPI_BF16, e.qkv, 3 * Wq);
+        g.bias = e.w + o[2];
+        CU(gemm_run(g, cs_));
+      }
+      {
+        // [Np, 3, heads*d] -> [Np, heads, 128] q / k / v with the 2-D RoPE on
+        // q and k (sp = 1 relayout; table row = patch row within its item)
         A2AArgs a{};
         a.sp = 1;
         a.rank = 0;
@@ -247,29 +344,28 @@ int Step::enc_forward() {
         for (int g = 0; g < 3; ++g) {
           a.g[g].heads_total = e.heads;
           a.g[g].col0 = g * Wq;
-          a.g[g].rope = 0;
+          a.g[g].rope = g < 2;
           a.g[g].full[0] = dst[g];
         }
         a.local[0] = e.qkv;
         a.local_ld = 3 * Wq;
         a.hd = e.d;
+        a.pos = e.rpos;
+        a.rope_tab = e.rope;
         CU(k_a2a_seq2head(a, cs_));
-        q = e.q;
-        k = e.k;
-        v = e.v;
-        ld = int64_t(e.heads) * 128;
       }
       {
         AttnArgs a{};
-        a.q = q;
-        a.k = k;
-        a.v = v;
+        a.q = e.q;
+        a.k = e.k;
+        a.v = e.v;
         a.o = e.o;
         a.lse = e.lse;  // not kept: the encoder has no backward
-        a.ldq = a.ldk = a.ldv = ld;
-        a.ldo = int64_t(e.heads) * 128;
-        a.seq_start = e.st;
-        a.seq_end = e.en;
+        a.ldq = a.ldk = a.ldv = ldh;
+        a.ldo = ldh;
+        const bool full = e.fullatt[size_t(i)];
+        a.seq_start = full ? e.st : e.wst;
+        a.seq_end = full ? e.en : e.wen;
         a.N = Np;
         a.hq = a.hk = e.heads;
         a.scale = 1.0f / std::sqrt(float(e.d));
@@ -277,7 +373,8 @@ int Step::enc_forward() {
         CU(k_attn_fwd_tc(a, cs_));
       }
       const bf16* o2 = e.o;
-      if (pad) {
+      int64_t ldo2 = ldh;
+      if (e.d != 128) {
         A2AArgs a{};
         a.sp = 1;
         a.rank = 0;
@@ -291,36 +388,45 @@ int Step::enc_forward() {
         a.hd = e.d;
         CU(k_a2a_head2seq(a, cs_));
         o2 = e.o2;
+        ldo2 = Wq;
       }
       {
-        GemmDesc g = egd(Np, He, Wq, o2, pad ? Wq : int64_t(e.heads) * 128, e.w + o[2], Wq,
-                         GEMM_EPI_F32_RESID, e.x, He);
+        GemmDesc g = egd(Np, He, Wq, o2, ldo2, e.w + o[3], Wq, GEMM_EPI_F32_RESID, e.x, He);
         g.R = e.x;
         g.ldr = He;
+        g.bias = e.w + o[4];
         CU(gemm_run(g, cs_));
       }
-      CU(k_rmsnorm_fwd(e.x, e.w + o[3], e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
+      CU(k_rmsnorm_fwd(e.x, e.w + o[5], e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
       {
-        GemmDesc g = egd(Np, 2 * F, He, e.h, He, e.w + o[4], He, GEMM_EPI_SWIGLU, nullptr, 2 * F);
+        GemmDesc g = egd(Np, 2 * F, He, e.h, He, e.w + o[6], He, GEMM_EPI_SWIGLU, nullptr, 2 * F);
         g.D2 = e.act;
         g.ldd2 = F;
+        g.bias = e.w + o[7];
         CU(gemm_run(g, cs_));
       }
       {
-        GemmDesc g = egd(Np, He, F, e.act, F, e.w + o[5], F, GEMM_EPI_F32_RESID, e.x, He);
+        GemmDesc g = egd(Np, He, F, e.act, F, e.w + o[8], F, GEMM_EPI_F32_RESID, e.x, He);
         g.R = e.x;
         g.ldr = He;
+        g.bias = e.w + o[9];
         CU(gemm_run(g, cs_));
       }
     }
     // merger: rmsnorm_q, 2x2 merge (4 consecutive patches = one [4 He] row), MLP with GELU
     CU(k_rmsnorm_fwd(e.x, e.w + e.o_lnq, e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
-    CU(gemm_run(egd(Np / 4, 4 * He, 4 * He, e.h, 4 * He, e.w + e.o_m0, 4 * He, GEMM_EPI_BF16, e.y1,
-                    4 * He),
-                cs_));
+    {
+      GemmDesc g = egd(Np / 4, 4 * He, 4 * He, e.h, 4 * He, e.w + e.o_m0, 4 * He, GEMM_EPI_BF16, e.y1,
+                       4 * He);
+      g.bias = e.w + e.o_m0b;
+      CU(gemm_run(g, cs_));
+    }
     CU(k_gelu_bf16(e.y1, int64_t(Np / 4) * 4 * He, cs_));
-    CU(gemm_run(egd(nf, H_, 4 * He, e.y1, 4 * He, e.w + e.o_m2, 4 * He, GEMM_EPI_BF16, e.feat, H_),
-                cs_));
+    {
+      GemmDesc g = egd(nf, H_, 4 * He, e.y1, 4 * He, e.w + e.o_m2, 4 * He, GEMM_EPI_BF16, e.feat, H_);
+      g.bias = e.w + e.o_m2b;
+      CU(gemm_run(g, cs_));
+    }
   }
   if (tr) {
     e1 = ev();
@@ -328,7 +434,8 @@ int Step::enc_forward() {
     mark("encoder." + e.name + mtag(), "encoder", 0, e0, e1);
     e0 = e1;
   }
-  // scatter.<mod>: feature rows -> the owning SP rank's feature buffer
+  // scatter.<mod>: feature rows -> the owning SP rank's feature buffer (rows
+  // in window order; dst_tok holds each row's placeholder token)
   FeatPeers fp{};
   for (int j = 0; j < int(p_.sp); ++j) fp.p[j] = reinterpret_cast<bf16*>(peer(j, off_feat_));
   CU(k_feat_scatter(e.feat, nf, H_, e.dst_rank, e.dst_tok, fp, cs_));

@@ -100,11 +100,15 @@ def global_routes(sessions, arch, plan, S):
 MAX_FLIP_RATE = 0.05  # fraction of tokens whose expert set differs from the oracle's own top-k (reported)
 
 
-def tiny_encoder(layers=2, hidden=640, heads=8, head_dim=80, ffn=512, patch_dim=96, tokens_per_item=16):
-    """Frozen ViT-shaped encoder module (oracle/encoder.py); arch.vocab = patch width."""
+def tiny_encoder(layers=2, hidden=640, heads=8, head_dim=80, ffn=512, patch_dim=96, tokens_per_item=16,
+                 window_merge=2):
+    """Frozen Qwen2.5-VL-shaped encoder module (oracle/encoder.py); arch.vocab =
+    patch width; window_merge 2 on the 8x8-patch items gives 4 windows, and the
+    default full-attention block is the last one."""
     return {"name": "vision", "kind": "encoder", "trainable": False, "tokens_per_item": tokens_per_item,
             "arch": {"layers": layers, "hidden": hidden, "heads": heads, "kv_heads": heads,
-                     "head_dim": head_dim, "ffn_dim": ffn, "vocab": patch_dim}}
+                     "head_dim": head_dim, "ffn_dim": ffn, "vocab": patch_dim,
+                     "window_merge": window_merge}}
 
 
 BF16_FLOOR_FACTOR = 1.5
