@@ -221,6 +221,21 @@ int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void*
                   int hq, int hk, int rows, int S, const int32_t* pos, const float* inv_freq,
                   void* stream);
 
+/* Ulysses exchanges as NVLink peer stores (kernels/a2a.cu), the kernels
+ * behind VeOmni's gather_seq_scatter_heads / gather_heads_scatter_seq
+ * (step_graph.cpp:224-239 a2a_q/k/v, a2a_out).
+ * seq2head: this SP rank's [rows*S/sp, (hq+2hk)*hd] q|k|v rows (row stride ld)
+ * go to every rank j's [rows*S, h/sp, 128] head-layout buffers q_dst[j],
+ * k_dst[j], v_dst[j] (device pointers, host arrays of sp entries; peers via
+ * CUDA IPC or peer access), RoPE on q/k when pos (global position ids [rows*S])
+ * and inv_freq ([hd/2]) are given.  head2seq: this rank's [rows*S, hq/sp, 128]
+ * attention output back to the token owners' [rows*S/sp, hq*hd] rows dst[j]. */
+int opx_ulysses_seq2head(const void* qkv, int64_t ld, void* const* q_dst, void* const* k_dst,
+                         void* const* v_dst, int sp, int rank, int rows, int S, int hq, int hk,
+                         int hd, const int32_t* pos, const float* inv_freq, void* stream);
+int opx_ulysses_head2seq(const void* o_heads, void* const* dst, int64_t ld, int sp, int rank,
+                         int rows, int S, int hq, int hd, void* stream);
+
 /* MoE routing (moe.cu): fp32 router logits with a fixed sequential K order, each
  * step one rounding of acc + h*w (the bf16 x bf16 product is exact), top-k with lower-index tie break, weights =
  * softmax renormalised over the selected experts (Qwen3 norm_topk_prob). */

@@ -495,6 +495,55 @@ int opx_rope_pack(const void* qkv, int64_t ld, void* q_full, void* k_full, void*
   OPX_CALL(k_a2a_seq2head(a, static_cast<cudaStream_t>(stream)), "opx_rope_pack");
 }
 
+int opx_ulysses_seq2head(const void* qkv, int64_t ld, void* const* q_dst, void* const* k_dst,
+                         void* const* v_dst, int sp, int rank, int rows, int S, int hq, int hk,
+                         int hd, const int32_t* pos, const float* inv_freq, void* stream) {
+  if (sp < 1 || sp > kMaxSp || rank < 0 || rank >= sp || hq % sp || hk % sp || S % sp) {
+    set_error("opx_ulysses_seq2head: bad sp/rank/head split");
+    return OPX_ERR_ARG;
+  }
+  A2AArgs a{};
+  a.sp = sp;
+  a.rank = rank;
+  a.rows = rows;
+  a.seq = S;
+  a.ngroups = 3;
+  a.g[0] = A2AGroup{hq, 0, pos ? 1 : 0, 0, {}};
+  a.g[1] = A2AGroup{hk, hq * hd, pos ? 1 : 0, 0, {}};
+  a.g[2] = A2AGroup{hk, (hq + hk) * hd, 0, 0, {}};
+  for (int j = 0; j < sp; ++j) {
+    a.g[0].full[j] = q_dst[j];
+    a.g[1].full[j] = k_dst[j];
+    a.g[2].full[j] = v_dst[j];
+  }
+  a.local[0] = const_cast<void*>(qkv);
+  a.local_ld = ld;
+  a.pos = pos;
+  a.inv_freq = inv_freq;
+  a.hd = hd;
+  OPX_CALL(k_a2a_seq2head(a, static_cast<cudaStream_t>(stream)), "opx_ulysses_seq2head");
+}
+
+int opx_ulysses_head2seq(const void* o_heads, void* const* dst, int64_t ld, int sp, int rank,
+                         int rows, int S, int hq, int hd, void* stream) {
+  if (sp < 1 || sp > kMaxSp || rank < 0 || rank >= sp || hq % sp || S % sp) {
+    set_error("opx_ulysses_head2seq: bad sp/rank/head split");
+    return OPX_ERR_ARG;
+  }
+  A2AArgs a{};
+  a.sp = sp;
+  a.rank = rank;
+  a.rows = rows;
+  a.seq = S;
+  a.ngroups = 1;
+  a.g[0].heads_total = hq;
+  a.g[0].full[0] = const_cast<void*>(o_heads);
+  for (int j = 0; j < sp; ++j) a.local[j] = dst[j];
+  a.local_ld = ld;
+  a.hd = hd;
+  OPX_CALL(k_a2a_head2seq(a, static_cast<cudaStream_t>(stream)), "opx_ulysses_head2seq");
+}
+
 int opx_moe_route(const void* h, const void* w, int T, int H, int E, int k, float* logits,
                   int32_t* idx, float* wts, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);

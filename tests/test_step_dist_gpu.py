@@ -147,6 +147,31 @@ def test_dist_moe_redispatch_path(monkeypatch):
 
 
 @gpu
+@pytest.mark.parametrize("env", [{"OPX_MOE_KEEP_X_MAX": "1"},
+                                 {"OPX_MOE_KEEP_GU_MARGIN_GB": "100000"}],
+                         ids=["mixed_kept_and_resent", "kept_x_gate_up_recomputed"])
+@pytest.mark.parametrize("overlap", [False, True])
+def test_dist_moe_partial_keep_paths(monkeypatch, env, overlap):
+    """recompute=none under memory pressure: only the top MoE layer keeps its
+    dispatch buffer (the lower one re-sends its tokens into the shared
+    buffer), or layers keep their tokens but recompute gate|up."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    from tests.step_common import tiny_moe
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    model = tiny_moe(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048, experts=64, top_k=4,
+                     expert_ffn=256)
+    plan = {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "recompute": "none",
+            "moe_overlap": overlap}
+    loss, sessions = _run(2, model, plan, 512, 2)
+    from paper_2508_02317_b200.runtime import synthetic_batch
+
+    compare_step(sessions, model, synthetic_batch(2048, 512, 2, seed=2508), plan, loss)
+
+
+@gpu
 def test_dist_c0_fsdp2_sp2_head_dim_64():
     """BASELINE C0 as specified: 2 layers, H=256, 4 heads of 64 (2 kv),
     ffn 768, V=2048, S=1024, FSDP2 x SP2 on 4 GPUs, global batch 2."""
