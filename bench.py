@@ -534,6 +534,21 @@ def main():
         m = arch["moe"]
         mlp_flops = 6.0 * T_loc * arch["hidden"] * m["expert_ffn_dim"] * m["top_k"]
     achieved = mlp_flops / node_s
+    # attention kernels (the kernels VERDICT r1 named furthest below roofline):
+    # exact causal varlen FLOPs of one layer's core on this rank's heads
+    # (4 d h sum(l^2)/2 forward, 2.5x that backward) / mean node time
+    sq_all = sum((b - a) ** 2 for cu in batch["cu_rows"][:plan["micro_batch"]] for a, b in zip(cu[:-1], cu[1:]))
+    hq_loc = arch["heads"] // plan["sp"]
+    attn_fwd_flops = 4.0 * arch["head_dim"] * hq_loc * sq_all / 2.0
+    attn = {}
+    for d_, mult in (("fwd", 1.0), ("bwd", 2.5)):
+        ts = [e["dur"] for e in trace["traceEvents"]
+              if e["name"].startswith(d_ + ".layer") and e["name"].endswith(".attn_core")]
+        if ts:
+            ach = attn_fwd_flops * mult / (statistics.mean(ts) * 1e-6)
+            attn[d_] = {"achieved": ach / 1e12, "peak": peak_sus / 1e12, "unit": "TFLOP/s",
+                        "frac": ach / peak_sus, "frac_of_burst": ach / peak,
+                        "launch_ms": statistics.mean(ts) * 1e-3, "flops_per_launch": attn_fwd_flops * mult}
     share = {}
     for e in trace["traceEvents"]:
         if e["tid"] != 0 or e["name"].endswith(".m0.moe"):  # parent span of the MoE sub-nodes
@@ -576,6 +591,7 @@ def main():
                      "note": "peak = the driver's sustained figure (cuBLAS bf16 8192^3 back to back under "
                              "the power cap); the node's tcgen05 GEMMs can exceed it (frac > 1), "
                              "frac_of_burst is against the burst figure"},
+        "roofline_attention": attn,
         "phase_share": {k: round(v / tot, 4) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:16]},
         "node_ms": {k: round(v * 1e3, 2) for k, v in sorted(share.items(), key=lambda kv: -kv[1])[:24]},
         "clocks": clk.summary(),
