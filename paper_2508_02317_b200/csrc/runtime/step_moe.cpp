@@ -405,6 +405,13 @@ GemmDesc grouped(int M, int N, int K, const bf16* A, int64_t lda, bool amn, cons
   g.d_group_stride = dstride;
   return g;
 }
+// moe_overlap: the two expert halves' GEMMs run concurrently on their two
+// streams (disjoint rows of every buffer; the ticketed GEMMs share the SMs);
+// OPX_MOE_SERIAL_HALVES=1 orders half B's GEMMs after half A's (round 1)
+bool moe_serial_halves() {
+  static const bool v = getenv("OPX_MOE_SERIAL_HALVES") && atoi(getenv("OPX_MOE_SERIAL_HALVES"));
+  return v;
+}
 }  // namespace
 
 int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* x_out) {
@@ -519,7 +526,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
     TRY(experts(0, h, cs_));
     CU(cudaEventRecord(gemm_a, cs_));
     mk("experts", "experts,a2a_combine");
-    CU(cudaStreamWaitEvent(xs2_, gemm_a, 0));
+    if (moe_serial_halves()) CU(cudaStreamWaitEvent(xs2_, gemm_a, 0));
     TRY(experts(h, El_, xs2_));
     TRY(barrier_ep3(xs2_));
     CU(cudaEventRecord(done_b, xs2_));
@@ -636,7 +643,7 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     TRY(experts_bwd(0, h, cs_));
     CU(cudaEventRecord(done_a, cs_));
     mk("experts", "experts,a2a_dispatch_grad");
-    CU(cudaStreamWaitEvent(xs2_, done_a, 0));
+    if (moe_serial_halves()) CU(cudaStreamWaitEvent(xs2_, done_a, 0));
     TRY(experts_bwd(h, El_, xs2_));
     TRY(barrier_ep3(xs2_));
     CU(cudaEventRecord(done_b, xs2_));
