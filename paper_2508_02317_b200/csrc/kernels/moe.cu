@@ -380,6 +380,30 @@ __global__ void combine_map_kernel(const int* __restrict__ counts_all, Layout L,
   off[i] = x;
 }
 
+// Combine: every valid row of local expert segment le goes back to its source
+// rank s, at s's sorted position of that pair (the combine map's tables);
+// one warp per row, 16-B stores along the row (coalesced NVLink writes)
+__global__ void combine_kernel(const bf16* __restrict__ src, int64_t ld_src,
+                               const int* __restrict__ cnt, const int* __restrict__ off, int ep,
+                               const int* __restrict__ g_start, bf16* const* __restrict__ dst,
+                               int64_t ld_dst, int W, int le_lo) {
+  const int lane = threadIdx.x & 31;
+  const int le = le_lo + blockIdx.y;
+  __shared__ int s_cnt[kMaxSp], s_off[kMaxSp];
+  if (threadIdx.x < ep) {
+    s_cnt[threadIdx.x] = cnt[le * ep + threadIdx.x];
+    s_off[threadIdx.x] = off[le * ep + threadIdx.x];
+  }
+  __syncthreads();
+  int n = 0;
+  for (int s = 0; s < ep; ++s) n += s_cnt[s];
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+    int s = 0, o = r;
+    while (o >= s_cnt[s]) o -= s_cnt[s], ++s;
+    copy_row(dst[s] + int64_t(s_off[s] + o) * ld_dst, src + int64_t(g_start[le] + r) * ld_src, W, lane);
+  }
+}
+
 // out[t] = resid[t] + sum_j w[t,j] * Y[pos(t,j)]  (fp32; one warp per token)
 __global__ void unpermute_kernel(const bf16* __restrict__ Y, int64_t ldy, const int* __restrict__ pos_of_pair,
                                  const float* __restrict__ wts, int T, int k, int H,
@@ -604,6 +628,20 @@ cudaError_t k_moe_combine_map(const int* counts_all, int ep, int E, int me, int*
   const int n = L.El * ep;
   ++g_kernel_launches;
   combine_map_kernel<<<(n + 255) / 256, 256, 0, s>>>(counts_all, L, me, cnt, off);
+  return cudaGetLastError();
+}
+
+cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* cnt, const int* off,
+                          int ep, int El, const int* g_start, __nv_bfloat16* const* dst,
+                          int64_t ld_dst, int W, int max_rows, cudaStream_t s, int le_lo, int le_n) {
+  static const int max_bx = getenv("OPX_COMBINE_BX") ? atoi(getenv("OPX_COMBINE_BX")) : 64;
+  int bx = (max_rows * 32 + 255) / 256 / El + 1;
+  if (bx > max_bx) bx = max_bx;
+  if (le_n < 0) le_n = El - le_lo;
+  if (le_n <= 0) return cudaSuccess;
+  dim3 grid(bx, le_n);
+  ++g_kernel_launches;
+  combine_kernel<<<grid, 256, 0, s>>>(src, ld_src, cnt, off, ep, g_start, dst, ld_dst, W, le_lo);
   return cudaGetLastError();
 }
 

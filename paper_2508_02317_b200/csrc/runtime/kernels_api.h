@@ -141,7 +141,13 @@ cudaError_t k_moe_dispatch(const __nv_bfloat16* src, int64_t ld_src, int per_pai
                            const int* pair_at, int P, int k, const int* counts_all,
                            const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
                            int64_t ld_dst, int W, cudaStream_t s, int le_lo = 0, int le_hi = -1);
-// [El][ep] row counts / destination offsets of the combine (GEMM_EPI_ROWMAP)
+// rows of local expert segments [le_lo, le_lo+le_n) back to their source ranks
+// (one warp per row) at the combine map's offsets
+cudaError_t k_moe_combine(const __nv_bfloat16* src, int64_t ld_src, const int* cnt, const int* off,
+                          int ep, int El, const int* g_start, __nv_bfloat16* const* dst,
+                          int64_t ld_dst, int W, int max_rows, cudaStream_t s, int le_lo = 0,
+                          int le_n = -1);
+// [El][ep] row counts / destination offsets of the combine (GEMM_EPI_ROWMAP / k_moe_combine)
 cudaError_t k_moe_combine_map(const int* counts_all, int ep, int E, int me, int* cnt, int* off,
                               cudaStream_t s);
 cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_of_pair,

@@ -408,6 +408,14 @@ GemmDesc grouped(int M, int N, int K, const bf16* A, int64_t lda, bool amn, cons
 // moe_overlap: the two expert halves' GEMMs run concurrently on their two
 // streams (disjoint rows of every buffer; the ticketed GEMMs share the SMs);
 // OPX_MOE_SERIAL_HALVES=1 orders half B's GEMMs after half A's (round 1)
+// OPX_MOE_FUSED_COMBINE=1: the combine / dX return ride in the expert GEMM
+// epilogues (GEMM_EPI_ROWMAP peer stores).  Off by default: row-per-thread
+// remote stores from the epilogue measured slower on C2/EP4 (143K vs 181K
+// tokens/s) than the warp-per-row combine kernel's coalesced 16-B stores.
+bool moe_fused_combine() {
+  static const bool v = getenv("OPX_MOE_FUSED_COMBINE") && atoi(getenv("OPX_MOE_FUSED_COMBINE"));
+  return v;
+}
 bool moe_serial_halves() {
   static const bool v = getenv("OPX_MOE_SERIAL_HALVES") && atoi(getenv("OPX_MOE_SERIAL_HALVES"));
   return v;
@@ -454,11 +462,14 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   CU(k_moe_groups(counts_all, ep_, E, ep_i_, g_start_, g_rows_, g_rows_pad_, g_total_, cs_));
   CU(k_moe_combine_map(counts_all, ep_, E, ep_i_, rm_cnt_, rm_off_, cs_));
   mk("a2a_counts");
-  // down projection of experts [lo, hi) whose epilogue stores every row
-  // straight into its token owner's combine buffer (the a2a_combine)
-  auto down_combine = [&](int lo, int n, cudaStream_t st) -> int {
+  // down projection of experts [lo, lo + n), then the a2a_combine: every row
+  // back to its token owner's combine buffer (or, fused, from the GEMM's
+  // epilogue straight away)
+  const bool fusedc = moe_fused_combine();
+  auto down = [&](int lo, int n, cudaStream_t st) -> int {
     GemmDesc g = grouped(0, H, Fe, act_e_, Fe, false, Wd + int64_t(lo) * H * Fe, Fe, false,
-                         GEMM_EPI_ROWMAP, y_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
+                         fusedc ? GEMM_EPI_ROWMAP : GEMM_EPI_BF16, y_e_, H, n, 0, g_start_ + lo,
+                         g_rows_ + lo, cap_rows_, 0);
     g.rm_dst = yback_tab_cur();
     g.rm_cnt = rm_cnt_ + int64_t(lo) * ep_;
     g.rm_off = rm_off_ + int64_t(lo) * ep_;
@@ -466,6 +477,13 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
     CU(gemm_run(g, st));
     return OPX_OK;
   };
+  auto combine = [&](int lo, int n, cudaStream_t st) -> int {
+    if (!fusedc)
+      CU(k_moe_combine(y_e_, H, rm_cnt_, rm_off_, ep_, El_, g_start_, yback_tab_cur(), H, H,
+                       int(cap_rows_), st, lo, n));
+    return OPX_OK;
+  };
+  const char* fused_tag = fusedc ? "experts,a2a_combine" : nullptr;
   // experts [lo, hi) of every rank: dispatch -> barrier -> gate|up + SwiGLU ->
   // down -> combine -> barrier, on stream st with barrier flag set `fs`
   auto phase = [&](int lo, int hi, cudaStream_t st, int fs, bool marks) -> int {
@@ -486,8 +504,10 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
       CU(gemm_run(g, st));
     }
     CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
-    TRY(down_combine(lo, n, st));
-    if (marks) mk("experts", "experts,a2a_combine");
+    TRY(down(lo, n, st));
+    if (marks) mk("experts", fused_tag);
+    TRY(combine(lo, n, st));
+    if (marks && !fusedc) mk("a2a_combine");
     TRY(fs ? barrier_ep3(st) : barrier_ep(st));
     if (marks) mk("a2a_wait");
     return OPX_OK;
@@ -521,15 +541,18 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
       g.ldd2 = Fe;
       CU(gemm_run(g, st));
       CU(k_moe_zero_pad(act_e_, Fe, Fe, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, st));
-      return down_combine(lo, n, st);
+      return down(lo, n, st);
     };
     TRY(experts(0, h, cs_));
     CU(cudaEventRecord(gemm_a, cs_));
-    mk("experts", "experts,a2a_combine");
+    mk("experts", fused_tag);
     if (moe_serial_halves()) CU(cudaStreamWaitEvent(xs2_, gemm_a, 0));
     TRY(experts(h, El_, xs2_));
+    TRY(combine(h, El_ - h, xs2_));
     TRY(barrier_ep3(xs2_));
     CU(cudaEventRecord(done_b, xs2_));
+    TRY(combine(0, h, cs_));
+    if (!fusedc) mk("a2a_combine");
     TRY(barrier_ep(cs_));
     CU(cudaStreamWaitEvent(cs_, done_b, 0));
     // the compute stream now waits for half B: its expert GEMMs, combine and barrier
@@ -589,6 +612,13 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     mk("gate_up_recompute");
   }
   CU(k_moe_combine_map(counts_all, ep_, E, ep_i_, rm_cnt_, rm_off_, cs_));
+  const bool fusedc = moe_fused_combine();
+  auto dx_return = [&](int lo, int n, cudaStream_t st) -> int {
+    if (!fusedc)
+      CU(k_moe_combine(dx_e_, H, rm_cnt_, rm_off_, ep_, El_, g_start_, d_dxback_peers_, H, H,
+                       int(cap_rows_), st, lo, n));
+    return OPX_OK;
+  };
   // weighted combine backward: per-pair output grads and router-weight grads
   CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
   // a2a_combine_grad: pair grads travel to the expert ranks (same layout as dispatch)
@@ -610,9 +640,10 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     CU(k_moe_swiglu_bwd(dact_e_, gu_e_, dgu_e_, g_start_ + lo, g_rows_ + lo, g_rows_pad_ + lo, n, Fe,
                         int(cap_rows_), st));
     {
-      // dX rows go straight back to their token owners (the a2a_dispatch_grad)
+      // dX rows (fused: straight from the epilogue) back to their token owners
       GemmDesc g = grouped(0, H, 2 * Fe, dgu_e_, 2 * Fe, false, Wgu + lo * gs_gu, H, true,
-                           GEMM_EPI_ROWMAP, dx_e_, H, n, 0, g_start_ + lo, g_rows_ + lo, cap_rows_, 0);
+                           fusedc ? GEMM_EPI_ROWMAP : GEMM_EPI_BF16, dx_e_, H, n, 0, g_start_ + lo,
+                           g_rows_ + lo, cap_rows_, 0);
       g.rm_dst = d_dxback_peers_;
       g.rm_cnt = rm_cnt_ + int64_t(lo) * ep_;
       g.rm_off = rm_off_ + int64_t(lo) * ep_;
@@ -642,11 +673,14 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     mk("a2a_wait");
     TRY(experts_bwd(0, h, cs_));
     CU(cudaEventRecord(done_a, cs_));
-    mk("experts", "experts,a2a_dispatch_grad");
+    mk("experts", fusedc ? "experts,a2a_dispatch_grad" : nullptr);
     if (moe_serial_halves()) CU(cudaStreamWaitEvent(xs2_, done_a, 0));
     TRY(experts_bwd(h, El_, xs2_));
+    TRY(dx_return(h, El_ - h, xs2_));
     TRY(barrier_ep3(xs2_));
     CU(cudaEventRecord(done_b, xs2_));
+    TRY(dx_return(0, h, cs_));
+    if (!fusedc) mk("a2a_dispatch_grad");
     TRY(barrier_ep(cs_));
     CU(cudaStreamWaitEvent(cs_, done_b, 0));
     mk("experts_b");  // half B's expert backward, dX combine and barrier
@@ -656,10 +690,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     mk("a2a_combine_grad");
     TRY(barrier_ep(cs_));
     mk("a2a_wait");
-    // a2a_dispatch_grad: input grads travel back to the token owners from
-    // the dgrad epilogue
+    // a2a_dispatch_grad: input grads travel back to the token owners
     TRY(experts_bwd(0, El_, cs_));
-    mk("experts", "experts,a2a_dispatch_grad");
+    mk("experts", fusedc ? "experts,a2a_dispatch_grad" : nullptr);
+    TRY(dx_return(0, El_, cs_));
+    if (!fusedc) mk("a2a_dispatch_grad");
     TRY(barrier_ep(cs_));
     mk("a2a_wait");
   }

@@ -157,3 +157,66 @@ def test_step_async_ulysses_fused_epilogue_matches_kernel_path():
     for n, g in out[False][1].items():
         d = np.abs(out[True][1][n] - g).max() / max(np.abs(g).max(), 1e-30)
         assert d < 1e-3, (n, d)
+
+
+def _batch_from_lengths(vocab, rows_lengths, seed=11):
+    """Global batch from explicit per-row sample lengths (each row sums to S)."""
+    rng = np.random.default_rng(seed)
+    S = sum(rows_lengths[0])
+    R = len(rows_lengths)
+    ids = rng.integers(0, vocab, size=(R, S)).astype(np.int32)
+    labels = np.full((R, S), -100, np.int32)
+    pos = np.zeros((R, S), np.int32)
+    cu_rows = []
+    for r, lens in enumerate(rows_lengths):
+        assert sum(lens) == S
+        cu = [0]
+        for l in lens:
+            a = cu[-1]
+            pos[r, a:a + l] = np.arange(l)
+            labels[r, a:a + l - 1] = ids[r, a + 1:a + l]
+            cu.append(a + l)
+        cu_rows.append(cu)
+    return {"ids": ids, "labels": labels, "pos": pos, "cu_rows": cu_rows}
+
+
+@gpu
+def test_step_extreme_varlen_packing():
+    """cu_seqlens edge cases (packing.hpp:20-31): 1-token samples (no
+    supervised token), samples straddling the 64-query / 128-key tile edges,
+    a row that is one full-length sample, and a row of many tiny samples."""
+    from paper_2508_02317_b200.runtime import Session
+
+    model = tiny_dense(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048)
+    lens = [[1, 1, 2, 63, 64, 65, 127, 128, 129, 1, 443],
+            [1024],
+            [3] * 300 + [124]]
+    batch = _batch_from_lengths(2048, lens)
+    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": 3, "recompute": "none"}
+    wl = {"seq_len": 1024, "micro_batch": 3, "global_batch": 3}
+    s = Session(cluster(1), model, wl, plan, EXEC, rank=0, device=0)
+    s.init_weights(EXEC["seed"])
+    s.load(batch)
+    r = s.run()
+    compare_step([s], model, batch, plan, r.loss)
+    s.close()
+
+
+@gpu
+def test_step_rejects_bad_cu_seqlens():
+    """The ABI refuses malformed cu_seqlens with the argument error code."""
+    from paper_2508_02317_b200 import OpxError
+    from paper_2508_02317_b200.runtime import Session
+
+    model = tiny_dense(layers=1)
+    plan = {"dp_replicate": 1, "dp_shard": 1, "sp": 1, "ep": 1, "micro_batch": 1}
+    wl = {"seq_len": 512, "micro_batch": 1, "global_batch": 1}
+    s = Session(cluster(1), model, wl, plan, EXEC, rank=0, device=0)
+    good = _batch_from_lengths(2048, [[200, 312]])
+    for cu in ([0, 300, 300, 512], [0, 200, 511], [1, 200, 512]):
+        bad = dict(good)
+        bad["cu_rows"] = [cu]
+        with pytest.raises(OpxError) as ei:
+            s.load(bad)
+        assert ei.value.code == 9
+    s.close()
