@@ -96,6 +96,9 @@ Step::~Step() {
     if (e) cudaEventDestroy(e);
   for (auto e : ev_mb_)
     if (e) cudaEventDestroy(e);
+  for (auto* v : {&enc_.ev_ag, &enc_.ev_use})
+    for (auto e : *v)
+      if (e) cudaEventDestroy(e);
   if (expert_comm_) ncclCommDestroy(expert_comm_);
   if (rep_comm_) ncclCommDestroy(rep_comm_);
   if (shard_comm_) ncclCommDestroy(shard_comm_);

@@ -296,12 +296,20 @@ class Step {
     bool on = false;
     std::string name;
     int He = 0, L = 0, heads = 0, d = 0, F = 0, pd = 0, tpi = 0;
-    bf16* w = nullptr;  // every weight and bias, 128-element aligned offsets
-    int64_t o_patch = 0, o_lnq = 0, o_m0 = 0, o_m0b = 0, o_m2 = 0, o_m2b = 0, numel = 0;
-    // per block (kBlk entries): norm1 | qkv | qkv bias | proj | proj bias | norm2 |
-    // gate_up | gate_up bias (128-interleaved like the weight) | down | down bias
+    // FSDP units of the frozen module (plan.cpp:95-107 shards every module):
+    // [0] patch embed, [1 + i] block i (params: norm1 | qkv | qkv bias | proj |
+    // proj bias | norm2 | gate_up | gate_up bias (128-interleaved like the
+    // weight) | down | down bias), [L + 1] merger (ln_q | mlp.0 | bias | mlp.2 |
+    // bias).  Each rank keeps its bf16 shard only (no optimizer state); the
+    // forward all-gathers unit i + 2 into slot i % 2 while unit i computes.
     static constexpr int kBlk = 10;
-    std::vector<int64_t> o_blk;
+    std::vector<Unit> units;
+    bf16* slot[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_ag, ev_use;
+    const bf16* wp(int unit, int param) const {
+      const Unit& u = units[size_t(unit)];
+      return u.full + u.params[size_t(param)].off;
+    }
     // Qwen2.5-VL geometry: g x g patches per item, windows of window_merge^2
     // merge units, full-attention blocks, 2-D RoPE (sin, cos) per patch of an
     // item in window order [P][d/2]

@@ -26,8 +26,10 @@
 // pass).  After an SP barrier every rank overwrites its placeholder
 // embeddings with the received rows; the backward zeroes their gradient rows
 // before the embedding scatter-add (the features are frozen).  The frozen
-// weights are replicated, not FSDP-sharded (no gradient or optimizer state;
-// sharding would trade ~1.3 GB at the 7B ViT for a per-step all-gather).
+// weights are FSDP-sharded like every module (plan.cpp:95-107): each rank
+// keeps a bf16 shard of every unit (patch embed, each block, the merger; no
+// gradient or optimizer state) and the forward all-gathers unit i + 2 into a
+// double-buffered slot on the comm stream while unit i computes.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -43,6 +45,7 @@ namespace opx {
     if (rc_ != OPX_OK) return rc_; \
   } while (0)
 #define CU(x) TRY(check((x), #x))
+#define NC(x) TRY(nccl((x), #x))
 
 namespace {
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -127,37 +130,78 @@ int Step::enc_setup() {
       }
   }
   const int64_t He = e.He, Wq = int64_t(e.heads) * e.d, F = e.F;
-  auto take = [&](int64_t n) {
-    const int64_t o = e.numel;
-    e.numel += round_up(n, 128);
-    return o;
+  // units and their params (HF names; init keys), sharded like the backbone's
+  auto add = [](Unit& u, const std::string& name, int64_t n, bool ones, int interleave = 0,
+                const std::string& kb = "", int64_t rows = 0, int64_t cols = 0) {
+    Param q;
+    q.name = q.key_a = name;
+    q.key_b = kb;
+    q.numel = n;
+    q.shape = {n};
+    q.off = u.numel;
+    q.ones = ones;
+    q.interleave = interleave;
+    q.rows_per_slab = rows;
+    q.cols = cols;
+    u.numel += round_up(n, 128);
+    u.params.push_back(q);
   };
-  e.o_patch = take(He * e.pd);
+  const std::string V = "visual.";
+  e.units.assign(size_t(e.L) + 2, Unit{});
+  add(e.units[0], V + "patch_embed.proj.weight", He * e.pd, false);
   for (int i = 0; i < e.L; ++i) {
-    e.o_blk.push_back(take(He));          // norm1
-    e.o_blk.push_back(take(3 * Wq * He)); // qkv
-    e.o_blk.push_back(take(3 * Wq));      // qkv bias
-    e.o_blk.push_back(take(He * Wq));     // proj
-    e.o_blk.push_back(take(He));          // proj bias
-    e.o_blk.push_back(take(He));          // norm2
-    e.o_blk.push_back(take(2 * F * He));  // gate|up (128-row interleave)
-    e.o_blk.push_back(take(2 * F));       // gate|up bias (same interleave)
-    e.o_blk.push_back(take(He * F));      // down
-    e.o_blk.push_back(take(He));          // down bias
+    Unit& u = e.units[size_t(1 + i)];
+    const std::string p = V + "blocks." + std::to_string(i) + ".";
+    add(u, p + "norm1.weight", He, true);
+    add(u, p + "attn.qkv.weight", 3 * Wq * He, false);
+    add(u, p + "attn.qkv.bias", 3 * Wq, false);
+    add(u, p + "attn.proj.weight", He * Wq, false);
+    add(u, p + "attn.proj.bias", He, false);
+    add(u, p + "norm2.weight", He, true);
+    add(u, p + "mlp.gate_proj.weight", 2 * F * He, false, 1, p + "mlp.up_proj.weight", 2 * F, He);
+    add(u, p + "mlp.gate_proj.bias", 2 * F, false, 1, p + "mlp.up_proj.bias", 2 * F, 1);
+    add(u, p + "mlp.down_proj.weight", He * F, false);
+    add(u, p + "mlp.down_proj.bias", He, false);
   }
-  e.o_lnq = take(He);
-  e.o_m0 = take(16 * He * He);
-  e.o_m0b = take(4 * He);
-  e.o_m2 = take(int64_t(H_) * 4 * He);
-  e.o_m2b = take(H_);
-  e.w = alloc<bf16>(size_t(e.numel));
+  {
+    Unit& u = e.units.back();
+    add(u, V + "merger.ln_q.weight", He, true);
+    add(u, V + "merger.mlp.0.weight", 16 * He * He, false);
+    add(u, V + "merger.mlp.0.bias", 4 * He, false);
+    add(u, V + "merger.mlp.2.weight", int64_t(H_) * 4 * He, false);
+    add(u, V + "merger.mlp.2.bias", H_, false);
+  }
+  const int nsh = int(p_.shard_degree());
+  const int my = shard_i_ * int(p_.sp) + sp_i_;
+  int64_t mx = 0;
+  for (Unit& u : e.units) {
+    u.name = "encoder";
+    u.P = nsh;
+    u.idx = my;
+    u.comm = shard_comm_;
+    u.padded = round_up(u.numel, 64 * int64_t(nsh));
+    u.shard = u.padded / nsh;
+    u.pshard = alloc<bf16>(size_t(u.shard));
+    if (!u.pshard) return cuda_fail(cudaErrorMemoryAllocation, "encoder weight shards");
+    if (nsh == 1) u.full = u.pshard;
+    mx = std::max(mx, u.padded);
+  }
+  if (nsh > 1) {
+    for (auto& sl : e.slot)
+      if (!(sl = alloc<bf16>(size_t(mx), false)))
+        return cuda_fail(cudaErrorMemoryAllocation, "encoder gather slots");
+    e.ev_ag.resize(e.units.size());
+    e.ev_use.resize(e.units.size());
+    for (auto* v : {&e.ev_ag, &e.ev_use})
+      for (auto& ev : *v) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
   d_fmask_ = alloc<int>(size_t(T_));
   // 2-D RoPE table of one item's patches in window order: pair (j, j + d/2)
   // turns by hpos * inv[j] (j < d/4) or wpos * inv[j - d/4] (rot_pos_emb,
   // apply_rotary_pos_emb_vision); sin/cos of the fp32 angle in double
   const int P = 4 * e.tpi, hd2 = e.d / 2, hd4 = e.d / 4;
   e.rope = alloc<float2>(size_t(P) * hd2, false);
-  if (!e.w || !d_fmask_ || !e.rope) return cuda_fail(cudaErrorMemoryAllocation, "encoder weights");
+  if (!d_fmask_ || !e.rope) return cuda_fail(cudaErrorMemoryAllocation, "encoder buffers");
   std::vector<float> inv(static_cast<size_t>(hd4));
   for (int i = 0; i < hd4; ++i)
     inv[size_t(i)] = float(1.0 / std::pow(e.rope_theta, double(2 * i) / double(hd2)));
@@ -177,39 +221,21 @@ int Step::enc_setup() {
 
 int Step::enc_init_weights(uint64_t seed) {
   if (!enc_.on) return OPX_OK;
-  Enc& e = enc_;
+  // each rank fills its shard of every unit (same counter-based init as the
+  // backbone: values depend on (name, logical index) only, oracle/encoder.py)
   const double c = 0.02 * std::sqrt(3.0) / 16777216.0;
-  const int64_t He = e.He, Wq = int64_t(e.heads) * e.d, F = e.F;
-  auto normal = [&](int64_t off, int64_t n, const std::string& name) -> int {
-    CU(k_init_param(nullptr, e.w + off, n, 0, param_key(name, seed), 0, c, 1.f, 0, 0, 0, cs_));
-    return OPX_OK;
-  };
-  auto ones = [&](int64_t off, int64_t n) -> int {
-    CU(k_init_param(nullptr, e.w + off, n, 0, 0, 0, 0.0, 1.f, 0, 0, 0, cs_));
-    return OPX_OK;
-  };
-  TRY(normal(e.o_patch, He * e.pd, "visual.patch_embed.proj.weight"));
-  for (int i = 0; i < e.L; ++i) {
-    const std::string p = "visual.blocks." + std::to_string(i) + ".";
-    const int64_t* o = &e.o_blk[size_t(i) * Enc::kBlk];
-    TRY(ones(o[0], He));
-    TRY(normal(o[1], 3 * Wq * He, p + "attn.qkv.weight"));
-    TRY(normal(o[2], 3 * Wq, p + "attn.qkv.bias"));
-    TRY(normal(o[3], He * Wq, p + "attn.proj.weight"));
-    TRY(normal(o[4], He, p + "attn.proj.bias"));
-    TRY(ones(o[5], He));
-    CU(k_init_param(nullptr, e.w + o[6], 2 * F * He, 0, param_key(p + "mlp.gate_proj.weight", seed),
-                    param_key(p + "mlp.up_proj.weight", seed), c, 1.f, 1, 2 * F, He, cs_));
-    CU(k_init_param(nullptr, e.w + o[7], 2 * F, 0, param_key(p + "mlp.gate_proj.bias", seed),
-                    param_key(p + "mlp.up_proj.bias", seed), c, 1.f, 1, 2 * F, 1, cs_));
-    TRY(normal(o[8], He * F, p + "mlp.down_proj.weight"));
-    TRY(normal(o[9], He, p + "mlp.down_proj.bias"));
+  for (Unit& u : enc_.units) {
+    const int64_t sb = int64_t(u.idx) * u.shard, se = sb + u.shard;
+    CU(cudaMemsetAsync(u.pshard, 0, size_t(u.shard) * 2, cs_));
+    for (const Param& q : u.params) {
+      const int64_t lo = std::max(sb, q.off), hi = std::min(se, q.off + q.numel);
+      if (hi <= lo) continue;
+      const uint64_t ka = param_key(q.key_a, seed);
+      const uint64_t kb = q.key_b.empty() ? 0 : param_key(q.key_b, seed);
+      CU(k_init_param(nullptr, u.pshard + (lo - sb), hi - lo, lo - q.off, ka, kb, q.ones ? 0.0 : c,
+                      1.0f, q.interleave, q.rows_per_slab, q.cols, cs_));
+    }
   }
-  TRY(ones(e.o_lnq, He));
-  TRY(normal(e.o_m0, 16 * He * He, "visual.merger.mlp.0.weight"));
-  TRY(normal(e.o_m0b, 4 * He, "visual.merger.mlp.0.bias"));
-  TRY(normal(e.o_m2, int64_t(H_) * 4 * He, "visual.merger.mlp.2.weight"));
-  TRY(normal(e.o_m2b, H_, "visual.merger.mlp.2.bias"));
   return OPX_OK;
 }
 
@@ -315,20 +341,58 @@ int Step::load_images(const uint16_t* pixels, int n, const int32_t* row, const i
 
 int Step::enc_forward() {
   Enc& e = enc_;
-  if (!e.on || e.n_all == 0) return OPX_OK;
+  if (!e.on) return OPX_OK;
   const bool tr = ex_.trace;
   cudaEvent_t e0 = tr ? ev() : nullptr, e1 = nullptr;
   if (tr) cudaEventRecord(e0, cs_);
   const int Np = e.n_loc * 4 * e.tpi, He = e.He, Wq = e.heads * e.d, F = e.F, nf = e.n_loc * e.tpi;
   const int64_t ldh = int64_t(e.heads) * 128;  // 128-padded head layout
-  if (Np > 0) {
-    CU(gemm_run(egd(Np, He, e.pd, e.pix, e.pd, e.w + e.o_patch, e.pd, GEMM_EPI_F32, e.x, He), cs_));
-    for (int i = 0; i < e.L; ++i) {
-      const int64_t* o = &e.o_blk[size_t(i) * Enc::kBlk];
-      CU(k_rmsnorm_fwd(e.x, e.w + o[0], e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
+  const int U = int(e.units.size());
+  const bool sharded = e.units[0].P > 1;
+  // FSDP: the unit gathers are collectives of the shard group, so every rank
+  // runs them whether or not it encodes items this step (one unit ahead)
+  auto gather = [&](int i) -> int {
+    Unit& u = e.units[size_t(i)];
+    u.full = e.slot[i % 2];
+    if (i >= 2) CU(cudaStreamWaitEvent(ms_, e.ev_use[size_t(i - 2)], 0));
+    cudaEvent_t a = tr ? ev() : nullptr;
+    if (tr) cudaEventRecord(a, ms_);
+    NC(ncclAllGather(u.pshard, u.full, size_t(u.shard), ncclBfloat16, u.comm, ms_));
+    CU(cudaEventRecord(e.ev_ag[size_t(i)], ms_));
+    if (tr) mark("fwd.ag.encoder." + e.name + ".u" + std::to_string(i) + mtag(), "encoder", 1, a,
+                 e.ev_ag[size_t(i)]);
+    return OPX_OK;
+  };
+  auto use = [&](int i) -> int {  // unit i's weights are needed on cs_ from here
+    if (!sharded) return OPX_OK;
+    CU(cudaStreamWaitEvent(cs_, e.ev_ag[size_t(i)], 0));
+    return OPX_OK;
+  };
+  auto done = [&](int i) -> int {  // unit i's compute is enqueued: its slot can be refilled
+    if (!sharded) return OPX_OK;
+    CU(cudaEventRecord(e.ev_use[size_t(i)], cs_));
+    if (i + 2 < U) TRY(gather(i + 2));
+    return OPX_OK;
+  };
+  if (sharded) {
+    CU(cudaEventRecord(e.ev_use[0], cs_));  // the slots' previous readers (last step) are done
+    CU(cudaStreamWaitEvent(ms_, e.ev_use[0], 0));
+    TRY(gather(0));
+    if (U > 1) TRY(gather(1));
+  }
+  const bool run = Np > 0;
+  TRY(use(0));
+  if (run)
+    CU(gemm_run(egd(Np, He, e.pd, e.pix, e.pd, e.wp(0, 0), e.pd, GEMM_EPI_F32, e.x, He), cs_));
+  TRY(done(0));
+  for (int i = 0; i < e.L; ++i) {
+    const int ui = 1 + i;
+    TRY(use(ui));
+    if (run) {
+      CU(k_rmsnorm_fwd(e.x, e.wp(ui, 0), e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
       {
-        GemmDesc g = egd(Np, 3 * Wq, He, e.h, He, e.w + o[1], He, GEMM_EPI_BF16, e.qkv, 3 * Wq);
-        g.bias = e.w + o[2];
+        GemmDesc g = egd(Np, 3 * Wq, He, e.h, He, e.wp(ui, 1), He, GEMM_EPI_BF16, e.qkv, 3 * Wq);
+        g.bias = e.wp(ui, 2);
         CU(gemm_run(g, cs_));
       }
       {
@@ -391,43 +455,50 @@ int Step::enc_forward() {
         ldo2 = Wq;
       }
       {
-        GemmDesc g = egd(Np, He, Wq, o2, ldo2, e.w + o[3], Wq, GEMM_EPI_F32_RESID, e.x, He);
+        GemmDesc g = egd(Np, He, Wq, o2, ldo2, e.wp(ui, 3), Wq, GEMM_EPI_F32_RESID, e.x, He);
         g.R = e.x;
         g.ldr = He;
-        g.bias = e.w + o[4];
+        g.bias = e.wp(ui, 4);
         CU(gemm_run(g, cs_));
       }
-      CU(k_rmsnorm_fwd(e.x, e.w + o[5], e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
+      CU(k_rmsnorm_fwd(e.x, e.wp(ui, 5), e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
       {
-        GemmDesc g = egd(Np, 2 * F, He, e.h, He, e.w + o[6], He, GEMM_EPI_SWIGLU, nullptr, 2 * F);
+        GemmDesc g = egd(Np, 2 * F, He, e.h, He, e.wp(ui, 6), He, GEMM_EPI_SWIGLU, nullptr, 2 * F);
         g.D2 = e.act;
         g.ldd2 = F;
-        g.bias = e.w + o[7];
+        g.bias = e.wp(ui, 7);
         CU(gemm_run(g, cs_));
       }
       {
-        GemmDesc g = egd(Np, He, F, e.act, F, e.w + o[8], F, GEMM_EPI_F32_RESID, e.x, He);
+        GemmDesc g = egd(Np, He, F, e.act, F, e.wp(ui, 8), F, GEMM_EPI_F32_RESID, e.x, He);
         g.R = e.x;
         g.ldr = He;
-        g.bias = e.w + o[9];
+        g.bias = e.wp(ui, 9);
         CU(gemm_run(g, cs_));
       }
     }
-    // merger: rmsnorm_q, 2x2 merge (4 consecutive patches = one [4 He] row), MLP with GELU
-    CU(k_rmsnorm_fwd(e.x, e.w + e.o_lnq, e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
+    TRY(done(ui));
+  }
+  // merger: rmsnorm_q, 2x2 merge (4 consecutive patches = one [4 He] row), MLP with GELU
+  const int um = U - 1;
+  TRY(use(um));
+  if (run) {
+    CU(k_rmsnorm_fwd(e.x, e.wp(um, 0), e.h, e.rstd, Np, He, ex_.rms_eps, cs_));
     {
-      GemmDesc g = egd(Np / 4, 4 * He, 4 * He, e.h, 4 * He, e.w + e.o_m0, 4 * He, GEMM_EPI_BF16, e.y1,
+      GemmDesc g = egd(Np / 4, 4 * He, 4 * He, e.h, 4 * He, e.wp(um, 1), 4 * He, GEMM_EPI_BF16, e.y1,
                        4 * He);
-      g.bias = e.w + e.o_m0b;
+      g.bias = e.wp(um, 2);
       CU(gemm_run(g, cs_));
     }
     CU(k_gelu_bf16(e.y1, int64_t(Np / 4) * 4 * He, cs_));
     {
-      GemmDesc g = egd(nf, H_, 4 * He, e.y1, 4 * He, e.w + e.o_m2, 4 * He, GEMM_EPI_BF16, e.feat, H_);
-      g.bias = e.w + e.o_m2b;
+      GemmDesc g = egd(nf, H_, 4 * He, e.y1, 4 * He, e.wp(um, 3), 4 * He, GEMM_EPI_BF16, e.feat, H_);
+      g.bias = e.wp(um, 4);
       CU(gemm_run(g, cs_));
     }
   }
+  TRY(done(um));
+  if (e.n_all == 0) return OPX_OK;  // no image in this SP group's rows: no scatter
   if (tr) {
     e1 = ev();
     cudaEventRecord(e1, cs_);

@@ -114,3 +114,30 @@ def test_rank_coords_match_cpp_mesh():
             assert [x for x in g["sp"] if r in x][0][pi] == r
             assert [x for x in g["replicate"] if r in x][0][ri] == r
             assert [x for x in g["shard"] if r in x][0][si * sp + pi] == r
+
+
+def test_accumulation_partition_covers_the_batch():
+    """global_batch = k * dp_width * micro_batch (step_graph.cpp:57): dp rank r
+    feeds rows [r*k*m, (r+1)*k*m) as k micro-batches, SP ranks split tokens;
+    together the ranks cover every token once, and the oracle's simulated
+    micro-batches walk the same rows in the same order."""
+    from paper_2508_02317_b200.runtime import accum_steps
+
+    b = synthetic_batch(997, 256, 8, seed=4)
+    plan = {"dp_replicate": 2, "dp_shard": 1, "sp": 2, "micro_batch": 2}
+    assert accum_steps(b, plan) == 2
+    seen = np.zeros((8, 256), int)
+    for r in range(4):
+        ids, labels, pos, cu, nv = local_slice(b, r, plan)
+        rep, sh, spi = rank_coords(r, plan)
+        dp = rep * plan["dp_shard"] + sh
+        rows = slice(dp * 4, (dp + 1) * 4)
+        assert np.array_equal(ids.reshape(4, 128), b["ids"][rows, spi * 128:(spi + 1) * 128])
+        assert cu[-1] == 4 * 256 and len(pos) == 4 * 256  # all k*m rows' positions / boundaries
+        seen[rows, spi * 128:(spi + 1) * 128] += 1
+    assert (seen == 1).all()
+    try:
+        accum_steps(synthetic_batch(997, 256, 6, seed=4), plan)
+        raise AssertionError("6 rows with dp_width*m = 4 must be rejected")
+    except ValueError:
+        pass
