@@ -115,6 +115,15 @@ def mlp_traffic(cfg: str, T_loc: int):
     return t["mlp_node_dram_bytes"] * T_loc / t["tokens"]
 
 
+def node_key(name: str) -> str:
+    """Trace node name -> its kind summed over layers and micro-batches:
+    fwd.layer3.m0.qkv_proj -> fwd.qkv_proj, bwd.head.m1 -> bwd.head."""
+    import re
+
+    n = re.sub(r"\.m\d+(?=\.|$)", "", name)
+    return re.sub(r"^(fwd|bwd)\.layer\d+\.", r"\1.", n)
+
+
 def nvlink_rates(trace, plan, arch, S):
     """Achieved per-GPU NVLink bytes/s of the all-to-all kernels (bytes that
     leave the rank, (P-1)/P of the payload, comm.cpp:8-22) over their traced
@@ -551,10 +560,9 @@ def main():
                         "launch_ms": statistics.mean(ts) * 1e-3, "flops_per_launch": attn_fwd_flops * mult}
     share = {}
     for e in trace["traceEvents"]:
-        if e["tid"] != 0 or e["name"].endswith(".m0.moe"):  # parent span of the MoE sub-nodes
+        if e["tid"] != 0 or node_key(e["name"]) in ("fwd.moe", "bwd.moe"):  # parent span of the MoE sub-nodes
             continue
-        key = e["name"].split(".m0.")[-1] if ".m0." in e["name"] else e["name"]
-        key = ("bwd." if e["name"].startswith("bwd") else "fwd." if e["name"].startswith("fwd.layer") else "") + key
+        key = node_key(e["name"])
         share[key] = share.get(key, 0.0) + e["dur"] * 1e-6
     tot = sum(share.values()) or 1.0
     line = {

@@ -36,7 +36,12 @@ constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BNC * BK * 2;  // 16 KB
 constexpr int QD = 4;                    // tile-id ring depth
 constexpr int Q_CONSUMERS = 1 + 1 + 4 + 4;  // peer producer, MMA, 2 x 4 epilogue warps
-constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+// fp32 epilogue staging: per epilogue warp a [32 rows][36] fp32 block, so the
+// fp32 stores / residual loads go out row-contiguous (4 rows x 128 B per warp
+// instruction) instead of one 16-B piece of 32 different rows
+constexpr int EPI_LD = 36;
+constexpr int OFF_EPI = STAGES * (A_BYTES + B_BYTES) + 512;
+constexpr int SMEM = OFF_EPI + 4 * 32 * EPI_LD * 4 + 1024;
 constexpr int THREADS = 256;
 
 struct P2 {
@@ -420,6 +425,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
             }
           }
+        }
+      } else if (p.epi == GEMM_EPI_F32 || p.epi == GEMM_EPI_F32_RESID || p.epi == GEMM_EPI_F32_ACCUM) {
+        float* stg = reinterpret_cast<float*>(smem + OFF_EPI) + ew * 32 * EPI_LD;
+        const int rbase = row0 + int(rank) * BM + ew * 32;  // this warp's first row
+#pragma unroll 1
+        for (int ch = 0; ch < BNP / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + ch * 32, v);
+          ptx::tmem_wait_ld();
+          const int col0 = nb * BNP + ch * 32;
+          if (col0 >= p.N) continue;  // warp-uniform
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.scale;
+          if (p.bias) epi::add_bias32(f, p.bias + col0);
+          // this thread's row into the staging block ...
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(stg + lane * EPI_LD + 4 * q) =
+                make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+          __syncwarp();
+          // ... and out four rows per instruction (8 lanes x 16 B per row)
+          const int c4 = (lane & 7) * 4, col = col0 + c4;
+#pragma unroll 2
+          for (int it = 0; it < 8; ++it) {
+            const int rr = it * 4 + (lane >> 3), r = rbase + rr;
+            const bool ok = (p.groups ? (r - p.g_start[g]) < p.g_rows[g] : r < p.M) && col < p.N;
+            if (!ok) continue;
+            float4 o = *reinterpret_cast<const float4*>(stg + rr * EPI_LD + c4);
+            float* d = reinterpret_cast<float*>(p.D) + int64_t(r) * p.ldd + col;
+            const float* rp = p.epi == GEMM_EPI_F32_RESID ? p.R + int64_t(r) * p.ldr + col
+                              : p.epi == GEMM_EPI_F32_ACCUM ? d
+                                                            : nullptr;
+            if (rp) {
+              const float4 rv = *reinterpret_cast<const float4*>(rp);
+              o.x += rv.x;
+              o.y += rv.y;
+              o.z += rv.z;
+              o.w += rv.w;
+            }
+            *reinterpret_cast<float4*>(d) = o;
+          }
+          __syncwarp();
         }
       } else {
 #pragma unroll 1

@@ -213,10 +213,19 @@ def test_step_rejects_bad_cu_seqlens():
     wl = {"seq_len": 512, "micro_batch": 1, "global_batch": 1}
     s = Session(cluster(1), model, wl, plan, EXEC, rank=0, device=0)
     good = _batch_from_lengths(2048, [[200, 312]])
-    for cu in ([0, 300, 300, 512], [0, 200, 511], [1, 200, 512]):
+    for cu in ([0, 300, 300, 512], [0, 200, 511]):
         bad = dict(good)
         bad["cu_rows"] = [cu]
         with pytest.raises(OpxError) as ei:
             s.load(bad)
         assert ei.value.code == 9
+    # straight through the C ABI: cu_seqlens must start at 0
+    import ctypes
+
+    from paper_2508_02317_b200 import lib
+
+    ids = np.zeros(512, np.int32)
+    cu = np.array([1, 200, 512], np.int32)
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    assert lib().opx_step_load_batch(s.h, vp(ids), vp(ids), vp(ids), vp(cu), 3, 10) == 9
     s.close()
