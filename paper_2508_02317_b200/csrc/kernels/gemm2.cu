@@ -436,6 +436,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           ptx::tmem_wait_ld();
           const int col0 = nb * BNP + ch * 32;
           if (col0 >= p.N) continue;  // warp-uniform
+          // the residual / accumulated values this lane adds (4 rows x 128 B
+          // per warp instruction), all 8 loads in flight before the staging
+          const int c4 = (lane & 7) * 4, col = col0 + c4;
+          float4 rv[8];
+          bool okr[8];
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = rbase + it * 4 + (lane >> 3);
+            okr[it] = (p.groups ? (r - p.g_start[g]) < p.g_rows[g] : r < p.M) && col < p.N;
+            rv[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (okr[it] && p.epi != GEMM_EPI_F32)
+              rv[it] = *reinterpret_cast<const float4*>(
+                  p.epi == GEMM_EPI_F32_RESID ? p.R + int64_t(r) * p.ldr + col
+                                              : reinterpret_cast<const float*>(p.D) + int64_t(r) * p.ldd + col);
+          }
           float f[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.scale;
@@ -447,25 +462,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
           __syncwarp();
           // ... and out four rows per instruction (8 lanes x 16 B per row)
-          const int c4 = (lane & 7) * 4, col = col0 + c4;
-#pragma unroll 2
+#pragma unroll
           for (int it = 0; it < 8; ++it) {
-            const int rr = it * 4 + (lane >> 3), r = rbase + rr;
-            const bool ok = (p.groups ? (r - p.g_start[g]) < p.g_rows[g] : r < p.M) && col < p.N;
-            if (!ok) continue;
+            if (!okr[it]) continue;
+            const int rr = it * 4 + (lane >> 3);
             float4 o = *reinterpret_cast<const float4*>(stg + rr * EPI_LD + c4);
-            float* d = reinterpret_cast<float*>(p.D) + int64_t(r) * p.ldd + col;
-            const float* rp = p.epi == GEMM_EPI_F32_RESID ? p.R + int64_t(r) * p.ldr + col
-                              : p.epi == GEMM_EPI_F32_ACCUM ? d
-                                                            : nullptr;
-            if (rp) {
-              const float4 rv = *reinterpret_cast<const float4*>(rp);
-              o.x += rv.x;
-              o.y += rv.y;
-              o.z += rv.z;
-              o.w += rv.w;
-            }
-            *reinterpret_cast<float4*>(d) = o;
+            o.x += rv[it].x;
+            o.y += rv[it].y;
+            o.z += rv[it].z;
+            o.w += rv[it].w;
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.D) + int64_t(rbase + rr) * p.ldd + col) = o;
           }
           __syncwarp();
         }
