@@ -65,6 +65,7 @@ struct P2 {
   const int* g_rows;
   A2AArgs s2h;  // GEMM_EPI_SEQ2HEAD
   const __nv_bfloat16* bias;  // optional column bias
+  int staged;                 // fp32 epilogues through the per-warp smem stage
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -426,7 +427,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
           }
         }
-      } else if (p.epi == GEMM_EPI_F32 || p.epi == GEMM_EPI_F32_RESID || p.epi == GEMM_EPI_F32_ACCUM) {
+      } else if (p.staged && (p.epi == GEMM_EPI_F32 || p.epi == GEMM_EPI_F32_RESID ||
+                              p.epi == GEMM_EPI_F32_ACCUM)) {
         float* stg = reinterpret_cast<float*>(smem + OFF_EPI) + ew * 32 * EPI_LD;
         const int rbase = row0 + int(rank) * BM + ew * 32;  // this warp's first row
 #pragma unroll 1
@@ -611,6 +613,10 @@ cudaError_t gemm2_run(const GemmDesc& g, int band, cudaStream_t s) {
   p.ldg2 = g.ldg2;
   p.scale = g.scale == 0.f ? 1.f : g.scale;
   p.bias = g.bias;
+  {
+    static const int staged = getenv("OPX_GEMM_EPI_STAGED") ? atoi(getenv("OPX_GEMM_EPI_STAGED")) : 1;
+    p.staged = staged;
+  }
   cudaEvent_t slot_done = nullptr;
   {
     cudaError_t e = ticket_acquire(s, &p.ctr, &slot_done);
