@@ -19,6 +19,7 @@
 #include <vector>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -611,19 +612,27 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
     const double budget = be ? atof(be) * 1e6 : 40e6, wave = num_sms() / 2;
     double best = 1e300;
     int band = 1;
-    for (int nb = 1;; nb = nb * 2 > nblk ? nblk : nb * 2) {
-      const double bands = double((nblk + nb - 1) / nb);
-      double b_traffic = double(nblk) * b_blk;
-      if (nb * b_blk > budget) {
-        const double m_per_wave = wave / nb < 1 ? 1 : wave / nb;
-        b_traffic *= double(mblk2) / m_per_wave;
+    // candidate bands: equal splits of the n-blocks (every band count), or
+    // (OPX_GEMM_BAND_POW2=1, round 1) power-of-two band widths
+    static const bool pow2 = getenv("OPX_GEMM_BAND_POW2") && atoi(getenv("OPX_GEMM_BAND_POW2"));
+    int prev = 0;
+    for (int i = 1;; ++i) {
+      const int nb = pow2 ? std::min(nblk, 1 << (i - 1)) : (nblk + i - 1) / i;
+      if (nb != prev) {
+        prev = nb;
+        const double bands = double((nblk + nb - 1) / nb);
+        double b_traffic = double(nblk) * b_blk;
+        if (nb * b_blk > budget) {
+          const double m_per_wave = wave / nb < 1 ? 1 : wave / nb;
+          b_traffic *= double(mblk2) / m_per_wave;
+        }
+        const double tot = a_bytes * bands + b_traffic;
+        if (tot < best * 0.999) {
+          best = tot;
+          band = nb;
+        }
       }
-      const double tot = a_bytes * bands + b_traffic;
-      if (tot < best * 0.999) {
-        best = tot;
-        band = nb;
-      }
-      if (nb == nblk) break;
+      if (pow2 ? nb == nblk : nb == 1) break;
     }
     return gemm2_run(g, band, s);
   }
