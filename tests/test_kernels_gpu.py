@@ -307,6 +307,54 @@ def test_rope_pack():
     assert torch.equal(vf.float(), x[:, hq + hk:])
 
 
+@gpu
+@pytest.mark.parametrize("hd", [128, 80])
+def test_ulysses_abi_seq2head_head2seq_roundtrip(hd):
+    """opx_ulysses_seq2head / head2seq (gather_seq_scatter_heads /
+    gather_heads_scatter_seq) at sp=1: q/k/v rows to the
+    128-padded head layout with RoPE on q/k, and the head layout back to
+    rows; without positions the round trip is the identity."""
+    import ctypes
+
+    torch.manual_seed(7)
+    rows, S_, hq, hk = 2, 96, 4, 2
+    N = rows * S_
+    W = (hq + 2 * hk) * hd
+    qkv = bf(torch.randn(N, W, device=DEV))
+    dst = {g: torch.zeros(N, h, 128, device=DEV, dtype=torch.bfloat16) for g, h in (("q", hq), ("k", hk), ("v", hk))}
+
+    def ptrs(t):
+        return (ctypes.c_void_p * 1)(t.data_ptr())
+
+    call("opx_ulysses_seq2head", P(qkv), W, ptrs(dst["q"]), ptrs(dst["k"]), ptrs(dst["v"]), 1, 0, rows, S_, hq, hk,
+         hd, None, None, S())
+    torch.cuda.synchronize()
+    x = qkv.float().view(N, hq + 2 * hk, hd)
+    assert torch.equal(dst["q"][..., :hd].float(), x[:, :hq])
+    assert torch.equal(dst["v"][..., :hd].float(), x[:, hq + hk:])
+    assert not dst["k"][..., hd:].any()  # padded lanes untouched
+    back = torch.zeros(N, hq * hd, device=DEV, dtype=torch.bfloat16)
+    call("opx_ulysses_head2seq", P(dst["q"]), ptrs(back), hq * hd, 1, 0, rows, S_, hq, hd, S())
+    torch.cuda.synchronize()
+    assert torch.equal(back.float(), qkv.float()[:, :hq * hd])
+    # with positions: RoPE on q and k only
+    pos = torch.cat([torch.arange(40), torch.arange(56), torch.arange(96)]).to(torch.int32).to(DEV)
+    inv = (1.0 / (1e6 ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))).float().to(DEV)
+    call("opx_ulysses_seq2head", P(qkv), W, ptrs(dst["q"]), ptrs(dst["k"]), ptrs(dst["v"]), 1, 0, rows, S_, hq, hk,
+         hd, P(pos), P(inv), S())
+    torch.cuda.synchronize()
+    ang = pos.float()[:, None] * inv[None, :]
+    cos, sin = torch.cos(torch.cat([ang, ang], -1)), torch.sin(torch.cat([ang, ang], -1))
+    h2 = hd // 2
+
+    def rope(t):
+        return t * cos[:, None] + torch.cat([-t[..., h2:], t[..., :h2]], -1) * sin[:, None]
+
+    assert rel_err(dst["q"][..., :hd], rope(x[:, :hq])) < 1e-2
+    assert rel_err(dst["k"][..., :hd], rope(x[:, hq:hq + hk])) < 1e-2
+    assert torch.equal(dst["v"][..., :hd].float(), x[:, hq + hk:])
+
+
 # ---------------------------------------------------------------- deterministic init
 @gpu
 def test_init_bit_identical_to_oracle():
