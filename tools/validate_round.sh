@@ -14,9 +14,11 @@ if [ "$N" = 2 ]; then
   CUDA_VISIBLE_DEVICES=0 timeout -s KILL 900 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_ref_n1.json 2> $O/bench_ref_n1.err
   CUDA_VISIBLE_DEVICES=0 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-file $O/launches.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_bench.log 2>&1
 else
-  timeout -s KILL 2400 python -m pytest tests/test_step_dist_gpu.py tests/test_encoder_gpu.py -q -rs -k "4-" > $O/pytest_gpu_4.log 2>&1; echo pytest_rc=$? >> $O/pytest_gpu_4.log
+  if [ -z "$SKIP_TESTS" ]; then
+    timeout -s KILL 2400 python -m pytest tests/test_step_dist_gpu.py tests/test_encoder_gpu.py -q -rs -k "4-" > $O/pytest_gpu_4.log 2>&1; echo pytest_rc=$? >> $O/pytest_gpu_4.log
+  fi
   for cfg in c1 c2 c3 c4; do
-    timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 2961${#cfg}${cfg:1:1} bench.py --gpus 4 --steps 5 --warmup 3 --config $cfg > $O/bench_${cfg}_n4.json 2> $O/bench_${cfg}_n4.err
+    timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 2961${cfg:1:1} bench.py --gpus 4 --steps 5 --warmup 3 --config $cfg > $O/bench_${cfg}_n4.json 2> $O/bench_${cfg}_n4.err
   done
 fi
 tail -n 3 $O/*.log
