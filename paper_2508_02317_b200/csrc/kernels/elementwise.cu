@@ -602,19 +602,23 @@ cudaError_t k_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __n
 
 cudaError_t k_adamw(float* p, float* m, float* v, const void* g, int g_bf16, __nv_bfloat16* pb,
                     int64_t n, float lr, float b1, float b2, float eps, float wd, int step,
-                    cudaStream_t s) {
+                    cudaStream_t s, int blocks_per_sm) {
   if (n % 4) return cudaErrorInvalidValue;
   if (n <= 0) return cudaSuccess;
   const double bc1 = 1.0 - std::pow(double(b1), step);
   const double bc2 = 1.0 - std::pow(double(b2), step);
+  // blocks_per_sm > 0 caps the grid (the optimizer overlapped with the
+  // backward must leave thread slots for the compute stream's kernels: eight
+  // resident 256-thread blocks per SM would take all 2048 and stall them)
+  int grid = grid_for(n / 4);
+  if (blocks_per_sm > 0 && grid > num_sms() * blocks_per_sm) grid = num_sms() * blocks_per_sm;
   ++g_kernel_launches;
   if (g_bf16)
-    adamw_kernel<bf16><<<grid_for(n / 4), NT, 0, s>>>(p, m, v, static_cast<const bf16*>(g), pb, n, lr,
-                                                      b1, b2, eps, wd, float(bc1), float(std::sqrt(bc2)));
+    adamw_kernel<bf16><<<grid, NT, 0, s>>>(p, m, v, static_cast<const bf16*>(g), pb, n, lr, b1, b2, eps,
+                                           wd, float(bc1), float(std::sqrt(bc2)));
   else
-    adamw_kernel<float><<<grid_for(n / 4), NT, 0, s>>>(p, m, v, static_cast<const float*>(g), pb, n,
-                                                       lr, b1, b2, eps, wd, float(bc1),
-                                                       float(std::sqrt(bc2)));
+    adamw_kernel<float><<<grid, NT, 0, s>>>(p, m, v, static_cast<const float*>(g), pb, n, lr, b1, b2,
+                                            eps, wd, float(bc1), float(std::sqrt(bc2)));
   return cudaGetLastError();
 }
 

@@ -35,7 +35,7 @@ cudaError_t k_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __n
 // g: fp32 or (g_bf16) bf16 gradients
 cudaError_t k_adamw(float* p, float* m, float* v, const void* g, int g_bf16, __nv_bfloat16* pb,
                     int64_t n, float lr, float b1, float b2, float eps, float wd, int step,
-                    cudaStream_t s);
+                    cudaStream_t s, int blocks_per_sm = 0);
 cudaError_t k_cast_f32_bf16(const float* x, __nv_bfloat16* y, int64_t n, cudaStream_t s);
 // acc = (first ? 0 : acc) + g (g fp32, or bf16 when g_bf16), n % 4 == 0
 cudaError_t k_grad_accum(float* acc, const void* g, int g_bf16, int64_t n, int first,

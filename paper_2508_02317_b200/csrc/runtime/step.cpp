@@ -119,8 +119,14 @@ int Step::opt_unit(Unit& u, cudaStream_t after, const std::string& name) {
   CU(cudaEventRecord(ready, after));
   CU(cudaStreamWaitEvent(os_, ready, 0));
   const bool acc = accum_ > 1;  // AdamW reads the fp32 micro-batch sum
+  // units updated while the backward still runs get a capped grid (they must
+  // not take every thread slot from the compute stream); the head, updated
+  // last and exposed, takes the whole GPU
+  static const int overlap_bps =
+      getenv("OPX_ADAMW_OVERLAP_BLOCKS") ? atoi(getenv("OPX_ADAMW_OVERLAP_BLOCKS")) : 2;
+  const int bps = &u == &units_[0] ? 0 : overlap_bps;
   CU(k_adamw(u.master, u.m, u.v, acc ? static_cast<void*>(u.gacc) : u.gshard, acc ? 0 : u.gbf,
-             u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps, ex_.wd, step_count_, os_));
+             u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps, ex_.wd, step_count_, os_, bps));
   if (ex_.trace) {
     cudaEvent_t done = ev();
     CU(cudaEventRecord(done, os_));

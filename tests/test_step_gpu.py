@@ -229,3 +229,17 @@ def test_step_rejects_bad_cu_seqlens():
     vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
     assert lib().opx_step_load_batch(s.h, vp(ids), vp(ids), vp(ids), vp(cu), 3, 10) == 9
     s.close()
+
+
+@gpu
+@pytest.mark.parametrize("sp_world", [1])
+def test_step_zero_layer_foundation_trains_its_head(sp_world):
+    """test_simulator.cpp:265-283: a zero-layer foundation still trains its
+    head (embedding -> final norm -> LM head -> CE, AdamW)."""
+    model = tiny_dense(layers=0, hidden=256, heads=2, kv=2, ffn=768, vocab=2048)
+    s, batch, plan, r = _run(model, 512, 2)
+    assert r.step_time_s > 0 and r.launches > 0
+    compare_step([s], model, batch, plan, r.loss)
+    ph = s.report_json()["phase_breakdown"]
+    assert "optimizer" in ph and not any(k.startswith("fwd.layer") for k in ph)
+    s.close()
