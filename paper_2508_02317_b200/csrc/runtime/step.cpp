@@ -119,11 +119,13 @@ int Step::opt_unit(Unit& u, cudaStream_t after, const std::string& name) {
   CU(cudaEventRecord(ready, after));
   CU(cudaStreamWaitEvent(os_, ready, 0));
   const bool acc = accum_ > 1;  // AdamW reads the fp32 micro-batch sum
-  // units updated while the backward still runs get a capped grid (they must
-  // not take every thread slot from the compute stream); the head, updated
-  // last and exposed, takes the whole GPU
+  // OPX_ADAMW_OVERLAP_BLOCKS caps the grid of the units updated while the
+  // backward still runs (blocks per SM; the exposed head update keeps the
+  // whole GPU).  Off by default: capping at 1-2 blocks per SM measured slower
+  // (C2/EP4 176-184K vs 190K tokens/s, C1 1 GPU equal) -- the longer AdamW
+  // overlaps more of the backward's HBM-bound kernels
   static const int overlap_bps =
-      getenv("OPX_ADAMW_OVERLAP_BLOCKS") ? atoi(getenv("OPX_ADAMW_OVERLAP_BLOCKS")) : 2;
+      getenv("OPX_ADAMW_OVERLAP_BLOCKS") ? atoi(getenv("OPX_ADAMW_OVERLAP_BLOCKS")) : 0;
   const int bps = &u == &units_[0] ? 0 : overlap_bps;
   CU(k_adamw(u.master, u.m, u.v, acc ? static_cast<void*>(u.gacc) : u.gshard, acc ? 0 : u.gbf,
              u.pshard, u.shard, ex_.lr, ex_.b1, ex_.b2, ex_.eps, ex_.wd, step_count_, os_, bps));

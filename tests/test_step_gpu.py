@@ -237,7 +237,7 @@ def test_step_zero_layer_foundation_trains_its_head(sp_world):
     """test_simulator.cpp:265-283: a zero-layer foundation still trains its
     head (embedding -> final norm -> LM head -> CE, AdamW)."""
     model = tiny_dense(layers=0, hidden=256, heads=2, kv=2, ffn=768, vocab=2048)
-    s, batch, plan, r = _run(model, 512, 2)
+    s, batch, plan, r = _run(model, 512, 2, trace=True)
     assert r.step_time_s > 0 and r.launches > 0
     compare_step([s], model, batch, plan, r.loss)
     ph = s.report_json()["phase_breakdown"]
