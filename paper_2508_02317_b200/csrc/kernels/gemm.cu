@@ -35,7 +35,12 @@ namespace {
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 1024 + 256;
+// bf16 epilogue staging: per epilogue warp [32 rows][40] bf16, so the output
+// leaves as 8 rows x 64 contiguous bytes per warp instruction instead of one
+// 16-B piece of 32 different rows
+constexpr int EPI_LD = 40;
+constexpr int EPI_OFF = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 512;
+constexpr int SMEM_BYTES = EPI_OFF + 4 * 32 * EPI_LD * 2 + 1024;
 constexpr int NUM_THREADS = 256;
 
 struct KParams {
@@ -64,6 +69,7 @@ struct KParams {
   const int* rm_off;
   int rm_ep;
   const __nv_bfloat16* bias;  // optional column bias
+  int staged;                 // bf16 epilogue through the per-warp smem stage
 };
 
 struct TileCoord {
@@ -340,6 +346,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
+      } else if (p.epi == GEMM_EPI_BF16 && p.staged) {
+        __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + EPI_OFF) + ew * 32 * EPI_LD;
+        const int rloc0 = c.mb * BM + ew * 32;  // this warp's first row (within the group)
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + ch * 32, v);
+          ptx::tmem_wait_ld();
+          const int col0 = c.nb * BN + ch * 32;
+          if (col0 >= p.N) continue;  // warp-uniform
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = empty_k ? 0.f : __uint_as_float(v[i]) * p.scale;
+          if (p.bias) epi::add_bias32(f, p.bias + col0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(stg + lane * EPI_LD + 8 * q) =
+                make_uint4(ptx::pack_bf16(f[8 * q], f[8 * q + 1]), ptx::pack_bf16(f[8 * q + 2], f[8 * q + 3]),
+                           ptx::pack_bf16(f[8 * q + 4], f[8 * q + 5]), ptx::pack_bf16(f[8 * q + 6], f[8 * q + 7]));
+          __syncwarp();
+          const int cc = (lane & 3) * 8, col = col0 + cc;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int rr = it * 8 + (lane >> 2);
+            const bool ok = ((p.groups && !p.grouped_k) ? (rloc0 + rr) < p.g_rows[c.g] : (c.m0 + ew * 32 + rr) < p.M) &&
+                            col < p.N;
+            if (ok)
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.D) + dgoff +
+                                        int64_t(c.m0 + ew * 32 + rr) * p.ldd + col) =
+                  *reinterpret_cast<const uint4*>(stg + rr * EPI_LD + cc);
+          }
+          __syncwarp();
+        }
       } else {
         // the output row: D's own, or (ROWMAP) its token owner's combine slot
         __nv_bfloat16* brow = reinterpret_cast<__nv_bfloat16*>(p.D) + dgoff + int64_t(row) * p.ldd;
@@ -601,6 +640,10 @@ static cudaError_t gemm_run_impl(const GemmDesc& g, cudaStream_t s) {
   kp.rm_off = g.rm_off;
   kp.rm_ep = g.rm_ep;
   kp.bias = g.bias;
+  {
+    static const int staged = getenv("OPX_GEMM_EPI_STAGED") ? atoi(getenv("OPX_GEMM_EPI_STAGED")) : 1;
+    kp.staged = staged;
+  }
   if (gm && grouped_2cta && !force_1cta && g.K % BK == 0 && g.epi != GEMM_EPI_ROWMAP)
     return gemm2_run(g, 1, s);
   if (!grouped && !force_1cta) {

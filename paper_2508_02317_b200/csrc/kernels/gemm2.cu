@@ -427,6 +427,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
           }
         }
+      } else if (p.staged && p.epi == GEMM_EPI_BF16) {
+        // bf16 through the same per-warp stage ([32][2 * EPI_LD] bf16): 8 rows
+        // x 64 contiguous bytes per warp store instruction
+        __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + OFF_EPI) + ew * 32 * (2 * EPI_LD);
+        const int rbase = row0 + int(rank) * BM + ew * 32;
+#pragma unroll 1
+        for (int ch = 0; ch < BNP / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tbase + ch * 32, v);
+          ptx::tmem_wait_ld();
+          const int col0 = nb * BNP + ch * 32;
+          if (col0 >= p.N) continue;  // warp-uniform
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.scale;
+          if (p.bias) epi::add_bias32(f, p.bias + col0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(stg + lane * (2 * EPI_LD) + 8 * q) =
+                make_uint4(ptx::pack_bf16(f[8 * q], f[8 * q + 1]), ptx::pack_bf16(f[8 * q + 2], f[8 * q + 3]),
+                           ptx::pack_bf16(f[8 * q + 4], f[8 * q + 5]), ptx::pack_bf16(f[8 * q + 6], f[8 * q + 7]));
+          __syncwarp();
+          const int cc = (lane & 3) * 8, col = col0 + cc;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int rr = it * 8 + (lane >> 2), r = rbase + rr;
+            const bool ok = (p.groups ? (r - p.g_start[g]) < p.g_rows[g] : r < p.M) && col < p.N;
+            if (ok)
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(r) * p.ldd + col) =
+                  *reinterpret_cast<const uint4*>(stg + rr * (2 * EPI_LD) + cc);
+          }
+          __syncwarp();
+        }
       } else if (p.staged && (p.epi == GEMM_EPI_F32 || p.epi == GEMM_EPI_F32_RESID ||
                               p.epi == GEMM_EPI_F32_ACCUM)) {
         float* stg = reinterpret_cast<float*>(smem + OFF_EPI) + ew * 32 * EPI_LD;
