@@ -316,6 +316,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 32; ++i) g[i] = __float_as_uint(bg[i]), u[i] = __float_as_uint(bu[i]);
           }
           const int f0 = c.nb * 128 + ch * 32;
+          if (p.staged) {
+            // act (and gate|up) rows out through the per-warp stage: 8 rows x
+            // 64 contiguous bytes per store instruction
+            if (f0 >= p.N / 2) continue;  // warp-uniform
+            uint32_t pa[16], pg[16], pu[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float2 gf = ptx::unpack_bf16(ptx::pack_bf16(__uint_as_float(g[2 * e]), __uint_as_float(g[2 * e + 1])));
+              const float2 uf = ptx::unpack_bf16(ptx::pack_bf16(__uint_as_float(u[2 * e]), __uint_as_float(u[2 * e + 1])));
+              pa[e] = ptx::pack_bf16(silu(gf.x) * uf.x, silu(gf.y) * uf.y);
+              pg[e] = ptx::pack_bf16(gf.x, gf.y);
+              pu[e] = ptx::pack_bf16(uf.x, uf.y);
+            }
+            __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + EPI_OFF) + ew * 32 * EPI_LD;
+            const int rloc0 = c.mb * BM + ew * 32, cc = (lane & 3) * 8;
+            auto out = [&](const uint32_t* w, __nv_bfloat16* base, int64_t ld) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<uint4*>(stg + lane * EPI_LD + 8 * q) =
+                    make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+              __syncwarp();
+#pragma unroll
+              for (int it = 0; it < 4; ++it) {
+                const int rr = it * 8 + (lane >> 2);
+                const bool ok = (p.groups && !p.grouped_k) ? (rloc0 + rr) < p.g_rows[c.g]
+                                                           : (c.m0 + ew * 32 + rr) < p.M;
+                if (ok)
+                  *reinterpret_cast<uint4*>(base + int64_t(c.m0 + ew * 32 + rr) * ld + cc) =
+                      *reinterpret_cast<const uint4*>(stg + rr * EPI_LD + cc);
+              }
+              __syncwarp();
+            };
+            out(pa, p.D2 + f0, p.ldd2);
+            if (p.D) {
+              __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(p.D) + c.nb * BN + ch * 32;
+              out(pg, gu, p.ldd);
+              out(pu, gu + 128, p.ldd);
+            }
+            continue;
+          }
           if (row_ok && f0 < p.N / 2) {
             __nv_bfloat16* act = p.D2 + int64_t(row) * p.ldd2 + f0;
             __nv_bfloat16* gu = p.D ? reinterpret_cast<__nv_bfloat16*>(p.D) + int64_t(row) * p.ldd +
