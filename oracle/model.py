@@ -298,15 +298,25 @@ def silu(x):
 
 
 def router_logits(h_bf16, w_bf16):
-    """fp32 logits with the GPU's fixed sequential K order: every step rounds
-    acc + h*w once (the bf16 x bf16 product is exact in fp32, so the kernel's
-    fused multiply-add and this multiply-then-add agree bit for bit;
-    kernels/moe.cu router kernel)."""
+    """fp32 logits in a defined summation order the GPU follows exactly
+    (kernels/moe.cu router kernel): for H % 128 == 0 the K range is split in
+    four quarters, each summed with k ascending -- every step rounds acc + h*w
+    once (the bf16 x bf16 product is exact in fp32, so the kernel's fused
+    multiply-add and this multiply-then-add agree bit for bit) -- and the
+    partials are combined as (p0 + p1) + (p2 + p3); otherwise one sequential
+    sum over all of K."""
     T, H = h_bf16.shape
-    acc = np.zeros((T, w_bf16.shape[0]), F32)
-    for kk in range(H):
-        acc = (acc + (h_bf16[:, kk:kk + 1] * w_bf16[None, :, kk]).astype(F32)).astype(F32)
-    return acc
+    splits = 4 if H % 128 == 0 else 1
+    q = H // splits
+    parts = []
+    for z in range(splits):
+        acc = np.zeros((T, w_bf16.shape[0]), F32)
+        for kk in range(z * q, (z + 1) * q):
+            acc = (acc + (h_bf16[:, kk:kk + 1] * w_bf16[None, :, kk]).astype(F32)).astype(F32)
+        parts.append(acc)
+    if splits == 1:
+        return parts[0]
+    return ((parts[0] + parts[1]).astype(F32) + (parts[2] + parts[3]).astype(F32)).astype(F32)
 
 
 def topk_route(logits, k):

@@ -23,8 +23,11 @@ namespace {
 using bf16 = __nv_bfloat16;
 
 // ---------------------------------------------------------------------------
-// router logits: logits[t, e] = sum_k h[t,k] * w[e,k], k ascending, fmul/fadd rn
-// (the CPU oracle's sequential order, so routing is bit-exact).  Block tile:
+// router logits: logits[t, e] = sum_k h[t,k] * w[e,k] in the oracle's defined
+// order (oracle/model.py router_logits), so routing is bit-exact: for H a
+// multiple of 128 the K range is split into 4 quarters, each summed with k
+// ascending (fmul/fadd rn) by its own block (blockIdx.z), and the partials are
+// combined as (p0 + p1) + (p2 + p3); otherwise one sequential sum.  Block tile:
 // 32 tokens x 128 experts (256 blocks at T = 8192, two per SM), K in chunks of
 // 32 staged through smem with 16-B loads; the next chunk is fetched into
 // registers while the current one is consumed.
@@ -32,11 +35,14 @@ constexpr int RT = 32, RE = 128, RK = 32;
 // 256 threads; thread (ty, tx): tokens ty*2 .. +1, experts tx*4 + {0..3}, 64 + tx*4 + {0..3}.
 __global__ void __launch_bounds__(256, 2) router_kernel(const bf16* __restrict__ h,
                                                         const bf16* __restrict__ w,
-                                                        float* __restrict__ logits, int T, int H,
-                                                        int E) {
+                                                        float* __restrict__ logits_all, int T, int H,
+                                                        int E, int ksplit) {
   __shared__ float sh[RK][RT + 4];
   __shared__ float sw[RK][RE + 4];
   const int t0 = blockIdx.x * RT, e0 = blockIdx.y * RE;
+  // this block's K quarter (ksplit = 4) or all of K, and its partial output
+  const int kb = blockIdx.z * (H / ksplit), ke = kb + H / ksplit;
+  float* __restrict__ logits = logits_all + int64_t(blockIdx.z) * T * E;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   // staging: h chunk = 32 tok x 32 k = 128 x 16 B (threads 0..127),
   //          w chunk = 128 exp x 32 k = 512 x 16 B (2 per thread)
@@ -83,11 +89,11 @@ __global__ void __launch_bounds__(256, 2) router_kernel(const bf16* __restrict__
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-  fetch(0);
-  for (int k0 = 0; k0 < H; k0 += RK) {
+  fetch(kb);
+  for (int k0 = kb; k0 < ke; k0 += RK) {
     stash();
     __syncthreads();
-    if (k0 + RK < H) fetch(k0 + RK);  // in flight during the FMAs below
+    if (k0 + RK < ke) fetch(k0 + RK);  // in flight during the FMAs below
 #pragma unroll 8
     for (int kk = 0; kk < RK; ++kk) {
       // this thread's experts: tx*4 + {0..3} and 64 + tx*4 + {0..3} (two
@@ -117,6 +123,14 @@ __global__ void __launch_bounds__(256, 2) router_kernel(const bf16* __restrict__
       if (e < E) logits[int64_t(t) * E + e] = acc[i][j];
     }
   }
+}
+
+// logits = (p0 + p1) + (p2 + p3) of the four K-quarter partials
+__global__ void router_combine_kernel(const float* __restrict__ part, float* __restrict__ logits,
+                                      int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    logits[i] = __fadd_rn(__fadd_rn(part[i], part[n + i]), __fadd_rn(part[2 * n + i], part[3 * n + i]));
 }
 
 // top-k per token (one warp per token), E <= 256, k <= 16
@@ -558,12 +572,21 @@ __global__ void swiglu_bwd_grouped_kernel(const bf16* __restrict__ dact, const b
 
 }  // namespace
 
+int k_moe_router_splits(int H) { return H % (4 * RK) == 0 ? 4 : 1; }
+
 cudaError_t k_moe_router(const __nv_bfloat16* h, const __nv_bfloat16* w, float* logits, int T,
-                         int H, int E, cudaStream_t s) {
+                         int H, int E, cudaStream_t s, float* partial) {
   if (H % RK || H % 8) return cudaErrorInvalidValue;
-  dim3 grid((T + RT - 1) / RT, (E + RE - 1) / RE);
+  const int ks = k_moe_router_splits(H);
+  if (ks > 1 && !partial) return cudaErrorInvalidValue;
+  dim3 grid((T + RT - 1) / RT, (E + RE - 1) / RE, ks);
   ++g_kernel_launches;
-  router_kernel<<<grid, 256, 0, s>>>(h, w, logits, T, H, E);
+  router_kernel<<<grid, 256, 0, s>>>(h, w, ks > 1 ? partial : logits, T, H, E, ks);
+  if (ks > 1) {
+    const int64_t n = int64_t(T) * E;
+    ++g_kernel_launches;
+    router_combine_kernel<<<int(std::min<int64_t>((n + 255) / 256, 4096)), 256, 0, s>>>(partial, logits, n);
+  }
   return cudaGetLastError();
 }
 

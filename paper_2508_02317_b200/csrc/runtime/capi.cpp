@@ -547,8 +547,14 @@ int opx_ulysses_head2seq(const void* o_heads, void* const* dst, int64_t ld, int 
 int opx_moe_route(const void* h, const void* w, int T, int H, int E, int k, float* logits,
                   int32_t* idx, float* wts, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* part = nullptr;
+  if (k_moe_router_splits(H) > 1) {
+    cudaError_t e = cudaMallocAsync(&part, size_t(k_moe_router_splits(H)) * T * E * sizeof(float), s);
+    if (e != cudaSuccess) return cuda_fail(e, "opx_moe_route scratch");
+  }
   cudaError_t e = k_moe_router(static_cast<const __nv_bfloat16*>(h),
-                               static_cast<const __nv_bfloat16*>(w), logits, T, H, E, s);
+                               static_cast<const __nv_bfloat16*>(w), logits, T, H, E, s, part);
+  if (part) cudaFreeAsync(part, s);
   if (e != cudaSuccess) return cuda_fail(e, "opx_moe_route");
   OPX_CALL(k_moe_topk(logits, T, E, k, idx, wts, s), "opx_moe_route");
 }

@@ -126,8 +126,11 @@ cudaError_t k_peer_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int 
 
 namespace opx {
 // moe.cu — routing, permutation and EP exchange (see the file header).
+// K-quarter count of the router's defined summation order (4 when H % 128 == 0)
+int k_moe_router_splits(int H);
+// partial: [splits][T][E] fp32 scratch (required when splits > 1)
 cudaError_t k_moe_router(const __nv_bfloat16* h, const __nv_bfloat16* w, float* logits, int T,
-                         int H, int E, cudaStream_t s);
+                         int H, int E, cudaStream_t s, float* partial = nullptr);
 cudaError_t k_moe_topk(const float* logits, int T, int E, int k, int* idx, float* wts,
                        cudaStream_t s);
 int k_moe_sort_chunks(int P);

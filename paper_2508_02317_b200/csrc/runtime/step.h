@@ -399,7 +399,7 @@ class Step {
   uint32_t epoch_ep_ = 0;
   bool in_recompute_ = false;       // layer_fwd called from layer_bwd
   std::vector<int*> route_idx_;     // [layer] forward top-k indices (T*k), for parity checks
-  float *r_logits_ = nullptr, *r_wts_ = nullptr, *r_dw_ = nullptr;
+  float *r_logits_ = nullptr, *r_wts_ = nullptr, *r_dw_ = nullptr, *r_logits_part_ = nullptr;
   int *r_idx_ = nullptr, *r_pos_ = nullptr, *r_pairat_ = nullptr, *r_cnt_ = nullptr,
       *r_excl_ = nullptr, *r_hist_ = nullptr, *g_start_ = nullptr, *g_rows_ = nullptr,
       *g_rows_pad_ = nullptr, *g_total_ = nullptr;

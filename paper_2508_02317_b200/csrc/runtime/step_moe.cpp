@@ -193,6 +193,9 @@ int Step::moe_alloc() {
   const size_t T = size_t(T_), P = T * size_t(topk_), cap = size_t(cap_rows_);
   const size_t E = size_t(E_), H = size_t(H_), Fe = size_t(Fe_);
   r_logits_ = alloc<float>(T * E, false);
+  if (k_moe_router_splits(H_) > 1 &&
+      !(r_logits_part_ = alloc<float>(size_t(k_moe_router_splits(H_)) * T * E, false)))
+    return cuda_fail(cudaErrorMemoryAllocation, "router partials");
   r_dw_ = alloc<float>(P, false);
   r_hist_ = alloc<int>(size_t(k_moe_sort_chunks(int(P))) * E);
   routes_.assign(off_counts_s_.size(), MoeRoute{});
@@ -450,7 +453,7 @@ int Step::moe_fwd(int l, const Unit& u, const Unit& eu, const float* x2, float* 
   }
   bf16** xpeers = xrecv_peers_of(xl);
   bf16* yback = yback_cur();
-  CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_));
+  CU(k_moe_router(h2_, Wr, r_logits_, T, H, E, cs_, r_logits_part_));
   CU(k_moe_topk(r_logits_, T, E, k, r_idx_, r_wts_, cs_));
   if (!in_recompute_ && route_idx_[size_t(l)])
     CU(cudaMemcpyAsync(route_idx_[size_t(l)] + int64_t(mb_) * P, r_idx_, size_t(P) * sizeof(int),
