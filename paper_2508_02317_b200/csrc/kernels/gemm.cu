@@ -386,9 +386,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-      } else if (p.epi == GEMM_EPI_BF16 && p.staged) {
+      } else if ((p.epi == GEMM_EPI_BF16 || p.epi == GEMM_EPI_ROWMAP) && p.staged) {
         __nv_bfloat16* stg = reinterpret_cast<__nv_bfloat16*>(smem + EPI_OFF) + ew * 32 * EPI_LD;
         const int rloc0 = c.mb * BM + ew * 32;  // this warp's first row (within the group)
+        // the 4 rows this lane stores (it * 8 + lane / 4): their destination
+        // rows -- D's own, or (ROWMAP) the token owner's combine slot
+        __nv_bfloat16* dst_row[4];
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2);
+          dst_row[it] = nullptr;
+          const bool ok = (p.groups && !p.grouped_k) ? (rloc0 + rr) < p.g_rows[c.g] : (c.m0 + ew * 32 + rr) < p.M;
+          if (!ok) continue;
+          if (p.epi == GEMM_EPI_ROWMAP) {
+            int rg = rloc0 + rr;
+            const int* cnt = p.rm_cnt + c.g * p.rm_ep;
+            int sidx = 0;
+            while (sidx + 1 < p.rm_ep && rg >= cnt[sidx]) rg -= cnt[sidx++];
+            dst_row[it] = p.rm_dst[sidx] + int64_t(p.rm_off[c.g * p.rm_ep + sidx] + rg) * p.ldd;
+          } else {
+            dst_row[it] = reinterpret_cast<__nv_bfloat16*>(p.D) + dgoff + int64_t(c.m0 + ew * 32 + rr) * p.ldd;
+          }
+        }
 #pragma unroll 1
         for (int ch = 0; ch < BN / 32; ++ch) {
           uint32_t v[32];
@@ -410,12 +429,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
             const int rr = it * 8 + (lane >> 2);
-            const bool ok = ((p.groups && !p.grouped_k) ? (rloc0 + rr) < p.g_rows[c.g] : (c.m0 + ew * 32 + rr) < p.M) &&
-                            col < p.N;
-            if (ok)
-              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.D) + dgoff +
-                                        int64_t(c.m0 + ew * 32 + rr) * p.ldd + col) =
-                  *reinterpret_cast<const uint4*>(stg + rr * EPI_LD + cc);
+            if (dst_row[it] && col < p.N)
+              *reinterpret_cast<uint4*>(dst_row[it] + col) = *reinterpret_cast<const uint4*>(stg + rr * EPI_LD + cc);
           }
           __syncwarp();
         }
