@@ -411,12 +411,14 @@ GemmDesc grouped(int M, int N, int K, const bf16* A, int64_t lda, bool amn, cons
 // moe_overlap: the two expert halves' GEMMs run concurrently on their two
 // streams (disjoint rows of every buffer; the ticketed GEMMs share the SMs);
 // OPX_MOE_SERIAL_HALVES=1 orders half B's GEMMs after half A's (round 1)
-// OPX_MOE_FUSED_COMBINE=1: the combine / dX return ride in the expert GEMM
-// epilogues (GEMM_EPI_ROWMAP peer stores).  Off by default: row-per-thread
-// remote stores from the epilogue measured slower on C2/EP4 (143K vs 181K
-// tokens/s) than the warp-per-row combine kernel's coalesced 16-B stores.
+// The combine / dX return ride in the expert GEMM epilogues (GEMM_EPI_ROWMAP:
+// rows peer-stored to their token owners through the per-warp stage, 8 rows x
+// 64 contiguous bytes per store instruction): C2/EP4 192K vs 188K tokens/s for
+// the separate warp-per-row combine kernel (OPX_MOE_FUSED_COMBINE=0).  Without
+// the staging (one 16-B store of 32 different rows per instruction) the fused
+// form had measured 143K.
 bool moe_fused_combine() {
-  static const bool v = getenv("OPX_MOE_FUSED_COMBINE") && atoi(getenv("OPX_MOE_FUSED_COMBINE"));
+  static const bool v = !getenv("OPX_MOE_FUSED_COMBINE") || atoi(getenv("OPX_MOE_FUSED_COMBINE"));
   return v;
 }
 bool moe_serial_halves() {
