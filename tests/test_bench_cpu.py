@@ -65,3 +65,13 @@ def test_moe_overlap_rates_count_both_halves_in_dispatch_nodes(bench):
     assert r["fwd_a2a_combine_GBps"] == pytest.approx(600.0, abs=0.1)
     assert r["bwd_a2a_combine_grad_GBps"] == pytest.approx(400.0, abs=0.1)
     assert r["bwd_a2a_dispatch_grad_GBps"] == pytest.approx(650.0, abs=0.1)
+
+
+def test_node_keys_merge_layers_and_micro_batches():
+    import bench
+
+    assert bench.node_key("fwd.layer3.m0.qkv_proj") == "fwd.qkv_proj"
+    assert bench.node_key("bwd.layer12.m1.mlp.dgrad_gu") == "bwd.mlp.dgrad_gu"
+    assert bench.node_key("bwd.head.m1") == "bwd.head"
+    assert bench.node_key("encoder.vision.m0") == "encoder.vision"
+    assert bench.node_key("optimizer") == "optimizer"
