@@ -4,21 +4,17 @@
 // One CTA per (pair of consecutive 128-query tiles, q head), 320 threads:
 //   warp 0       TMA producer: Q0/Q1 once, K tiles (128 keys) into a 2-stage
 //                ring, V into a single buffer (3-D maps over [tokens, heads, 128])
-//   warp 1       MMA issuer (one elected lane), per key tile j and tile t:
-//                  O_t += P_t(j) V(j)   (A = P_t from TMEM, B = V from smem)
-//                  S_t(j+1) = Q_t K^T   (into the same TMEM columns)
-//                in tile order 0, 1, so one tile's softmax runs while the
-//                tensor pipe works on the other tile's PV + QK^T.
+//   warp 1       MMA issuer (one elected lane), order per key tile j:
+//                  S0(j+1) = Q0 K^T, S1(j+1) = Q1 K^T      (TMEM, 128 cols each)
+//                  O0 += P0(j) V(j), O1 += P1(j) V(j)      (TMEM, 128 cols each)
+//                so the QK^T of the next tile runs under the current softmax.
 //   warps 2..5   softmax warpgroup of tile 0, warps 6..9 of tile 1: one query
 //                row per thread (TMEM lane); masking from per-token seq_start;
 //                lazy rescaling of O in TMEM (only when the row max grows by
 //                > 2^8); a quarter of the exponentials on the FMA pipe (degree-3
-//                polynomial, 8.6e-5 rel. error) to relieve MUFU; P -> bf16 pairs
-//                written back over S_t's first 64 TMEM columns (the A operand of
-//                the PV MMA: no P round trip through shared memory, which cut
-//                the per-key-tile smem traffic from ~384 to ~256 KB);
-//                epilogue O/l -> bf16, lse.
-// TMEM: S_0 | S_1 (P_t aliases S_t) | O_0 | O_1 -- 512 columns.
+//                polynomial, 8.6e-5 rel. error) to relieve MUFU; P -> bf16 ->
+//                128B-swizzled smem for the PV MMA; epilogue O/l -> bf16, lse.
+// The two warpgroups ping-pong against the single tensor-core pipe.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -36,8 +32,8 @@ using bf16 = __nv_bfloat16;
 constexpr int BM = 128, BN = 128, D = 128;
 constexpr int TILE_BYTES = 128 * 128 * 2;  // 32 KB: [128 rows][128] bf16 as two 64-col SW128 blocks
 constexpr int FWD_THREADS = 320;
-// smem: Q0 | Q1 | K[0] | K[1] | V | barriers
-constexpr int FWD_SMEM = 1024 + TILE_BYTES * 5 + 256;
+// smem: Q0 | Q1 | K[0] | K[1] | V | P0 | P1 | barriers
+constexpr int FWD_SMEM = 1024 + TILE_BYTES * 7 + 256;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESH = 8.0f;
 // 1/POLY_SHARE of the exponentials go to the FMA-pipe polynomial (0: none).
@@ -71,13 +67,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   auto sQ = [&](int i) { return smem + i * TILE_BYTES; };
   auto sK = [&](int i) { return smem + (2 + i) * TILE_BYTES; };
   uint8_t* sV = smem + 4 * TILE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * TILE_BYTES);
+  auto sP = [&](int i) { return smem + (5 + i) * TILE_BYTES; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 7 * TILE_BYTES);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;   // [2]
   uint64_t* k_empty = bars + 3;  // [2]
   uint64_t* v_full = bars + 5;
   uint64_t* v_empty = bars + 6;
   uint64_t* s_full = bars + 7;   // [2] per tile
+  uint64_t* s_empty = bars + 9;  // [2]
   uint64_t* p_full = bars + 11;  // [2]
   uint64_t* o_done = bars + 13;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
@@ -103,6 +101,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_empty[i], 128);
       ptx::mbar_init(&p_full[i], 128);
       ptx::mbar_init(&o_done[i], 1);
     }
@@ -146,51 +145,49 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false, false);
     constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(BM, D, false, true);
-    const uint32_t qa0 = ptx::smem_u32(sQ(0));
+    const uint32_t qa0 = ptx::smem_u32(sQ(0)), pa0 = ptx::smem_u32(sP(0));
     const uint32_t va = ptx::smem_u32(sV);
     ptx::mbar_wait(q_full, 0);
-    // S_t(j) = Q_t K(j)^T into TS(t); its columns held P_t(j-1), whose PV MMA
-    // was issued just before (the tensor pipe runs one thread's MMAs in order)
-    auto issue_s = [&](int j, int t) {
-      const uint32_t ka = ptx::smem_u32(sK(j & 1));
-      ptx::tc_fence_after();
-      if (lane == 0) {
+    auto issue_s = [&](int j) {
+      const int st = j & 1;
+      ptx::mbar_wait(&k_full[st], (j >> 1) & 1);
+      const uint32_t ka = ptx::smem_u32(sK(st));
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k)
-          ptx::mma_bf16_ss(TS(t), kdesc(qa0 + uint32_t(t) * TILE_BYTES, k), kdesc(ka, k), idesc_s, k != 0);
-        ptx::mma_commit(&s_full[t]);
+      for (int t = 0; t < 2; ++t) {
+        if (j > 0) ptx::mbar_wait(&s_empty[t], (j - 1) & 1);
+        ptx::tc_fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k)
+            ptx::mma_bf16_ss(TS(t), kdesc(qa0 + uint32_t(t) * TILE_BYTES, k), kdesc(ka, k), idesc_s, k != 0);
+          ptx::mma_commit(&s_full[t]);
+        }
+        __syncwarp();
       }
+      if (lane == 0) ptx::mma_commit(&k_empty[st]);
       __syncwarp();
     };
-    ptx::mbar_wait(&k_full[0], 0);
-    issue_s(0, 0);
-    issue_s(0, 1);
-    if (lane == 0) ptx::mma_commit(&k_empty[0]);
-    __syncwarp();
-    for (int j = 0; j < nkv; ++j) {
-      const bool more = j + 1 < nkv;
+    auto issue_pv = [&](int j) {
       ptx::mbar_wait(v_full, j & 1);
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        ptx::mbar_wait(&p_full[t], j & 1);  // P_t(j) in TMEM, O_t rescaled
+        ptx::mbar_wait(&p_full[t], j & 1);
         ptx::tc_fence_after();
         if (lane == 0) {
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            ptx::mma_bf16_ts(TO(t), TS(t) + uint32_t(k) * 8, mndesc(va, k), idesc_o, (j | k) != 0);
+            ptx::mma_bf16_ss(TO(t), kdesc(pa0 + uint32_t(t) * TILE_BYTES, k), mndesc(va, k), idesc_o, (j | k) != 0);
           ptx::mma_commit(&o_done[t]);
         }
         __syncwarp();
-        if (more) {
-          if (t == 0) ptx::mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-          issue_s(j + 1, t);
-        }
       }
-      if (lane == 0) {
-        ptx::mma_commit(v_empty);
-        if (more) ptx::mma_commit(&k_empty[(j + 1) & 1]);
-      }
+      if (lane == 0) ptx::mma_commit(v_empty);
       __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nkv; ++j) {
+      if (j + 1 < nkv) issue_s(j + 1);
+      issue_pv(j);
     }
   } else {
     // ---------------- softmax warpgroups ----------------
@@ -202,6 +199,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const int sst = valid_row ? p.seq_start[row] : 0x7fffffff;
     const int kend = p.causal ? row + 1 : (valid_row ? p.seq_end[row] : 0);  // keys [sst, kend)
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
+    uint8_t* myP = sP(t);
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(&s_full[t], j & 1);
@@ -215,6 +213,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
       }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&s_empty[t]);
       const int kbase = kv0 + j * BN;
       const bool full_vis = kbase >= sst && kbase + BN <= kend;
       // row max of the raw scores (scale > 0), 3-input max
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       float sum_lo, sum_hi;
       f2unpack(sum2, sum_lo, sum_hi);
       const float sum = sum_lo + sum_hi;
-      if (j > 0) ptx::mbar_wait(&o_done[t], (j - 1) & 1);  // PV(j-1) done: O stable
+      if (j > 0) ptx::mbar_wait(&o_done[t], (j - 1) & 1);  // PV(j-1) done: O stable, P free
       ptx::tc_fence_after();
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
@@ -273,16 +273,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       }
       l = l * alpha + sum;
       m_used = m_new;
-      // P_t(j) as bf16 pairs over S_t's first 64 columns (this thread's row;
-      // S_t(j) is in registers, S_t(j+1) is issued only after PV_t(j))
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pw[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pw[i] = __float_as_uint(s[c * 16 + i]);
-        ptx::tmem_st16(TS(t) + lane_off + uint32_t(c) * 16, pw);
-      }
-      ptx::tmem_wait_st();
+      for (int c = 0; c < 16; ++c)
+        *reinterpret_cast<uint4*>(myP + sw_off(r, c)) =
+            make_uint4(__float_as_uint(s[c * 4]), __float_as_uint(s[c * 4 + 1]),
+                       __float_as_uint(s[c * 4 + 2]), __float_as_uint(s[c * 4 + 3]));
+      ptx::fence_proxy_async();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&p_full[t]);
     }
