@@ -363,6 +363,9 @@ def main():
     ap.add_argument("--config", default="c1")
     ap.add_argument("--impl", default="opx", choices=["opx", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # also a single-sample row (l = S), where the exact FLOPs equal
+    # the reference formula's full causal S (diagnostic line, not the default)
+    ap.add_argument("--single-sample", action="store_true")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -440,7 +443,7 @@ def main():
           "trace": True}
     sess = Session(cluster_for(n), model, wl, plan, ex, rank=rank, device=local, dist=dist)
     sess.init_weights(2508)
-    batch = synthetic_batch(arch["vocab"], S, rows, seed=2508)
+    batch = synthetic_batch(arch["vocab"], S, rows, seed=2508, single_sample=args.single_sample)
     enc = next((m for m in model["modules"] if m["kind"] == "encoder"), None)
     if enc:
         from paper_2508_02317_b200.runtime import rank_coords, synthetic_images
@@ -581,7 +584,7 @@ def main():
                    "parallelism": f"fsdp{plan['dp_shard']}xsp{plan['sp']}",
                    "recompute": plan["recompute"], "kept_layers": kept,
                    "async_ulysses": bool(plan.get("async_ulysses", False)),
-                   "packing": "lognormal varlen, 0 padding",
+                   "packing": "one sample per row" if args.single_sample else "lognormal varlen, 0 padding",
                    "l2": "inputs+weights >> 126 MB L2 (no flush needed)",
                    "peak_kind": peak_kind},
         "loss": losses[-1],
