@@ -82,7 +82,7 @@ struct Params {
   const int* seq_end;
   int N, hq, hk;
   float scale, scale_log2;
-  int skip_dq;  // debug: measure without the dQ reduction
+  int skip_dq;  // debug: 1 = measure without the dQ reduction, 2 = without its staging too
   long long* prof;  // debug (OPX_ATTN_PROF=<cta>): clock64 stamps [64 iters][16] of one CTA
   int prof_cta;
   int splits;   // q-head splits per kv head
@@ -296,10 +296,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (dq_issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       bar_sync_dq();  // staging buffer free
       if (dq_issuer) PROF(j + 1, 12);
+      if (p.skip_dq < 2) {
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[q * D + r] = __uint_as_float(qa[q]) * p.scale;
+        for (int q = 0; q < 32; ++q) stage[q * D + r] = __uint_as_float(qa[q]) * p.scale;
 #pragma unroll
-      for (int q = 0; q < 32; ++q) stage[(32 + q) * D + r] = __uint_as_float(qb[q]) * p.scale;
+        for (int q = 0; q < 32; ++q) stage[(32 + q) * D + r] = __uint_as_float(qb[q]) * p.scale;
+      }
       ptx::fence_proxy_async();
       bar_sync_dq();
       if (dq_issuer) PROF(j + 1, 13);
@@ -600,7 +602,7 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
   p.hk = a.hk;
   p.scale = a.scale;
   p.scale_log2 = a.scale * LOG2E;
-  p.skip_dq = getenv("OPX_DEBUG_SKIP_DQ") != nullptr;
+  p.skip_dq = getenv("OPX_DEBUG_SKIP_DQ") ? atoi(getenv("OPX_DEBUG_SKIP_DQ")) : 0;  // 1: no reduce, 2: no stage either
   static long long* prof = nullptr;
   p.prof = nullptr;
   p.prof_cta = getenv("OPX_ATTN_PROF") ? atoi(getenv("OPX_ATTN_PROF")) : -1;
