@@ -328,17 +328,13 @@ __global__ void zero_pad_kernel(bf16* __restrict__ buf, int64_t ld, int W,
   }
 }
 
-// Dispatch: for every pair in this rank's sorted order, copy its token row
-// (src row = pair / k, or the pair row itself when per_pair) to the expert
-// rank's receive buffer.  One warp per pair, 16 B per lane.
-__global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, int per_pair,
-                                const int* __restrict__ pair_at, int P, int k,
-                                const int* __restrict__ counts_all, const int* __restrict__ excl,
-                                Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst,
-                                int W, int le_lo, int le_hi) {
-  // smem: [ep][El+1] segment starts of every destination rank, then per expert
-  // this rank's sorted offset (excl) and the rows earlier ranks put before ours
-  extern __shared__ int st[];
+// Destination tables of the dispatch addressing, in smem (int[route_smem_ints]):
+// [ep][El+1] segment starts of every destination rank, then per expert this
+// rank's sorted offset (excl) and the rows earlier ranks put before ours.
+// Filled by the whole block; the caller syncs.
+__host__ __device__ inline int route_smem_ints(const Layout& L) { return L.ep * (L.El + 1) + 2 * L.E; }
+__device__ void route_tables(const int* __restrict__ counts_all, const int* __restrict__ excl,
+                             const Layout& L, int me, int* st) {
   int* sx = st + L.ep * (L.El + 1);
   int* sb = sx + L.E;
   if (threadIdx.x < L.ep) {
@@ -356,21 +352,41 @@ __global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, in
     for (int s = 0; s < me; ++s) before += counts_all[s * L.E + e];
     sb[e] = before;
   }
+}
+// receive row (on rank d, local expert le) of sorted position pos
+__device__ __forceinline__ int route_row(int pos, const int* st, const Layout& L, int& d, int& le) {
+  const int* sx = st + L.ep * (L.El + 1);
+  const int* sb = sx + L.E;
+  // expert of this sorted position: largest e with excl[e] <= pos (E <= 1024)
+  int lo = 0, hi = L.E - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sx[mid] <= pos) lo = mid; else hi = mid - 1;
+  }
+  const int e = lo;
+  d = e / L.El;
+  le = e % L.El;
+  return st[d * (L.El + 1) + le] + sb[e] + (pos - sx[e]);
+}
+
+// Dispatch: for every pair in this rank's sorted order, copy its token row
+// (src row = pair / k, or the pair row itself when per_pair) to the expert
+// rank's receive buffer.  One warp per pair, 16 B per lane.
+__global__ void dispatch_kernel(const bf16* __restrict__ src, int64_t ld_src, int per_pair,
+                                const int* __restrict__ pair_at, int P, int k,
+                                const int* __restrict__ counts_all, const int* __restrict__ excl,
+                                Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst,
+                                int W, int le_lo, int le_hi) {
+  extern __shared__ int st[];
+  route_tables(counts_all, excl, L, me, st);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   for (int pos = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pos < P;
        pos += (gridDim.x * blockDim.x) >> 5) {
     const int p = pair_at[pos];
-    // expert of this sorted position: largest e with excl[e] <= pos (E <= 1024)
-    int lo = 0, hi = L.E - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (sx[mid] <= pos) lo = mid; else hi = mid - 1;
-    }
-    const int e = lo;
-    const int d = e / L.El, le = e % L.El;
+    int d, le;
+    const int row = route_row(pos, st, L, d, le);
     if (le < le_lo || le >= le_hi) continue;  // another phase's experts (moe_overlap)
-    const int row = st[d * (L.El + 1) + le] + sb[e] + (pos - sx[e]);
     const bf16* s = src + int64_t(per_pair ? pos : p / k) * ld_src;
     bf16* o = dst[d] + int64_t(row) * ld_dst;
     copy_row(o, s, W, lane);
@@ -444,11 +460,22 @@ __global__ void unpermute_kernel(const bf16* __restrict__ Y, int64_t ldy, const 
 
 // backward of the weighted combine (one warp per token):
 //   dYp[pos(t,j)] = bf16(w[t,j] * dx[t]);  dw[t,j] = <dx[t], Y[pos(t,j)]>
-// dx[t] stays in registers (MAXC chunks of 256 columns, 8 per lane, 16-B accesses)
-template <int MAXC>
+// dx[t] stays in registers (MAXC chunks of 256 columns, 8 per lane, 16-B accesses).
+// ROUTE (the a2a_combine_grad fused in): the dY row of sorted position pos is
+// stored straight into its expert rank's receive buffer, at the row the
+// dispatch addressing gives it (peer stores over NVLink; the local share as
+// plain stores), instead of into dYp for a separate dispatch pass to re-read.
+template <int MAXC, bool ROUTE>
 __global__ void combine_bwd_kernel(const float* __restrict__ dx, const bf16* __restrict__ Y, int64_t ldy,
                                    const int* __restrict__ pos_of_pair, const float* __restrict__ wts,
-                                   int T, int k, int H, bf16* __restrict__ dYp, float* __restrict__ dw) {
+                                   int T, int k, int H, bf16* __restrict__ dYp, float* __restrict__ dw,
+                                   const int* __restrict__ counts_all, const int* __restrict__ excl,
+                                   Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst) {
+  extern __shared__ int st[];
+  if (ROUTE) {
+    route_tables(counts_all, excl, L, me, st);
+    __syncthreads();
+  }
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -466,13 +493,24 @@ __global__ void combine_bwd_kernel(const float* __restrict__ dx, const bf16* __r
     const int pos = pos_of_pair[t * k + j];
     const float wj = wts[t * k + j];
     const bf16* yr = Y + int64_t(pos) * ldy + lane * 8;
-    bf16* dr = dYp + int64_t(pos) * ldy + lane * 8;
+    bf16* dr;
+    if (ROUTE) {
+      int d, le;
+      const int row = route_row(pos, st, L, d, le);
+      dr = dst[d] + int64_t(row) * ld_dst + lane * 8;
+    } else {
+      dr = dYp + int64_t(pos) * ldy + lane * 8;
+    }
+    // the whole Y row first (16 B per lane per chunk), then the stores
+    uint4 yq[MAXC];
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i)
+      if (i < nc) yq[i] = *reinterpret_cast<const uint4*>(yr + i * 256);
     float dot = 0.f;
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
       if (i >= nc) break;
-      const uint4 q = *reinterpret_cast<const uint4*>(yr + i * 256);
-      const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+      const uint32_t v[4] = {yq[i].x, yq[i].y, yq[i].z, yq[i].w};
       uint32_t o[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -679,16 +717,30 @@ cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_
 
 cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t ldy,
                               const int* pos_of_pair, const float* wts, int T, int k, int H,
-                              __nv_bfloat16* dYp, float* dw, cudaStream_t s) {
+                              __nv_bfloat16* dYp, float* dw, cudaStream_t s, const int* counts_all,
+                              const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
+                              int64_t ld_dst) {
   if (H % 256 || H > 4096) return cudaErrorInvalidValue;
+  Layout L{ep, E, ep > 0 ? E / ep : 0};
+  const bool route = dst != nullptr;
+  if (route && (ep < 1 || E % ep || E > 1024)) return cudaErrorInvalidValue;
+  const int smem = route ? route_smem_ints(L) * int(sizeof(int)) : 0;
   ++g_kernel_launches;
   const int blocks = (T * 32 + 255) / 256;
+#define OPX_CB(C)                                                                                    \
+  (route ? combine_bwd_kernel<C, true><<<blocks, 256, smem, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, \
+                                                                  dYp, dw, counts_all, excl, L, me,   \
+                                                                  dst, ld_dst)                       \
+         : combine_bwd_kernel<C, false><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H,  \
+                                                                dYp, dw, counts_all, excl, L, me, dst, \
+                                                                ld_dst))
   if (H <= 1024)
-    combine_bwd_kernel<4><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
+    OPX_CB(4);
   else if (H <= 2048)
-    combine_bwd_kernel<8><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
+    OPX_CB(8);
   else
-    combine_bwd_kernel<16><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, dYp, dw);
+    OPX_CB(16);
+#undef OPX_CB
   return cudaGetLastError();
 }
 

@@ -421,6 +421,18 @@ bool moe_fused_combine() {
   static const bool v = !getenv("OPX_MOE_FUSED_COMBINE") || atoi(getenv("OPX_MOE_FUSED_COMBINE"));
   return v;
 }
+// the a2a_combine_grad (dY rows to the expert ranks) fused into the combine
+// backward: each dY row is peer-stored to its receive row as it is computed,
+// instead of written locally and re-read by a dispatch pass.  Measured:
+// C2 slice 1 GPU 122.5K vs 121.2K tokens/s (combine_bwd + dispatch 3.8 -> 2.5 ms);
+// C2/EP4 with moe_overlap 192.8K vs 196.2K -- there the per-half dispatch on
+// the two streams lets half B's expert backward start earlier, so the
+// overlap path keeps it.  OPX_MOE_FUSED_DY: unset = fused outside the
+// moe_overlap path, 1 = always, 0 = never.
+int moe_fused_dy_mode() {
+  static const int v = getenv("OPX_MOE_FUSED_DY") ? atoi(getenv("OPX_MOE_FUSED_DY")) : -1;
+  return v;
+}
 bool moe_serial_halves() {
   static const bool v = getenv("OPX_MOE_SERIAL_HALVES") && atoi(getenv("OPX_MOE_SERIAL_HALVES"));
   return v;
@@ -624,10 +636,17 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
                        int(cap_rows_), st, lo, n));
     return OPX_OK;
   };
-  // weighted combine backward: per-pair output grads and router-weight grads
-  CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
-  // a2a_combine_grad: pair grads travel to the expert ranks (same layout as dispatch)
-  mk("combine_bwd");
+  // weighted combine backward: per-pair output grads and router-weight grads;
+  // a2a_combine_grad: pair grads travel to the expert ranks (same layout as
+  // dispatch) -- fused: stored there straight from the combine backward
+  const bool overlap = p_.moe_overlap && ep_ > 1 && El_ >= 2 && xs2_;
+  const bool fdy = moe_fused_dy_mode() < 0 ? !overlap : moe_fused_dy_mode() > 0;
+  if (fdy)
+    CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, nullptr, r_dw_, cs_, counts_all,
+                         r_excl_, ep_, E, ep_i_, d_dyrecv_peers_, H));
+  else
+    CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
+  mk("combine_bwd", fdy ? "combine_bwd,a2a_combine_grad" : nullptr);
   // experts [lo, hi): zero-pad, dgrad/wgrad of down, SwiGLU backward,
   // dgrad/wgrad of gate|up (wgrad K = 128-padded segment rows)
   auto experts_bwd = [&](int lo, int hi, cudaStream_t st) -> int {
@@ -661,19 +680,22 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
                 st));
     return OPX_OK;
   };
-  if (p_.moe_overlap && ep_ > 1 && El_ >= 2 && xs2_) {
+  if (overlap) {
     // moe_overlap: the second expert half's dY dispatch overlaps the first
     // half's expert backward, and the first half's dX combine the second's
     const int h = El_ / 2;
     cudaEvent_t ready = ev(), done_a = ev(), done_b = ev();
     CU(cudaEventRecord(ready, cs_));
     CU(cudaStreamWaitEvent(xs2_, ready, 0));
-    CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                      d_dyrecv_peers_, H, H, xs2_, h, El_));
+    if (!fdy)
+      CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                        d_dyrecv_peers_, H, H, xs2_, h, El_));
     TRY(barrier_ep3(xs2_));
-    CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                      d_dyrecv_peers_, H, H, cs_, 0, h));
-    mk("a2a_combine_grad");
+    if (!fdy) {
+      CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                        d_dyrecv_peers_, H, H, cs_, 0, h));
+      mk("a2a_combine_grad");
+    }
     TRY(barrier_ep(cs_));
     mk("a2a_wait");
     TRY(experts_bwd(0, h, cs_));
@@ -690,9 +712,11 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     CU(cudaStreamWaitEvent(cs_, done_b, 0));
     mk("experts_b");  // half B's expert backward, dX combine and barrier
   } else {
-    CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
-                      d_dyrecv_peers_, H, H, cs_));
-    mk("a2a_combine_grad");
+    if (!fdy) {
+      CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
+                        d_dyrecv_peers_, H, H, cs_));
+      mk("a2a_combine_grad");
+    }
     TRY(barrier_ep(cs_));
     mk("a2a_wait");
     // a2a_dispatch_grad: input grads travel back to the token owners

@@ -172,6 +172,31 @@ def test_dist_moe_partial_keep_paths(monkeypatch, env, overlap):
 
 
 @gpu
+@pytest.mark.parametrize("fused_dy", ["0", "1"])
+def test_dist_moe_dy_dispatch_modes(monkeypatch, fused_dy):
+    """The backward's dY rows reach the expert ranks either through a
+    dispatch pass after the combine backward (OPX_MOE_FUSED_DY=0) or peer-
+    stored by the combine backward itself (=1), under moe_overlap (whose
+    default is the per-half dispatch)."""
+    if NGPU < 2:
+        pytest.skip("needs 2 GPUs")
+    from tests.step_common import tiny_moe
+
+    monkeypatch.setenv("OPX_MOE_FUSED_DY", fused_dy)
+    model = tiny_moe(layers=2, hidden=512, heads=4, kv=2, ffn=768, vocab=2048, experts=64, top_k=4,
+                     expert_ffn=256)
+    plan = {"dp_replicate": 1, "dp_shard": 2, "sp": 1, "ep": 2, "micro_batch": 1, "recompute": "none",
+            "moe_overlap": True}
+    loss, sessions = _run(2, model, plan, 512, 2)
+    from paper_2508_02317_b200.runtime import synthetic_batch
+
+    compare_step(sessions, model, synthetic_batch(2048, 512, 2, seed=2508), plan, loss)
+    for s in sessions:
+        names = _comm_nodes(s.out[("trace", 0)])
+        assert sum(x.endswith(".a2a_combine_grad") for x in names) >= 2, names
+
+
+@gpu
 def test_dist_c0_fsdp2_sp2_head_dim_64():
     """BASELINE C0 as specified: 2 layers, H=256, 4 heads of 64 (2 kv),
     ffn 768, V=2048, S=1024, FSDP2 x SP2 on 4 GPUs, global batch 2."""
