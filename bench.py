@@ -222,12 +222,19 @@ class Clocks:
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a few hundred ms to start: wait for its first row
+            # so a short timed region (C2 on 1 GPU: ~0.35 s) still gets samples;
+            # rows seen before the region are kept apart
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5 and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
+        self.n0 = len(self.rows)
         return self
 
     def _read(self):
@@ -243,18 +250,19 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        rows = self.rows[self.n0:] or self.rows
+        sm = [float(r[0]) for r in rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for i, n in enumerate(names):
                 if len(r) > 4 + i and r[4 + i].lower().startswith("active"):
                     reasons.add(n)
         loaded = [s for s in sm if s > 500] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(rows)}
 
 
 # ---------------------------------------------------------------------------
@@ -469,11 +477,12 @@ def main():
     sess.load(batch)
     for _ in range(args.warmup):
         sess.run()
-    if dist:
-        dist.barrier()
     times, walls, launches, losses, enq = [], [], 0, [], []
     kept = 0
     with Clocks(local) as clk:
+        if dist:  # after every rank's clock sampler is up
+            dist.barrier()
+        torch.cuda.synchronize()
         for _ in range(args.steps):
             t0 = time.perf_counter()
             sess.load(batch)          # H2D of this step's inputs (host buffers)
