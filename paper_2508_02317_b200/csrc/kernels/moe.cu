@@ -470,7 +470,8 @@ __global__ void combine_bwd_kernel(const float* __restrict__ dx, const bf16* __r
                                    const int* __restrict__ pos_of_pair, const float* __restrict__ wts,
                                    int T, int k, int H, bf16* __restrict__ dYp, float* __restrict__ dw,
                                    const int* __restrict__ counts_all, const int* __restrict__ excl,
-                                   Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst) {
+                                   Layout L, int me, bf16* const* __restrict__ dst, int64_t ld_dst,
+                                   int le_lo, int le_hi) {
   extern __shared__ int st[];
   if (ROUTE) {
     route_tables(counts_all, excl, L, me, st);
@@ -497,6 +498,7 @@ __global__ void combine_bwd_kernel(const float* __restrict__ dx, const bf16* __r
     if (ROUTE) {
       int d, le;
       const int row = route_row(pos, st, L, d, le);
+      if (le < le_lo || le >= le_hi) continue;  // the other expert half's pair (moe_overlap)
       dr = dst[d] + int64_t(row) * ld_dst + lane * 8;
     } else {
       dr = dYp + int64_t(pos) * ldy + lane * 8;
@@ -719,9 +721,10 @@ cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t l
                               const int* pos_of_pair, const float* wts, int T, int k, int H,
                               __nv_bfloat16* dYp, float* dw, cudaStream_t s, const int* counts_all,
                               const int* excl, int ep, int E, int me, __nv_bfloat16* const* dst,
-                              int64_t ld_dst) {
+                              int64_t ld_dst, int le_lo, int le_hi) {
   if (H % 256 || H > 4096) return cudaErrorInvalidValue;
   Layout L{ep, E, ep > 0 ? E / ep : 0};
+  if (le_hi < 0) le_hi = L.El;
   const bool route = dst != nullptr;
   if (route && (ep < 1 || E % ep || E > 1024)) return cudaErrorInvalidValue;
   const int smem = route ? route_smem_ints(L) * int(sizeof(int)) : 0;
@@ -730,10 +733,10 @@ cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t l
 #define OPX_CB(C)                                                                                    \
   (route ? combine_bwd_kernel<C, true><<<blocks, 256, smem, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H, \
                                                                   dYp, dw, counts_all, excl, L, me,   \
-                                                                  dst, ld_dst)                       \
+                                                                  dst, ld_dst, le_lo, le_hi)         \
          : combine_bwd_kernel<C, false><<<blocks, 256, 0, s>>>(dx, Y, ldy, pos_of_pair, wts, T, k, H,  \
                                                                 dYp, dw, counts_all, excl, L, me, dst, \
-                                                                ld_dst))
+                                                                ld_dst, 0, 0))
   if (H <= 1024)
     OPX_CB(4);
   else if (H <= 2048)

@@ -157,13 +157,14 @@ cudaError_t k_moe_unpermute(const __nv_bfloat16* Y, int64_t ldy, const int* pos_
                             const float* wts, int T, int k, int H, const float* resid, float* out,
                             cudaStream_t s);
 // dst != nullptr: the dY rows go straight to the expert ranks' receive buffers
-// (the a2a_combine_grad fused in, k_moe_dispatch's addressing) instead of dYp
+// (the a2a_combine_grad fused in, k_moe_dispatch's addressing) instead of dYp;
+// then only pairs of local experts [le_lo, le_hi) are processed (dw included)
 cudaError_t k_moe_combine_bwd(const float* dx, const __nv_bfloat16* Y, int64_t ldy,
                               const int* pos_of_pair, const float* wts, int T, int k, int H,
                               __nv_bfloat16* dYp, float* dw, cudaStream_t s,
                               const int* counts_all = nullptr, const int* excl = nullptr, int ep = 0,
                               int E = 0, int me = 0, __nv_bfloat16* const* dst = nullptr,
-                              int64_t ld_dst = 0);
+                              int64_t ld_dst = 0, int le_lo = 0, int le_hi = -1);
 cudaError_t k_moe_publish_counts(const int* counts, int* const* tables, int ep, int me, int E,
                                  cudaStream_t s);
 cudaError_t k_moe_swiglu_bwd(const __nv_bfloat16* dact, const __nv_bfloat16* gu, __nv_bfloat16* dgu,

@@ -425,10 +425,10 @@ bool moe_fused_combine() {
 // backward: each dY row is peer-stored to its receive row as it is computed,
 // instead of written locally and re-read by a dispatch pass.  Measured:
 // C2 slice 1 GPU 122.5K vs 121.2K tokens/s (combine_bwd + dispatch 3.8 -> 2.5 ms);
-// C2/EP4 with moe_overlap 192.8K vs 196.2K -- there the per-half dispatch on
-// the two streams lets half B's expert backward start earlier, so the
-// overlap path keeps it.  OPX_MOE_FUSED_DY: unset = fused outside the
-// moe_overlap path, 1 = always, 0 = never.
+// C2/EP4 with moe_overlap, one fused pass over all pairs: 192.8K vs 196.2K
+// (the per-half dispatch on two streams let half B's expert backward start
+// earlier), hence the per-half fused passes there.  OPX_MOE_FUSED_DY=0
+// restores the separate dispatch.
 int moe_fused_dy_mode() {
   static const int v = getenv("OPX_MOE_FUSED_DY") ? atoi(getenv("OPX_MOE_FUSED_DY")) : -1;
   return v;
@@ -640,13 +640,21 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
   // a2a_combine_grad: pair grads travel to the expert ranks (same layout as
   // dispatch) -- fused: stored there straight from the combine backward
   const bool overlap = p_.moe_overlap && ep_ > 1 && El_ >= 2 && xs2_;
-  const bool fdy = moe_fused_dy_mode() < 0 ? !overlap : moe_fused_dy_mode() > 0;
-  if (fdy)
-    CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, nullptr, r_dw_, cs_, counts_all,
-                         r_excl_, ep_, E, ep_i_, d_dyrecv_peers_, H));
-  else
+  const bool fdy = moe_fused_dy_mode() != 0;
+  // fused: local experts [lo, hi) of every rank (moe_overlap issues the halves
+  // on two streams, half B first)
+  auto combine_bwd_to = [&](int lo, int hi, cudaStream_t st) -> int {
+    CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, nullptr, r_dw_, st, counts_all,
+                         r_excl_, ep_, E, ep_i_, d_dyrecv_peers_, H, lo, hi));
+    return OPX_OK;
+  };
+  if (fdy && !overlap) {
+    TRY(combine_bwd_to(0, El_, cs_));
+    mk("combine_bwd", "combine_bwd,a2a_combine_grad");
+  } else if (!fdy) {
     CU(k_moe_combine_bwd(dx_, yback, H, r_pos_, r_wts_, T, k, H, dyp_, r_dw_, cs_));
-  mk("combine_bwd", fdy ? "combine_bwd,a2a_combine_grad" : nullptr);
+    mk("combine_bwd");
+  }
   // experts [lo, hi): zero-pad, dgrad/wgrad of down, SwiGLU backward,
   // dgrad/wgrad of gate|up (wgrad K = 128-padded segment rows)
   auto experts_bwd = [&](int lo, int hi, cudaStream_t st) -> int {
@@ -687,11 +695,16 @@ int Step::moe_bwd(int l, const Unit& u, Unit& eu, void* G, void* Ge, float* dh2)
     cudaEvent_t ready = ev(), done_a = ev(), done_b = ev();
     CU(cudaEventRecord(ready, cs_));
     CU(cudaStreamWaitEvent(xs2_, ready, 0));
-    if (!fdy)
+    if (fdy)
+      TRY(combine_bwd_to(h, El_, xs2_));
+    else
       CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
                         d_dyrecv_peers_, H, H, xs2_, h, El_));
     TRY(barrier_ep3(xs2_));
-    if (!fdy) {
+    if (fdy) {
+      TRY(combine_bwd_to(0, h, cs_));
+      mk("combine_bwd", "combine_bwd,a2a_combine_grad");
+    } else {
       CU(k_moe_dispatch(dyp_, H, 1, r_pairat_, P, k, counts_all, r_excl_, ep_, E, ep_i_,
                         d_dyrecv_peers_, H, H, cs_, 0, h));
       mk("a2a_combine_grad");
