@@ -144,6 +144,14 @@ int opx_step_tensor_info(opx_step* st, const char* name, int64_t* numel, int64_t
  * with phase names from step_graph.cpp (fwd.layer<i>, bwd.layer<i>, fwd.head,
  * bwd.head, encoder, optimizer).  len receives strlen; cap must exceed it. */
 int opx_step_report_json(opx_step* st, char* out_json, size_t cap, size_t* len);
+/* exposed_comm_seconds (simulator.cpp:71-104; replaces its private helper,
+ * used by report() at simulator.cpp:118): seconds of the comm intervals
+ * [comm_start[i], comm_end[i]) that no compute interval covers.  Intervals may
+ * overlap or nest (several streams).  Host-only, no GPU; the step's
+ * exposed_comm / comm_wait_s are this over its measured node intervals. */
+double opx_exposed_comm_seconds(const double* compute_start, const double* compute_end,
+                                int64_t n_compute, const double* comm_start,
+                                const double* comm_end, int64_t n_comm);
 /* Chrome trace of the last step in simulator.cpp:133-151's schema. */
 int opx_step_trace(opx_step* st, char* out_json, size_t cap, size_t* len);
 int opx_step_destroy(opx_step* st);

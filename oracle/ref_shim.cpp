@@ -193,4 +193,33 @@ int ref_reshard_plan(long long numel, long long src_parts, long long dst_parts, 
   }
 }
 
+// the reference's report() (simulator.cpp:108-130) on a one-device timeline of
+// n intervals (chan 0 = compute, 1 = comm): exposed comm in seconds
+int ref_exposed_comm(const double* start, const double* end, const int* chan, long long n,
+                     double makespan, double* exposed_s) {
+  StepGraph g;
+  Timeline tl;
+  tl.world = 1;
+  tl.makespan = makespan;
+  for (long long i = 0; i < n; ++i) {
+    OpNode nd;
+    nd.id = i;
+    nd.kind = chan[i] ? NodeKind::collective : NodeKind::compute;
+    nd.name = "n" + std::to_string(i);
+    nd.phase = "p";
+    g.nodes.push_back(nd);
+    tl.events.push_back(TimelineEvent{0, chan[i], start[i], end[i], i});
+    tl.node_start.push_back(start[i]);
+    tl.node_end.push_back(end[i]);
+  }
+  ParallelPlan p;
+  ModelSpec m;
+  ClusterSpec c;
+  c.gpu.peak_flops = 1.0;
+  WorkloadSpec w;
+  const StepReport r = report(tl, g, p, m, c, w);
+  *exposed_s = r.exposed_comm * makespan;
+  return 0;
+}
+
 }  // extern "C"

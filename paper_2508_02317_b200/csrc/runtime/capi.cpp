@@ -1,4 +1,5 @@
 // C-ABI: error plumbing, plan-layer entry points and kernel-level wrappers.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <sstream>
@@ -28,6 +29,30 @@ uint64_t fnv1a64(const char* s) {
     h *= 0x100000001b3ull;
   }
   return h;
+}
+
+// simulator.cpp:71-104: comm intervals sorted by start, each walked against
+// the compute intervals (sorted by start) that overlap it; a compute interval
+// nested inside one already passed leaves the cursor where it is
+double exposed_comm_seconds(std::vector<std::pair<double, double>>& compute,
+                            std::vector<std::pair<double, double>>& comm) {
+  std::sort(compute.begin(), compute.end());
+  std::sort(comm.begin(), comm.end());
+  double exposed = 0;
+  size_t ci = 0;
+  for (const auto& [start, end] : comm) {
+    double cur = start;
+    while (ci < compute.size() && compute[ci].second <= cur) ++ci;
+    for (size_t j = ci; cur < end; ++j) {
+      if (j >= compute.size() || compute[j].first >= end) {
+        exposed += end - cur;
+        break;
+      }
+      if (compute[j].first > cur) exposed += compute[j].first - cur;
+      cur = std::max(cur, compute[j].second);
+    }
+  }
+  return exposed;
 }
 
 uint64_t param_key(const std::string& name, uint64_t seed) {
@@ -379,6 +404,15 @@ int opx_attn_bwd_tc(const void* q, const void* k, const void* v, const void* o, 
   a.lddv = ld_kv;
   a.delta = delta;
   OPX_CALL(k_attn_bwd_tc(a, static_cast<cudaStream_t>(stream)), "opx_attn_bwd_tc");
+}
+
+double opx_exposed_comm_seconds(const double* compute_start, const double* compute_end,
+                                int64_t n_compute, const double* comm_start,
+                                const double* comm_end, int64_t n_comm) {
+  std::vector<std::pair<double, double>> compute, comm;
+  for (int64_t i = 0; i < n_compute; ++i) compute.push_back({compute_start[i], compute_end[i]});
+  for (int64_t i = 0; i < n_comm; ++i) comm.push_back({comm_start[i], comm_end[i]});
+  return opx::exposed_comm_seconds(compute, comm);
 }
 
 int opx_pack(const int64_t* ids, const int64_t* lengths, int64_t n, int64_t target, int policy,

@@ -1468,25 +1468,7 @@ void Step::measure_nodes(opx_step_report* r) {
     if (t.comm) r->comm_s += b - a;
   }
   cudaGetLastError();
-  std::sort(compute.begin(), compute.end());
-  std::sort(comm.begin(), comm.end());
-  double exposed = 0;
-  size_t ci = 0;
-  for (const auto& [start, end] : comm) {
-    double cur = start;
-    while (ci < compute.size() && compute[ci].second <= cur) ++ci;
-    // intervals on several streams can nest: scan every compute interval
-    // starting before `end` (sorted by start), advancing the covered cursor
-    for (size_t j = ci; cur < end; ++j) {
-      if (j >= compute.size() || compute[j].first >= end) {
-        exposed += end - cur;
-        break;
-      }
-      if (compute[j].second <= cur) continue;
-      if (compute[j].first > cur) exposed += compute[j].first - cur;
-      cur = std::max(cur, compute[j].second);
-    }
-  }
+  const double exposed = exposed_comm_seconds(compute, comm);
   r->comm_wait_s = exposed;
   r->exposed_comm = r->step_time_s > 0 ? exposed / r->step_time_s : 0.0;
 }
