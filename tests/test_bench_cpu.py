@@ -75,3 +75,20 @@ def test_node_keys_merge_layers_and_micro_batches():
     assert bench.node_key("bwd.head.m1") == "bwd.head"
     assert bench.node_key("encoder.vision.m0") == "encoder.vision"
     assert bench.node_key("optimizer") == "optimizer"
+
+
+@pytest.mark.parametrize("cfg", ["c0", "c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_bench_plans_validate_at_every_gpu_count(bench, cfg, n):
+    """The plan bench.py runs for each config at 1/2/4/8 GPUs (the driver's
+    scaling sweep) passes the reference's validation (plan.cpp:19-83, through
+    libopx's differential-tested validator) and resolves to world n."""
+    from paper_2508_02317_b200 import plan as P
+
+    pl, m, S = bench.plan_for(cfg, n), bench.model_for(cfg, n), bench.seq_for(cfg)
+    rows = pl["dp_replicate"] * pl["dp_shard"] * pl["micro_batch"]
+    wl = {"seq_len": S, "micro_batch": pl["micro_batch"], "global_batch": rows}
+    if cfg == "c3":
+        wl["modality_mix"] = {"vision": bench.C3_IMAGE_MIX, "text": 1.0 - bench.C3_IMAGE_MIX}
+    assert P.validate(bench.cluster_for(n), m, wl, pl) == []
+    assert P.resolve(bench.cluster_for(n), m, wl, pl)["world"] == n
