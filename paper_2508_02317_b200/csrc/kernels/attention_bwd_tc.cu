@@ -85,6 +85,7 @@ struct Params {
   int skip_dq;  // debug: 1 = measure without the dQ reduction, 2 = without its staging too
   long long* prof;  // debug (OPX_ATTN_PROF=<cta>): clock64 stamps [64 iters][16] of one CTA
   int prof_cta;
+  int band;     // CTA order (attn::cta_order)
   int splits;   // q-head splits per kv head
   int f32kv;    // dK/dV go to fp32 [N, hk, 128] through tdk/tdv (reduce-add if splits > 1)
 };
@@ -145,8 +146,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* stage = reinterpret_cast<float*>(smem + OFF_STAGE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k0 = blockIdx.x * BK;
-  const int kh = blockIdx.y / p.splits, sidx = blockIdx.y % p.splits;
+  int bx, by;
+  cta_order(p.band, bx, by);
+  const int k0 = bx * BK;
+  const int kh = by / p.splits, sidx = by % p.splits;
   const int G = p.hq / p.hk;
   const int hbase = kh * G + (sidx * G) / p.splits;
   const int nh = ((sidx + 1) * G) / p.splits - (sidx * G) / p.splits;
@@ -613,6 +616,7 @@ cudaError_t k_attn_bwd_tc(const AttnArgs& a, cudaStream_t s) {
   }
   p.splits = splits;
   p.f32kv = f32kv;
+  p.band = cta_band("OPX_ATTN_BAND", 0, splits, a.hk * splits);
   dim3 grid((a.N + BK - 1) / BK, a.hk * splits);
   ++g_kernel_launches;
   attn_bwd_tc_kernel<<<grid, THREADS, SMEM, s>>>(mq, mk, mv, mdo, mdq, mdk, mdv, p);

@@ -52,6 +52,7 @@ struct FwdParams {
   const int* seq_end;  // bidirectional mode only
   int N, hq, hk, npairs, causal;
   float scale_log2;
+  int band;  // CTA order (attn::cta_order)
 };
 
 
@@ -81,8 +82,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = p.npairs - 1 - int(blockIdx.x);  // heavy (late) tiles first
-  const int h = blockIdx.y;
+  int bx, by;
+  cta_order(p.band, bx, by);
+  const int pair = p.npairs - 1 - bx;  // heavy (late) tiles first
+  const int h = by;
   const int kh = h / (p.hq / p.hk);
   const int q0 = pair * 2 * BM;
   const int qlast = min(q0 + 2 * BM, p.N) - 1;
@@ -340,6 +343,7 @@ cudaError_t k_attn_fwd_tc(const AttnArgs& a, cudaStream_t s) {
   p.hk = a.hk;
   p.npairs = (a.N + 2 * BM - 1) / (2 * BM);
   p.scale_log2 = a.scale * LOG2E;
+  p.band = cta_band("OPX_ATTN_FWD_BAND", 0, a.hq / a.hk, a.hq);
   dim3 grid(p.npairs, a.hq);
   ++g_kernel_launches;
   attn_fwd_tc_kernel<<<grid, FWD_THREADS, FWD_SMEM, s>>>(mq, mk, mv, p);

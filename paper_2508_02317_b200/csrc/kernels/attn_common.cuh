@@ -5,12 +5,43 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "ptx.cuh"
 
 namespace opx {
 namespace attn {
+
+// CTA order: the grid is (tiles, heads); with band > 1 the linear block id
+// walks bands of `band` heads tile-major (every head of the band at tile 0,
+// then tile 1, ...), so the heaviest tiles of the LAST heads no longer start
+// in the final wave (the causal tail).  band == 1 is the plain x-fastest order.
+// Default band = the GQA group (its q heads share the K/V tiles; their Q/dO
+// stay within L2): 7q/1kv (C1 SP4 rank shape) fwd 870 -> 930, bwd 795 -> 872
+// TF/s; 28q/4kv within noise (fwd +1-3 %, bwd +-1 %); a band over all 28
+// heads lost 3-4 % in the backward (Q/dO of 28 heads overflow L2).
+// gridDim.y must be a multiple of band.
+static __device__ __forceinline__ void cta_order(int band, int& bx, int& by) {
+  if (band <= 1) {
+    bx = blockIdx.x;
+    by = blockIdx.y;
+    return;
+  }
+  const int L = blockIdx.x + gridDim.x * blockIdx.y;
+  const int per = band * gridDim.x;
+  const int b = L / per, r = L % per;
+  bx = r / band;
+  by = b * band + r % band;
+}
+// band from the environment variable `name` (default `def`; 0 = the GQA
+// group size g); a band that does not divide ny falls back to 1
+static inline int cta_band(const char* name, int def, int g, int ny) {
+  const char* e = getenv(name);
+  int b = e ? atoi(e) : def;
+  if (b == 0) b = g;
+  return (b > 1 && ny % b == 0) ? b : 1;
+}
 
 static __device__ __forceinline__ uint64_t kdesc(uint32_t base, int k) {
   // K-major SW128 operand of a [128][128] tile stored as two 64-col blocks

@@ -1,6 +1,7 @@
 """Microbenchmark: attention fwd/bwd TFLOP/s on the C1 (Qwen2-7B 32K) shapes."""
 import ctypes
 import math
+import os
 import sys
 
 import torch
@@ -16,9 +17,12 @@ def P(t):
 
 def main():
     S = torch.cuda.current_stream().cuda_stream
-    for (N, hq, hk) in [(32768, 7, 1), (32768, 28, 4)]:
+    shapes = [(32768, 7, 1, False), (32768, 28, 4, False), (32768, 28, 4, True)]
+    if os.environ.get("BENCH_ATTN_SHAPES"):  # e.g. "1,2": a subset of the shapes
+        shapes = [shapes[int(i)] for i in os.environ["BENCH_ATTN_SHAPES"].split(",")]
+    for (N, hq, hk, single) in shapes:
         b = synthetic_batch(1000, N, 1, seed=2508)
-        cu = b["cu_rows"][0]
+        cu = [0, N] if single else b["cu_rows"][0]
         st = torch.empty(N, dtype=torch.int32)
         en = torch.empty(N, dtype=torch.int32)
         sq = 0
@@ -41,7 +45,7 @@ def main():
         dv32 = torch.empty_like(dk32)
         flops = 4 * 128 * hq * sq / 2  # causal fwd
         sc = 1 / math.sqrt(128)
-        names = ["opx_attn_fwd_tc", "opx_attn_bwd_tc"] + [f"split{sp}" for sp in range(0, hq // hk + 1)]
+        names = ["opx_attn_fwd_tc", "split0"]  # split0: the step's path (fp32 dK/dV, one q head per CTA)
         for name in names:
             def run():
                 if name.startswith("split"):
@@ -67,7 +71,8 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
             f = flops * (2.5 if ("bwd" in name or "split" in name) else 1.0)
-            print(f"{name:18s} N={N} hq={hq} hk={hk}: {ms:8.3f} ms  {f / ms / 1e9:8.1f} TFLOP/s")
+            tag = " single" if single else ""
+            print(f"{name:18s} N={N} hq={hq} hk={hk}{tag}: {ms:8.3f} ms  {f / ms / 1e9:8.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
