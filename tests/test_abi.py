@@ -47,3 +47,18 @@ def test_step_report_struct_matches_header():
             fields.append((n.strip(), typ))
     want = {"double": ctypes.c_double, "int64_t": ctypes.c_int64}
     assert [(n, want[t]) for n, t in fields] == [(n, t) for n, t in StepReport._fields_]
+
+
+def test_missing_native_library_fails_loudly():
+    """No fallback: with libopx.so absent every entry point raises."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("from paper_2508_02317_b200 import lib, OpxError\n"
+            "try:\n    lib()\nexcept OpxError as e:\n    print('raised', e.code)\n")
+    env = dict(os.environ, OPX_LIB_PATH="/nonexistent/libopx.so")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=120)
+    assert out.stdout.strip() == "raised 6", out.stdout + out.stderr
